@@ -1,0 +1,187 @@
+"""Pins for the oracle's verify (C1): accept test, first rejection, residual /
+bonus inverse-CDF sample and the emitted-token layout.
+
+The decisive pin is distributional: verify-then-resample must reproduce exact
+target autoregressive sampling (brute force over all strings).
+The rest are special cases the texts spell out and invariants
+(S:145-147)."""
+import numpy as np
+import pytest
+import scipy.special as sps
+
+import oracle
+import synth
+from tests import spec_sim
+
+
+def oracle_verify_fn(cu, tokens, target, draft, seeds):
+    r = oracle.verify(cu, tokens, target, draft, seeds, oracle.F32)
+    return r.accepted_len, r.emitted
+
+
+@pytest.mark.parametrize("V,L,seed", [(4, 3, 11), (8, 3, 12), (2, 3, 13)])
+def test_distribution_exact_bruteforce(V, L, seed):
+    """S:584 acceptance #1: V <= 8, depth 3, 10^6 runs, TV <= 0.01 and chi^2."""
+    tab = spec_sim.Tables(V, L, seed)
+    codes = spec_sim.run_generation(tab, 10 ** 6, oracle_verify_fn, seed)
+    spec_sim.check_distribution(tab, codes)
+
+
+def test_first_position_rejection_rate_is_tv():
+    """P(reject at position 0) = 1 - sum_v min(p_v, q_v) = TV(p, q) when
+    x ~ q (rejection sampling)."""
+    tab = spec_sim.Tables(6, 2, 21, sigma_n=1.2)
+    n = 400_000
+    rec = {}
+
+    def keep(cu, tokens, acc, emitted):
+        rec["acc"] = acc.copy()
+
+    spec_sim.run_generation(tab, n, oracle_verify_fn, 21, k_max=1, record_first=keep)
+    tv = 0.5 * np.abs(tab.P[0] - tab.Q[0]).sum()
+    rate = np.mean(rec["acc"] == 0)
+    sd = np.sqrt(tv * (1 - tv) / n)
+    assert abs(rate - tv) < 5 * sd
+
+
+def _batch(V, k, seed, dtype=np.float32, same=False):
+    r = np.random.default_rng(seed)
+    B = len(k)
+    cu = synth.cu_from_k(k)
+    nk = int(cu[-1])
+    t = r.normal(0, 3, (nk + B, V)).astype(dtype)
+    if same:
+        d = np.stack([t[cu[i] + i + j] for i in range(B) for j in range(k[i])]) if nk else t[:0]
+    else:
+        d = (r.normal(0, 3, (nk, V))).astype(dtype)
+    tok = r.integers(0, V, nk).astype(np.int32)
+    seeds = synth.slot_seeds(seed, 0, cu)
+    return cu, tok, t, d, seeds
+
+
+def test_draft_equals_target_accepts_all_and_bonus_follows_p():
+    """draft == target -> accepted_count == k always; the bonus token is
+    then distributed as p of target row k."""
+    k = [3, 1, 4, 2] * 50
+    cu, tok, t, d, seeds = _batch(16, k, 3, same=True)
+    r = oracle.verify(cu, tok, t, d, seeds, oracle.F32)
+    assert (r.accepted_len == np.asarray(k)).all()
+    assert np.all(r.log_ratio == 0.0)
+    assert np.all(r.kld == 0.0)
+    # bonus row draws: same target row repeated, many seeds -> frequencies ~ p
+    V, n = 5, 200_000
+    row = np.float32([0.0, 1.0, -0.5, 2.0, 0.3])
+    t = np.tile(row, (2 * n, 1))
+    d = np.tile(row, (n, 1))
+    cu1 = synth.cu_from_k(np.ones(n, np.int64))
+    s = synth.slot_seeds(99, 0, cu1)
+    r = oracle.verify(cu1, np.zeros(n, np.int32), t, d, s, oracle.F32)
+    assert (r.accepted_len == 1).all()
+    bonus = r.emitted[1::2]
+    freq = np.bincount(bonus, minlength=V) / n
+    p = sps.softmax(row.astype(np.float64))
+    assert np.max(np.abs(freq - p)) < 5 * np.sqrt(p * (1 - p) / n).max()
+
+
+def test_disjoint_one_hot_rejects_and_recovers_target_token():
+    """draft one-hot at x, target one-hot at x' -> a = 0, token x'."""
+    V = 8
+    n = 64
+    t = np.full((2 * n, V), -1e4, np.float32)
+    d = np.full((n, V), -1e4, np.float32)
+    t[0::2, 5] = 0.0
+    t[1::2, :] = 0.0
+    d[:, 2] = 0.0
+    cu = synth.cu_from_k(np.ones(n, np.int64))
+    r = oracle.verify(cu, np.full(n, 2, np.int32), t, d, synth.slot_seeds(7, 0, cu), oracle.F32)
+    assert (r.accepted_len == 0).all()
+    assert (r.emitted[0::2] == 5).all()
+    assert (r.emitted[1::2] == -1).all()
+
+
+def test_worked_example_v2():
+    """t=(0,0), d=(0, ln 3) [fp32], x=1: r = 2/3 (up to fp32 rounding of ln 3);
+    residual (0.25, 0) -> recovery is token 0. seed 0: u_acc=0.399 < 2/3 ->
+    accept; seed 1: u_acc=0.890 -> reject -> token 0."""
+    t = np.float32([[0.0, 0.0], [0.0, 0.0]])
+    d = np.float32([[0.0, np.log(3.0)]])
+    cu = np.int32([0, 1])
+    tok = np.int32([1])
+    r0 = oracle.verify(cu, tok, t, d, np.uint64([0, 5]), oracle.F32)
+    assert abs(np.exp(r0.log_ratio[0]) - 2 / 3) < 1e-7
+    assert r0.accepted_len[0] == 1 and r0.emitted[0] == 1
+    r1 = oracle.verify(cu, tok, t, d, np.uint64([1, 5]), oracle.F32)
+    assert r1.accepted_len[0] == 0 and r1.emitted[0] == 0 and r1.emitted[1] == -1
+    assert abs(r1.samp_diag[0, 0] - 0.25) < 1e-7   # residual mass R = TV = 1/4
+
+
+def test_prefix_shape_and_layout():
+    """emitted = accepted prefix + exactly one token + pads;
+    KLD at every position."""
+    k = synth.random_k(300, 8, 5)
+    cu, tok, t, d, seeds = _batch(50, k, 6)
+    r = oracle.verify(cu, tok, t, d, seeds, oracle.F32)
+    for i in range(len(k)):
+        a = r.accepted_len[i]
+        s0 = cu[i] + i
+        assert 0 <= a <= k[i]
+        assert (r.emitted[s0:s0 + a] == tok[cu[i]:cu[i] + a]).all()
+        assert 0 <= r.emitted[s0 + a] < 50
+        assert (r.emitted[s0 + a + 1:s0 + k[i] + 1] == -1).all()
+        acc = r.u_acc[s0:s0 + k[i]] < np.minimum(1, np.exp(r.log_ratio[cu[i]:cu[i] + k[i]]))
+        first = np.argmin(acc) if not acc.all() else k[i]
+        assert first == a
+    assert np.all(r.kld > 0)
+
+
+def test_accepted_len_invariant_to_tokens_after_rejection():
+    """changing draft tokens after the first rejection changes nothing."""
+    k = synth.random_k(200, 6, 8, k_min=2)
+    cu, tok, t, d, seeds = _batch(30, k, 9)
+    r = oracle.verify(cu, tok, t, d, seeds, oracle.F32)
+    tok2 = tok.copy()
+    for i in range(len(k)):
+        a = r.accepted_len[i]
+        for j in range(a + 1, k[i]):
+            tok2[cu[i] + j] = (tok2[cu[i] + j] + 7) % 30
+    r2 = oracle.verify(cu, tok2, t, d, seeds, oracle.F32)
+    assert (r.accepted_len == r2.accepted_len).all()
+    for i in range(len(k)):
+        s0 = cu[i] + i
+        a = r.accepted_len[i]
+        assert (r.emitted[s0:s0 + a + 1] == r2.emitted[s0:s0 + a + 1]).all()
+
+
+def test_bf16_matches_fp32_on_exact_values():
+    """bf16 patterns convert exactly: integer-valued logits give identical results."""
+    k = [2, 3, 1]
+    r = np.random.default_rng(10)
+    cu = synth.cu_from_k(k)
+    nk = int(cu[-1])
+    t = r.integers(-8, 8, (nk + 3, 40)).astype(np.float32)
+    d = r.integers(-8, 8, (nk, 40)).astype(np.float32)
+    tok = r.integers(0, 40, nk).astype(np.int32)
+    s = synth.slot_seeds(1, 1, cu)
+
+    def bf(x):
+        return (x.view(np.uint32) >> 16).astype(np.uint16)
+
+    a = oracle.verify(cu, tok, t, d, s, oracle.F32)
+    b = oracle.verify(cu, tok, bf(t), bf(d), s, oracle.BF16)
+    assert (a.emitted == b.emitted).all() and np.array_equal(a.kld, b.kld)
+
+
+def test_multithreaded_identical():
+    k = synth.random_k(64, 8, 3)
+    cu, tok, t, d, seeds = _batch(100, k, 4)
+    a = oracle.verify(cu, tok, t, d, seeds, oracle.F32, nthreads=1)
+    b = oracle.verify(cu, tok, t, d, seeds, oracle.F32, nthreads=7)
+    assert (a.emitted == b.emitted).all() and np.array_equal(a.kld, b.kld)
+
+
+def test_invalid_inputs_raise():
+    cu = np.int32([0, 1])
+    t = np.zeros((2, 4), np.float32)
+    d = np.zeros((1, 4), np.float32)
+    with pytest.raises(ValueError):
+        oracle.verify(cu, np.int32([9]), t, d, np.uint64([0, 1]), oracle.F32)
