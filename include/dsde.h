@@ -1,0 +1,275 @@
+/*
+ * dsde.h — C-ABI of the B200-native DSDE speculative-verification hot path.
+ *
+ * DSDE = "Dynamic Speculative Decoding Engine", arXiv 2509.01083.
+ * Citation keys: P:n = PAPER.md line n; S:n = SPEC.md line n; D1..D17 =
+ * the readings of the paper listed in DESIGN.md §3.
+ *
+ * The library (libdsde.so) exports exactly the functions declared here.
+ * Signatures use plain pointers, sizes and opaque handles only.
+ *
+ * Conventions for every entry point:
+ *   - Pointers are DEVICE pointers on the calling thread's current CUDA
+ *     device unless the parameter says "host".
+ *   - Calls that take a `stream` (a cudaStream_t passed as void*) only
+ *     enqueue work on it; none of them synchronises the host, allocates
+ *     memory or copies device->host. NULL = the legacy default stream.
+ *   - The caller owns every input, output and workspace buffer. The library
+ *     owns dsde_state (device memory allocated in dsde_state_create, never in
+ *     a hot call) and dsde_comm.
+ *   - Calls on one dsde_state must be serialised (same stream, or ordered);
+ *     separate states are independent.
+ *   - Outputs are bit-deterministic for identical inputs and launch
+ *     configuration (no float atomics; every reduction has a fixed order).
+ *   - Synchronous argument errors return DSDE_ERR_ARG (or DSDE_ERR_STATE)
+ *     and launch nothing. DSDE_ERR_CUDA / DSDE_ERR_NCCL mirror a failed
+ *     launch / collective.
+ *   - Data errors that can only be seen on the device (see dsde_verify) set
+ *     a sticky error word in the state; read it with dsde_get_device_error.
+ *     A device-side error never causes an out-of-bounds access.
+ */
+#ifndef DSDE_H_
+#define DSDE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSDE_ABI_VERSION 1
+
+typedef enum {
+    DSDE_OK = 0,
+    DSDE_ERR_ARG = -1,    /* invalid argument; nothing launched              */
+    DSDE_ERR_CUDA = -2,   /* CUDA launch / runtime error                     */
+    DSDE_ERR_NCCL = -3,   /* NCCL unavailable or collective failed           */
+    DSDE_ERR_STATE = -4,  /* B larger than the state's capacity, bad slot    */
+    DSDE_ERR_DEVICE = -5  /* returned by dsde_get_device_error only          */
+} dsde_status;
+
+typedef enum { DSDE_F32 = 0, DSDE_BF16 = 1 } dsde_dtype;
+
+/* Reserved padding token id written into unused emitted-token slots when a
+ * sequence accepts fewer than k_i drafts ("a reserved padding token
+ * ID prevents invalid token identifiers from propagating"). */
+#define DSDE_PAD (-1)
+
+/* Largest per-sequence speculation length accepted by dsde_verify. */
+#define DSDE_MAX_SL 16
+/* Largest KLD history window (n_long) a state can hold. */
+#define DSDE_MAX_WINDOW 64
+
+/* Device-side error codes (dsde_get_device_error). */
+#define DSDE_DERR_NONE 0
+#define DSDE_DERR_BAD_SL 1        /* k_i outside [1, DSDE_MAX_SL] or cu_sl not monotone */
+#define DSDE_DERR_BAD_TOKEN 2     /* draft token outside [0, V)                          */
+#define DSDE_DERR_NONFINITE 3     /* non-finite logits in a row                          */
+#define DSDE_DERR_ROWS 4          /* cu_sl[B] != total_draft_rows                         */
+#define DSDE_DERR_BAD_SLOT 5      /* state slot outside [0, max_seqs)                     */
+
+/* Per-slot bits of the optional `flags` output of dsde_verify. */
+#define DSDE_FLAG_ACCEPT_NEAR_TIE 1  /* |u_acc - min(1, p/q)| < 1e-6 at this position      */
+#define DSDE_FLAG_SAMPLE_NEAR_TIE 2  /* |u_smp - C/R| < 1e-6 at a CDF edge of the draw      */
+#define DSDE_FLAG_FALLBACK 4         /* residual mass 0: the token was drawn from p (D7)  */
+#define DSDE_FLAG_OVERFLOW 8         /* a draft logit exceeded the reference by > 80 nats */
+
+/* Adapter configuration; defaults from the paper / SPEC (dsde_config_default).
+ * Validity (S:173-174 plus D11/D17): 0 < delta <= 1; 1 <= n_short < n_long
+ * <= DSDE_MAX_WINDOW; sl_min >= 1; sl_min < sl_ceiling <= DSDE_MAX_SL;
+ * epsilon > 0; calib_steps >= 0; 1 <= calib_sl <= sl_ceiling;
+ * window_unit in {0,1}; cap_mode in {0,1}. */
+typedef struct {
+    double delta;      /* decay factor of Eq.5, 0.85                         */
+    int n_short;       /* short window, 10                                   */
+    int n_long;        /* long window, 30                                    */
+    int sl_min;        /* SL_min, 2                                          */
+    int sl_ceiling;    /* hard bound on the calibrated SL_max (D17), 8               */
+    double epsilon;    /* Eq.1 epsilon, 1e-6                                 */
+    int calib_steps;   /* preliminary steps of Eq.1 (D12), 5                  */
+    int calib_sl;      /* SL used while calibrating (D12), 4                         */
+    int window_unit;   /* 0 = per-token KLD observations (default), 1 = per-step means (D8) */
+    int cap_mode;      /* 0 = no cap (cap = max SL^), 1 = Eq.11 mean / MSE cap (default)     */
+} dsde_config;
+
+typedef struct dsde_state_s* dsde_state; /* per-sequence KLD ring, calibration, SL_max, error word */
+typedef struct dsde_comm_s* dsde_comm;   /* an NCCL communicator; NULL = single GPU                 */
+
+/* Fills *cfg (host) with the defaults above. */
+void dsde_config_default(dsde_config* cfg);
+
+/* Human-readable name of a status code (static string). */
+const char* dsde_status_string(dsde_status s);
+
+/* ABI version of the loaded library (== DSDE_ABI_VERSION). */
+int dsde_abi_version(void);
+
+/* ---------------------------------------------------------------------- */
+/* State                                                                   */
+/* ---------------------------------------------------------------------- */
+
+/* Creates a state for up to max_seqs sequences (slots 0..max_seqs-1) on the
+ * current device and zero-initialises it (synchronously). cfg is host memory
+ * and is copied. Errors: DSDE_ERR_ARG for an invalid cfg or max_seqs < 1;
+ * DSDE_ERR_CUDA if the allocation fails. */
+dsde_status dsde_state_create(const dsde_config* cfg, int max_seqs, dsde_state* out);
+
+/* Starts new requests: clears history, calibration and SL_max of the n slots
+ * listed in `slots` (device int32[n]). Asynchronous on stream. */
+dsde_status dsde_state_reset(dsde_state st, const int32_t* slots, int n, void* stream);
+
+/* Frees the state (synchronises the device first). NULL is accepted. */
+dsde_status dsde_state_destroy(dsde_state st);
+
+/* Size in bytes of the state's per-sequence device image (export/import). */
+size_t dsde_state_bytes(dsde_state st);
+
+/* Copies the per-sequence device image to / from `buf` (device, >=
+ * dsde_state_bytes bytes), asynchronously on stream. Used to checkpoint,
+ * replay and teacher-force ("adapter state dump/restore"). */
+dsde_status dsde_state_export(dsde_state st, void* buf, size_t bytes, void* stream);
+dsde_status dsde_state_import(dsde_state st, const void* buf, size_t bytes, void* stream);
+
+/* Reads (and does not clear) the sticky device error word: *code is one of
+ * DSDE_DERR_*, *seq the batch index of the first offending sequence (-1 if
+ * none). Host pointers. Synchronises the device. */
+dsde_status dsde_get_device_error(dsde_state st, int32_t* code, int32_t* seq);
+
+/* Clears the device error word (asynchronous on stream). */
+dsde_status dsde_clear_device_error(dsde_state st, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* Verify: §8(a) steps a1-a4                                               */
+/* ---------------------------------------------------------------------- */
+
+/* Workspace bytes dsde_verify needs for these sizes (host function). */
+size_t dsde_verify_workspace_size(int B, int total_draft_rows, int V, dsde_dtype dtype);
+
+/* One batched speculative-verification step ("Ragged Q").
+ *
+ * Sequence i in [0,B) drafted k_i = cu_sl[i+1]-cu_sl[i] tokens
+ * x_{i,0..k_i-1}. For every draft position j it computes, from
+ * the target logits t (row cu_sl[i]+i+j) and draft logits d (row
+ * cu_sl[i]+j), with p = softmax(t), q = softmax(d):
+ *   kld[cu_sl[i]+j]  = KL(p || q) = sum_v p_v log(p_v/q_v)   (D1, D3)
+ *   acc_j            = u_acc(i,j) < min(1, p(x_j)/q(x_j))     (D5)
+ * and a_i = first j with !acc_j, else k_i (prefix shape). The final
+ * token is drawn by inverse CDF in ascending token id (D7) from
+ *   normalize(max(0, p - q)) of position a_i  if a_i < k_i (recovery), or
+ *   p of target row k_i                       if a_i = k_i (bonus token),
+ * using u_smp(i, a_i). The two uniforms of slot (i,j) are
+ *   (u_acc, u_smp) = res53 pairs of Philox4x32-10(key = seed, ctr = 0)   (D6).
+ *
+ * Arguments:
+ *   B, V              batch size (>= 1) and vocabulary size (>= 2).
+ *   dtype             DSDE_BF16 or DSDE_F32 logits.
+ *   total_draft_rows  host copy of cu_sl[B] = sum_i k_i (grid sizing without
+ *                     a device->host read); checked on the device.
+ *   cu_sl             int32[B+1], exclusive prefix sum of k_i, cu_sl[0] = 0.
+ *   draft_tokens      int32[total_draft_rows], token x_{i,j} at cu_sl[i]+j.
+ *   target_logits     [total_draft_rows + B, ld_t] row-major; row cu_sl[i]+i+j
+ *                     for j in [0,k_i] (row k_i = the bonus position).
+ *   draft_logits      [total_draft_rows, ld_d] row-major.
+ *   ld_t, ld_d        leading dimensions in elements, >= V; base pointers and
+ *                     rows must be 16-byte aligned.
+ *   seeds             uint64[total_draft_rows + B], one per output slot
+ *                     (i,j), j in [0,k_i], at index cu_sl[i]+i+j.
+ *   accepted_len      out int32[B]: a_i in [0,k_i]; -1 for a sequence with a
+ *                     device-detected data error.
+ *   emitted_tokens    out int32[total_draft_rows + B]: slot cu_sl[i]+i+j holds
+ *                     x_{i,j} for j < a_i, the drawn token at j = a_i, and
+ *                     DSDE_PAD for j > a_i.
+ *   kld               out float[total_draft_rows]: KL at every draft position,
+ *                     including positions after the first rejection (D3).
+ *   flags             optional out uint8[total_draft_rows + B] (NULL ok):
+ *                     DSDE_FLAG_* bits per slot.
+ *   workspace         device scratch of >= dsde_verify_workspace_size bytes,
+ *                     256-byte aligned, not used concurrently by another call.
+ *   st                state whose error word receives device-detected errors.
+ *   stream            CUDA stream.
+ * Device-detected data errors (sticky, first one wins): k_i outside
+ * [1, DSDE_MAX_SL] or cu_sl not monotone, a token outside [0,V), non-finite
+ * logits, cu_sl[B] != total_draft_rows. The offending sequence gets
+ * accepted_len -1, all-pad tokens and NaN KLD; the others are unaffected. */
+dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_draft_rows,
+                        const int32_t* cu_sl, const int32_t* draft_tokens,
+                        const void* target_logits, int64_t ld_t,
+                        const void* draft_logits, int64_t ld_d,
+                        const uint64_t* seeds, int32_t* accepted_len,
+                        int32_t* emitted_tokens, float* kld, uint8_t* flags,
+                        void* workspace, size_t ws_bytes, dsde_state st, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* Signal + SL prediction: §8(a) steps a5-a6                               */
+/* ---------------------------------------------------------------------- */
+
+/* Observes one verification step for B sequences and predicts SL^_i.
+ * Per sequence (slot = slots[i]):
+ *   1. append KL_{i,0..k_i-1} in position order to the history ring of
+ *      capacity n_long, oldest evicted (Fig.5); with
+ *      window_unit = 1 the step mean is appended instead (D8);
+ *   2. mu_last = mean of this step's KLDs;
+ *   3. for the first calib_steps observed steps accumulate SL_A,max = max
+ *      a_i, the mean and max KLD; at the last one set SL_max by Eq.1
+ *      rounded half-even and clamped to [sl_min+1, sl_ceiling] (D11, D12);
+ *   4. Var_w over the most recent min(n, n_short) and min(n, n_long)
+ *      observations with alpha_i = delta^(i-1), i = 1 most recent (Eq.5-7,
+ *      P:214-223), by a weighted Welford recurrence in fp64;
+ *   5. WVIR = Var_short / Var_long (Eq.4); WVIR = 1 while n < n_short
+ *      (D9) or Var_long < 1e-12 (D10);
+ *   6. SF = exp(2 mu_last) - 1 (Eq.3); penalty = SF * WVIR;
+ *   7. SL^ = rint((1 - penalty)(SL_max - SL_min) + SL_min) if penalty <= 1,
+ *      else SL_min (Eq.8), clamped to [SL_min, SL_max]; while
+ *      calibrating SL^ = calib_sl.
+ * Arguments: slots int32[B] state slots; cu_sl, kld, accepted_len as produced
+ * by dsde_verify; sl_hat out int32[B]; diag optional out double[B][8] =
+ * (mu_last, sf, var_short, var_long, wvir, penalty, x_pre_round, sl_max)
+ * (var_* are NaN during warm-up; x_pre_round is NaN while calibrating).
+ * A sequence whose accepted_len is -1 (verify data error) is left untouched
+ * and gets sl_hat = sl_min. */
+dsde_status dsde_update_signal(dsde_state st, int B, const int32_t* slots,
+                               const int32_t* cu_sl, const float* kld,
+                               const int32_t* accepted_len, int32_t* sl_hat,
+                               double* diag, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* Adaptive cap and next SL: §8(a) step a7                                 */
+/* ---------------------------------------------------------------------- */
+
+/* Batch-wide cap (Eq.9-11) and next speculation lengths.
+ * cap = round-half-even(sum_i SL^_i / N) over the N sequences of the batch
+ * that have finished calibration, in exact int64 arithmetic (D14); with a
+ * communicator the sum and N are all-reduced over all ranks first (the only
+ * cross-GPU exchange of the path). cap_mode 0: cap = max SL^ (no cap).
+ * N == 0: cap = sl_ceiling. Then
+ *   next_sl_i = calibrating ? calib_sl : min(SL^_i, cap),
+ *   next_sl_i = min(next_sl_i, budget_i) if budget != NULL.
+ * Arguments: slots int32[B]; sl_hat int32[B] from dsde_update_signal; budget
+ * optional int32[B] (remaining tokens, >= 1); next_sl out int32[B]; cap out
+ * int32[1]; comm NULL for a single GPU. */
+dsde_status dsde_next_sl(dsde_state st, int B, const int32_t* slots, const int32_t* sl_hat,
+                         const int32_t* budget, int32_t* next_sl, int32_t* cap,
+                         dsde_comm comm, void* stream);
+
+/* Host-callable form of the cap rule used by dsde_next_sl (same code): the
+ * cap from the global exact partial (sum of SL^, N, max SL^). Lets callers
+ * that all-reduce the partial themselves (and the CPU tests) apply it. */
+int32_t dsde_cap_value(const dsde_config* cfg, int64_t sum_sl_hat, int64_t n_active,
+                       int64_t max_sl_hat);
+
+/* ---------------------------------------------------------------------- */
+/* Multi-GPU: one NCCL communicator over the ranks of one box              */
+/* ---------------------------------------------------------------------- */
+
+/* NCCL is resolved at run time from the process (the copy torch already
+ * loaded, else libnccl.so.2); without it these return DSDE_ERR_NCCL. */
+dsde_status dsde_comm_unique_id(uint8_t id[128]);                 /* host; rank 0 */
+dsde_status dsde_comm_init(const uint8_t id[128], int nranks, int rank, dsde_comm* out);
+dsde_status dsde_comm_destroy(dsde_comm comm);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DSDE_H_ */

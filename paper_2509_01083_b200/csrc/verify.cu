@@ -1,0 +1,761 @@
+// verify.cu — dsde_verify: the fused speculative-verification pass (§8(a) a1-a4).
+//
+// Pipeline (all on the caller's stream, no host synchronisation):
+//   1. k_stream<T, PAIR>   one CTA per (draft position row, vocab chunk): a single
+//                          streaming read of the target row and the draft row slice,
+//                          chunk max/argmax, then S = sum e_v, A = sum e_v w_v,
+//                          D = sum e_v g(w_v) about the chunk argmax (a1).
+//   2. k_finalize          one warp per sequence, one lane per position: fp64 merge of
+//                          the chunk partials about the row argmax, KL, log p/q, the
+//                          Philox accept test, the first rejection a_i, token layout (a2-a3).
+//   3. k_stream<T, BONUS>  (M, S) chunk partials of target row k_i, only for sequences
+//                          that accepted every draft (a4, bonus branch).
+//   4. k_sample_mass       per (sequence, chunk): residual max(0, p - q) or bonus p mass.
+//   5. k_sample_select     per sequence: fp64 prefix over chunk masses, block scan inside
+//                          the crossing chunk: the smallest token with C_v > u R (D7).
+//
+// Numerics: with e_v = exp(t_v - M), w_v = (t_v - d_v) - C, C = t - d at
+// the argmax of t, and g(w) = exp(-w) - 1 + w >= 0:
+//   KL(p||q) = D/S + (log1p(y) - y),  y = (D - A)/S = E_p[exp(-w)] - 1,
+//   log p(x)/q(x) = (t_x - d_x) - C + log1p(y),
+//   q_v / p_v = exp(-(w_v + log1p(y))).
+// D sums non-negative terms, so the small-KL regime has no cancellation (the naive
+// E_p[t - d] - LSE_t + LSE_d form loses ~1e-3 relative at KL ~ 1e-3).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "state.cuh"
+
+namespace dsde {
+
+constexpr int kThreads = 256;
+
+template <typename T>
+struct Traits;
+template <>
+struct Traits<uint16_t> {      // bf16 bit patterns
+  static constexpr int VEC = 8;  // elements per 16-byte vector
+  static constexpr int NV = 4;   // vectors per thread per row
+};
+template <>
+struct Traits<float> {
+  static constexpr int VEC = 4;
+  static constexpr int NV = 4;
+};
+template <typename T>
+__host__ __device__ constexpr int chunk_elems() {
+  return kThreads * Traits<T>::VEC * Traits<T>::NV;
+}
+
+struct ChunkPartial {  // 48 bytes
+  double S, A, D;      // about (M, dstar) of this chunk
+  float M;             // chunk max of t
+  float dstar;         // d at the chunk argmax
+  int idx;             // chunk argmax (smallest index among ties)
+  int flags;           // DSDE_FLAG_OVERFLOW
+  int pad[2];
+};
+static_assert(sizeof(ChunkPartial) == 48, "ChunkPartial layout");
+
+enum { MODE_NONE = 0, MODE_RESIDUAL = 1, MODE_BONUS = 2, MODE_ERROR = 3 };
+
+struct SeqRec {  // 64 bytes
+  int mode;
+  int slot;          // output slot of the drawn token, cu_sl[i] + i + a_i
+  long long trow;    // target row to draw from
+  long long drow;    // draft row (residual only)
+  float M;           // reference max of t (residual)
+  int pad0;
+  double C;          // reference t - d (residual)
+  double lam;        // log1p(y) = log(sum_v p_v exp(-w_v)) (residual)
+  double u;          // u_smp of the slot
+  double pad1;
+};
+static_assert(sizeof(SeqRec) == 64, "SeqRec layout");
+
+struct VerifyWs {
+  ChunkPartial* part;  // [(total + B) * nchunks]
+  SeqRec* rec;         // [B]
+  double* mass;        // [B * nchunks]
+};
+
+__host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+inline int n_chunks(int V, dsde_dtype dt) {
+  const int ch = dt == DSDE_BF16 ? chunk_elems<uint16_t>() : chunk_elems<float>();
+  return (V + ch - 1) / ch;
+}
+
+inline size_t ws_layout(int B, int total, int V, dsde_dtype dt, VerifyWs* ws, char* base) {
+  const int nc = n_chunks(V, dt);
+  size_t off = 0;
+  const size_t p_bytes = align256(sizeof(ChunkPartial) * (size_t)(total + B) * nc);
+  const size_t r_bytes = align256(sizeof(SeqRec) * (size_t)B);
+  const size_t m_bytes = align256(sizeof(double) * (size_t)B * nc);
+  if (ws) {
+    ws->part = reinterpret_cast<ChunkPartial*>(base + off);
+    ws->rec = reinterpret_cast<SeqRec*>(base + off + p_bytes);
+    ws->mass = reinterpret_cast<double*>(base + off + p_bytes + r_bytes);
+  }
+  return p_bytes + r_bytes + m_bytes;
+}
+
+// ---------------------------------------------------------------------------
+// Row slices: thread `tid` of chunk c owns, in the streaming layout, the
+// elements c*CH + (v*256 + tid)*VEC + e (v < NV, e < VEC): every load
+// instruction of a warp reads 512 contiguous bytes.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void load_slice_strided(const T* row, int V, int c, float (&x)[Traits<T>::VEC * Traits<T>::NV]) {
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV;
+  const int base = c * chunk_elems<T>();
+  uint4 raw[NV];
+  bool full[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int e0 = base + (v * kThreads + threadIdx.x) * VEC;
+    full[v] = e0 + VEC <= V;
+    if (full[v]) raw[v] = ld_stream_v4(row + e0);
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int e0 = base + (v * kThreads + threadIdx.x) * VEC;
+    if (full[v]) {
+      if constexpr (sizeof(T) == 2) {
+        const uint32_t w[4] = {raw[v].x, raw[v].y, raw[v].z, raw[v].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          x[v * VEC + 2 * q] = bf16_lo(w[q]);
+          x[v * VEC + 2 * q + 1] = bf16_hi(w[q]);
+        }
+      } else {
+        x[v * VEC + 0] = __uint_as_float(raw[v].x);
+        x[v * VEC + 1] = __uint_as_float(raw[v].y);
+        x[v * VEC + 2] = __uint_as_float(raw[v].z);
+        x[v * VEC + 3] = __uint_as_float(raw[v].w);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        x[v * VEC + e] = (e0 + e < V) ? load_logit<T>(row + e0 + e) : -1e30f;
+    }
+  }
+}
+
+struct StreamArgs {
+  const void* tl;
+  long long ld_t;
+  const void* dl;
+  long long ld_d;
+  const int32_t* cu_sl;
+  int B, V, nchunks, total;
+  ChunkPartial* part;
+  const SeqRec* rec;
+};
+
+__device__ __forceinline__ void arg_better(float& m, int& mi, float& md, float m2, int i2, float d2) {
+  if (m2 > m || (m2 == m && i2 < mi)) {
+    m = m2;
+    mi = i2;
+    md = d2;
+  }
+}
+
+// g(w) = exp(-w) - 1 + w for |w| < 1 by its Taylor series to w^11
+// (truncation < 5e-9 relative): no cancellation near w = 0.
+__device__ __forceinline__ float g_series(float w) {
+  const float u = -w;
+  float p = 2.505210838544172e-08f;           // 1/11!
+  p = fmaf(p, u, 2.755731922398589e-07f);     // 1/10!
+  p = fmaf(p, u, 2.7557319223985893e-06f);    // 1/9!
+  p = fmaf(p, u, 2.48015873015873e-05f);      // 1/8!
+  p = fmaf(p, u, 1.984126984126984e-04f);     // 1/7!
+  p = fmaf(p, u, 1.388888888888889e-03f);     // 1/6!
+  p = fmaf(p, u, 8.333333333333333e-03f);     // 1/5!
+  p = fmaf(p, u, 4.166666666666667e-02f);     // 1/4!
+  p = fmaf(p, u, 1.666666666666667e-01f);     // 1/3!
+  p = fmaf(p, u, 0.5f);                       // 1/2!
+  return (u * u) * p;
+}
+
+// a1: one CTA per (row, chunk). PAIR: draft row r = blockIdx / nchunks paired with
+// target row r + i (i = sequence of r). !PAIR: target row k_i of sequence
+// i = blockIdx / nchunks if it accepted every draft (bonus), partials at row total + i.
+template <typename T, bool PAIR>
+__global__ void __launch_bounds__(kThreads) k_stream(StreamArgs a) {
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, E = VEC * NV;
+  const int c = blockIdx.x % a.nchunks;
+  const long long rl = blockIdx.x / a.nchunks;
+  long long trow, drow = 0, prow;
+  if (PAIR) {
+    drow = rl;
+    int lo = 0, hi = a.B - 1;  // sequence of draft row: last i with cu_sl[i] <= r
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(a.cu_sl + mid) <= drow) lo = mid; else hi = mid - 1;
+    }
+    trow = drow + lo;
+    prow = drow;
+  } else {
+    const SeqRec r = a.rec[rl];
+    if (r.mode != MODE_BONUS) return;
+    trow = r.trow;
+    prow = a.total + rl;
+  }
+  const T* tp = reinterpret_cast<const T*>(a.tl) + trow * a.ld_t;
+  float t[E], d[E];
+  load_slice_strided<T>(tp, a.V, c, t);
+  if (PAIR) {
+    const T* dp = reinterpret_cast<const T*>(a.dl) + drow * a.ld_d;
+    load_slice_strided<T>(dp, a.V, c, d);
+  }
+
+  // chunk max of t and its smallest-index argmax (the reference of w)
+  const int base = c * chunk_elems<T>();
+  float m = -INFINITY, md = 0.f;
+  int mi = 0x7fffffff;
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const int idx = base + (v * kThreads + threadIdx.x) * VEC + e;
+      if (idx < a.V && t[v * VEC + e] > m) {
+        m = t[v * VEC + e];
+        mi = idx;
+        md = PAIR ? d[v * VEC + e] : 0.f;
+      }
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(kFull, m, o);
+    const int i2 = __shfl_xor_sync(kFull, mi, o);
+    const float d2 = __shfl_xor_sync(kFull, md, o);
+    arg_better(m, mi, md, m2, i2, d2);
+  }
+  __shared__ float s_m[kThreads / 32], s_d[kThreads / 32];
+  __shared__ int s_i[kThreads / 32];
+  __shared__ double s_sum[3][kThreads / 32];
+  __shared__ int s_flag;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_flag = 0;
+  if (lane == 0) {
+    s_m[warp] = m;
+    s_i[warp] = mi;
+    s_d[warp] = md;
+  }
+  __syncthreads();
+  float M = s_m[0], dstar = s_d[0];
+  int Mi = s_i[0];
+#pragma unroll
+  for (int w = 1; w < kThreads / 32; ++w) arg_better(M, Mi, dstar, s_m[w], s_i[w], s_d[w]);
+
+  const float ML2 = M * kLog2e, DL2 = dstar * kLog2e;
+  float S = 0.f, A2 = 0.f, D = 0.f;
+  bool ovf = false;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    if (PAIR) {
+      bool need = false;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const float xt = fmaf(t[v * VEC + e], kLog2e, -ML2);
+        const float xd = fmaf(d[v * VEC + e], kLog2e, -DL2);
+        const float ee = fast_exp2(xt);
+        ovf |= xd > 115.f;
+        const float f = fast_exp2(fminf(xd, 115.f));
+        const float w2 = xt - xd;  // w in log2 units
+        const float ew2 = ee * w2;
+        const bool exact = (xt > -8.f) && (fabsf(w2) < 1.4426950408889634f);
+        const float dterm = fmaf(ew2, kLn2, f - ee);  // e (exp(-w) - 1 + w)
+        S += ee;
+        A2 += ew2;
+        D += exact ? 0.f : dterm;
+        need |= exact;
+      }
+      if (__any_sync(kFull, need)) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const float xt = fmaf(t[v * VEC + e], kLog2e, -ML2);
+          const float xd = fmaf(d[v * VEC + e], kLog2e, -DL2);
+          const float w2 = xt - xd;
+          if ((xt > -8.f) && (fabsf(w2) < 1.4426950408889634f)) {
+            D = fmaf(fast_exp2(xt), g_series(w2 * kLn2), D);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) S += fast_exp2(fmaf(t[v * VEC + e], kLog2e, -ML2));
+    }
+  }
+  double Sd = warp_sum((double)S);
+  double Ad = PAIR ? warp_sum((double)A2) : 0.0;
+  double Dd = PAIR ? warp_sum((double)D) : 0.0;
+  if (ovf) s_flag = DSDE_FLAG_OVERFLOW;  // benign race: same value
+  if (lane == 0) {
+    s_sum[0][warp] = Sd;
+    s_sum[1][warp] = Ad;
+    s_sum[2][warp] = Dd;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s0 = 0, s1 = 0, s2 = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      s0 += s_sum[0][w];
+      s1 += s_sum[1][w];
+      s2 += s_sum[2][w];
+    }
+    ChunkPartial p;
+    p.S = s0;
+    p.A = s1 * kLn2d;
+    p.D = s2;
+    p.M = M;
+    p.dstar = dstar;
+    p.idx = Mi;
+    p.flags = s_flag;
+    p.pad[0] = p.pad[1] = 0;
+    a.part[prow * a.nchunks + c] = p;
+  }
+}
+
+// Merged statistics of one row about the row argmax.
+struct RowStats {
+  double M, C, S, A, D;
+  int flags;
+};
+
+// fp64 merge of chunk partials in chunk order. The reference is the chunk
+// with the largest M (earliest on ties, so the row's smallest-index argmax).
+// Chunk c's w is shifted by Delta = C_c - C:
+//   S += s S_c,  A += s (A_c + S_c Delta),
+//   D += s (e^-Delta D_c - A_c expm1(-Delta) + S_c g(Delta)),  s = e^(M_c - M).
+__device__ RowStats merge_row(const ChunkPartial* P, int nchunks, bool pair) {
+  int cref = 0;
+  float Mref = P[0].M;
+  for (int c = 1; c < nchunks; ++c)
+    if (P[c].M > Mref) {
+      Mref = P[c].M;
+      cref = c;
+    }
+  RowStats r;
+  r.M = (double)Mref;
+  r.C = pair ? (double)Mref - (double)P[cref].dstar : 0.0;
+  r.S = r.A = r.D = 0.0;
+  r.flags = 0;
+  for (int c = 0; c < nchunks; ++c) {
+    const ChunkPartial q = P[c];
+    const double s = exp((double)q.M - r.M);
+    r.S += s * q.S;
+    r.flags |= q.flags;
+    if (pair) {
+      const double dl = ((double)q.M - (double)q.dstar) - r.C;
+      const double em = expm1(-dl);
+      r.A += s * (q.A + q.S * dl);
+      r.D += s * (exp(-dl) * q.D - q.A * em + q.S * (em + dl));
+    }
+  }
+  return r;
+}
+
+struct FinArgs {
+  int B, V, total, nchunks;
+  const int32_t* cu_sl;
+  const int32_t* tokens;
+  const void* tl;
+  long long ld_t;
+  const void* dl;
+  long long ld_d;
+  const uint64_t* seeds;
+  const ChunkPartial* part;
+  int32_t* acc_len;
+  int32_t* emitted;
+  float* kld;
+  uint8_t* flags;
+  SeqRec* rec;
+  int32_t* err;
+};
+
+// a2 + a3: one warp per sequence, lane j = draft position j (k_i <= 16 < 32);
+// lane k_i also draws the uniforms of the bonus slot.
+template <typename T>
+__global__ void __launch_bounds__(128) k_finalize(FinArgs a) {
+  const int i = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= a.B) return;
+  const int c0 = __ldg(a.cu_sl + i), c1 = __ldg(a.cu_sl + i + 1);
+  const int k = c1 - c0;
+  const bool range_ok = c0 >= 0 && k >= 1 && k <= DSDE_MAX_SL && c1 <= a.total;
+  const bool rows_ok = (i != a.B - 1) || (c1 == a.total);
+  if (!range_ok || !rows_ok) {
+    if (lane == 0) {
+      a.acc_len[i] = -1;
+      a.rec[i].mode = MODE_ERROR;
+      raise_device_error(a.err, range_ok ? DSDE_DERR_ROWS : DSDE_DERR_BAD_SL, i);
+    }
+    return;
+  }
+  const long long slot0 = (long long)c0 + i;
+  double kl = 0.0, lr = 0.0, C = 0.0, lam = 0.0, M = 0.0;
+  bool acc = false, near = false, bad_tok = false, nonfin = false;
+  int rflags = 0;
+  Uniforms u = {0.0, 0.0};
+  if (lane <= k) u = philox_uniforms(__ldg(a.seeds + slot0 + lane));
+  if (lane < k) {
+    const long long drow = (long long)c0 + lane;
+    const int x = __ldg(a.tokens + drow);
+    bad_tok = x < 0 || x >= a.V;
+    const RowStats r = merge_row(a.part + drow * a.nchunks, a.nchunks, true);
+    rflags = r.flags;
+    nonfin = !(isfinite(r.S) && isfinite(r.A) && isfinite(r.D) && r.S > 0.0 && isfinite(r.M) &&
+               isfinite(r.C));
+    const double y = (r.D - r.A) / r.S;
+    lam = log1p(y);
+    kl = fmax(0.0, r.D / r.S + (lam - y));
+    C = r.C;
+    M = r.M;
+    if (!bad_tok) {
+      const T* tp = reinterpret_cast<const T*>(a.tl) + (drow + i) * a.ld_t;
+      const T* dp = reinterpret_cast<const T*>(a.dl) + drow * a.ld_d;
+      const double tx = (double)load_logit<T>(tp + x), dx = (double)load_logit<T>(dp + x);
+      lr = (tx - dx) - C + lam;
+      nonfin |= !isfinite(lr);
+    }
+    const double pacc = lr >= 0.0 ? 1.0 : exp(lr);
+    acc = u.acc < pacc;
+    near = fabs(u.acc - pacc) < 1e-6;
+  }
+  const unsigned bt = __ballot_sync(kFull, bad_tok);
+  const unsigned nf = __ballot_sync(kFull, nonfin);
+  const unsigned am = __ballot_sync(kFull, acc);
+  if (bt | nf) {
+    if (lane < k) a.kld[c0 + lane] = NAN;
+    if (lane <= k) {
+      a.emitted[slot0 + lane] = DSDE_PAD;
+      if (a.flags) a.flags[slot0 + lane] = 0;
+    }
+    if (lane == 0) {
+      a.acc_len[i] = -1;
+      a.rec[i].mode = MODE_ERROR;
+      raise_device_error(a.err, bt ? DSDE_DERR_BAD_TOKEN : DSDE_DERR_NONFINITE, i);
+    }
+    return;
+  }
+  const int acc_run = __ffs(~am) - 1;  // first rejected lane (lanes >= k never accept)
+  const int aa = acc_run < k ? acc_run : k;
+  if (lane < k) a.kld[c0 + lane] = (float)kl;
+  if (lane <= k) {
+    a.emitted[slot0 + lane] = lane < aa ? __ldg(a.tokens + c0 + lane) : DSDE_PAD;
+    if (a.flags) {
+      uint8_t f = (uint8_t)(rflags & DSDE_FLAG_OVERFLOW);
+      if (near && lane <= aa && lane < k) f |= DSDE_FLAG_ACCEPT_NEAR_TIE;
+      a.flags[slot0 + lane] = f;
+    }
+  }
+  if (lane == 0) a.acc_len[i] = aa;
+  if (lane == aa) {
+    SeqRec r;
+    r.slot = (int)(slot0 + aa);
+    r.trow = slot0 + aa;
+    r.u = u.smp;
+    r.pad0 = 0;
+    if (aa < k) {
+      r.mode = MODE_RESIDUAL;
+      r.drow = (long long)c0 + aa;
+      r.M = (float)M;
+      r.C = C;
+      r.lam = lam;
+    } else {
+      r.mode = MODE_BONUS;
+      r.drow = -1;
+      r.M = 0.f;
+      r.C = 0.0;
+      r.lam = 0.0;
+    }
+    a.rec[i] = r;
+  }
+}
+
+struct SampArgs {
+  int B, V, nchunks, total;
+  const void* tl;
+  long long ld_t;
+  const void* dl;
+  long long ld_d;
+  const ChunkPartial* part;
+  const SeqRec* rec;
+  double* mass;
+  int32_t* emitted;
+  uint8_t* flags;
+};
+
+// Weights of the final draw for the E contiguous elements [c*CH + tid*E, +E):
+//   residual: rho_v = e_v * max(0, -expm1(-z_v)), z_v = (t_v - d_v) - C + lam
+//             (q_v / p_v = exp(-z_v)); z_v is formed in fp64 so the offset in
+//             t - d cancels exactly;
+//   bonus / p-fallback: e_v = exp(t_v - M).
+// Both are p_v * S (resp. max(0, p_v - q_v) * S), a common positive scale.
+template <typename T>
+__device__ __forceinline__ void draw_weights(const SampArgs& a, const SeqRec& r, float M, bool resid,
+                                             int c, float (&w)[Traits<T>::VEC * Traits<T>::NV]) {
+  constexpr int E = Traits<T>::VEC * Traits<T>::NV;
+  const int e0 = c * chunk_elems<T>() + threadIdx.x * E;
+  const T* tp = reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t;
+  const T* dp = reinterpret_cast<const T*>(a.dl) + (resid ? r.drow : 0) * a.ld_d;
+  const float ML2 = M * kLog2e;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int v = e0 + e;
+    float wt = 0.f;
+    if (v < a.V) {
+      const float tv = load_logit<T>(tp + v);
+      const float ev = fast_exp2(fmaf(tv, kLog2e, -ML2));
+      if (resid) {
+        const float dv = load_logit<T>(dp + v);
+        const float z = (float)((((double)tv - (double)dv) - r.C) + r.lam);
+        wt = z > 0.f ? ev * -expm1f(-z) : 0.f;
+      } else {
+        wt = ev;
+      }
+    }
+    w[e] = wt;
+  }
+}
+
+__device__ __forceinline__ double block_sum(double v, double* s_w) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) s_w[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) t += s_w[w];
+  return t;
+}
+
+// Reference max of the bonus row (merge of its (M, S) partials).
+__device__ __forceinline__ float bonus_max(const SampArgs& a, int i) {
+  const ChunkPartial* P = a.part + (long long)(a.total + i) * a.nchunks;
+  float M = P[0].M;
+  for (int c = 1; c < a.nchunks; ++c) M = fmaxf(M, P[c].M);
+  return M;
+}
+
+// a4 (1/2): mass of the draw weights per (sequence, chunk).
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_sample_mass(SampArgs a) {
+  constexpr int E = Traits<T>::VEC * Traits<T>::NV;
+  const int i = blockIdx.x / a.nchunks, c = blockIdx.x % a.nchunks;
+  const SeqRec r = a.rec[i];
+  if (r.mode != MODE_RESIDUAL && r.mode != MODE_BONUS) return;
+  const bool resid = r.mode == MODE_RESIDUAL;
+  const float M = resid ? r.M : bonus_max(a, i);
+  float w[E];
+  draw_weights<T>(a, r, M, resid, c, w);
+  float s = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) s += w[e];
+  __shared__ double s_w[kThreads / 32];
+  const double tot = block_sum((double)s, s_w);
+  if (threadIdx.x == 0) a.mass[(long long)i * a.nchunks + c] = tot;
+}
+
+// a4 (2/2): inverse CDF in ascending token id (D7): the smallest v with
+// C_v > u R. C_v = (fp64 prefix of chunk masses) + (fp64 block scan of
+// per-thread fp32 sums) + (per-thread fp32 running sum).
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_sample_select(SampArgs a) {
+  constexpr int E = Traits<T>::VEC * Traits<T>::NV;
+  const int i = blockIdx.x;
+  const SeqRec r = a.rec[i];
+  if (r.mode != MODE_RESIDUAL && r.mode != MODE_BONUS) return;
+  bool resid = r.mode == MODE_RESIDUAL;
+  float M = resid ? r.M : bonus_max(a, i);
+  __shared__ double s_w[kThreads / 32];
+  __shared__ double s_scan[kThreads];
+  __shared__ int s_cand;
+  __shared__ int s_chunk;
+  __shared__ double s_base, s_R, s_target;
+  uint8_t fl = 0;
+  const double* mass = a.mass + (long long)i * a.nchunks;
+  if (threadIdx.x == 0) {
+    double R = 0.0;
+    for (int c = 0; c < a.nchunks; ++c) R += mass[c];
+    s_R = R;
+  }
+  __syncthreads();
+  if (!(s_R > 0.0)) {
+    // D7 fallback: residual mass 0 -> draw from p of the same target row.
+    resid = false;
+    fl |= DSDE_FLAG_FALLBACK;
+    M = r.M;
+    double cum = 0.0;
+    for (int c = 0; c < a.nchunks; ++c) {
+      float w[E];
+      draw_weights<T>(a, r, M, false, c, w);
+      float s = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) s += w[e];
+      const double tot = block_sum((double)s, s_w);
+      if (threadIdx.x == 0) a.mass[(long long)i * a.nchunks + c] = tot;
+      cum += tot;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_R = cum;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double R = s_R, target = r.u * R;
+    double cum = 0.0;
+    int cs = a.nchunks - 1;
+    double base = 0.0;
+    for (int c = 0; c < a.nchunks; ++c) {
+      const double m = mass[c];
+      if (cum + m > target) {
+        cs = c;
+        base = cum;
+        break;
+      }
+      cum += m;
+      base = cum - m;  // if no crossing: the last chunk, base before it
+    }
+    s_chunk = cs;
+    s_base = base;
+    s_target = target;
+    s_cand = 0x7fffffff;
+  }
+  __syncthreads();
+  const int c = s_chunk;
+  float w[E];
+  draw_weights<T>(a, r, M, resid, c, w);
+  float s = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) s += w[e];
+  // exclusive block scan of the per-thread sums (fp64, Hillis-Steele in smem)
+  s_scan[threadIdx.x] = (double)s;
+  __syncthreads();
+  for (int o = 1; o < kThreads; o <<= 1) {
+    const double add = threadIdx.x >= o ? s_scan[threadIdx.x - o] : 0.0;
+    __syncthreads();
+    s_scan[threadIdx.x] += add;
+    __syncthreads();
+  }
+  const double pre = s_base + (threadIdx.x > 0 ? s_scan[threadIdx.x - 1] : 0.0);
+  const double target = s_target;
+  const int e0 = c * chunk_elems<T>() + threadIdx.x * E;
+  int cand = 0x7fffffff;
+  float run = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    run += w[e];
+    if (cand == 0x7fffffff && w[e] > 0.f && pre + (double)run > target) cand = e0 + e;
+  }
+  if (cand != 0x7fffffff) atomicMin(&s_cand, cand);
+  __syncthreads();
+  int tok = s_cand;
+  if (tok == 0x7fffffff) {
+    // rounding corner (u R within an ulp of the chunk total): the last token of
+    // the chunk with positive weight; flagged as a near tie.
+    __syncthreads();
+    int last = -1;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (w[e] > 0.f) last = e0 + e;
+    if (threadIdx.x == 0) s_cand = -1;
+    __syncthreads();
+    if (last >= 0) atomicMax(&s_cand, last);
+    __syncthreads();
+    tok = s_cand;
+    fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
+  }
+  if (tok >= e0 && tok < e0 + E) {
+    // owner: C_{v-1}/R and C_v/R for the tie flag
+    float run2 = 0.f;
+    double lo = pre, hi = pre;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const double before = pre + (double)run2;
+      run2 += w[e];
+      if (e0 + e == tok) {
+        lo = before;
+        hi = pre + (double)run2;
+      }
+    }
+    const double R = s_R;
+    if (fabs(r.u - lo / R) < 1e-6 || fabs(r.u - hi / R) < 1e-6) fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
+    a.emitted[r.slot] = tok;
+    if (a.flags) a.flags[r.slot] |= fl;
+  } else if (tok < 0 && threadIdx.x == 0) {
+    a.emitted[r.slot] = 0;  // unreachable: R > 0 implies a positive weight exists
+    if (a.flags) a.flags[r.slot] |= fl;
+  }
+}
+
+template <typename T>
+cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const int32_t* tokens,
+                          const void* tl, int64_t ld_t, const void* dl, int64_t ld_d,
+                          const uint64_t* seeds, int32_t* acc_len, int32_t* emitted, float* kld,
+                          uint8_t* flags, const VerifyWs& ws, int32_t* err, cudaStream_t s) {
+  const int nc = (V + chunk_elems<T>() - 1) / chunk_elems<T>();
+  StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, nc, total, ws.part, ws.rec};
+  if (total > 0) {
+    k_stream<T, true><<<(unsigned)((long long)total * nc), kThreads, 0, s>>>(sa);
+  }
+  FinArgs fa{B, V, total, nc, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, ws.part,
+             acc_len, emitted, kld, flags, ws.rec, err};
+  k_finalize<T><<<(B + 3) / 4, 128, 0, s>>>(fa);
+  k_stream<T, false><<<(unsigned)((long long)B * nc), kThreads, 0, s>>>(sa);
+  SampArgs pa{B, V, nc, total, tl, ld_t, dl, ld_d, ws.part, ws.rec, ws.mass, emitted, flags};
+  k_sample_mass<T><<<(unsigned)((long long)B * nc), kThreads, 0, s>>>(pa);
+  k_sample_select<T><<<B, kThreads, 0, s>>>(pa);
+  return cudaGetLastError();
+}
+
+}  // namespace dsde
+
+using namespace dsde;
+
+extern "C" size_t dsde_verify_workspace_size(int B, int total_draft_rows, int V, dsde_dtype dtype) {
+  if (B < 1 || V < 2 || total_draft_rows < 0) return 0;
+  return ws_layout(B, total_draft_rows, V, dtype, nullptr, nullptr);
+}
+
+extern "C" dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_draft_rows,
+                                   const int32_t* cu_sl, const int32_t* draft_tokens,
+                                   const void* target_logits, int64_t ld_t,
+                                   const void* draft_logits, int64_t ld_d,
+                                   const uint64_t* seeds, int32_t* accepted_len,
+                                   int32_t* emitted_tokens, float* kld, uint8_t* flags,
+                                   void* workspace, size_t ws_bytes, dsde_state st, void* stream) {
+  if (!st || !cu_sl || !draft_tokens || !target_logits || !draft_logits || !seeds ||
+      !accepted_len || !emitted_tokens || !kld || !workspace)
+    return DSDE_ERR_ARG;
+  if (B < 1 || V < 2 || total_draft_rows < B || total_draft_rows > B * DSDE_MAX_SL)
+    return DSDE_ERR_ARG;
+  if (dtype != DSDE_F32 && dtype != DSDE_BF16) return DSDE_ERR_ARG;
+  if (ld_t < V || ld_d < V) return DSDE_ERR_ARG;
+  const size_t esz = dtype == DSDE_BF16 ? 2 : 4;
+  if ((((uintptr_t)target_logits) | ((uintptr_t)draft_logits)) & 15) return DSDE_ERR_ARG;
+  if (((size_t)ld_t * esz) % 16 || ((size_t)ld_d * esz) % 16) return DSDE_ERR_ARG;
+  if (((uintptr_t)workspace) & 255) return DSDE_ERR_ARG;
+  const size_t need = ws_layout(B, total_draft_rows, V, dtype, nullptr, nullptr);
+  if (ws_bytes < need) return DSDE_ERR_ARG;
+  const int nc = n_chunks(V, dtype);
+  if ((long long)(total_draft_rows + B) * nc > 0x7fffffffLL) return DSDE_ERR_ARG;
+  VerifyWs ws;
+  ws_layout(B, total_draft_rows, V, dtype, &ws, reinterpret_cast<char*>(workspace));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (dtype == DSDE_BF16)
+    e = launch_verify<uint16_t>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
+                                draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld,
+                                flags, ws, st->err, s);
+  else
+    e = launch_verify<float>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
+                             draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld, flags,
+                             ws, st->err, s);
+  return e == cudaSuccess ? DSDE_OK : DSDE_ERR_CUDA;
+}

@@ -1,0 +1,176 @@
+"""GPU parity of dsde_verify against the fp64 oracle (bands in tests/parity.py).
+
+Sizes span several vocab chunks and a ragged tail; edge cases cover tiny V,
+V not a multiple of the vector width, ld > V, k = 1 and k = 16, identical and
+disjoint rows, device-detected data errors, determinism, and the brute-force
+distribution test through the CUDA path."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests import parity, spec_sim
+from tests.gpu_util import dsde, gpu_verify, make_host_batch, oracle_verify, to_device_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def m():
+    return dsde()
+
+
+@pytest.fixture(scope="module")
+def state(m):
+    return m.State(m.Config.default(), 4096)
+
+
+def _check(m, state, host, dtype, ld_pad=0, expect_ties_max=None):
+    dev = to_device_inputs(host, dtype, ld_pad=ld_pad)
+    acc, em, kl, fl = gpu_verify(m, state, dev)
+    o = oracle_verify(host)
+    rep = parity.compare_verify(host["cu_sl"], acc, em, kl, o)
+    assert rep.ok(), str(rep)
+    code, _ = state.device_error()
+    assert code == 0
+    return rep, (acc, em, kl, fl), o
+
+
+@pytest.mark.parametrize("V,dtype,kmax,B", [
+    (32000, torch.float32, 4, 4),         # config 1 shape
+    (32000, torch.bfloat16, 8, 64),       # config 2 shape
+    (128256, torch.bfloat16, 8, 12),      # config 3-5 row shape (sampled batch)
+    (50000, torch.bfloat16, 8, 9),        # ragged last chunk
+    (8193, torch.float32, 16, 5),         # one element past a chunk
+    (1003, torch.bfloat16, 3, 7),         # V not a multiple of 8
+    (2, torch.float32, 2, 16), (3, torch.bfloat16, 1, 16), (8, torch.bfloat16, 5, 16),
+])
+def test_verify_parity(m, state, V, dtype, kmax, B):
+    k = synth.random_k(B, kmax, V + B)
+    for prof in (("code",), ("dialogue", "low")):
+        host = make_host_batch(V, k, seed=V * 7 + B, dtype=dtype, profiles=prof)
+        _check(m, state, host, dtype)
+
+
+def test_verify_ld_padding(m, state):
+    k = synth.random_k(6, 8, 3)
+    host = make_host_batch(20000, k, seed=5)
+    _check(m, state, host, torch.bfloat16, ld_pad=24)
+
+
+def test_verify_k1_and_k16(m, state):
+    host = make_host_batch(32000, [1] * 20, seed=8, dtype=torch.float32)
+    _check(m, state, host, torch.float32)
+    host = make_host_batch(32000, [16] * 6, seed=9)
+    _check(m, state, host, torch.bfloat16)
+
+
+def test_identical_rows_kl_zero_accept_all(m, state):
+    k = [3, 5, 1, 8]
+    host = make_host_batch(40000, k, seed=10)
+    cu = host["cu_sl"]
+    for i in range(len(k)):
+        for j in range(k[i]):
+            host["draft"][cu[i] + j] = host["target"][cu[i] + i + j]
+    rep, (acc, em, kl, fl), o = _check(m, state, host, torch.bfloat16)
+    assert np.all(kl == 0.0)
+    assert list(acc) == k
+
+
+def test_disjoint_one_hot(m, state):
+    V, n = 5000, 8
+    t = np.full((2 * n, V), -1e4, np.float32)
+    d = np.full((n, V), -1e4, np.float32)
+    t[0::2, 17] = 0.0
+    t[1::2, :] = 0.0
+    d[:, 4000] = 0.0
+    cu = synth.cu_from_k(np.ones(n, np.int64))
+    host = dict(cu_sl=cu, target=t, draft=d, draft_tokens=np.full(n, 4000, np.int32),
+                seeds=synth.slot_seeds(3, 0, cu))
+    rep, (acc, em, kl, fl), o = _check(m, state, host, torch.float32)
+    assert (acc == 0).all() and (em[0::2] == 17).all() and (em[1::2] == -1).all()
+
+
+def test_large_config_sampled_rows(m, state):
+    """Config 3 at full size (B=256, V=128256, bf16) in the bench's launch
+    configuration; the oracle checks a sample of 24 sequences."""
+    B, V = 256, 128256
+    w = synth.Workload(B=B, V=V, dtype=torch.bfloat16, profiles=("code",), seed=77)
+    k = synth.random_k(B, 8, 77)
+    s = synth.generate_step(w, 3, k, device="cuda")
+    dev = dict(cu_sl=s.cu_sl, draft_tokens=s.draft_tokens, target=s.target, draft=s.draft,
+               seeds=s.seeds, V=V)
+    acc, em, kl, fl = gpu_verify(m, state, dev)
+    host = s.host_arrays()
+    ids = np.random.default_rng(1).choice(B, 24, replace=False)
+    sub = parity.subset_batch(host, ids)
+    o = oracle_verify(sub)
+    a2, e2, k2 = parity.gather_subset_outputs(host["cu_sl"], ids, acc, em, kl)
+    rep = parity.compare_verify(sub["cu_sl"], a2, e2, k2, o, seq_ids=ids)
+    assert rep.ok(), str(rep)
+    # properties that hold at any size, on every sequence
+    cu = host["cu_sl"]
+    for i in range(B):
+        a = acc[i]
+        assert 0 <= a <= k[i]
+        s0 = cu[i] + i
+        assert (em[s0:s0 + a] == host["draft_tokens"][cu[i]:cu[i] + a]).all()
+        assert 0 <= em[s0 + a] < V and (em[s0 + a + 1:s0 + k[i] + 1] == -1).all()
+    assert np.all(kl >= 0) and np.all(np.isfinite(kl))
+
+
+def test_deterministic(m, state):
+    k = synth.random_k(32, 8, 11)
+    host = make_host_batch(128256, k, seed=12)
+    dev = to_device_inputs(host, torch.bfloat16)
+    r1 = gpu_verify(m, state, dev)
+    r2 = gpu_verify(m, state, dev)
+    for a, b in zip(r1[:3], r2[:3]):
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+def test_device_errors(m):
+    st = m.State(m.Config.default(), 64)
+    k = [2, 3, 2]
+    host = make_host_batch(1000, k, seed=13)
+    # bad token in sequence 1
+    h = dict(host)
+    h["draft_tokens"] = host["draft_tokens"].copy()
+    h["draft_tokens"][3] = 5000
+    acc, em, kl, fl = gpu_verify(m, st, to_device_inputs(h, torch.bfloat16))
+    assert acc[1] == -1 and acc[0] >= 0 and acc[2] >= 0
+    assert st.device_error() == (2, 1)
+    st.clear_error()
+    torch.cuda.synchronize()
+    assert st.device_error() == (0, -1)
+    # non-finite logits in sequence 2
+    h = dict(host)
+    h["target"] = host["target"].copy()
+    h["target"][host["cu_sl"][2] + 2, 10] = 0x7FC0  # bf16 NaN
+    acc, em, kl, fl = gpu_verify(m, st, to_device_inputs(h, torch.bfloat16))
+    assert acc[2] == -1 and np.isnan(kl[host["cu_sl"][2]:]).all()
+    assert st.device_error()[0] == 3
+    st.clear_error()
+    # k = 0 for sequence 0 (cu_sl not strictly increasing)
+    h = dict(host)
+    h["cu_sl"] = np.int32([0, 0, 5, 7])
+    dev = to_device_inputs(h, torch.bfloat16)
+    acc, em, kl, fl = gpu_verify(m, st, dev)
+    assert acc[0] == -1
+    assert st.device_error()[0] == 1
+    st.close()
+
+
+def test_distribution_bruteforce_gpu(m, state):
+    """S:584 through the CUDA path: V=8, depth 3, 10^6 runs."""
+    st = m.State(m.Config.default(), 1)
+
+    def fn(cu, tokens, target, draft, seeds):
+        host = dict(cu_sl=cu, draft_tokens=tokens, target=target, draft=draft, seeds=seeds)
+        acc, em, kl, fl = gpu_verify(m, st, to_device_inputs(host, torch.float32), with_flags=False)
+        return acc, em
+
+    tab = spec_sim.Tables(8, 3, 31)
+    codes = spec_sim.run_generation(tab, 10 ** 6, fn, 31)
+    spec_sim.check_distribution(tab, codes)
