@@ -50,9 +50,9 @@ __host__ __device__ constexpr int chunk_elems() {
 }
 
 struct ChunkPartial {  // 48 bytes
-  double S, A, D;      // about (M, dstar) of this chunk
+  double S, A, D;      // about (M, C) of this chunk
   float M;             // chunk max of t
-  float dstar;         // d at the chunk argmax
+  float C;             // t - d at the chunk argmax (fp32, as used for w)
   int idx;             // chunk argmax (smallest index among ties)
   int flags;           // DSDE_FLAG_OVERFLOW
   int pad[2];
@@ -163,21 +163,45 @@ __device__ __forceinline__ void arg_better(float& m, int& mi, float& md, float m
   }
 }
 
-// g(w) = exp(-w) - 1 + w for |w| < 1 by its Taylor series to w^11
-// (truncation < 5e-9 relative): no cancellation near w = 0.
-__device__ __forceinline__ float g_series(float w) {
+// g(w) = exp(-w) - 1 + w >= 0, accurate to ~1e-7 relative for every w:
+//   |w| < 1: g = u^2 h(u), u = -w, h(u) = (e^u - 1 - u)/u^2 by a degree-7
+//            near-minimax polynomial (Chebyshev fit on [-1,1]; 1.1e-7 relative
+//            in fp32 Horner, tools/fit_g.py) — no cancellation near w = 0;
+//   |w| >= 1: g = (2^(-w log2 e) - 1) + w (MUFU); relative error <= 4 ulp there.
+// The argument of 2^x is clamped at 126 (draft logit > ~87 nats above the
+// reference): `ovf` reports it (DSDE_FLAG_OVERFLOW).
+__device__ __forceinline__ float g_of_w(float w, bool& ovf) {
   const float u = -w;
-  float p = 2.505210838544172e-08f;           // 1/11!
-  p = fmaf(p, u, 2.755731922398589e-07f);     // 1/10!
-  p = fmaf(p, u, 2.7557319223985893e-06f);    // 1/9!
-  p = fmaf(p, u, 2.48015873015873e-05f);      // 1/8!
-  p = fmaf(p, u, 1.984126984126984e-04f);     // 1/7!
-  p = fmaf(p, u, 1.388888888888889e-03f);     // 1/6!
-  p = fmaf(p, u, 8.333333333333333e-03f);     // 1/5!
-  p = fmaf(p, u, 4.166666666666667e-02f);     // 1/4!
-  p = fmaf(p, u, 1.666666666666667e-01f);     // 1/3!
-  p = fmaf(p, u, 0.5f);                       // 1/2!
-  return (u * u) * p;
+  float p = 2.812654656736413e-06f;
+  p = fmaf(p, u, 2.5358644052175805e-05f);
+  p = fmaf(p, u, 1.9836986029986292e-04f);
+  p = fmaf(p, u, 1.3885394437238574e-03f);
+  p = fmaf(p, u, 8.33334494382143e-03f);
+  p = fmaf(p, u, 4.166673496365547e-02f);
+  p = fmaf(p, u, 1.666666716337204e-01f);
+  p = fmaf(p, u, 0.5f);
+  const float small = (u * u) * p;
+  const float x = u * kLog2e;
+  ovf |= x > 126.f;
+  const float big = (fast_exp2(fminf(x, 126.f)) - 1.f) + w;
+  return fabsf(w) < 1.f ? small : big;
+}
+
+// w = (t - d) - C. For bf16 inputs t - d is exact in fp32 (8-bit significands,
+// exponent gap <= 16 in practice); for fp32 inputs the difference is carried as
+// an unevaluated sum (TwoDiff, Knuth) so w keeps full fp32 accuracy.
+template <typename T>
+__device__ __forceinline__ float diff_ref(float t, float d, float C);
+template <>
+__device__ __forceinline__ float diff_ref<uint16_t>(float t, float d, float C) {
+  return (t - d) - C;
+}
+template <>
+__device__ __forceinline__ float diff_ref<float>(float t, float d, float C) {
+  const float hi = __fsub_rn(t, d);
+  const float bb = __fsub_rn(hi, t);
+  const float lo = __fadd_rn(__fsub_rn(t, __fsub_rn(hi, bb)), __fsub_rn(-d, bb));
+  return __fadd_rn(__fsub_rn(hi, C), lo);
 }
 
 // a1: one CTA per (row, chunk). PAIR: draft row r = blockIdx / nchunks paired with
@@ -251,47 +275,22 @@ __global__ void __launch_bounds__(kThreads) k_stream(StreamArgs a) {
 #pragma unroll
   for (int w = 1; w < kThreads / 32; ++w) arg_better(M, Mi, dstar, s_m[w], s_i[w], s_d[w]);
 
-  const float ML2 = M * kLog2e, DL2 = dstar * kLog2e;
-  float S = 0.f, A2 = 0.f, D = 0.f;
+  const float ML2 = M * kLog2e;
+  const float Cf = M - dstar;  // reference t - d (exact for bf16 inputs); stored as used
+  float S = 0.f, A = 0.f, D = 0.f;
   bool ovf = false;
 #pragma unroll
-  for (int v = 0; v < NV; ++v) {
+  for (int q = 0; q < E; ++q) {
+    const float e = fast_exp2(fmaf(t[q], kLog2e, -ML2));
+    S += e;
     if (PAIR) {
-      bool need = false;
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) {
-        const float xt = fmaf(t[v * VEC + e], kLog2e, -ML2);
-        const float xd = fmaf(d[v * VEC + e], kLog2e, -DL2);
-        const float ee = fast_exp2(xt);
-        ovf |= xd > 115.f;
-        const float f = fast_exp2(fminf(xd, 115.f));
-        const float w2 = xt - xd;  // w in log2 units
-        const float ew2 = ee * w2;
-        const bool exact = (xt > -8.f) && (fabsf(w2) < 1.4426950408889634f);
-        const float dterm = fmaf(ew2, kLn2, f - ee);  // e (exp(-w) - 1 + w)
-        S += ee;
-        A2 += ew2;
-        D += exact ? 0.f : dterm;
-        need |= exact;
-      }
-      if (__any_sync(kFull, need)) {
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const float xt = fmaf(t[v * VEC + e], kLog2e, -ML2);
-          const float xd = fmaf(d[v * VEC + e], kLog2e, -DL2);
-          const float w2 = xt - xd;
-          if ((xt > -8.f) && (fabsf(w2) < 1.4426950408889634f)) {
-            D = fmaf(fast_exp2(xt), g_series(w2 * kLn2), D);
-          }
-        }
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) S += fast_exp2(fmaf(t[v * VEC + e], kLog2e, -ML2));
+      const float w = diff_ref<T>(t[q], d[q], Cf);
+      A = fmaf(e, w, A);
+      D = fmaf(e, g_of_w(w, ovf), D);
     }
   }
   double Sd = warp_sum((double)S);
-  double Ad = PAIR ? warp_sum((double)A2) : 0.0;
+  double Ad = PAIR ? warp_sum((double)A) : 0.0;
   double Dd = PAIR ? warp_sum((double)D) : 0.0;
   if (ovf) s_flag = DSDE_FLAG_OVERFLOW;  // benign race: same value
   if (lane == 0) {
@@ -310,10 +309,10 @@ __global__ void __launch_bounds__(kThreads) k_stream(StreamArgs a) {
     }
     ChunkPartial p;
     p.S = s0;
-    p.A = s1 * kLn2d;
+    p.A = s1;
     p.D = s2;
     p.M = M;
-    p.dstar = dstar;
+    p.C = Cf;
     p.idx = Mi;
     p.flags = s_flag;
     p.pad[0] = p.pad[1] = 0;
@@ -342,7 +341,7 @@ __device__ RowStats merge_row(const ChunkPartial* P, int nchunks, bool pair) {
     }
   RowStats r;
   r.M = (double)Mref;
-  r.C = pair ? (double)Mref - (double)P[cref].dstar : 0.0;
+  r.C = pair ? (double)P[cref].C : 0.0;
   r.S = r.A = r.D = 0.0;
   r.flags = 0;
   for (int c = 0; c < nchunks; ++c) {
@@ -351,7 +350,7 @@ __device__ RowStats merge_row(const ChunkPartial* P, int nchunks, bool pair) {
     r.S += s * q.S;
     r.flags |= q.flags;
     if (pair) {
-      const double dl = ((double)q.M - (double)q.dstar) - r.C;
+      const double dl = (double)q.C - r.C;
       const double em = expm1(-dl);
       r.A += s * (q.A + q.S * dl);
       r.D += s * (exp(-dl) * q.D - q.A * em + q.S * (em + dl));

@@ -174,3 +174,25 @@ def test_distribution_bruteforce_gpu(m, state):
     tab = spec_sim.Tables(8, 3, 31)
     codes = spec_sim.run_generation(tab, 10 ** 6, fn, 31)
     spec_sim.check_distribution(tab, codes)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("sigma_n", [0.002, 0.01, 0.05, 0.3, 1.5])
+def test_kl_precision_small_and_large(m, state, dtype, sigma_n):
+    """KL within 1e-5 relative (+1e-9 abs) from KL ~ 1e-6 to several nats,
+    with peaked (sigma_t = 8) and flat (sigma_t = 3) rows and a draft offset."""
+    r = np.random.default_rng(int(sigma_n * 1e4))
+    V, B, k = 128256 if dtype == torch.bfloat16 else 32000, 6, 3
+    cu = synth.cu_from_k(np.full(B, k))
+    nk = B * k
+    sig_t = np.repeat(r.choice([3.0, 8.0], nk + B), 1)[:, None]
+    t = (r.standard_normal((nk + B, V)) * sig_t).astype(np.float32)
+    rows = np.arange(nk) + np.repeat(np.arange(B), k)
+    d = (t[rows] + sigma_n * r.standard_normal((nk, V)) + r.uniform(-4, 4, (nk, 1))).astype(np.float32)
+    if dtype == torch.bfloat16:
+        t = (t.view(np.uint32) >> 16).astype(np.uint16)
+        d = (d.view(np.uint32) >> 16).astype(np.uint16)
+    host = dict(cu_sl=cu, target=t, draft=d, draft_tokens=r.integers(0, V, nk).astype(np.int32),
+                seeds=synth.slot_seeds(5, 0, cu))
+    rep, _, o = _check(m, state, host, dtype)
+    print(f"sigma_n={sigma_n} {dtype}: KL range {o.kld.min():.3e}..{o.kld.max():.3e} max rel {rep.kl_max_rel:.2e}")
