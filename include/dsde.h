@@ -73,7 +73,7 @@ typedef enum { DSDE_F32 = 0, DSDE_BF16 = 1 } dsde_dtype;
 #define DSDE_FLAG_ACCEPT_NEAR_TIE 1  /* |u_acc - min(1, p/q)| < 1e-6 at this position      */
 #define DSDE_FLAG_SAMPLE_NEAR_TIE 2  /* |u_smp - C/R| < 1e-6 at a CDF edge of the draw      */
 #define DSDE_FLAG_FALLBACK 4         /* residual mass 0: the token was drawn from p (D7)  */
-#define DSDE_FLAG_OVERFLOW 8         /* a draft logit exceeded the reference by > 80 nats */
+#define DSDE_FLAG_OVERFLOW 8         /* a draft logit exceeds the reference by > 64 nats: reference lowered (informational) */
 
 /* Adapter configuration; defaults from the paper / SPEC (dsde_config_default).
  * Validity (S:173-174 plus D11/D17): 0 < delta <= 1; 1 <= n_short < n_long

@@ -1,10 +1,9 @@
 // signal.cu — dsde_update_signal (§8(a) a5-a6) and dsde_next_sl (a7).
 //
-// a5/a6: one thread per sequence. The KLD history is a per-slot fp64 ring of
-// capacity n_long (Fig.5). Weighted variances (Eq.5-7)
-// use West's weighted incremental recurrence (CACM 22(9), 1979) over the ring,
-// most recent observation first (alpha_1 = 1), snapshotting the short window
-// on the way to the long one — one pass, no second sweep.
+// a5/a6: one warp per sequence. The KLD history is a per-slot fp64 ring of
+// capacity n_long (Fig.5). Weighted variances (Eq.5-7):
+// lanes hold the observations most recent first with alpha_i = delta^(i-1);
+// the weighted mean and variance are two warp-wide fp64 reductions per window.
 // a7: exact int64 partials (sum SL^, N, max SL^) -> optional NCCL all-reduce
 // -> cap (Eq.11 with round-half-even, D14) -> next SL.
 #include <cuda_runtime.h>
@@ -30,12 +29,6 @@ struct SignalArgs {
   int32_t* err;
 };
 
-__device__ __forceinline__ void ring_push(SeqState& s, int cap, double x) {
-  s.ring[s.head] = x;
-  s.head = s.head + 1 == cap ? 0 : s.head + 1;
-  if (s.count < cap) s.count++;
-}
-
 // Eq.1 + D11: SL_max = clamp(rint(raw), sl_min + 1, sl_ceiling).
 __host__ __device__ inline int calib_sl_max(const dsde_config& c, int sl_a_max, double mu,
                                             double mx) {
@@ -47,97 +40,152 @@ __host__ __device__ inline int calib_sl_max(const dsde_config& c, int sl_a_max, 
   return (int)r;
 }
 
-__global__ void k_update_signal(SignalArgs a) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// One warp per sequence. Lane m holds history observations m and m + 32
+// (most recent first, alpha = delta^m); the weighted mean and variance of
+// Eq.6-7 are two warp-wide fp64 passes over the short and long windows.
+__global__ void __launch_bounds__(128) k_update_signal(SignalArgs a) {
+  const int i = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (i >= a.B) return;
   const dsde_config& c = a.cfg;
   const int slot = a.slots[i];
   double* dg = a.diag ? a.diag + 8 * (long long)i : nullptr;
   if (slot < 0 || slot >= a.max_seqs) {
-    a.sl_hat[i] = c.sl_min;
-    raise_device_error(a.err, DSDE_DERR_BAD_SLOT, i);
+    if (lane == 0) {
+      a.sl_hat[i] = c.sl_min;
+      raise_device_error(a.err, DSDE_DERR_BAD_SLOT, i);
+    }
     return;
   }
   SeqState& s = a.seq[slot];
   const int c0 = a.cu_sl[i], k = a.cu_sl[i + 1] - c0;
   if (a.acc_len[i] < 0 || k < 1 || k > DSDE_MAX_SL || c0 < 0) {
-    a.sl_hat[i] = c.sl_min;  // verify flagged this sequence; leave its state untouched
-    s.last_sl_hat = c.sl_min;
-    if (dg)
-      for (int q = 0; q < 8; ++q) dg[q] = NAN;
+    if (lane == 0) {
+      a.sl_hat[i] = c.sl_min;  // verify flagged this sequence; its state is left untouched
+      s.last_sl_hat = c.sl_min;
+    }
+    if (dg && lane < 8) dg[lane] = NAN;
     return;
   }
-  // 1-2: mu_last and history append (D8: per-token or per-step unit)
-  double sum = 0.0;
-  for (int j = 0; j < k; ++j) sum += (double)a.kld[c0 + j];
-  const double mu_last = sum / (double)k;
+  // 1-2: mu_last and the history append (Fig.5; D8)
+  const double x = lane < k ? (double)a.kld[c0 + lane] : 0.0;
+  const double mu_last = wsum(x) / (double)k;
+  const int cap = c.n_long;
+  const int head0 = s.head, count0 = s.count;
+  int n_new;
   if (c.window_unit == 0) {
-    for (int j = 0; j < k; ++j) ring_push(s, c.n_long, (double)a.kld[c0 + j]);
+    // oldest evicted by overwrite; if k > n_long only the last n_long are kept
+    if (lane < k && lane >= k - cap) s.ring[(head0 + lane) % cap] = x;
+    n_new = k;
   } else {
-    ring_push(s, c.n_long, mu_last);
+    if (lane == 0) s.ring[head0] = mu_last;
+    n_new = 1;
   }
-  s.steps++;
+  const int head = (head0 + n_new) % cap;
+  const int count = min(count0 + n_new, cap);
   // 3: calibration (Eq.1; D12)
-  if (c.calib_steps < 1 && s.sl_max == 0) s.sl_max = c.sl_ceiling;
-  if (s.steps <= c.calib_steps) {
-    if (a.acc_len[i] > s.sl_a_max) s.sl_a_max = a.acc_len[i];
-    for (int j = 0; j < k; ++j) {
-      const double x = (double)a.kld[c0 + j];
-      s.kld_sum += x;
-      s.kld_cnt += 1;
-      if (x > s.kld_max) s.kld_max = x;
-    }
-    if (s.steps == c.calib_steps)
-      s.sl_max = calib_sl_max(c, s.sl_a_max, s.kld_sum / (double)s.kld_cnt, s.kld_max);
+  const int steps = s.steps + 1;
+  const double ksum = wsum(x);
+  double kmax = x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) kmax = fmax(kmax, __shfl_xor_sync(kFull, kmax, o));
+  int sl_max = s.sl_max;
+  if (c.calib_steps < 1 && sl_max == 0) sl_max = c.sl_ceiling;
+  int sl_a_max = s.sl_a_max;
+  double kld_sum = s.kld_sum, kld_max = s.kld_max;
+  long long kld_cnt = s.kld_cnt;
+  if (steps <= c.calib_steps) {
+    sl_a_max = max(sl_a_max, a.acc_len[i]);
+    kld_sum += ksum;
+    kld_cnt += k;
+    kld_max = fmax(kld_max, kmax);
+    if (steps == c.calib_steps) sl_max = calib_sl_max(c, sl_a_max, kld_sum / (double)kld_cnt, kld_max);
   }
-  // 4-5: weighted variances, most recent first, and WVIR (Eq.4; D9, D10)
+  __syncwarp();
+  // 4-5: weighted variances (Eq.5-7) and WVIR (Eq.4; D9, D10)
   double var_s = NAN, var_l = NAN, wvir = 1.0;
-  if (s.count >= c.n_short) {
-    double W = 0.0, mean = 0.0, S2 = 0.0, alpha = 1.0;
-    int pos = s.head;
-    for (int n = 1; n <= s.count; ++n) {
-      pos = pos == 0 ? c.n_long - 1 : pos - 1;
-      const double x = s.ring[pos];
-      const double Wn = W + alpha;
-      const double q = x - mean;
-      const double r = q * alpha / Wn;
-      mean += r;
-      S2 += W * q * r;
-      W = Wn;
-      alpha *= c.delta;
-      if (n == c.n_short) var_s = S2 / W;
+  if (count >= c.n_short) {
+    double xs[2], al[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int m = lane + 32 * h;  // m = 0 is the most recent observation
+      xs[h] = m < count ? s.ring[(head - 1 - m + 2 * cap) % cap] : 0.0;
+      al[h] = m < count ? pow(c.delta, (double)m) : 0.0;
     }
-    var_l = S2 / W;
+    double wv[2];
+#pragma unroll
+    for (int win = 0; win < 2; ++win) {
+      const int N = win == 0 ? c.n_short : count;
+      double sa = 0.0, sax = 0.0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = lane + 32 * h;
+        if (m < N) {
+          sa += al[h];
+          sax += al[h] * xs[h];
+        }
+      }
+      sa = wsum(sa);
+      const double mu = wsum(sax) / sa;
+      double sv = 0.0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = lane + 32 * h;
+        if (m < N) {
+          const double e = xs[h] - mu;
+          sv += al[h] * e * e;
+        }
+      }
+      wv[win] = wsum(sv) / sa;
+    }
+    var_s = wv[0];
+    var_l = wv[1];
     wvir = var_l < 1e-12 ? 1.0 : var_s / var_l;
   }
   // 6-7: SF (Eq.3), penalty and Eq.8
   const double sf = expm1(2.0 * mu_last);
   const double penalty = sf * wvir;
-  const bool calibrating = s.steps < c.calib_steps;
+  const bool calibrating = steps < c.calib_steps;
   int out;
-  double x = NAN;
+  double xr = NAN;
   if (calibrating) {
     out = c.calib_sl;
   } else {
-    x = penalty <= 1.0 ? (1.0 - penalty) * (double)(s.sl_max - c.sl_min) + (double)c.sl_min
-                       : (double)c.sl_min;
-    double rr = rint(x);
+    xr = penalty <= 1.0 ? (1.0 - penalty) * (double)(sl_max - c.sl_min) + (double)c.sl_min
+                        : (double)c.sl_min;
+    double rr = rint(xr);
     if (rr < c.sl_min) rr = c.sl_min;
-    if (rr > s.sl_max) rr = s.sl_max;
+    if (rr > sl_max) rr = sl_max;
     out = (int)rr;
   }
-  s.calibrating = calibrating ? 1 : 0;
-  s.last_sl_hat = out;
-  a.sl_hat[i] = out;
-  if (dg) {
+  if (lane == 0) {
+    s.head = head;
+    s.count = count;
+    s.steps = steps;
+    s.sl_a_max = sl_a_max;
+    s.kld_sum = kld_sum;
+    s.kld_cnt = kld_cnt;
+    s.kld_max = kld_max;
+    s.sl_max = sl_max;
+    s.calibrating = calibrating ? 1 : 0;
+    s.last_sl_hat = out;
+    a.sl_hat[i] = out;
+  }
+  if (dg && lane == 0) {
     dg[0] = mu_last;
     dg[1] = sf;
     dg[2] = var_s;
     dg[3] = var_l;
     dg[4] = wvir;
     dg[5] = penalty;
-    dg[6] = x;
-    dg[7] = (double)s.sl_max;
+    dg[6] = xr;
+    dg[7] = (double)sl_max;
   }
 }
 
@@ -257,7 +305,7 @@ extern "C" dsde_status dsde_update_signal(dsde_state st, int B, const int32_t* s
   if (B > st->max_seqs) return DSDE_ERR_STATE;
   SignalArgs a{st->cfg, B, st->max_seqs, slots, cu_sl, kld, accepted_len, sl_hat, diag, st->seq,
                st->err};
-  k_update_signal<<<(B + 127) / 128, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  k_update_signal<<<(B + 3) / 4, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
   return cudaGetLastError() == cudaSuccess ? DSDE_OK : DSDE_ERR_CUDA;
 }
 

@@ -55,7 +55,8 @@ struct ChunkPartial {  // 48 bytes
   float C;             // t - d at the chunk argmax (fp32, as used for w)
   int idx;             // chunk argmax (smallest index among ties)
   int flags;           // DSDE_FLAG_OVERFLOW
-  int pad[2];
+  float maxd;          // max of d over the chunk (overflow-safe reference bound)
+  int pad;
 };
 static_assert(sizeof(ChunkPartial) == 48, "ChunkPartial layout");
 
@@ -163,14 +164,15 @@ __device__ __forceinline__ void arg_better(float& m, int& mi, float& md, float m
   }
 }
 
-// g(w) = exp(-w) - 1 + w >= 0, accurate to ~1e-7 relative for every w:
-//   |w| < 1: g = u^2 h(u), u = -w, h(u) = (e^u - 1 - u)/u^2 by a degree-7
+// e * g(w), g(w) = exp(-w) - 1 + w >= 0, to ~1e-7 relative for every w:
+//   |w| < 1: e u^2 h(u), u = -w, h(u) = (e^u - 1 - u)/u^2 by a degree-7
 //            near-minimax polynomial (Chebyshev fit on [-1,1]; 1.1e-7 relative
 //            in fp32 Horner, tools/fit_g.py) — no cancellation near w = 0;
-//   |w| >= 1: g = (2^(-w log2 e) - 1) + w (MUFU); relative error <= 4 ulp there.
-// The argument of 2^x is clamped at 126 (draft logit > ~87 nats above the
-// reference): `ovf` reports it (DSDE_FLAG_OVERFLOW).
-__device__ __forceinline__ float g_of_w(float w, bool& ovf) {
+//   |w| >= 1: e exp(-w) - e + e w, with e exp(-w) = 2^(xt - w log2 e) formed in
+//            one exponent (= exp(d - (M - C)) <= e^64 by the choice of C), so no
+//            intermediate overflows; relative error <= ~4 ulp there.
+// xt = (t - M) log2 e and e = 2^xt.
+__device__ __forceinline__ float e_g(float e, float xt, float w) {
   const float u = -w;
   float p = 2.812654656736413e-06f;
   p = fmaf(p, u, 2.5358644052175805e-05f);
@@ -180,10 +182,9 @@ __device__ __forceinline__ float g_of_w(float w, bool& ovf) {
   p = fmaf(p, u, 4.166673496365547e-02f);
   p = fmaf(p, u, 1.666666716337204e-01f);
   p = fmaf(p, u, 0.5f);
-  const float small = (u * u) * p;
-  const float x = u * kLog2e;
-  ovf |= x > 126.f;
-  const float big = (fast_exp2(fminf(x, 126.f)) - 1.f) + w;
+  const float small = e * ((u * u) * p);
+  const float f = fast_exp2(fmaf(u, kLog2e, xt));
+  const float big = fmaf(e, w, f - e);
   return fabsf(w) < 1.f ? small : big;
 }
 
@@ -238,13 +239,14 @@ __global__ void __launch_bounds__(kThreads) k_stream(StreamArgs a) {
 
   // chunk max of t and its smallest-index argmax (the reference of w)
   const int base = c * chunk_elems<T>();
-  float m = -INFINITY, md = 0.f;
+  float m = -INFINITY, md = 0.f, dmax = -INFINITY;
   int mi = 0x7fffffff;
 #pragma unroll
   for (int v = 0; v < NV; ++v)
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
       const int idx = base + (v * kThreads + threadIdx.x) * VEC + e;
+      if (PAIR) dmax = fmaxf(dmax, d[v * VEC + e]);  // padding is -1e30
       if (idx < a.V && t[v * VEC + e] > m) {
         m = t[v * VEC + e];
         mi = idx;
@@ -257,42 +259,48 @@ __global__ void __launch_bounds__(kThreads) k_stream(StreamArgs a) {
     const int i2 = __shfl_xor_sync(kFull, mi, o);
     const float d2 = __shfl_xor_sync(kFull, md, o);
     arg_better(m, mi, md, m2, i2, d2);
+    if (PAIR) dmax = fmaxf(dmax, __shfl_xor_sync(kFull, dmax, o));
   }
-  __shared__ float s_m[kThreads / 32], s_d[kThreads / 32];
+  __shared__ float s_m[kThreads / 32], s_d[kThreads / 32], s_dmax[kThreads / 32];
   __shared__ int s_i[kThreads / 32];
   __shared__ double s_sum[3][kThreads / 32];
-  __shared__ int s_flag;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) s_flag = 0;
   if (lane == 0) {
     s_m[warp] = m;
     s_i[warp] = mi;
     s_d[warp] = md;
+    s_dmax[warp] = dmax;
   }
   __syncthreads();
-  float M = s_m[0], dstar = s_d[0];
+  float M = s_m[0], dstar = s_d[0], Dmax = s_dmax[0];
   int Mi = s_i[0];
 #pragma unroll
-  for (int w = 1; w < kThreads / 32; ++w) arg_better(M, Mi, dstar, s_m[w], s_i[w], s_d[w]);
+  for (int w = 1; w < kThreads / 32; ++w) {
+    arg_better(M, Mi, dstar, s_m[w], s_i[w], s_d[w]);
+    Dmax = fmaxf(Dmax, s_dmax[w]);
+  }
 
   const float ML2 = M * kLog2e;
-  const float Cf = M - dstar;  // reference t - d (exact for bf16 inputs); stored as used
+  // Reference C = t - d at the chunk argmax (exact for bf16 inputs), lowered if
+  // needed so that e_v exp(-w_v) = exp(d_v - (M - C)) <= e^64 for every v in the
+  // chunk: no fp32 overflow even for draft logits far above the reference
+  // (disjoint supports). Stored as used.
+  const float Cf = PAIR ? fminf(M - dstar, (M - Dmax) + 64.f) : 0.f;
   float S = 0.f, A = 0.f, D = 0.f;
-  bool ovf = false;
 #pragma unroll
   for (int q = 0; q < E; ++q) {
-    const float e = fast_exp2(fmaf(t[q], kLog2e, -ML2));
+    const float xt = fmaf(t[q], kLog2e, -ML2);
+    const float e = fast_exp2(xt);
     S += e;
     if (PAIR) {
       const float w = diff_ref<T>(t[q], d[q], Cf);
       A = fmaf(e, w, A);
-      D = fmaf(e, g_of_w(w, ovf), D);
+      D += e_g(e, xt, w);
     }
   }
   double Sd = warp_sum((double)S);
   double Ad = PAIR ? warp_sum((double)A) : 0.0;
   double Dd = PAIR ? warp_sum((double)D) : 0.0;
-  if (ovf) s_flag = DSDE_FLAG_OVERFLOW;  // benign race: same value
   if (lane == 0) {
     s_sum[0][warp] = Sd;
     s_sum[1][warp] = Ad;
@@ -314,8 +322,9 @@ __global__ void __launch_bounds__(kThreads) k_stream(StreamArgs a) {
     p.M = M;
     p.C = Cf;
     p.idx = Mi;
-    p.flags = s_flag;
-    p.pad[0] = p.pad[1] = 0;
+    p.flags = (PAIR && Cf < M - dstar) ? DSDE_FLAG_OVERFLOW : 0;
+    p.maxd = Dmax;
+    p.pad = 0;
     a.part[prow * a.nchunks + c] = p;
   }
 }
@@ -327,33 +336,49 @@ struct RowStats {
 };
 
 // fp64 merge of chunk partials in chunk order. The reference is the chunk
-// with the largest M (earliest on ties, so the row's smallest-index argmax).
-// Chunk c's w is shifted by Delta = C_c - C:
-//   S += s S_c,  A += s (A_c + S_c Delta),
-//   D += s (e^-Delta D_c - A_c expm1(-Delta) + S_c g(Delta)),  s = e^(M_c - M).
+// with the largest M (earliest on ties, so the row's smallest-index argmax),
+// lowered like the chunk references so that every v has
+// d_v - (M - C) <= 64 (all merged terms stay finite in fp64).
+// Chunk c's w is shifted by Delta = C_c - C; with s = e^(M_c - M) and
+// E1 = s e^-Delta:
+//   S += s S_c,   A += s (A_c + S_c Delta),
+//   D += E1 D_c - A_c s expm1(-Delta) + S_c s g(Delta),  g(x) = expm1(-x) + x.
 __device__ RowStats merge_row(const ChunkPartial* P, int nchunks, bool pair) {
   int cref = 0;
-  float Mref = P[0].M;
-  for (int c = 1; c < nchunks; ++c)
+  float Mref = P[0].M, maxd = P[0].maxd;
+  for (int c = 1; c < nchunks; ++c) {
     if (P[c].M > Mref) {
       Mref = P[c].M;
       cref = c;
     }
+    maxd = fmaxf(maxd, P[c].maxd);
+  }
   RowStats r;
   r.M = (double)Mref;
-  r.C = pair ? (double)P[cref].C : 0.0;
+  r.C = pair ? fmin((double)P[cref].C, (r.M - (double)maxd) + 64.0) : 0.0;
   r.S = r.A = r.D = 0.0;
   r.flags = 0;
   for (int c = 0; c < nchunks; ++c) {
     const ChunkPartial q = P[c];
-    const double s = exp((double)q.M - r.M);
+    const double ls = (double)q.M - r.M;
+    const double s = exp(ls);
     r.S += s * q.S;
     r.flags |= q.flags;
     if (pair) {
       const double dl = (double)q.C - r.C;
-      const double em = expm1(-dl);
-      r.A += s * (q.A + q.S * dl);
-      r.D += s * (exp(-dl) * q.D - q.A * em + q.S * (em + dl));
+      double sem, sg, E1;  // s expm1(-dl), s g(dl), s e^-dl
+      if (fabs(dl) < 1.0) {
+        const double em = expm1(-dl);
+        sem = s * em;
+        sg = s * (em + dl);
+        E1 = s + sem;
+      } else {
+        E1 = exp(ls - dl);
+        sem = E1 - s;
+        sg = sem + s * dl;
+      }
+      r.A += s * q.A + s * q.S * dl;
+      r.D += E1 * q.D - q.A * sem + q.S * sg;
     }
   }
   return r;

@@ -23,6 +23,8 @@ def to_device_inputs(host: dict, dtype: torch.dtype, device="cuda", ld_pad: int 
     """numpy host batch (oracle format) -> device tensors for dsde_verify."""
     t, d = host["target"], host["draft"]
     V = t.shape[1]
+    esz = 2 if dtype == torch.bfloat16 else 4
+    ld_pad += (-(V + ld_pad) * esz) % 16 // esz   # rows must start 16-byte aligned
     def dev(x):
         if dtype == torch.bfloat16:
             a = torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).view(torch.bfloat16)
