@@ -25,6 +25,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "state.cuh"
 
@@ -143,6 +145,15 @@ __device__ __forceinline__ void load_slice_strided(const T* row, int V, int c, f
         x[v * VEC + e] = (e0 + e < V) ? load_logit<T>(row + e0 + e) : -1e30f;
     }
   }
+}
+
+template <typename T>
+__device__ __forceinline__ float load_logit_smem(const T* p);
+template <>
+__device__ __forceinline__ float load_logit_smem<float>(const float* p) { return *p; }
+template <>
+__device__ __forceinline__ float load_logit_smem<uint16_t>(const uint16_t* p) {
+  return bf16_bits_to_float(*p);
 }
 
 struct StreamArgs {
@@ -329,6 +340,317 @@ __global__ void __launch_bounds__(kThreads) k_stream(StreamArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// a1, production path: persistent CTAs (2 per SM) with a 3-stage ring of
+// 32 KB shared-memory stages filled by 1-D TMA bulk copies
+// (cp.async.bulk + mbarrier complete_tx). Item q = (draft row r, chunk c),
+// q = blockIdx.x + j * gridDim.x, i.e. the grid sweeps rows in order. Each
+// thread lifts its 2 x 32 logits of the chunk into registers, which frees
+// the stage after the first barrier: the refill of that stage (item j + 3)
+// is in flight while the statistics of item j are computed. Element math is
+// packed two-wide (FFMA2/FADD2/FMUL2) with two MUFU.EX2 per element.
+// Same partials and numerics as k_stream.
+// ---------------------------------------------------------------------------
+constexpr int kStages = 3;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+struct StreamTmaArgs {
+  const void* tl;
+  long long ld_t;
+  const void* dl;
+  long long ld_d;
+  const int32_t* cu_sl;
+  int B, V, nchunks, total;
+  ChunkPartial* part;
+};
+
+template <typename T>
+__host__ __device__ constexpr int stage_row_bytes() {
+  return chunk_elems<T>() * (int)sizeof(T);
+}
+template <typename T>
+__host__ __device__ constexpr int stream_tma_smem() {
+  return kStages * 2 * stage_row_bytes<T>() + kStages * 8;
+}
+
+template <typename T>
+__device__ __forceinline__ void unpack16(uint4 raw, float* x);
+template <>
+__device__ __forceinline__ void unpack16<uint16_t>(uint4 raw, float* x) {
+  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    x[2 * h] = bf16_lo(w[h]);
+    x[2 * h + 1] = bf16_hi(w[h]);
+  }
+}
+template <>
+__device__ __forceinline__ void unpack16<float>(uint4 raw, float* x) {
+  x[0] = __uint_as_float(raw.x);
+  x[1] = __uint_as_float(raw.y);
+  x[2] = __uint_as_float(raw.z);
+  x[3] = __uint_as_float(raw.w);
+}
+
+template <typename T>
+__device__ __forceinline__ float2 diff2(float2 t, float2 d, float C);
+template <>
+__device__ __forceinline__ float2 diff2<uint16_t>(float2 t, float2 d, float C) {
+  return __fadd2_rn(__fadd2_rn(t, make_float2(-d.x, -d.y)), make_float2(-C, -C));
+}
+template <>
+__device__ __forceinline__ float2 diff2<float>(float2 t, float2 d, float C) {
+  return make_float2(diff_ref<float>(t.x, d.x, C), diff_ref<float>(t.y, d.y, C));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 2) k_stream_tma(StreamTmaArgs a) {
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, E = VEC * NV, CH = chunk_elems<T>();
+  constexpr int ROWB = stage_row_bytes<T>();
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * 2 * ROWB);
+  __shared__ float s_m[2][kThreads / 32], s_d[2][kThreads / 32], s_dx[2][kThreads / 32];
+  __shared__ int s_i[2][kThreads / 32];
+  __shared__ float s_sum[2][3][kThreads / 32];
+  const long long n_items = (long long)a.total * a.nchunks;
+  const int G = gridDim.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  auto issue = [&](long long q, int stage) {
+    const long long r = q / a.nchunks;
+    const int c = (int)(q - r * a.nchunks);
+    int lo = 0, hi = a.B - 1;  // sequence of draft row r
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(a.cu_sl + mid) <= r) lo = mid; else hi = mid - 1;
+    }
+    const int c0 = c * CH;
+    const int n_el = min(CH, a.V - c0);
+    const uint32_t bytes = (uint32_t)(n_el * (int)sizeof(T)) & ~15u;
+    uint8_t* dst = smem + stage * 2 * ROWB;
+    if (bytes) {
+      mbar_arrive_expect_tx(&full[stage], 2 * bytes);
+      bulk_g2s(dst, reinterpret_cast<const T*>(a.tl) + (r + lo) * a.ld_t + c0, bytes, &full[stage]);
+      bulk_g2s(dst + ROWB, reinterpret_cast<const T*>(a.dl) + r * a.ld_d + c0, bytes, &full[stage]);
+    } else {
+      mbar_arrive(&full[stage]);
+    }
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < kStages; ++s) {
+      const long long q = blockIdx.x + (long long)s * G;
+      if (q < n_items) issue(q, s);
+    }
+
+  const float2 L2 = make_float2(kLog2e, kLog2e), nL2 = make_float2(-kLog2e, -kLog2e);
+  // h(-w) coefficients in powers of w (alternating signs of tools/fit_g.py's)
+  const float2 K7 = make_float2(-2.812654656736413e-06f, -2.812654656736413e-06f);
+  const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
+  const float2 K5 = make_float2(-1.9836986029986292e-04f, -1.9836986029986292e-04f);
+  const float2 K4 = make_float2(1.3885394437238574e-03f, 1.3885394437238574e-03f);
+  const float2 K3 = make_float2(-8.33334494382143e-03f, -8.33334494382143e-03f);
+  const float2 K2 = make_float2(4.166673496365547e-02f, 4.166673496365547e-02f);
+  const float2 K1 = make_float2(-1.666666716337204e-01f, -1.666666716337204e-01f);
+  const float2 K0 = make_float2(0.5f, 0.5f);
+
+  int j = 0;
+  for (long long q = blockIdx.x; q < n_items; q += G, ++j) {
+    const int stage = j % kStages;
+    const uint32_t par = (uint32_t)(j / kStages) & 1u;
+    const int buf = j & 1;
+    const long long r = q / a.nchunks;
+    const int c = (int)(q - r * a.nchunks);
+    const int c0 = c * CH;
+    const int n_el = min(CH, a.V - c0);
+    const int bulk_el = (int)(((uint32_t)(n_el * (int)sizeof(T)) & ~15u) / sizeof(T));
+    mbar_wait(&full[stage], par);
+    const T* st = reinterpret_cast<const T*>(smem + stage * 2 * ROWB);
+    const T* sd = reinterpret_cast<const T*>(smem + stage * 2 * ROWB + ROWB);
+    float t[E], d[E];
+    if (n_el == CH) {  // every chunk but the last of a row: unchecked 128-bit LDS
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int e0 = (v * kThreads + tid) * VEC;
+        unpack16<T>(*reinterpret_cast<const uint4*>(st + e0), t + v * VEC);
+        unpack16<T>(*reinterpret_cast<const uint4*>(sd + e0), d + v * VEC);
+      }
+    } else {
+      // last chunk: bulk-copied part from shared memory, an unaligned tail
+      // (V * sizeof(T) not a multiple of 16) from global memory, padding after V
+      long long trow = 0;
+      if (bulk_el < n_el) {
+        int lo = 0, hi = a.B - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (__ldg(a.cu_sl + mid) <= r) lo = mid; else hi = mid - 1;
+        }
+        trow = r + lo;
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int e0 = (v * kThreads + tid) * VEC;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const int idx = e0 + e;
+          float tv = -1e30f, dv = -1e30f;
+          if (idx < bulk_el) {
+            tv = load_logit_smem(st + idx);
+            dv = load_logit_smem(sd + idx);
+          } else if (idx < n_el) {
+            tv = load_logit<T>(reinterpret_cast<const T*>(a.tl) + trow * a.ld_t + c0 + idx);
+            dv = load_logit<T>(reinterpret_cast<const T*>(a.dl) + r * a.ld_d + c0 + idx);
+          }
+          t[v * VEC + e] = tv;
+          d[v * VEC + e] = dv;
+        }
+      }
+    }
+    // phase 1: chunk max / smallest-index argmax of t, max of d
+    float m = -INFINITY, md = 0.f, dmax = -INFINITY;
+    int mi = 0x7fffffff;
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const int idx = (v * kThreads + tid) * VEC + e;
+        dmax = fmaxf(dmax, d[v * VEC + e]);  // padding (-1e30) never wins over real logits
+        if (t[v * VEC + e] > m) {
+          m = t[v * VEC + e];
+          mi = c0 + idx;
+          md = d[v * VEC + e];
+        }
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(kFull, m, o);
+      const int i2 = __shfl_xor_sync(kFull, mi, o);
+      const float d2 = __shfl_xor_sync(kFull, md, o);
+      arg_better(m, mi, md, m2, i2, d2);
+      dmax = fmaxf(dmax, __shfl_xor_sync(kFull, dmax, o));
+    }
+    if (lane == 0) {
+      s_m[buf][warp] = m;
+      s_i[buf][warp] = mi;
+      s_d[buf][warp] = md;
+      s_dx[buf][warp] = dmax;
+    }
+    __syncthreads();  // B1: every thread holds its slice; the stage is free
+    if (tid == 0) {
+      const long long qn = q + (long long)kStages * G;
+      if (qn < n_items) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(qn, stage);
+      }
+    }
+    float M = s_m[buf][0], dstar = s_d[buf][0], Dmax = s_dx[buf][0];
+    int Mi = s_i[buf][0];
+#pragma unroll
+    for (int w = 1; w < kThreads / 32; ++w) {
+      arg_better(M, Mi, dstar, s_m[buf][w], s_i[buf][w], s_d[buf][w]);
+      Dmax = fmaxf(Dmax, s_dx[buf][w]);
+    }
+    const float Cf = fminf(M - dstar, (M - Dmax) + 64.f);
+    const float ML2 = M * kLog2e;
+    const float2 nML2 = make_float2(-ML2, -ML2);
+    float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
+#pragma unroll
+    for (int h = 0; h < E; h += 2) {
+      const float2 tt = make_float2(t[h], t[h + 1]), dd = make_float2(d[h], d[h + 1]);
+      const float2 xt = __ffma2_rn(tt, L2, nML2);
+      const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
+      const float2 w = diff2<T>(tt, dd, Cf);
+      S2 = __fadd2_rn(S2, e);
+      A2 = __ffma2_rn(e, w, A2);
+      float2 p = __ffma2_rn(K7, w, K6);
+      p = __ffma2_rn(p, w, K5);
+      p = __ffma2_rn(p, w, K4);
+      p = __ffma2_rn(p, w, K3);
+      p = __ffma2_rn(p, w, K2);
+      p = __ffma2_rn(p, w, K1);
+      p = __ffma2_rn(p, w, K0);
+      const float2 sm = __fmul2_rn(__fmul2_rn(e, __fmul2_rn(w, w)), p);
+      const float2 arg = __ffma2_rn(w, nL2, xt);
+      const float2 f = make_float2(fast_exp2(arg.x), fast_exp2(arg.y));
+      const float2 bg = __ffma2_rn(e, w, __fadd2_rn(f, make_float2(-e.x, -e.y)));
+      const float2 term = make_float2(fabsf(w.x) < 1.f ? sm.x : bg.x, fabsf(w.y) < 1.f ? sm.y : bg.y);
+      D2 = __fadd2_rn(D2, term);
+    }
+    float S = S2.x + S2.y, A = A2.x + A2.y, D = D2.x + D2.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      S += __shfl_xor_sync(kFull, S, o);
+      A += __shfl_xor_sync(kFull, A, o);
+      D += __shfl_xor_sync(kFull, D, o);
+    }
+    if (lane == 0) {
+      s_sum[buf][0][warp] = S;
+      s_sum[buf][1][warp] = A;
+      s_sum[buf][2][warp] = D;
+    }
+    __syncthreads();  // B2
+    if (tid == 0) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) {
+        s0 += (double)s_sum[buf][0][w];
+        s1 += (double)s_sum[buf][1][w];
+        s2 += (double)s_sum[buf][2][w];
+      }
+      ChunkPartial p;
+      p.S = s0;
+      p.A = s1;
+      p.D = s2;
+      p.M = M;
+      p.C = Cf;
+      p.idx = Mi;
+      p.flags = Cf < M - dstar ? DSDE_FLAG_OVERFLOW : 0;
+      p.maxd = Dmax;
+      p.pad = 0;
+      a.part[r * a.nchunks + c] = p;
+    }
+  }
+}
+
 // Merged statistics of one row about the row argmax.
 struct RowStats {
   double M, C, S, A, D;
@@ -435,9 +757,12 @@ __global__ void __launch_bounds__(128) k_finalize(FinArgs a) {
     rflags = r.flags;
     nonfin = !(isfinite(r.S) && isfinite(r.A) && isfinite(r.D) && r.S > 0.0 && isfinite(r.M) &&
                isfinite(r.C));
+    // y = E_p[exp(-w)] - 1. KL = D/S + (log1p(y) - y) has no cancellation for
+    // small KL; when y > 1 (the draft puts far more mass away from the
+    // reference, e.g. disjoint supports) the equal form A/S + log1p(y) is used.
     const double y = (r.D - r.A) / r.S;
     lam = log1p(y);
-    kl = fmax(0.0, r.D / r.S + (lam - y));
+    kl = fmax(0.0, y <= 1.0 ? r.D / r.S + (lam - y) : r.A / r.S + lam);
     C = r.C;
     M = r.M;
     if (!bad_tok) {
@@ -726,7 +1051,19 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   const int nc = (V + chunk_elems<T>() - 1) / chunk_elems<T>();
   StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, nc, total, ws.part, ws.rec};
   if (total > 0) {
-    k_stream<T, true><<<(unsigned)((long long)total * nc), kThreads, 0, s>>>(sa);
+    static bool attr_set = false;
+    constexpr int smem = stream_tma_smem<T>();
+    if (!attr_set) {
+      cudaFuncSetAttribute(k_stream_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr_set = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long items = (long long)total * nc;
+    const int grid = (int)std::min<long long>(items, 2LL * sms);
+    StreamTmaArgs ta{tl, ld_t, dl, ld_d, cu_sl, B, V, nc, total, ws.part};
+    k_stream_tma<T><<<grid, kThreads, smem, s>>>(ta);
   }
   FinArgs fa{B, V, total, nc, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, ws.part,
              acc_len, emitted, kld, flags, ws.rec, err};
