@@ -1,18 +1,16 @@
 // verify.cu — dsde_verify: the fused speculative-verification pass (§8(a) a1-a4).
 //
-// Pipeline (all on the caller's stream, no host synchronisation):
-//   1. k_stream<T, PAIR>   one CTA per (draft position row, vocab chunk): a single
-//                          streaming read of the target row and the draft row slice,
-//                          chunk max/argmax, then S = sum e_v, A = sum e_v w_v,
-//                          D = sum e_v g(w_v) about the chunk argmax (a1).
-//   2. k_finalize          one warp per sequence, one lane per position: fp64 merge of
-//                          the chunk partials about the row argmax, KL, log p/q, the
-//                          Philox accept test, the first rejection a_i, token layout (a2-a3).
-//   3. k_stream<T, BONUS>  (M, S) chunk partials of target row k_i, only for sequences
-//                          that accepted every draft (a4, bonus branch).
-//   4. k_sample_mass       per (sequence, chunk): residual max(0, p - q) or bonus p mass.
-//   5. k_sample_select     per sequence: fp64 prefix over chunk masses, block scan inside
-//                          the crossing chunk: the smallest token with C_v > u R (D7).
+// Pipeline (all on the caller's stream, no host synchronisation; 3 launches):
+//   1. k_stream_tma   persistent CTAs, TMA-bulk ring: one streaming read of every
+//                     (draft position row, vocab chunk) of the target and draft
+//                     logits; chunk max/argmax, then S = sum e_v, A = sum e_v w_v,
+//                     D = sum e_v g(w_v) about the chunk reference (a1).
+//   2. k_finalize     one warp per sequence, one lane per position: fp64 merge of
+//                     the chunk partials about the row reference, KL, log p/q, the
+//                     Philox accept test, the first rejection a_i, token layout (a2-a3).
+//   3. k_sample       per (sequence, chunk): draw-weight mass of the residual
+//                     max(0, p - q) (row a_i) or of p (bonus row k_i); the last CTA
+//                     of each sequence selects the smallest token with C_v > u R (a4, D7).
 //
 // Numerics: with e_v = exp(t_v - M), w_v = (t_v - d_v) - C, C = t - d at
 // the argmax of t, and g(w) = exp(-w) - 1 + w >= 0:
@@ -81,7 +79,9 @@ static_assert(sizeof(SeqRec) == 64, "SeqRec layout");
 struct VerifyWs {
   ChunkPartial* part;  // [(total + B) * nchunks]
   SeqRec* rec;         // [B]
-  double* mass;        // [B * nchunks]
+  double* mass;        // [B * nchunks] draw-weight mass per chunk
+  float* cmax;         // [B * nchunks] chunk max of t (bonus draws)
+  int* counter;        // [B] chunks done per sequence (last-block election)
 };
 
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -97,54 +97,16 @@ inline size_t ws_layout(int B, int total, int V, dsde_dtype dt, VerifyWs* ws, ch
   const size_t p_bytes = align256(sizeof(ChunkPartial) * (size_t)(total + B) * nc);
   const size_t r_bytes = align256(sizeof(SeqRec) * (size_t)B);
   const size_t m_bytes = align256(sizeof(double) * (size_t)B * nc);
+  const size_t x_bytes = align256(sizeof(float) * (size_t)B * nc);
+  const size_t c_bytes = align256(sizeof(int) * (size_t)B);
   if (ws) {
     ws->part = reinterpret_cast<ChunkPartial*>(base + off);
     ws->rec = reinterpret_cast<SeqRec*>(base + off + p_bytes);
     ws->mass = reinterpret_cast<double*>(base + off + p_bytes + r_bytes);
+    ws->cmax = reinterpret_cast<float*>(base + off + p_bytes + r_bytes + m_bytes);
+    ws->counter = reinterpret_cast<int*>(base + off + p_bytes + r_bytes + m_bytes + x_bytes);
   }
-  return p_bytes + r_bytes + m_bytes;
-}
-
-// ---------------------------------------------------------------------------
-// Row slices: thread `tid` of chunk c owns, in the streaming layout, the
-// elements c*CH + (v*256 + tid)*VEC + e (v < NV, e < VEC): every load
-// instruction of a warp reads 512 contiguous bytes.
-// ---------------------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ void load_slice_strided(const T* row, int V, int c, float (&x)[Traits<T>::VEC * Traits<T>::NV]) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV;
-  const int base = c * chunk_elems<T>();
-  uint4 raw[NV];
-  bool full[NV];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    const int e0 = base + (v * kThreads + threadIdx.x) * VEC;
-    full[v] = e0 + VEC <= V;
-    if (full[v]) raw[v] = ld_stream_v4(row + e0);
-  }
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    const int e0 = base + (v * kThreads + threadIdx.x) * VEC;
-    if (full[v]) {
-      if constexpr (sizeof(T) == 2) {
-        const uint32_t w[4] = {raw[v].x, raw[v].y, raw[v].z, raw[v].w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          x[v * VEC + 2 * q] = bf16_lo(w[q]);
-          x[v * VEC + 2 * q + 1] = bf16_hi(w[q]);
-        }
-      } else {
-        x[v * VEC + 0] = __uint_as_float(raw[v].x);
-        x[v * VEC + 1] = __uint_as_float(raw[v].y);
-        x[v * VEC + 2] = __uint_as_float(raw[v].z);
-        x[v * VEC + 3] = __uint_as_float(raw[v].w);
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < VEC; ++e)
-        x[v * VEC + e] = (e0 + e < V) ? load_logit<T>(row + e0 + e) : -1e30f;
-    }
-  }
+  return p_bytes + r_bytes + m_bytes + x_bytes + c_bytes;
 }
 
 template <typename T>
@@ -155,17 +117,6 @@ template <>
 __device__ __forceinline__ float load_logit_smem<uint16_t>(const uint16_t* p) {
   return bf16_bits_to_float(*p);
 }
-
-struct StreamArgs {
-  const void* tl;
-  long long ld_t;
-  const void* dl;
-  long long ld_d;
-  const int32_t* cu_sl;
-  int B, V, nchunks, total;
-  ChunkPartial* part;
-  const SeqRec* rec;
-};
 
 __device__ __forceinline__ void arg_better(float& m, int& mi, float& md, float m2, int i2, float d2) {
   if (m2 > m || (m2 == m && i2 < mi)) {
@@ -214,130 +165,6 @@ __device__ __forceinline__ float diff_ref<float>(float t, float d, float C) {
   const float bb = __fsub_rn(hi, t);
   const float lo = __fadd_rn(__fsub_rn(t, __fsub_rn(hi, bb)), __fsub_rn(-d, bb));
   return __fadd_rn(__fsub_rn(hi, C), lo);
-}
-
-// a1: one CTA per (row, chunk). PAIR: draft row r = blockIdx / nchunks paired with
-// target row r + i (i = sequence of r). !PAIR: target row k_i of sequence
-// i = blockIdx / nchunks if it accepted every draft (bonus), partials at row total + i.
-template <typename T, bool PAIR>
-__global__ void __launch_bounds__(kThreads) k_stream(StreamArgs a) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, E = VEC * NV;
-  const int c = blockIdx.x % a.nchunks;
-  const long long rl = blockIdx.x / a.nchunks;
-  long long trow, drow = 0, prow;
-  if (PAIR) {
-    drow = rl;
-    int lo = 0, hi = a.B - 1;  // sequence of draft row: last i with cu_sl[i] <= r
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (__ldg(a.cu_sl + mid) <= drow) lo = mid; else hi = mid - 1;
-    }
-    trow = drow + lo;
-    prow = drow;
-  } else {
-    const SeqRec r = a.rec[rl];
-    if (r.mode != MODE_BONUS) return;
-    trow = r.trow;
-    prow = a.total + rl;
-  }
-  const T* tp = reinterpret_cast<const T*>(a.tl) + trow * a.ld_t;
-  float t[E], d[E];
-  load_slice_strided<T>(tp, a.V, c, t);
-  if (PAIR) {
-    const T* dp = reinterpret_cast<const T*>(a.dl) + drow * a.ld_d;
-    load_slice_strided<T>(dp, a.V, c, d);
-  }
-
-  // chunk max of t and its smallest-index argmax (the reference of w)
-  const int base = c * chunk_elems<T>();
-  float m = -INFINITY, md = 0.f, dmax = -INFINITY;
-  int mi = 0x7fffffff;
-#pragma unroll
-  for (int v = 0; v < NV; ++v)
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      const int idx = base + (v * kThreads + threadIdx.x) * VEC + e;
-      if (PAIR) dmax = fmaxf(dmax, d[v * VEC + e]);  // padding is -1e30
-      if (idx < a.V && t[v * VEC + e] > m) {
-        m = t[v * VEC + e];
-        mi = idx;
-        md = PAIR ? d[v * VEC + e] : 0.f;
-      }
-    }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float m2 = __shfl_xor_sync(kFull, m, o);
-    const int i2 = __shfl_xor_sync(kFull, mi, o);
-    const float d2 = __shfl_xor_sync(kFull, md, o);
-    arg_better(m, mi, md, m2, i2, d2);
-    if (PAIR) dmax = fmaxf(dmax, __shfl_xor_sync(kFull, dmax, o));
-  }
-  __shared__ float s_m[kThreads / 32], s_d[kThreads / 32], s_dmax[kThreads / 32];
-  __shared__ int s_i[kThreads / 32];
-  __shared__ double s_sum[3][kThreads / 32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) {
-    s_m[warp] = m;
-    s_i[warp] = mi;
-    s_d[warp] = md;
-    s_dmax[warp] = dmax;
-  }
-  __syncthreads();
-  float M = s_m[0], dstar = s_d[0], Dmax = s_dmax[0];
-  int Mi = s_i[0];
-#pragma unroll
-  for (int w = 1; w < kThreads / 32; ++w) {
-    arg_better(M, Mi, dstar, s_m[w], s_i[w], s_d[w]);
-    Dmax = fmaxf(Dmax, s_dmax[w]);
-  }
-
-  const float ML2 = M * kLog2e;
-  // Reference C = t - d at the chunk argmax (exact for bf16 inputs), lowered if
-  // needed so that e_v exp(-w_v) = exp(d_v - (M - C)) <= e^64 for every v in the
-  // chunk: no fp32 overflow even for draft logits far above the reference
-  // (disjoint supports). Stored as used.
-  const float Cf = PAIR ? fminf(M - dstar, (M - Dmax) + 64.f) : 0.f;
-  float S = 0.f, A = 0.f, D = 0.f;
-#pragma unroll
-  for (int q = 0; q < E; ++q) {
-    const float xt = fmaf(t[q], kLog2e, -ML2);
-    const float e = fast_exp2(xt);
-    S += e;
-    if (PAIR) {
-      const float w = diff_ref<T>(t[q], d[q], Cf);
-      A = fmaf(e, w, A);
-      D += e_g(e, xt, w);
-    }
-  }
-  double Sd = warp_sum((double)S);
-  double Ad = PAIR ? warp_sum((double)A) : 0.0;
-  double Dd = PAIR ? warp_sum((double)D) : 0.0;
-  if (lane == 0) {
-    s_sum[0][warp] = Sd;
-    s_sum[1][warp] = Ad;
-    s_sum[2][warp] = Dd;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s0 = 0, s1 = 0, s2 = 0;
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) {
-      s0 += s_sum[0][w];
-      s1 += s_sum[1][w];
-      s2 += s_sum[2][w];
-    }
-    ChunkPartial p;
-    p.S = s0;
-    p.A = s1;
-    p.D = s2;
-    p.M = M;
-    p.C = Cf;
-    p.idx = Mi;
-    p.flags = (PAIR && Cf < M - dstar) ? DSDE_FLAG_OVERFLOW : 0;
-    p.maxd = Dmax;
-    p.pad = 0;
-    a.part[prow * a.nchunks + c] = p;
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -721,6 +548,7 @@ struct FinArgs {
   float* kld;
   uint8_t* flags;
   SeqRec* rec;
+  int* counter;
   int32_t* err;
 };
 
@@ -803,7 +631,10 @@ __global__ void __launch_bounds__(128) k_finalize(FinArgs a) {
       a.flags[slot0 + lane] = f;
     }
   }
-  if (lane == 0) a.acc_len[i] = aa;
+  if (lane == 0) {
+    a.acc_len[i] = aa;
+    a.counter[i] = 0;
+  }
   if (lane == aa) {
     SeqRec r;
     r.slot = (int)(slot0 + aa);
@@ -838,40 +669,9 @@ struct SampArgs {
   double* mass;
   int32_t* emitted;
   uint8_t* flags;
+  float* cmax;
+  int* counter;
 };
-
-// Weights of the final draw for the E contiguous elements [c*CH + tid*E, +E):
-//   residual: rho_v = e_v * max(0, -expm1(-z_v)), z_v = (t_v - d_v) - C + lam
-//             (q_v / p_v = exp(-z_v)); z_v is formed in fp64 so the offset in
-//             t - d cancels exactly;
-//   bonus / p-fallback: e_v = exp(t_v - M).
-// Both are p_v * S (resp. max(0, p_v - q_v) * S), a common positive scale.
-template <typename T>
-__device__ __forceinline__ void draw_weights(const SampArgs& a, const SeqRec& r, float M, bool resid,
-                                             int c, float (&w)[Traits<T>::VEC * Traits<T>::NV]) {
-  constexpr int E = Traits<T>::VEC * Traits<T>::NV;
-  const int e0 = c * chunk_elems<T>() + threadIdx.x * E;
-  const T* tp = reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t;
-  const T* dp = reinterpret_cast<const T*>(a.dl) + (resid ? r.drow : 0) * a.ld_d;
-  const float ML2 = M * kLog2e;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int v = e0 + e;
-    float wt = 0.f;
-    if (v < a.V) {
-      const float tv = load_logit<T>(tp + v);
-      const float ev = fast_exp2(fmaf(tv, kLog2e, -ML2));
-      if (resid) {
-        const float dv = load_logit<T>(dp + v);
-        const float z = (float)((((double)tv - (double)dv) - r.C) + r.lam);
-        wt = z > 0.f ? ev * -expm1f(-z) : 0.f;
-      } else {
-        wt = ev;
-      }
-    }
-    w[e] = wt;
-  }
-}
 
 __device__ __forceinline__ double block_sum(double v, double* s_w) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -885,135 +685,211 @@ __device__ __forceinline__ double block_sum(double v, double* s_w) {
   return t;
 }
 
-// Reference max of the bonus row (merge of its (M, S) partials).
-__device__ __forceinline__ float bonus_max(const SampArgs& a, int i) {
-  const ChunkPartial* P = a.part + (long long)(a.total + i) * a.nchunks;
-  float M = P[0].M;
-  for (int c = 1; c < a.nchunks; ++c) M = fmaxf(M, P[c].M);
-  return M;
+// ---------------------------------------------------------------------------
+// a4, production path: one launch per step for every draw. CTA (i, c) forms the
+// draw weights of chunk c of sequence i (contiguous E elements per thread,
+// 128-bit loads) and their mass; the last CTA of sequence i to finish
+// (atomic counter, threadfence) selects the token: fp64 prefix over chunk
+// masses, then a block scan inside the crossing chunk, re-read from L2.
+//   residual: rho_v = e_v max(0, -expm1(-z_v)), z_v = w_v + lam, w_v exact
+//             ((t - d) - C as in the stream), lam added as hi + lo floats;
+//   bonus:    e_v = exp(t_v - M_c) about the chunk max M_c, rescaled by
+//             exp(M_c - M) in fp64 (single pass over the row, no stats pass).
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void load_contig(const T* row, int V, int e0, float (&x)[Traits<T>::VEC * Traits<T>::NV]) {
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV;
+  if (e0 + VEC * NV <= V) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(row + e0 + v * VEC);
+      unpack16<T>(raw, x + v * VEC);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC * NV; ++e) x[e] = (e0 + e < V) ? load_logit<T>(row + e0 + e) : -INFINITY;
+  }
 }
 
-// a4 (1/2): mass of the draw weights per (sequence, chunk).
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_sample_mass(SampArgs a) {
+__device__ __forceinline__ void draw_weights2(const SampArgs& a, const SeqRec& r, bool resid, float M,
+                                              int c, float (&w)[Traits<T>::VEC * Traits<T>::NV]) {
+  constexpr int E = Traits<T>::VEC * Traits<T>::NV;
+  const int e0 = c * chunk_elems<T>() + threadIdx.x * E;
+  float t[E];
+  load_contig<T>(reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t, a.V, e0, t);
+  const float ML2 = M * kLog2e;
+  if (resid) {
+    float d[E];
+    load_contig<T>(reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d, a.V, e0, d);
+    const float Cf = (float)r.C;  // exact: r.C is an fp32 value
+    const float lhi = (float)r.lam, llo = (float)(r.lam - (double)lhi);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const float ev = fast_exp2(fmaf(t[e], kLog2e, -ML2));  // 0 for padding (-inf)
+      const float z = (diff_ref<T>(t[e], d[e], Cf) + lhi) + llo;
+      w[e] = (z > 0.f && e0 + e < a.V) ? ev * -expm1f(-z) : 0.f;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) w[e] = fast_exp2(fmaf(t[e], kLog2e, -ML2));
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_sample(SampArgs a) {
   constexpr int E = Traits<T>::VEC * Traits<T>::NV;
   const int i = blockIdx.x / a.nchunks, c = blockIdx.x % a.nchunks;
   const SeqRec r = a.rec[i];
   if (r.mode != MODE_RESIDUAL && r.mode != MODE_BONUS) return;
   const bool resid = r.mode == MODE_RESIDUAL;
-  const float M = resid ? r.M : bonus_max(a, i);
-  float w[E];
-  draw_weights<T>(a, r, M, resid, c, w);
-  float s = 0.f;
-#pragma unroll
-  for (int e = 0; e < E; ++e) s += w[e];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __shared__ double s_w[kThreads / 32];
-  const double tot = block_sum((double)s, s_w);
-  if (threadIdx.x == 0) a.mass[(long long)i * a.nchunks + c] = tot;
-}
-
-// a4 (2/2): inverse CDF in ascending token id (D7): the smallest v with
-// C_v > u R. C_v = (fp64 prefix of chunk masses) + (fp64 block scan of
-// per-thread fp32 sums) + (per-thread fp32 running sum).
-template <typename T>
-__global__ void __launch_bounds__(kThreads) k_sample_select(SampArgs a) {
-  constexpr int E = Traits<T>::VEC * Traits<T>::NV;
-  const int i = blockIdx.x;
-  const SeqRec r = a.rec[i];
-  if (r.mode != MODE_RESIDUAL && r.mode != MODE_BONUS) return;
-  bool resid = r.mode == MODE_RESIDUAL;
-  float M = resid ? r.M : bonus_max(a, i);
-  __shared__ double s_w[kThreads / 32];
+  __shared__ float s_f[kThreads / 32];
   __shared__ double s_scan[kThreads];
-  __shared__ int s_cand;
-  __shared__ int s_chunk;
-  __shared__ double s_base, s_R, s_target;
-  uint8_t fl = 0;
-  const double* mass = a.mass + (long long)i * a.nchunks;
-  if (threadIdx.x == 0) {
-    double R = 0.0;
-    for (int c = 0; c < a.nchunks; ++c) R += mass[c];
-    s_R = R;
+  __shared__ int s_last, s_cand, s_cs;
+  __shared__ double s_base, s_target, s_R, s_scale;
+  __shared__ float s_Mcs;
+
+  // chunk max of t (bonus reference) — the residual reference is the row's M
+  auto chunk_max = [&](int cc) -> float {
+    const int e0 = cc * chunk_elems<T>() + tid * E;
+    float t[E];
+    load_contig<T>(reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t, a.V, e0, t);
+    float m = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < E; ++e) m = fmaxf(m, t[e]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+    __syncthreads();
+    if (lane == 0) s_f[warp] = m;
+    __syncthreads();
+    float M = s_f[0];
+#pragma unroll
+    for (int w = 1; w < kThreads / 32; ++w) M = fmaxf(M, s_f[w]);
+    return M;
+  };
+
+  const float Mc = resid ? r.M : chunk_max(c);
+  float w[E];
+  draw_weights2<T>(a, r, resid, Mc, c, w);
+  float sum = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) sum += w[e];
+  const double tot = block_sum((double)sum, s_w);
+  if (tid == 0) {
+    a.mass[(long long)i * a.nchunks + c] = tot;
+    a.cmax[(long long)i * a.nchunks + c] = Mc;
+    __threadfence();
+    const int done = atomicAdd(a.counter + i, 1);
+    s_last = done == a.nchunks - 1;
   }
   __syncthreads();
-  if (!(s_R > 0.0)) {
-    // D7 fallback: residual mass 0 -> draw from p of the same target row.
-    resid = false;
-    fl |= DSDE_FLAG_FALLBACK;
-    M = r.M;
-    double cum = 0.0;
-    for (int c = 0; c < a.nchunks; ++c) {
-      float w[E];
-      draw_weights<T>(a, r, M, false, c, w);
-      float s = 0.f;
-#pragma unroll
-      for (int e = 0; e < E; ++e) s += w[e];
-      const double tot = block_sum((double)s, s_w);
-      if (threadIdx.x == 0) a.mass[(long long)i * a.nchunks + c] = tot;
-      cum += tot;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_R = cum;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const double R = s_R, target = r.u * R;
-    double cum = 0.0;
-    int cs = a.nchunks - 1;
-    double base = 0.0;
-    for (int c = 0; c < a.nchunks; ++c) {
-      const double m = mass[c];
+  if (!s_last) return;
+  __threadfence();
+
+  // ---- last CTA of sequence i: select the token (D7) ----
+  uint8_t fl = 0;
+  if (tid == 0) {
+    const double* mass = a.mass + (long long)i * a.nchunks;
+    const float* cm = a.cmax + (long long)i * a.nchunks;
+    double Mg = -INFINITY;
+    if (!resid)
+      for (int cc = 0; cc < a.nchunks; ++cc) Mg = fmax(Mg, (double)__ldcg(cm + cc));
+    double R = 0.0;
+    for (int cc = 0; cc < a.nchunks; ++cc)
+      R += (resid ? 1.0 : exp((double)__ldcg(cm + cc) - Mg)) * __ldcg(mass + cc);
+    s_R = R;
+    const double target = r.u * R;
+    double cum = 0.0, base = 0.0;
+    int cs = -1;
+    for (int cc = 0; cc < a.nchunks; ++cc) {
+      const double sc = resid ? 1.0 : exp((double)__ldcg(cm + cc) - Mg);
+      const double m = sc * __ldcg(mass + cc);
+      if (m > 0.0) cs = cc;  // fallback: last chunk with mass
       if (cum + m > target) {
-        cs = c;
+        cs = cc;
         base = cum;
         break;
       }
       cum += m;
-      base = cum - m;  // if no crossing: the last chunk, base before it
+      base = cum - m;
     }
-    s_chunk = cs;
+    s_cs = cs;
     s_base = base;
     s_target = target;
+    s_scale = (cs >= 0 && !resid) ? exp((double)__ldcg(cm + cs) - Mg) : 1.0;
+    s_Mcs = cs >= 0 ? __ldcg(cm + cs) : 0.f;
     s_cand = 0x7fffffff;
   }
   __syncthreads();
-  const int c = s_chunk;
-  float w[E];
-  draw_weights<T>(a, r, M, resid, c, w);
-  float s = 0.f;
+  const int cs = s_cs;
+  if (cs < 0) {
+    // D7 fallback: residual mass 0 (p <= q everywhere in fp32, only reachable
+    // through rounding since a rejection needs p(x) < q(x)): draw from p of the
+    // same target row, the slow way (one pass for the total, one for the scan).
+    __shared__ int s_tok;
+    double R = 0.0;
+    for (int cc = 0; cc < a.nchunks; ++cc) {
+      draw_weights2<T>(a, r, false, r.M, cc, w);
+      float s2 = 0.f;
 #pragma unroll
-  for (int e = 0; e < E; ++e) s += w[e];
-  // exclusive block scan of the per-thread sums (fp64, Hillis-Steele in smem)
-  s_scan[threadIdx.x] = (double)s;
+      for (int e = 0; e < E; ++e) s2 += w[e];
+      R += block_sum((double)s2, s_w);
+    }
+    if (tid == 0) {
+      const double target = r.u * R;
+      double cum = 0.0;
+      int tok = 0;
+      for (int v = 0; v < a.V; ++v) {
+        const float tv = load_logit<T>(reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t + v);
+        const float wv = fast_exp2(fmaf(tv, kLog2e, -r.M * kLog2e));
+        cum += (double)wv;
+        if (wv > 0.f && cum > target) {
+          tok = v;
+          break;
+        }
+        if (wv > 0.f) tok = v;
+      }
+      s_tok = tok;
+      a.emitted[r.slot] = tok;
+      if (a.flags) a.flags[r.slot] |= DSDE_FLAG_FALLBACK;
+    }
+    return;
+  }
+  if (cs != c) draw_weights2<T>(a, r, resid, resid ? r.M : s_Mcs, cs, w);
+  float ssum = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) ssum += w[e];
+  const double scale = s_scale;
+  s_scan[tid] = scale * (double)ssum;
   __syncthreads();
   for (int o = 1; o < kThreads; o <<= 1) {
-    const double add = threadIdx.x >= o ? s_scan[threadIdx.x - o] : 0.0;
+    const double add = tid >= o ? s_scan[tid - o] : 0.0;
     __syncthreads();
-    s_scan[threadIdx.x] += add;
+    s_scan[tid] += add;
     __syncthreads();
   }
-  const double pre = s_base + (threadIdx.x > 0 ? s_scan[threadIdx.x - 1] : 0.0);
+  const double pre = s_base + (tid > 0 ? s_scan[tid - 1] : 0.0);
   const double target = s_target;
-  const int e0 = c * chunk_elems<T>() + threadIdx.x * E;
+  const int e0 = cs * chunk_elems<T>() + tid * E;
   int cand = 0x7fffffff;
   float run = 0.f;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     run += w[e];
-    if (cand == 0x7fffffff && w[e] > 0.f && pre + (double)run > target) cand = e0 + e;
+    if (cand == 0x7fffffff && w[e] > 0.f && pre + scale * (double)run > target) cand = e0 + e;
   }
   if (cand != 0x7fffffff) atomicMin(&s_cand, cand);
   __syncthreads();
   int tok = s_cand;
-  if (tok == 0x7fffffff) {
-    // rounding corner (u R within an ulp of the chunk total): the last token of
-    // the chunk with positive weight; flagged as a near tie.
-    __syncthreads();
+  if (tok == 0x7fffffff) {  // rounding corner: last positive-weight token of the chunk
     int last = -1;
 #pragma unroll
     for (int e = 0; e < E; ++e)
       if (w[e] > 0.f) last = e0 + e;
-    if (threadIdx.x == 0) s_cand = -1;
+    __syncthreads();
+    if (tid == 0) s_cand = -1;
     __syncthreads();
     if (last >= 0) atomicMax(&s_cand, last);
     __syncthreads();
@@ -1021,24 +897,20 @@ __global__ void __launch_bounds__(kThreads) k_sample_select(SampArgs a) {
     fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
   }
   if (tok >= e0 && tok < e0 + E) {
-    // owner: C_{v-1}/R and C_v/R for the tie flag
     float run2 = 0.f;
     double lo = pre, hi = pre;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const double before = pre + (double)run2;
+      const double before = pre + scale * (double)run2;
       run2 += w[e];
       if (e0 + e == tok) {
         lo = before;
-        hi = pre + (double)run2;
+        hi = pre + scale * (double)run2;
       }
     }
     const double R = s_R;
     if (fabs(r.u - lo / R) < 1e-6 || fabs(r.u - hi / R) < 1e-6) fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
     a.emitted[r.slot] = tok;
-    if (a.flags) a.flags[r.slot] |= fl;
-  } else if (tok < 0 && threadIdx.x == 0) {
-    a.emitted[r.slot] = 0;  // unreachable: R > 0 implies a positive weight exists
     if (a.flags) a.flags[r.slot] |= fl;
   }
 }
@@ -1049,7 +921,6 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
                           const uint64_t* seeds, int32_t* acc_len, int32_t* emitted, float* kld,
                           uint8_t* flags, const VerifyWs& ws, int32_t* err, cudaStream_t s) {
   const int nc = (V + chunk_elems<T>() - 1) / chunk_elems<T>();
-  StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, nc, total, ws.part, ws.rec};
   if (total > 0) {
     static bool attr_set = false;
     constexpr int smem = stream_tma_smem<T>();
@@ -1066,12 +937,11 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
     k_stream_tma<T><<<grid, kThreads, smem, s>>>(ta);
   }
   FinArgs fa{B, V, total, nc, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, ws.part,
-             acc_len, emitted, kld, flags, ws.rec, err};
+             acc_len, emitted, kld, flags, ws.rec, ws.counter, err};
   k_finalize<T><<<(B + 3) / 4, 128, 0, s>>>(fa);
-  k_stream<T, false><<<(unsigned)((long long)B * nc), kThreads, 0, s>>>(sa);
-  SampArgs pa{B, V, nc, total, tl, ld_t, dl, ld_d, ws.part, ws.rec, ws.mass, emitted, flags};
-  k_sample_mass<T><<<(unsigned)((long long)B * nc), kThreads, 0, s>>>(pa);
-  k_sample_select<T><<<B, kThreads, 0, s>>>(pa);
+  SampArgs pa{B, V, nc, total, tl, ld_t, dl, ld_d, ws.part, ws.rec, ws.mass, emitted, flags,
+              ws.cmax, ws.counter};
+  k_sample<T><<<(unsigned)((long long)B * nc), kThreads, 0, s>>>(pa);
   return cudaGetLastError();
 }
 
