@@ -25,6 +25,8 @@
 
 #include <algorithm>
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "state.cuh"
 
@@ -478,6 +480,337 @@ __global__ void __launch_bounds__(kThreads, 2) k_stream_tma(StreamTmaArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// a1, warp-specialised stream (the launched path). Per CTA: 1 producer warp +
+// 8 consumer warps, 2 CTAs per SM, a 3-stage ring of 32 KB stages filled by
+// 1-D TMA bulk copies. No CTA-wide barrier in the loop: every consumer warp
+// owns 1/8 of each chunk, finds its own reference (max / smallest-index argmax
+// of t, max of d) with shuffles, accumulates S, A, D about it and posts a warp
+// partial; mbarriers hand stages back to the producer, which refills them and
+// merges the 8 warp partials of the chunk in fp64 (same re-referencing as
+// merge_row) into the chunk partial.
+// ---------------------------------------------------------------------------
+constexpr int kCWarps = 8;
+constexpr int kWsThreads = 32 * (kCWarps + 1);
+constexpr int kWsStages = 3;
+
+struct WarpPartial {  // 32 bytes
+  float S, A, D;      // about (M, C) of the warp slice
+  float M, C, dstar, maxd;
+  int idx;
+};
+
+template <typename T>
+__host__ __device__ constexpr int stream_ws_smem() {
+  return kWsStages * 2 * stage_row_bytes<T>() + kWsStages * 2 * kCWarps * (int)sizeof(WarpPartial) +
+         3 * kWsStages * 8;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ void issue_item(const StreamTmaArgs& a, long long q, uint8_t* dst,
+                                           uint64_t* bar) {
+  constexpr int CH = chunk_elems<T>(), ROWB = stage_row_bytes<T>();
+  const long long r = q / a.nchunks;
+  const int c = (int)(q - r * a.nchunks);
+  int lo = 0, hi = a.B - 1;  // sequence of draft row r
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(a.cu_sl + mid) <= r) lo = mid; else hi = mid - 1;
+  }
+  const int c0 = c * CH;
+  const int n_el = min(CH, a.V - c0);
+  const uint32_t bytes = (uint32_t)(n_el * (int)sizeof(T)) & ~15u;
+  if (bytes) {
+    mbar_arrive_expect_tx(bar, 2 * bytes);
+    bulk_g2s(dst, reinterpret_cast<const T*>(a.tl) + (r + lo) * a.ld_t + c0, bytes, bar);
+    bulk_g2s(dst + ROWB, reinterpret_cast<const T*>(a.dl) + r * a.ld_d + c0, bytes, bar);
+  } else {
+    mbar_arrive(bar);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, E = VEC * NV, CH = chunk_elems<T>();
+  constexpr int ROWB = stage_row_bytes<T>();
+  constexpr int SL = CH / kCWarps;  // elements of a chunk owned by one consumer warp
+  extern __shared__ __align__(128) uint8_t smem[];
+  WarpPartial* slots = reinterpret_cast<WarpPartial*>(smem + kWsStages * 2 * ROWB);
+  uint64_t* full = reinterpret_cast<uint64_t*>(slots + kWsStages * 2 * kCWarps);
+  uint64_t* consumed = full + kWsStages;
+  uint64_t* ready = consumed + kWsStages;
+  const long long n_items = (long long)a.total * a.nchunks;
+  const int G = gridDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWsStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&consumed[s], kCWarps);
+      mbar_init(&ready[s], kCWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kCWarps) {
+    // ---------------- producer / merger warp ----------------
+    if (lane == 0)
+      for (int s = 0; s < kWsStages; ++s) {
+        const long long q = blockIdx.x + (long long)s * G;
+        if (q < n_items) issue_item<T>(a, q, smem + s * 2 * ROWB, &full[s]);
+      }
+    int j = 0;
+    for (long long q = blockIdx.x; q < n_items; q += G, ++j) {
+      const int s = j % kWsStages;
+      const uint32_t round = (uint32_t)(j / kWsStages);
+      mbar_wait(&consumed[s], round & 1u);
+      const long long qn = q + (long long)kWsStages * G;
+      if (lane == 0 && qn < n_items) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_item<T>(a, qn, smem + s * 2 * ROWB, &full[s]);
+      }
+      mbar_wait(&ready[s], round & 1u);
+      const WarpPartial* wp = slots + (s * 2 + (round & 1u)) * kCWarps;
+      // chunk reference: the warp with the largest M (smallest idx on ties)
+      float Mr = -INFINITY, dr = 0.f, mx = -INFINITY;
+      int ir = 0x7fffffff, flags = 0;
+#pragma unroll
+      for (int w = 0; w < kCWarps; ++w) {
+        arg_better(Mr, ir, dr, wp[w].M, wp[w].idx, wp[w].dstar);
+        mx = fmaxf(mx, wp[w].maxd);
+        flags |= (wp[w].C < wp[w].M - wp[w].dstar) ? DSDE_FLAG_OVERFLOW : 0;
+      }
+      const float Cc = fminf(Mr - dr, (Mr - mx) + 64.f);
+      if (Cc < Mr - dr) flags |= DSDE_FLAG_OVERFLOW;
+      double S = 0.0, A = 0.0, D = 0.0;
+      if (lane < kCWarps) {
+        const WarpPartial p = wp[lane];
+        const double ls = (double)p.M - (double)Mr;
+        const double sc = exp(ls);
+        const double dl = (double)p.C - (double)Cc;
+        double sem, sg, E1;
+        if (fabs(dl) < 1.0) {
+          const double em = expm1(-dl);
+          sem = sc * em;
+          sg = sc * (em + dl);
+          E1 = sc + sem;
+        } else {
+          E1 = exp(ls - dl);
+          sem = E1 - sc;
+          sg = sem + sc * dl;
+        }
+        S = sc * (double)p.S;
+        A = sc * (double)p.A + sc * (double)p.S * dl;
+        D = E1 * (double)p.D - (double)p.A * sem + (double)p.S * sg;
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        S += __shfl_xor_sync(kFull, S, o);
+        A += __shfl_xor_sync(kFull, A, o);
+        D += __shfl_xor_sync(kFull, D, o);
+      }
+      if (lane == 0) {
+        ChunkPartial cp;
+        cp.S = S;
+        cp.A = A;
+        cp.D = D;
+        cp.M = Mr;
+        cp.C = Cc;
+        cp.idx = ir;
+        cp.flags = flags;
+        cp.maxd = mx;
+        cp.pad = 0;
+        a.part[q] = cp;
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const float2 L2 = make_float2(kLog2e, kLog2e), nL2 = make_float2(-kLog2e, -kLog2e);
+  const float2 K7 = make_float2(-2.812654656736413e-06f, -2.812654656736413e-06f);
+  const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
+  const float2 K5 = make_float2(-1.9836986029986292e-04f, -1.9836986029986292e-04f);
+  const float2 K4 = make_float2(1.3885394437238574e-03f, 1.3885394437238574e-03f);
+  const float2 K3 = make_float2(-8.33334494382143e-03f, -8.33334494382143e-03f);
+  const float2 K2 = make_float2(4.166673496365547e-02f, 4.166673496365547e-02f);
+  const float2 K1 = make_float2(-1.666666716337204e-01f, -1.666666716337204e-01f);
+  const float2 K0 = make_float2(0.5f, 0.5f);
+  int j = 0;
+  for (long long q = blockIdx.x; q < n_items; q += G, ++j) {
+    const int s = j % kWsStages;
+    const uint32_t round = (uint32_t)(j / kWsStages);
+    const long long r = q / a.nchunks;
+    const int c = (int)(q - r * a.nchunks);
+    const int c0 = c * CH;
+    const int n_el = min(CH, a.V - c0);
+    mbar_wait(&full[s], round & 1u);
+    const T* st = reinterpret_cast<const T*>(smem + s * 2 * ROWB);
+    const T* sd = reinterpret_cast<const T*>(smem + s * 2 * ROWB + ROWB);
+    float t[E], d[E];
+    float mt = -INFINITY, md = -INFINITY;
+    if (n_el == CH) {
+      uint4 rt[NV], rd[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int e0 = warp * SL + (v * 32 + lane) * VEC;
+        rt[v] = *reinterpret_cast<const uint4*>(st + e0);
+        rd[v] = *reinterpret_cast<const uint4*>(sd + e0);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&consumed[s]);
+      if constexpr (sizeof(T) == 2) {
+        __nv_bfloat162 bt = *reinterpret_cast<const __nv_bfloat162*>(&rt[0].x);
+        __nv_bfloat162 bd = *reinterpret_cast<const __nv_bfloat162*>(&rd[0].x);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const uint32_t wt[4] = {rt[v].x, rt[v].y, rt[v].z, rt[v].w};
+          const uint32_t wd[4] = {rd[v].x, rd[v].y, rd[v].z, rd[v].w};
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            bt = __hmax2(bt, *reinterpret_cast<const __nv_bfloat162*>(&wt[h]));
+            bd = __hmax2(bd, *reinterpret_cast<const __nv_bfloat162*>(&wd[h]));
+          }
+        }
+        mt = fmaxf(__low2float(bt), __high2float(bt));
+        md = fmaxf(__low2float(bd), __high2float(bd));
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        unpack16<T>(rt[v], t + v * VEC);
+        unpack16<T>(rd[v], d + v * VEC);
+      }
+      if constexpr (sizeof(T) != 2) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          mt = fmaxf(mt, t[e]);
+          md = fmaxf(md, d[e]);
+        }
+      }
+    } else {
+      // last chunk of a row: bulk-copied part from shared memory, an unaligned
+      // tail (V * sizeof(T) not a multiple of 16) from global, padding after V
+      const int bulk_el = (int)(((uint32_t)(n_el * (int)sizeof(T)) & ~15u) / sizeof(T));
+      long long trow = 0;
+      if (bulk_el < n_el) {
+        int lo = 0, hi = a.B - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (__ldg(a.cu_sl + mid) <= r) lo = mid; else hi = mid - 1;
+        }
+        trow = r + lo;
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int e0 = warp * SL + (v * 32 + lane) * VEC;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const int idx = e0 + e;
+          float tv = -1e30f, dv = -1e30f;
+          if (idx < bulk_el) {
+            tv = load_logit_smem(st + idx);
+            dv = load_logit_smem(sd + idx);
+          } else if (idx < n_el) {
+            tv = load_logit<T>(reinterpret_cast<const T*>(a.tl) + trow * a.ld_t + c0 + idx);
+            dv = load_logit<T>(reinterpret_cast<const T*>(a.dl) + r * a.ld_d + c0 + idx);
+          }
+          t[v * VEC + e] = tv;
+          d[v * VEC + e] = dv;
+          mt = fmaxf(mt, tv);
+          md = fmaxf(md, dv);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&consumed[s]);
+    }
+    // warp reference: max of t, its smallest element index, d there; max of d
+    const float M = warp_max(mt);
+    const float Dmax = warp_max(md);
+    int fv = -1, owner = 0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      bool hit = false;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) hit |= (t[v * VEC + e] == M);
+      const unsigned b = __ballot_sync(kFull, hit);
+      if (fv < 0 && b) {
+        fv = v;
+        owner = __ffs(b) - 1;
+      }
+    }
+    int Mi = 0x7fffffff;
+    float dstar = 0.f;
+    if (fv >= 0) {
+      int my_i = 0x7fffffff;
+      float my_d = 0.f;
+      if (lane == owner) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int e = VEC - 1; e >= 0; --e)
+            if (v == fv && t[v * VEC + e] == M) {
+              my_i = c0 + warp * SL + (v * 32 + lane) * VEC + e;
+              my_d = d[v * VEC + e];
+            }
+      }
+      Mi = __shfl_sync(kFull, my_i, owner);
+      dstar = __shfl_sync(kFull, my_d, owner);
+    }
+    const float Cw = fminf(M - dstar, (M - Dmax) + 64.f);
+    const float ML2 = M * kLog2e;
+    const float2 nML2 = make_float2(-ML2, -ML2);
+    float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
+#pragma unroll
+    for (int h = 0; h < E; h += 2) {
+      const float2 tt = make_float2(t[h], t[h + 1]), dd = make_float2(d[h], d[h + 1]);
+      const float2 xt = __ffma2_rn(tt, L2, nML2);
+      const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
+      const float2 w = diff2<T>(tt, dd, Cw);
+      S2 = __fadd2_rn(S2, e);
+      A2 = __ffma2_rn(e, w, A2);
+      float2 p = __ffma2_rn(K7, w, K6);
+      p = __ffma2_rn(p, w, K5);
+      p = __ffma2_rn(p, w, K4);
+      p = __ffma2_rn(p, w, K3);
+      p = __ffma2_rn(p, w, K2);
+      p = __ffma2_rn(p, w, K1);
+      p = __ffma2_rn(p, w, K0);
+      const float2 sm = __fmul2_rn(__fmul2_rn(e, __fmul2_rn(w, w)), p);
+      const float2 arg = __ffma2_rn(w, nL2, xt);
+      const float2 f = make_float2(fast_exp2(arg.x), fast_exp2(arg.y));
+      const float2 bg = __ffma2_rn(e, w, __fadd2_rn(f, make_float2(-e.x, -e.y)));
+      const float2 term = make_float2(fabsf(w.x) < 1.f ? sm.x : bg.x, fabsf(w.y) < 1.f ? sm.y : bg.y);
+      D2 = __fadd2_rn(D2, term);
+    }
+    float S = S2.x + S2.y, A = A2.x + A2.y, D = D2.x + D2.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      S += __shfl_xor_sync(kFull, S, o);
+      A += __shfl_xor_sync(kFull, A, o);
+      D += __shfl_xor_sync(kFull, D, o);
+    }
+    if (lane == 0) {
+      WarpPartial p;
+      p.S = S;
+      p.A = A;
+      p.D = D;
+      p.M = M;
+      p.C = Cw;
+      p.dstar = dstar;
+      p.maxd = Dmax;
+      p.idx = Mi;
+      slots[(s * 2 + (round & 1u)) * kCWarps + warp] = p;
+      mbar_arrive(&ready[s]);
+    }
+  }
+}
+
 // Merged statistics of one row about the row argmax.
 struct RowStats {
   double M, C, S, A, D;
@@ -923,9 +1256,9 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   const int nc = (V + chunk_elems<T>() - 1) / chunk_elems<T>();
   if (total > 0) {
     static bool attr_set = false;
-    constexpr int smem = stream_tma_smem<T>();
+    constexpr int smem = stream_ws_smem<T>();
     if (!attr_set) {
-      cudaFuncSetAttribute(k_stream_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_stream_ws<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr_set = true;
     }
     int dev = 0, sms = 148;
@@ -934,7 +1267,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
     const long long items = (long long)total * nc;
     const int grid = (int)std::min<long long>(items, 2LL * sms);
     StreamTmaArgs ta{tl, ld_t, dl, ld_d, cu_sl, B, V, nc, total, ws.part};
-    k_stream_tma<T><<<grid, kThreads, smem, s>>>(ta);
+    k_stream_ws<T><<<grid, kWsThreads, smem, s>>>(ta);
   }
   FinArgs fa{B, V, total, nc, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, ws.part,
              acc_len, emitted, kld, flags, ws.rec, ws.counter, err};

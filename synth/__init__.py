@@ -72,8 +72,9 @@ def slot_seeds(global_seed: int, step: int, cu_sl: np.ndarray) -> np.ndarray:
 class Profile:
     """Acceptance profile of one sequence.
 
-    sigma_n values were chosen with tools/calibrate_profiles.py, which runs
-    the oracle on sampled rows; alpha is the per-position acceptance target
+    sigma_n values were chosen with tools/calibrate_profiles.py (bisection on
+    the mean of sum_v min(p_v, q_v) over sampled rows of this generator at
+    V = 128256, stable phase); alpha is the per-position acceptance target
     derived from the paper's Table I block efficiencies and the
     low-acceptance regime of P:427 (k_opt = 2)."""
     name: str
@@ -85,11 +86,11 @@ class Profile:
 
 PROFILES = {
     # code: BE 5.87 @ SL=8 -> alpha ~ 0.888
-    "code": Profile("code", 0.89, 6.0, 8.0, 0.30),
+    "code": Profile("code", 0.89, 6.0, 8.0, 0.43),
     # dialogue: BE 4.81 @ SL=8 -> alpha ~ 0.832; flatter rows mixed in
-    "dialogue": Profile("dialogue", 0.83, 4.0, 8.0, 0.42),
+    "dialogue": Profile("dialogue", 0.83, 4.0, 8.0, 0.61),
     # low: Gemma-27B/2B regime, k_opt = 2 -> alpha ~ 0.5
-    "low": Profile("low", 0.50, 6.0, 8.0, 1.60),
+    "low": Profile("low", 0.50, 6.0, 8.0, 2.50),
 }
 
 
