@@ -506,6 +506,15 @@ __host__ __device__ constexpr int stream_ws_smem() {
          3 * kWsStages * 8;
 }
 
+// max that propagates NaN (a NaN logit must reach the non-finite check)
+__device__ __forceinline__ float max_nan(float a, float b) { return (b > a || b != b) ? b : a; }
+
+__device__ __forceinline__ float warp_max_nan(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max_nan(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
@@ -674,7 +683,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
           const uint32_t wd[4] = {rd[v].x, rd[v].y, rd[v].z, rd[v].w};
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
-            bt = __hmax2(bt, *reinterpret_cast<const __nv_bfloat162*>(&wt[h]));
+            bt = __hmax2_nan(bt, *reinterpret_cast<const __nv_bfloat162*>(&wt[h]));  // NaN propagates
             bd = __hmax2(bd, *reinterpret_cast<const __nv_bfloat162*>(&wd[h]));
           }
         }
@@ -689,7 +698,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
       if constexpr (sizeof(T) != 2) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          mt = fmaxf(mt, t[e]);
+          mt = max_nan(mt, t[e]);
           md = fmaxf(md, d[e]);
         }
       }
@@ -722,7 +731,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
           }
           t[v * VEC + e] = tv;
           d[v * VEC + e] = dv;
-          mt = fmaxf(mt, tv);
+          mt = max_nan(mt, tv);
           md = fmaxf(md, dv);
         }
       }
@@ -730,8 +739,21 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
       if (lane == 0) mbar_arrive(&consumed[s]);
     }
     // warp reference: max of t, its smallest element index, d there; max of d
-    const float M = warp_max(mt);
+    const float M = warp_max_nan(mt);
     const float Dmax = warp_max(md);
+    if (M <= -1e30f) {  // slice beyond V (padding only): an empty partial (NaN is not empty)
+      if (lane == 0) {
+        WarpPartial p;
+        p.S = p.A = p.D = 0.f;
+        p.M = -INFINITY;
+        p.C = p.dstar = 0.f;
+        p.maxd = -INFINITY;
+        p.idx = 0x7fffffff;
+        slots[(s * 2 + (round & 1u)) * kCWarps + warp] = p;
+        mbar_arrive(&ready[s]);
+      }
+      continue;
+    }
     int fv = -1, owner = 0;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
@@ -1019,15 +1041,18 @@ __device__ __forceinline__ double block_sum(double v, double* s_w) {
 }
 
 // ---------------------------------------------------------------------------
-// a4, production path: one launch per step for every draw. CTA (i, c) forms the
-// draw weights of chunk c of sequence i (contiguous E elements per thread,
-// 128-bit loads) and their mass; the last CTA of sequence i to finish
-// (atomic counter, threadfence) selects the token: fp64 prefix over chunk
-// masses, then a block scan inside the crossing chunk, re-read from L2.
-//   residual: rho_v = e_v max(0, -expm1(-z_v)), z_v = w_v + lam, w_v exact
-//             ((t - d) - C as in the stream), lam added as hi + lo floats;
-//   bonus:    e_v = exp(t_v - M_c) about the chunk max M_c, rescaled by
-//             exp(M_c - M) in fp64 (single pass over the row, no stats pass).
+// a4: one launch for every draw of the step. CTA (i, c) forms the draw weights
+// of chunk c of sequence i (E contiguous elements per thread, 128-bit loads)
+// and their mass; the last CTA of sequence i to finish (atomic counter +
+// threadfence) selects the token: fp64 prefix over the chunk masses, then a
+// shuffle-based block scan inside the crossing chunk (re-read from L2).
+//   residual: rho_v = e_v (1 - exp(-z_v)) for z_v > 0, else 0, with
+//             e_v = exp(t_v - M), z_v = w_v + lam, w_v = (t_v - d_v) - C exact,
+//             lam added as hi + lo floats; 1 - exp(-z) = z (1 - z h(-z)) for
+//             z < 1 (no cancellation), 1 - 2^(-z log2 e) otherwise;
+//   bonus:    p_v up to a scale: exp(t_v - m_t) about the thread's max m_t,
+//             threads rescaled by exp(m_t - M) in fp64 (one pass over the row).
+// Every per-thread value is recomputed bit-identically by the select pass.
 // ---------------------------------------------------------------------------
 template <typename T>
 __device__ __forceinline__ void load_contig(const T* row, int V, int e0, float (&x)[Traits<T>::VEC * Traits<T>::NV]) {
@@ -1044,29 +1069,58 @@ __device__ __forceinline__ void load_contig(const T* row, int V, int e0, float (
   }
 }
 
+// Draw weights of the thread's elements of chunk c; returns the thread's
+// reference (residual: the row reference M; bonus: the thread max of t).
 template <typename T>
-__device__ __forceinline__ void draw_weights2(const SampArgs& a, const SeqRec& r, bool resid, float M,
-                                              int c, float (&w)[Traits<T>::VEC * Traits<T>::NV]) {
+__device__ __forceinline__ float draw_weights(const SampArgs& a, const SeqRec& r, bool resid, int c,
+                                              float (&w)[Traits<T>::VEC * Traits<T>::NV]) {
   constexpr int E = Traits<T>::VEC * Traits<T>::NV;
   const int e0 = c * chunk_elems<T>() + threadIdx.x * E;
   float t[E];
   load_contig<T>(reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t, a.V, e0, t);
-  const float ML2 = M * kLog2e;
   if (resid) {
     float d[E];
     load_contig<T>(reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d, a.V, e0, d);
-    const float Cf = (float)r.C;  // exact: r.C is an fp32 value
+    const float Cf = (float)r.C;  // exact: r.C holds an fp32 value
     const float lhi = (float)r.lam, llo = (float)(r.lam - (double)lhi);
+    const float ML2 = r.M * kLog2e;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const float ev = fast_exp2(fmaf(t[e], kLog2e, -ML2));  // 0 for padding (-inf)
       const float z = (diff_ref<T>(t[e], d[e], Cf) + lhi) + llo;
-      w[e] = (z > 0.f && e0 + e < a.V) ? ev * -expm1f(-z) : 0.f;
+      float pz = -2.812654656736413e-06f;  // h(-z), h as in e_g
+      pz = fmaf(pz, z, 2.5358644052175805e-05f);
+      pz = fmaf(pz, z, -1.9836986029986292e-04f);
+      pz = fmaf(pz, z, 1.3885394437238574e-03f);
+      pz = fmaf(pz, z, -8.33334494382143e-03f);
+      pz = fmaf(pz, z, 4.166673496365547e-02f);
+      pz = fmaf(pz, z, -1.666666716337204e-01f);
+      pz = fmaf(pz, z, 0.5f);
+      const float one_m = z < 1.f ? z * fmaf(-z, pz, 1.f) : 1.f - fast_exp2(-z * kLog2e);
+      w[e] = (z > 0.f && e0 + e < a.V) ? ev * one_m : 0.f;
     }
-  } else {
-#pragma unroll
-    for (int e = 0; e < E; ++e) w[e] = fast_exp2(fmaf(t[e], kLog2e, -ML2));
+    return r.M;
   }
+  float m = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < E; ++e) m = fmaxf(m, t[e]);
+  const float mL2 = m * kLog2e;
+#pragma unroll
+  for (int e = 0; e < E; ++e) w[e] = m == -INFINITY ? 0.f : fast_exp2(fmaf(t[e], kLog2e, -mL2));
+  return m;
+}
+
+__device__ __forceinline__ float block_max(float v, float* s_f) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+  __syncthreads();
+  if (lane == 0) s_f[warp] = v;
+  __syncthreads();
+  float m = s_f[0];
+#pragma unroll
+  for (int w = 1; w < kThreads / 32; ++w) m = fmaxf(m, s_f[w]);
+  return m;
 }
 
 template <typename T>
@@ -1079,37 +1133,18 @@ __global__ void __launch_bounds__(kThreads) k_sample(SampArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __shared__ double s_w[kThreads / 32];
   __shared__ float s_f[kThreads / 32];
-  __shared__ double s_scan[kThreads];
   __shared__ int s_last, s_cand, s_cs;
   __shared__ double s_base, s_target, s_R, s_scale;
   __shared__ float s_Mcs;
 
-  // chunk max of t (bonus reference) — the residual reference is the row's M
-  auto chunk_max = [&](int cc) -> float {
-    const int e0 = cc * chunk_elems<T>() + tid * E;
-    float t[E];
-    load_contig<T>(reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t, a.V, e0, t);
-    float m = -INFINITY;
-#pragma unroll
-    for (int e = 0; e < E; ++e) m = fmaxf(m, t[e]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
-    __syncthreads();
-    if (lane == 0) s_f[warp] = m;
-    __syncthreads();
-    float M = s_f[0];
-#pragma unroll
-    for (int w = 1; w < kThreads / 32; ++w) M = fmaxf(M, s_f[w]);
-    return M;
-  };
-
-  const float Mc = resid ? r.M : chunk_max(c);
   float w[E];
-  draw_weights2<T>(a, r, resid, Mc, c, w);
+  float mt = draw_weights<T>(a, r, resid, c, w);
   float sum = 0.f;
 #pragma unroll
   for (int e = 0; e < E; ++e) sum += w[e];
-  const double tot = block_sum((double)sum, s_w);
+  const float Mc = resid ? r.M : block_max(mt, s_f);
+  const double ft = (resid || mt == -INFINITY) ? (resid ? 1.0 : 0.0) : exp((double)mt - (double)Mc);
+  const double tot = block_sum(ft * (double)sum, s_w);
   if (tid == 0) {
     a.mass[(long long)i * a.nchunks + c] = tot;
     a.cmax[(long long)i * a.nchunks + c] = Mc;
@@ -1139,14 +1174,12 @@ __global__ void __launch_bounds__(kThreads) k_sample(SampArgs a) {
     for (int cc = 0; cc < a.nchunks; ++cc) {
       const double sc = resid ? 1.0 : exp((double)__ldcg(cm + cc) - Mg);
       const double m = sc * __ldcg(mass + cc);
-      if (m > 0.0) cs = cc;  // fallback: last chunk with mass
-      if (cum + m > target) {
-        cs = cc;
+      if (m > 0.0) {
+        cs = cc;  // if no crossing is found: the last chunk with mass
         base = cum;
-        break;
       }
+      if (m > 0.0 && cum + m > target) break;
       cum += m;
-      base = cum - m;
     }
     s_cs = cs;
     s_base = base;
@@ -1158,17 +1191,18 @@ __global__ void __launch_bounds__(kThreads) k_sample(SampArgs a) {
   __syncthreads();
   const int cs = s_cs;
   if (cs < 0) {
-    // D7 fallback: residual mass 0 (p <= q everywhere in fp32, only reachable
-    // through rounding since a rejection needs p(x) < q(x)): draw from p of the
-    // same target row, the slow way (one pass for the total, one for the scan).
-    __shared__ int s_tok;
+    // D7 fallback: residual mass 0 (p <= q everywhere in fp32; a rejection needs
+    // p(x) < q(x), so only rounding reaches this): draw from p of the same
+    // target row, the slow way.
     double R = 0.0;
+    SeqRec rb = r;
+    rb.mode = MODE_BONUS;
     for (int cc = 0; cc < a.nchunks; ++cc) {
-      draw_weights2<T>(a, r, false, r.M, cc, w);
+      const float m2 = draw_weights<T>(a, rb, false, cc, w);
       float s2 = 0.f;
 #pragma unroll
       for (int e = 0; e < E; ++e) s2 += w[e];
-      R += block_sum((double)s2, s_w);
+      R += block_sum(m2 == -INFINITY ? 0.0 : exp((double)m2 - (double)r.M) * (double)s2, s_w);
     }
     if (tid == 0) {
       const double target = r.u * R;
@@ -1176,34 +1210,34 @@ __global__ void __launch_bounds__(kThreads) k_sample(SampArgs a) {
       int tok = 0;
       for (int v = 0; v < a.V; ++v) {
         const float tv = load_logit<T>(reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t + v);
-        const float wv = fast_exp2(fmaf(tv, kLog2e, -r.M * kLog2e));
-        cum += (double)wv;
-        if (wv > 0.f && cum > target) {
-          tok = v;
-          break;
-        }
-        if (wv > 0.f) tok = v;
+        const double wv = exp((double)tv - (double)r.M);
+        cum += wv;
+        if (wv > 0.0) tok = v;
+        if (wv > 0.0 && cum > target) break;
       }
-      s_tok = tok;
       a.emitted[r.slot] = tok;
       if (a.flags) a.flags[r.slot] |= DSDE_FLAG_FALLBACK;
     }
     return;
   }
-  if (cs != c) draw_weights2<T>(a, r, resid, resid ? r.M : s_Mcs, cs, w);
+  if (cs != c) mt = draw_weights<T>(a, r, resid, cs, w);
   float ssum = 0.f;
 #pragma unroll
   for (int e = 0; e < E; ++e) ssum += w[e];
-  const double scale = s_scale;
-  s_scan[tid] = scale * (double)ssum;
-  __syncthreads();
-  for (int o = 1; o < kThreads; o <<= 1) {
-    const double add = tid >= o ? s_scan[tid - o] : 0.0;
-    __syncthreads();
-    s_scan[tid] += add;
-    __syncthreads();
+  // thread factor: chunk scale x thread scale (bonus), 1 (residual)
+  const double f = resid ? 1.0 : (mt == -INFINITY ? 0.0 : s_scale * exp((double)mt - (double)s_Mcs));
+  // exclusive block scan of f * ssum (fp64): warp shuffles + warp totals
+  double x = f * (double)ssum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
   }
-  const double pre = s_base + (tid > 0 ? s_scan[tid - 1] : 0.0);
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  double wbase = 0.0;
+  for (int ww = 0; ww < warp; ++ww) wbase += s_w[ww];
+  const double pre = s_base + wbase + x - f * (double)ssum;
   const double target = s_target;
   const int e0 = cs * chunk_elems<T>() + tid * E;
   int cand = 0x7fffffff;
@@ -1211,7 +1245,7 @@ __global__ void __launch_bounds__(kThreads) k_sample(SampArgs a) {
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     run += w[e];
-    if (cand == 0x7fffffff && w[e] > 0.f && pre + scale * (double)run > target) cand = e0 + e;
+    if (cand == 0x7fffffff && w[e] > 0.f && pre + f * (double)run > target) cand = e0 + e;
   }
   if (cand != 0x7fffffff) atomicMin(&s_cand, cand);
   __syncthreads();
@@ -1234,11 +1268,11 @@ __global__ void __launch_bounds__(kThreads) k_sample(SampArgs a) {
     double lo = pre, hi = pre;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const double before = pre + scale * (double)run2;
+      const double before = pre + f * (double)run2;
       run2 += w[e];
       if (e0 + e == tok) {
         lo = before;
-        hi = pre + scale * (double)run2;
+        hi = pre + f * (double)run2;
       }
     }
     const double R = s_R;
