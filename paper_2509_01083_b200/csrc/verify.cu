@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_stream_tma(StreamTmaArgs a) {
 // merge_row) into the chunk partial.
 // ---------------------------------------------------------------------------
 constexpr int kCWarps = 8;
-constexpr int kWsThreads = 32 * (kCWarps + 1);
+constexpr int kWsThreads = 32 * (kCWarps + 2);  // + TMA producer warp + merger warp
 constexpr int kWsStages = 3;
 
 struct WarpPartial {  // 32 bytes
@@ -503,7 +503,7 @@ struct WarpPartial {  // 32 bytes
 template <typename T>
 __host__ __device__ constexpr int stream_ws_smem() {
   return kWsStages * 2 * stage_row_bytes<T>() + kWsStages * 2 * kCWarps * (int)sizeof(WarpPartial) +
-         3 * kWsStages * 8;
+         6 * kWsStages * 8;
 }
 
 // max that propagates NaN (a NaN logit must reach the non-finite check)
@@ -553,7 +553,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
   WarpPartial* slots = reinterpret_cast<WarpPartial*>(smem + kWsStages * 2 * ROWB);
   uint64_t* full = reinterpret_cast<uint64_t*>(slots + kWsStages * 2 * kCWarps);
   uint64_t* consumed = full + kWsStages;
-  uint64_t* ready = consumed + kWsStages;
+  uint64_t* ready = consumed + kWsStages;  // [stage][2]: 8 warp partials posted
+  uint64_t* freeb = ready + 2 * kWsStages;  // [stage][2]: merger done with the slot set
   const long long n_items = (long long)a.total * a.nchunks;
   const int G = gridDim.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -561,31 +562,43 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
     for (int s = 0; s < kWsStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&consumed[s], kCWarps);
-      mbar_init(&ready[s], kCWarps);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&ready[2 * s + b], kCWarps);
+        mbar_init(&freeb[2 * s + b], 1);
+      }
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
   if (warp == kCWarps) {
-    // ---------------- producer / merger warp ----------------
-    if (lane == 0)
+    // ---------------- TMA producer warp: refills a stage as soon as the 8
+    // consumer warps have lifted it into registers ----------------
+    if (lane == 0) {
       for (int s = 0; s < kWsStages; ++s) {
         const long long q = blockIdx.x + (long long)s * G;
         if (q < n_items) issue_item<T>(a, q, smem + s * 2 * ROWB, &full[s]);
       }
+      int j = 0;
+      for (long long q = blockIdx.x; q + (long long)kWsStages * G < n_items; q += G, ++j) {
+        const int s = j % kWsStages;
+        mbar_wait(&consumed[s], (uint32_t)(j / kWsStages) & 1u);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_item<T>(a, q + (long long)kWsStages * G, smem + s * 2 * ROWB, &full[s]);
+      }
+    }
+    return;
+  }
+  if (warp == kCWarps + 1) {
+    // ---------------- merger warp: 8 warp partials -> chunk partial (fp64) ----------------
     int j = 0;
     for (long long q = blockIdx.x; q < n_items; q += G, ++j) {
       const int s = j % kWsStages;
       const uint32_t round = (uint32_t)(j / kWsStages);
-      mbar_wait(&consumed[s], round & 1u);
-      const long long qn = q + (long long)kWsStages * G;
-      if (lane == 0 && qn < n_items) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_item<T>(a, qn, smem + s * 2 * ROWB, &full[s]);
-      }
-      mbar_wait(&ready[s], round & 1u);
-      const WarpPartial* wp = slots + (s * 2 + (round & 1u)) * kCWarps;
+      // slot set (s, b) is used for the u-th time in this round
+      const uint32_t b = round & 1u, u = round >> 1;
+      mbar_wait(&ready[2 * s + b], u & 1u);
+      const WarpPartial* wp = slots + (s * 2 + b) * kCWarps;
       // chunk reference: the warp with the largest M (smallest idx on ties)
       float Mr = -INFINITY, dr = 0.f, mx = -INFINITY;
       int ir = 0x7fffffff, flags = 0;
@@ -598,8 +611,10 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
       const float Cc = fminf(Mr - dr, (Mr - mx) + 64.f);
       if (Cc < Mr - dr) flags |= DSDE_FLAG_OVERFLOW;
       double S = 0.0, A = 0.0, D = 0.0;
+      const WarpPartial p = wp[lane < kCWarps ? lane : 0];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&freeb[2 * s + b]);  // slot set reusable
       if (lane < kCWarps) {
-        const WarpPartial p = wp[lane];
         const double ls = (double)p.M - (double)Mr;
         const double sc = exp(ls);
         const double dl = (double)p.C - (double)Cc;
@@ -741,16 +756,18 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
     // warp reference: max of t, its smallest element index, d there; max of d
     const float M = warp_max_nan(mt);
     const float Dmax = warp_max(md);
+    const uint32_t sb = round & 1u, su = round >> 1;  // slot set (s, sb), use su
     if (M <= -1e30f) {  // slice beyond V (padding only): an empty partial (NaN is not empty)
       if (lane == 0) {
+        if (su > 0) mbar_wait(&freeb[2 * s + sb], (su - 1) & 1u);
         WarpPartial p;
         p.S = p.A = p.D = 0.f;
         p.M = -INFINITY;
         p.C = p.dstar = 0.f;
         p.maxd = -INFINITY;
         p.idx = 0x7fffffff;
-        slots[(s * 2 + (round & 1u)) * kCWarps + warp] = p;
-        mbar_arrive(&ready[s]);
+        slots[(s * 2 + sb) * kCWarps + warp] = p;
+        mbar_arrive(&ready[2 * s + sb]);
       }
       continue;
     }
@@ -827,8 +844,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
       p.dstar = dstar;
       p.maxd = Dmax;
       p.idx = Mi;
-      slots[(s * 2 + (round & 1u)) * kCWarps + warp] = p;
-      mbar_arrive(&ready[s]);
+      if (su > 0) mbar_wait(&freeb[2 * s + sb], (su - 1) & 1u);
+      slots[(s * 2 + sb) * kCWarps + warp] = p;
+      mbar_arrive(&ready[2 * s + sb]);
     }
   }
 }
