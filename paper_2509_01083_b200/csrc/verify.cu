@@ -120,6 +120,9 @@ __device__ __forceinline__ float load_logit_smem<uint16_t>(const uint16_t* p) {
   return bf16_bits_to_float(*p);
 }
 
+// max that propagates NaN (a NaN logit must reach the non-finite check)
+__device__ __forceinline__ float max_nan(float a, float b) { return (b > a || b != b) ? b : a; }
+
 __device__ __forceinline__ void arg_better(float& m, int& mi, float& md, float m2, int i2, float d2) {
   if (m2 > m || (m2 == m && i2 < mi)) {
     m = m2;
@@ -170,17 +173,8 @@ __device__ __forceinline__ float diff_ref<float>(float t, float d, float C) {
 }
 
 // ---------------------------------------------------------------------------
-// a1, production path: persistent CTAs (2 per SM) with a 3-stage ring of
-// 32 KB shared-memory stages filled by 1-D TMA bulk copies
-// (cp.async.bulk + mbarrier complete_tx). Item q = (draft row r, chunk c),
-// q = blockIdx.x + j * gridDim.x, i.e. the grid sweeps rows in order. Each
-// thread lifts its 2 x 32 logits of the chunk into registers, which frees
-// the stage after the first barrier: the refill of that stage (item j + 3)
-// is in flight while the statistics of item j are computed. Element math is
-// packed two-wide (FFMA2/FADD2/FMUL2) with two MUFU.EX2 per element.
-// Same partials and numerics as k_stream.
+// mbarrier / TMA bulk-copy primitives (PTX), packed element helpers
 // ---------------------------------------------------------------------------
-constexpr int kStages = 3;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -231,10 +225,6 @@ template <typename T>
 __host__ __device__ constexpr int stage_row_bytes() {
   return chunk_elems<T>() * (int)sizeof(T);
 }
-template <typename T>
-__host__ __device__ constexpr int stream_tma_smem() {
-  return kStages * 2 * stage_row_bytes<T>() + kStages * 8;
-}
 
 template <typename T>
 __device__ __forceinline__ void unpack16(uint4 raw, float* x);
@@ -266,238 +256,28 @@ __device__ __forceinline__ float2 diff2<float>(float2 t, float2 d, float C) {
   return make_float2(diff_ref<float>(t.x, d.x, C), diff_ref<float>(t.y, d.y, C));
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kThreads, 2) k_stream_tma(StreamTmaArgs a) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, E = VEC * NV, CH = chunk_elems<T>();
-  constexpr int ROWB = stage_row_bytes<T>();
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * 2 * ROWB);
-  __shared__ float s_m[2][kThreads / 32], s_d[2][kThreads / 32], s_dx[2][kThreads / 32];
-  __shared__ int s_i[2][kThreads / 32];
-  __shared__ float s_sum[2][3][kThreads / 32];
-  const long long n_items = (long long)a.total * a.nchunks;
-  const int G = gridDim.x;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-  auto issue = [&](long long q, int stage) {
-    const long long r = q / a.nchunks;
-    const int c = (int)(q - r * a.nchunks);
-    int lo = 0, hi = a.B - 1;  // sequence of draft row r
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (__ldg(a.cu_sl + mid) <= r) lo = mid; else hi = mid - 1;
-    }
-    const int c0 = c * CH;
-    const int n_el = min(CH, a.V - c0);
-    const uint32_t bytes = (uint32_t)(n_el * (int)sizeof(T)) & ~15u;
-    uint8_t* dst = smem + stage * 2 * ROWB;
-    if (bytes) {
-      mbar_arrive_expect_tx(&full[stage], 2 * bytes);
-      bulk_g2s(dst, reinterpret_cast<const T*>(a.tl) + (r + lo) * a.ld_t + c0, bytes, &full[stage]);
-      bulk_g2s(dst + ROWB, reinterpret_cast<const T*>(a.dl) + r * a.ld_d + c0, bytes, &full[stage]);
-    } else {
-      mbar_arrive(&full[stage]);
-    }
-  };
-
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0)
-    for (int s = 0; s < kStages; ++s) {
-      const long long q = blockIdx.x + (long long)s * G;
-      if (q < n_items) issue(q, s);
-    }
-
-  const float2 L2 = make_float2(kLog2e, kLog2e), nL2 = make_float2(-kLog2e, -kLog2e);
-  // h(-w) coefficients in powers of w (alternating signs of tools/fit_g.py's)
-  const float2 K7 = make_float2(-2.812654656736413e-06f, -2.812654656736413e-06f);
-  const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
-  const float2 K5 = make_float2(-1.9836986029986292e-04f, -1.9836986029986292e-04f);
-  const float2 K4 = make_float2(1.3885394437238574e-03f, 1.3885394437238574e-03f);
-  const float2 K3 = make_float2(-8.33334494382143e-03f, -8.33334494382143e-03f);
-  const float2 K2 = make_float2(4.166673496365547e-02f, 4.166673496365547e-02f);
-  const float2 K1 = make_float2(-1.666666716337204e-01f, -1.666666716337204e-01f);
-  const float2 K0 = make_float2(0.5f, 0.5f);
-
-  int j = 0;
-  for (long long q = blockIdx.x; q < n_items; q += G, ++j) {
-    const int stage = j % kStages;
-    const uint32_t par = (uint32_t)(j / kStages) & 1u;
-    const int buf = j & 1;
-    const long long r = q / a.nchunks;
-    const int c = (int)(q - r * a.nchunks);
-    const int c0 = c * CH;
-    const int n_el = min(CH, a.V - c0);
-    const int bulk_el = (int)(((uint32_t)(n_el * (int)sizeof(T)) & ~15u) / sizeof(T));
-    mbar_wait(&full[stage], par);
-    const T* st = reinterpret_cast<const T*>(smem + stage * 2 * ROWB);
-    const T* sd = reinterpret_cast<const T*>(smem + stage * 2 * ROWB + ROWB);
-    float t[E], d[E];
-    if (n_el == CH) {  // every chunk but the last of a row: unchecked 128-bit LDS
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int e0 = (v * kThreads + tid) * VEC;
-        unpack16<T>(*reinterpret_cast<const uint4*>(st + e0), t + v * VEC);
-        unpack16<T>(*reinterpret_cast<const uint4*>(sd + e0), d + v * VEC);
-      }
-    } else {
-      // last chunk: bulk-copied part from shared memory, an unaligned tail
-      // (V * sizeof(T) not a multiple of 16) from global memory, padding after V
-      long long trow = 0;
-      if (bulk_el < n_el) {
-        int lo = 0, hi = a.B - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (__ldg(a.cu_sl + mid) <= r) lo = mid; else hi = mid - 1;
-        }
-        trow = r + lo;
-      }
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int e0 = (v * kThreads + tid) * VEC;
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const int idx = e0 + e;
-          float tv = -1e30f, dv = -1e30f;
-          if (idx < bulk_el) {
-            tv = load_logit_smem(st + idx);
-            dv = load_logit_smem(sd + idx);
-          } else if (idx < n_el) {
-            tv = load_logit<T>(reinterpret_cast<const T*>(a.tl) + trow * a.ld_t + c0 + idx);
-            dv = load_logit<T>(reinterpret_cast<const T*>(a.dl) + r * a.ld_d + c0 + idx);
-          }
-          t[v * VEC + e] = tv;
-          d[v * VEC + e] = dv;
-        }
-      }
-    }
-    // phase 1: chunk max / smallest-index argmax of t, max of d
-    float m = -INFINITY, md = 0.f, dmax = -INFINITY;
-    int mi = 0x7fffffff;
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) {
-        const int idx = (v * kThreads + tid) * VEC + e;
-        dmax = fmaxf(dmax, d[v * VEC + e]);  // padding (-1e30) never wins over real logits
-        if (t[v * VEC + e] > m) {
-          m = t[v * VEC + e];
-          mi = c0 + idx;
-          md = d[v * VEC + e];
-        }
-      }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float m2 = __shfl_xor_sync(kFull, m, o);
-      const int i2 = __shfl_xor_sync(kFull, mi, o);
-      const float d2 = __shfl_xor_sync(kFull, md, o);
-      arg_better(m, mi, md, m2, i2, d2);
-      dmax = fmaxf(dmax, __shfl_xor_sync(kFull, dmax, o));
-    }
-    if (lane == 0) {
-      s_m[buf][warp] = m;
-      s_i[buf][warp] = mi;
-      s_d[buf][warp] = md;
-      s_dx[buf][warp] = dmax;
-    }
-    __syncthreads();  // B1: every thread holds its slice; the stage is free
-    if (tid == 0) {
-      const long long qn = q + (long long)kStages * G;
-      if (qn < n_items) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(qn, stage);
-      }
-    }
-    float M = s_m[buf][0], dstar = s_d[buf][0], Dmax = s_dx[buf][0];
-    int Mi = s_i[buf][0];
-#pragma unroll
-    for (int w = 1; w < kThreads / 32; ++w) {
-      arg_better(M, Mi, dstar, s_m[buf][w], s_i[buf][w], s_d[buf][w]);
-      Dmax = fmaxf(Dmax, s_dx[buf][w]);
-    }
-    const float Cf = fminf(M - dstar, (M - Dmax) + 64.f);
-    const float ML2 = M * kLog2e;
-    const float2 nML2 = make_float2(-ML2, -ML2);
-    float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
-#pragma unroll
-    for (int h = 0; h < E; h += 2) {
-      const float2 tt = make_float2(t[h], t[h + 1]), dd = make_float2(d[h], d[h + 1]);
-      const float2 xt = __ffma2_rn(tt, L2, nML2);
-      const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
-      const float2 w = diff2<T>(tt, dd, Cf);
-      S2 = __fadd2_rn(S2, e);
-      A2 = __ffma2_rn(e, w, A2);
-      float2 p = __ffma2_rn(K7, w, K6);
-      p = __ffma2_rn(p, w, K5);
-      p = __ffma2_rn(p, w, K4);
-      p = __ffma2_rn(p, w, K3);
-      p = __ffma2_rn(p, w, K2);
-      p = __ffma2_rn(p, w, K1);
-      p = __ffma2_rn(p, w, K0);
-      const float2 sm = __fmul2_rn(__fmul2_rn(e, __fmul2_rn(w, w)), p);
-      const float2 arg = __ffma2_rn(w, nL2, xt);
-      const float2 f = make_float2(fast_exp2(arg.x), fast_exp2(arg.y));
-      const float2 bg = __ffma2_rn(e, w, __fadd2_rn(f, make_float2(-e.x, -e.y)));
-      const float2 term = make_float2(fabsf(w.x) < 1.f ? sm.x : bg.x, fabsf(w.y) < 1.f ? sm.y : bg.y);
-      D2 = __fadd2_rn(D2, term);
-    }
-    float S = S2.x + S2.y, A = A2.x + A2.y, D = D2.x + D2.y;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      S += __shfl_xor_sync(kFull, S, o);
-      A += __shfl_xor_sync(kFull, A, o);
-      D += __shfl_xor_sync(kFull, D, o);
-    }
-    if (lane == 0) {
-      s_sum[buf][0][warp] = S;
-      s_sum[buf][1][warp] = A;
-      s_sum[buf][2][warp] = D;
-    }
-    __syncthreads();  // B2
-    if (tid == 0) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-#pragma unroll
-      for (int w = 0; w < kThreads / 32; ++w) {
-        s0 += (double)s_sum[buf][0][w];
-        s1 += (double)s_sum[buf][1][w];
-        s2 += (double)s_sum[buf][2][w];
-      }
-      ChunkPartial p;
-      p.S = s0;
-      p.A = s1;
-      p.D = s2;
-      p.M = M;
-      p.C = Cf;
-      p.idx = Mi;
-      p.flags = Cf < M - dstar ? DSDE_FLAG_OVERFLOW : 0;
-      p.maxd = Dmax;
-      p.pad = 0;
-      a.part[r * a.nchunks + c] = p;
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
-// a1, warp-specialised stream (the launched path). Per CTA: 1 producer warp +
-// 8 consumer warps, 2 CTAs per SM, a 3-stage ring of 32 KB stages filled by
-// 1-D TMA bulk copies. No CTA-wide barrier in the loop: every consumer warp
-// owns 1/8 of each chunk, finds its own reference (max / smallest-index argmax
-// of t, max of d) with shuffles, accumulates S, A, D about it and posts a warp
-// partial; mbarriers hand stages back to the producer, which refills them and
-// merges the 8 warp partials of the chunk in fp64 (same re-referencing as
-// merge_row) into the chunk partial.
+// a1, warp-specialised stream (the launched path). Per CTA: 8 consumer warps,
+// 1 TMA producer warp, 1 merger warp; 2 CTAs per SM; a 3-stage ring of 32 KB
+// stages filled by 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx).
+// Items q = (draft row r, chunk c) are swept in order, q = blockIdx.x + j*grid.
+// No CTA-wide barrier in the loop:
+//   * a consumer warp lifts its 1/8 of the chunk (t and d) into registers,
+//     releases the stage (mbarrier `consumed`), takes its own reference
+//     M = max t, C = M - max d (so e^{t-M} e^{-w} = e^{d - max d} <= 1: no
+//     overflow for any input), accumulates S, A, D with packed FFMA2 math and
+//     posts a warp partial (mbarriers `ready` / `freeb` guard the slot sets);
+//   * the producer refills a stage as soon as it is consumed;
+//   * the merger folds the 8 warp partials into the chunk partial in fp64
+//     (same re-referencing as merge_row).
 // ---------------------------------------------------------------------------
 constexpr int kCWarps = 8;
 constexpr int kWsThreads = 32 * (kCWarps + 2);  // + TMA producer warp + merger warp
 constexpr int kWsStages = 3;
 
-struct WarpPartial {  // 32 bytes
+struct WarpPartial {  // 24 bytes
   float S, A, D;      // about (M, C) of the warp slice
-  float M, C, dstar, maxd;
-  int idx;
+  float M, C, maxd;
 };
 
 template <typename T>
@@ -506,27 +286,34 @@ __host__ __device__ constexpr int stream_ws_smem() {
          6 * kWsStages * 8;
 }
 
-// max that propagates NaN (a NaN logit must reach the non-finite check)
-__device__ __forceinline__ float max_nan(float a, float b) { return (b > a || b != b) ? b : a; }
-
-__device__ __forceinline__ float warp_max_nan(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = max_nan(v, __shfl_xor_sync(kFull, v, o));
-  return v;
-}
-
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
   return v;
 }
 
+// q -> (draft row r, chunk c), advanced by the grid stride without divisions
+struct ItemCursor {
+  long long r;
+  int c;
+  __device__ void init(long long q, int nchunks) {
+    r = q / nchunks;
+    c = (int)(q - r * nchunks);
+  }
+  __device__ void advance(int dr, int dc, int nchunks) {
+    r += dr;
+    c += dc;
+    if (c >= nchunks) {
+      c -= nchunks;
+      r += 1;
+    }
+  }
+};
+
 template <typename T>
-__device__ __forceinline__ void issue_item(const StreamTmaArgs& a, long long q, uint8_t* dst,
+__device__ __forceinline__ void issue_item(const StreamTmaArgs& a, long long r, int c, uint8_t* dst,
                                            uint64_t* bar) {
   constexpr int CH = chunk_elems<T>(), ROWB = stage_row_bytes<T>();
-  const long long r = q / a.nchunks;
-  const int c = (int)(q - r * a.nchunks);
   int lo = 0, hi = a.B - 1;  // sequence of draft row r
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -553,10 +340,11 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
   WarpPartial* slots = reinterpret_cast<WarpPartial*>(smem + kWsStages * 2 * ROWB);
   uint64_t* full = reinterpret_cast<uint64_t*>(slots + kWsStages * 2 * kCWarps);
   uint64_t* consumed = full + kWsStages;
-  uint64_t* ready = consumed + kWsStages;  // [stage][2]: 8 warp partials posted
+  uint64_t* ready = consumed + kWsStages;   // [stage][2]: 8 warp partials posted
   uint64_t* freeb = ready + 2 * kWsStages;  // [stage][2]: merger done with the slot set
   const long long n_items = (long long)a.total * a.nchunks;
   const int G = gridDim.x;
+  const int dr = G / a.nchunks, dc = G % a.nchunks;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kWsStages; ++s) {
@@ -572,50 +360,51 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
   __syncthreads();
 
   if (warp == kCWarps) {
-    // ---------------- TMA producer warp: refills a stage as soon as the 8
-    // consumer warps have lifted it into registers ----------------
+    // ---------------- TMA producer: refill a stage once it is consumed ----------------
     if (lane == 0) {
-      for (int s = 0; s < kWsStages; ++s) {
-        const long long q = blockIdx.x + (long long)s * G;
-        if (q < n_items) issue_item<T>(a, q, smem + s * 2 * ROWB, &full[s]);
+      ItemCursor it;
+      it.init(blockIdx.x, a.nchunks);
+      long long q = blockIdx.x;
+      for (int s = 0; s < kWsStages && q < n_items; ++s, q += G) {
+        issue_item<T>(a, it.r, it.c, smem + s * 2 * ROWB, &full[s]);
+        it.advance(dr, dc, a.nchunks);
       }
-      int j = 0;
-      for (long long q = blockIdx.x; q + (long long)kWsStages * G < n_items; q += G, ++j) {
-        const int s = j % kWsStages;
-        mbar_wait(&consumed[s], (uint32_t)(j / kWsStages) & 1u);
+      int s = 0;
+      uint32_t round = 0;
+      for (; q < n_items; q += G) {
+        mbar_wait(&consumed[s], round & 1u);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_item<T>(a, q + (long long)kWsStages * G, smem + s * 2 * ROWB, &full[s]);
+        issue_item<T>(a, it.r, it.c, smem + s * 2 * ROWB, &full[s]);
+        it.advance(dr, dc, a.nchunks);
+        if (++s == kWsStages) {
+          s = 0;
+          ++round;
+        }
       }
     }
     return;
   }
   if (warp == kCWarps + 1) {
-    // ---------------- merger warp: 8 warp partials -> chunk partial (fp64) ----------------
-    int j = 0;
-    for (long long q = blockIdx.x; q < n_items; q += G, ++j) {
-      const int s = j % kWsStages;
-      const uint32_t round = (uint32_t)(j / kWsStages);
-      // slot set (s, b) is used for the u-th time in this round
-      const uint32_t b = round & 1u, u = round >> 1;
+    // ---------------- merger: 8 warp partials -> chunk partial (fp64) ----------------
+    int s = 0;
+    uint32_t round = 0;
+    for (long long q = blockIdx.x; q < n_items; q += G) {
+      const uint32_t b = round & 1u, u = round >> 1;  // slot set (s, b), its u-th use
       mbar_wait(&ready[2 * s + b], u & 1u);
       const WarpPartial* wp = slots + (s * 2 + b) * kCWarps;
-      // chunk reference: the warp with the largest M (smallest idx on ties)
-      float Mr = -INFINITY, dr = 0.f, mx = -INFINITY;
-      int ir = 0x7fffffff, flags = 0;
+      float Mr = -INFINITY, Dx = -INFINITY;
 #pragma unroll
       for (int w = 0; w < kCWarps; ++w) {
-        arg_better(Mr, ir, dr, wp[w].M, wp[w].idx, wp[w].dstar);
-        mx = fmaxf(mx, wp[w].maxd);
-        flags |= (wp[w].C < wp[w].M - wp[w].dstar) ? DSDE_FLAG_OVERFLOW : 0;
+        Mr = fmaxf(Mr, wp[w].M);
+        Dx = fmaxf(Dx, wp[w].maxd);
       }
-      const float Cc = fminf(Mr - dr, (Mr - mx) + 64.f);
-      if (Cc < Mr - dr) flags |= DSDE_FLAG_OVERFLOW;
-      double S = 0.0, A = 0.0, D = 0.0;
       const WarpPartial p = wp[lane < kCWarps ? lane : 0];
       __syncwarp();
       if (lane == 0) mbar_arrive(&freeb[2 * s + b]);  // slot set reusable
+      const float Cc = Mr - Dx;
+      double S = 0.0, A = 0.0, D = 0.0;
       if (lane < kCWarps) {
-        const double ls = (double)p.M - (double)Mr;
+        const double ls = (double)p.M - (double)Mr;  // -inf for an empty slice
         const double sc = exp(ls);
         const double dl = (double)p.C - (double)Cc;
         double sem, sg, E1;
@@ -646,11 +435,15 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
         cp.D = D;
         cp.M = Mr;
         cp.C = Cc;
-        cp.idx = ir;
-        cp.flags = flags;
-        cp.maxd = mx;
+        cp.idx = 0;
+        cp.flags = 0;
+        cp.maxd = Dx;
         cp.pad = 0;
         a.part[q] = cp;
+      }
+      if (++s == kWsStages) {
+        s = 0;
+        ++round;
       }
     }
     return;
@@ -658,6 +451,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
 
   // ---------------- consumer warps ----------------
   const float2 L2 = make_float2(kLog2e, kLog2e), nL2 = make_float2(-kLog2e, -kLog2e);
+  // h(-w) coefficients in powers of w (alternating signs of tools/fit_g.py's)
   const float2 K7 = make_float2(-2.812654656736413e-06f, -2.812654656736413e-06f);
   const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
   const float2 K5 = make_float2(-1.9836986029986292e-04f, -1.9836986029986292e-04f);
@@ -666,13 +460,12 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
   const float2 K2 = make_float2(4.166673496365547e-02f, 4.166673496365547e-02f);
   const float2 K1 = make_float2(-1.666666716337204e-01f, -1.666666716337204e-01f);
   const float2 K0 = make_float2(0.5f, 0.5f);
-  int j = 0;
-  for (long long q = blockIdx.x; q < n_items; q += G, ++j) {
-    const int s = j % kWsStages;
-    const uint32_t round = (uint32_t)(j / kWsStages);
-    const long long r = q / a.nchunks;
-    const int c = (int)(q - r * a.nchunks);
-    const int c0 = c * CH;
+  ItemCursor it;
+  it.init(blockIdx.x, a.nchunks);
+  int s = 0;
+  uint32_t round = 0;
+  for (long long q = blockIdx.x; q < n_items; q += G) {
+    const int c0 = it.c * CH;
     const int n_el = min(CH, a.V - c0);
     mbar_wait(&full[s], round & 1u);
     const T* st = reinterpret_cast<const T*>(smem + s * 2 * ROWB);
@@ -702,7 +495,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
             bd = __hmax2(bd, *reinterpret_cast<const __nv_bfloat162*>(&wd[h]));
           }
         }
-        mt = fmaxf(__low2float(bt), __high2float(bt));
+        const float lo = __low2float(bt), hi = __high2float(bt);
+        mt = (lo != lo || hi != hi) ? NAN : fmaxf(lo, hi);
         md = fmaxf(__low2float(bd), __high2float(bd));
       }
 #pragma unroll
@@ -726,9 +520,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
         int lo = 0, hi = a.B - 1;
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
-          if (__ldg(a.cu_sl + mid) <= r) lo = mid; else hi = mid - 1;
+          if (__ldg(a.cu_sl + mid) <= it.r) lo = mid; else hi = mid - 1;
         }
-        trow = r + lo;
+        trow = it.r + lo;
       }
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
@@ -742,7 +536,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
             dv = load_logit_smem(sd + idx);
           } else if (idx < n_el) {
             tv = load_logit<T>(reinterpret_cast<const T*>(a.tl) + trow * a.ld_t + c0 + idx);
-            dv = load_logit<T>(reinterpret_cast<const T*>(a.dl) + r * a.ld_d + c0 + idx);
+            dv = load_logit<T>(reinterpret_cast<const T*>(a.dl) + it.r * a.ld_d + c0 + idx);
           }
           t[v * VEC + e] = tv;
           d[v * VEC + e] = dv;
@@ -753,100 +547,68 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&consumed[s]);
     }
-    // warp reference: max of t, its smallest element index, d there; max of d
-    const float M = warp_max_nan(mt);
+    // warp reference: M = max t (NaN if any t is NaN), C = M - max d
+    float M = warp_max(mt);
+    if (__any_sync(kFull, mt != mt)) M = NAN;
     const float Dmax = warp_max(md);
-    const uint32_t sb = round & 1u, su = round >> 1;  // slot set (s, sb), use su
+    const uint32_t sb = round & 1u, su = round >> 1;  // slot set (s, sb), its su-th use
+    WarpPartial p;
     if (M <= -1e30f) {  // slice beyond V (padding only): an empty partial (NaN is not empty)
-      if (lane == 0) {
-        if (su > 0) mbar_wait(&freeb[2 * s + sb], (su - 1) & 1u);
-        WarpPartial p;
-        p.S = p.A = p.D = 0.f;
-        p.M = -INFINITY;
-        p.C = p.dstar = 0.f;
-        p.maxd = -INFINITY;
-        p.idx = 0x7fffffff;
-        slots[(s * 2 + sb) * kCWarps + warp] = p;
-        mbar_arrive(&ready[2 * s + sb]);
+      p.S = p.A = p.D = 0.f;
+      p.M = -INFINITY;
+      p.C = 0.f;
+      p.maxd = -INFINITY;
+    } else {
+      const float Cw = M - Dmax;
+      const float ML2 = M * kLog2e;
+      const float2 nML2 = make_float2(-ML2, -ML2);
+      float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
+#pragma unroll
+      for (int h = 0; h < E; h += 2) {
+        const float2 tt = make_float2(t[h], t[h + 1]), dd = make_float2(d[h], d[h + 1]);
+        const float2 xt = __ffma2_rn(tt, L2, nML2);
+        const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
+        const float2 w = diff2<T>(tt, dd, Cw);
+        S2 = __fadd2_rn(S2, e);
+        A2 = __ffma2_rn(e, w, A2);
+        float2 pp = __ffma2_rn(K7, w, K6);
+        pp = __ffma2_rn(pp, w, K5);
+        pp = __ffma2_rn(pp, w, K4);
+        pp = __ffma2_rn(pp, w, K3);
+        pp = __ffma2_rn(pp, w, K2);
+        pp = __ffma2_rn(pp, w, K1);
+        pp = __ffma2_rn(pp, w, K0);
+        const float2 sm = __fmul2_rn(__fmul2_rn(e, __fmul2_rn(w, w)), pp);
+        const float2 arg = __ffma2_rn(w, nL2, xt);  // (d - max d) log2 e <= 0
+        const float2 f = make_float2(fast_exp2(arg.x), fast_exp2(arg.y));
+        const float2 bg = __ffma2_rn(e, w, __fadd2_rn(f, make_float2(-e.x, -e.y)));
+        const float2 term =
+            make_float2(fabsf(w.x) < 1.f ? sm.x : bg.x, fabsf(w.y) < 1.f ? sm.y : bg.y);
+        D2 = __fadd2_rn(D2, term);
       }
-      continue;
-    }
-    int fv = -1, owner = 0;
+      float S = S2.x + S2.y, A = A2.x + A2.y, D = D2.x + D2.y;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      bool hit = false;
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) hit |= (t[v * VEC + e] == M);
-      const unsigned b = __ballot_sync(kFull, hit);
-      if (fv < 0 && b) {
-        fv = v;
-        owner = __ffs(b) - 1;
+      for (int o = 16; o > 0; o >>= 1) {
+        S += __shfl_xor_sync(kFull, S, o);
+        A += __shfl_xor_sync(kFull, A, o);
+        D += __shfl_xor_sync(kFull, D, o);
       }
-    }
-    int Mi = 0x7fffffff;
-    float dstar = 0.f;
-    if (fv >= 0) {
-      int my_i = 0x7fffffff;
-      float my_d = 0.f;
-      if (lane == owner) {
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-          for (int e = VEC - 1; e >= 0; --e)
-            if (v == fv && t[v * VEC + e] == M) {
-              my_i = c0 + warp * SL + (v * 32 + lane) * VEC + e;
-              my_d = d[v * VEC + e];
-            }
-      }
-      Mi = __shfl_sync(kFull, my_i, owner);
-      dstar = __shfl_sync(kFull, my_d, owner);
-    }
-    const float Cw = fminf(M - dstar, (M - Dmax) + 64.f);
-    const float ML2 = M * kLog2e;
-    const float2 nML2 = make_float2(-ML2, -ML2);
-    float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
-#pragma unroll
-    for (int h = 0; h < E; h += 2) {
-      const float2 tt = make_float2(t[h], t[h + 1]), dd = make_float2(d[h], d[h + 1]);
-      const float2 xt = __ffma2_rn(tt, L2, nML2);
-      const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
-      const float2 w = diff2<T>(tt, dd, Cw);
-      S2 = __fadd2_rn(S2, e);
-      A2 = __ffma2_rn(e, w, A2);
-      float2 p = __ffma2_rn(K7, w, K6);
-      p = __ffma2_rn(p, w, K5);
-      p = __ffma2_rn(p, w, K4);
-      p = __ffma2_rn(p, w, K3);
-      p = __ffma2_rn(p, w, K2);
-      p = __ffma2_rn(p, w, K1);
-      p = __ffma2_rn(p, w, K0);
-      const float2 sm = __fmul2_rn(__fmul2_rn(e, __fmul2_rn(w, w)), p);
-      const float2 arg = __ffma2_rn(w, nL2, xt);
-      const float2 f = make_float2(fast_exp2(arg.x), fast_exp2(arg.y));
-      const float2 bg = __ffma2_rn(e, w, __fadd2_rn(f, make_float2(-e.x, -e.y)));
-      const float2 term = make_float2(fabsf(w.x) < 1.f ? sm.x : bg.x, fabsf(w.y) < 1.f ? sm.y : bg.y);
-      D2 = __fadd2_rn(D2, term);
-    }
-    float S = S2.x + S2.y, A = A2.x + A2.y, D = D2.x + D2.y;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      S += __shfl_xor_sync(kFull, S, o);
-      A += __shfl_xor_sync(kFull, A, o);
-      D += __shfl_xor_sync(kFull, D, o);
-    }
-    if (lane == 0) {
-      WarpPartial p;
       p.S = S;
       p.A = A;
       p.D = D;
       p.M = M;
       p.C = Cw;
-      p.dstar = dstar;
       p.maxd = Dmax;
-      p.idx = Mi;
+    }
+    if (lane == 0) {
       if (su > 0) mbar_wait(&freeb[2 * s + sb], (su - 1) & 1u);
       slots[(s * 2 + sb) * kCWarps + warp] = p;
       mbar_arrive(&ready[2 * s + sb]);
+    }
+    it.advance(dr, dc, a.nchunks);
+    if (++s == kWsStages) {
+      s = 0;
+      ++round;
     }
   }
 }
@@ -857,27 +619,22 @@ struct RowStats {
   int flags;
 };
 
-// fp64 merge of chunk partials in chunk order. The reference is the chunk
-// with the largest M (earliest on ties, so the row's smallest-index argmax),
-// lowered like the chunk references so that every v has
-// d_v - (M - C) <= 64 (all merged terms stay finite in fp64).
-// Chunk c's w is shifted by Delta = C_c - C; with s = e^(M_c - M) and
-// E1 = s e^-Delta:
+// fp64 merge of chunk partials in chunk order about the row reference
+// M = max_c M_c and C = fp32(M - max_v d_v) (so every merged term
+// e^{t-M} e^{-w} = e^{d - max d} <= 1; C is an fp32 value so the sampling
+// pass can rebuild w exactly). Chunk c's w is shifted by Delta = C_c - C; with
+// s = e^(M_c - M) and E1 = s e^-Delta:
 //   S += s S_c,   A += s (A_c + S_c Delta),
 //   D += E1 D_c - A_c s expm1(-Delta) + S_c s g(Delta),  g(x) = expm1(-x) + x.
 __device__ RowStats merge_row(const ChunkPartial* P, int nchunks, bool pair) {
-  int cref = 0;
   float Mref = P[0].M, maxd = P[0].maxd;
   for (int c = 1; c < nchunks; ++c) {
-    if (P[c].M > Mref) {
-      Mref = P[c].M;
-      cref = c;
-    }
+    Mref = max_nan(Mref, P[c].M);
     maxd = fmaxf(maxd, P[c].maxd);
   }
   RowStats r;
   r.M = (double)Mref;
-  r.C = pair ? fmin((double)P[cref].C, (r.M - (double)maxd) + 64.0) : 0.0;
+  r.C = pair ? (double)(Mref - maxd) : 0.0;
   r.S = r.A = r.D = 0.0;
   r.flags = 0;
   for (int c = 0; c < nchunks; ++c) {
