@@ -53,7 +53,9 @@ __device__ __forceinline__ float fast_exp2(float x) {
 }
 
 // bf16 pair in a 32-bit word -> two exact fp32 values.
-__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+// (byte permutes run on the ALU pipe; a plain shift is often lowered to IMAD,
+// which competes with the FFMA2 stream on the FMA pipe)
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(__byte_perm(w, 0u, 0x1044)); }
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 
 __device__ __forceinline__ float bf16_bits_to_float(uint16_t b) {

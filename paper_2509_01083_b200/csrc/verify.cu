@@ -81,8 +81,8 @@ static_assert(sizeof(SeqRec) == 64, "SeqRec layout");
 struct VerifyWs {
   ChunkPartial* part;  // [(total + B) * nchunks]
   SeqRec* rec;         // [B]
-  double* mass;        // [B * nchunks] draw-weight mass per chunk
-  float* cmax;         // [B * nchunks] chunk max of t (bonus draws)
+  double* mass;        // [B * nchunks * 8] draw-weight mass per warp sub-chunk
+  float* cmax;         // [B * nchunks * 8] reference of each sub-chunk mass (bonus)
   int* counter;        // [B] chunks done per sequence (last-block election)
 };
 
@@ -98,8 +98,8 @@ inline size_t ws_layout(int B, int total, int V, dsde_dtype dt, VerifyWs* ws, ch
   size_t off = 0;
   const size_t p_bytes = align256(sizeof(ChunkPartial) * (size_t)(total + B) * nc);
   const size_t r_bytes = align256(sizeof(SeqRec) * (size_t)B);
-  const size_t m_bytes = align256(sizeof(double) * (size_t)B * nc);
-  const size_t x_bytes = align256(sizeof(float) * (size_t)B * nc);
+  const size_t m_bytes = align256(sizeof(double) * (size_t)B * nc * 8);  // per warp sub-chunk
+  const size_t x_bytes = align256(sizeof(float) * (size_t)B * nc * 8);
   const size_t c_bytes = align256(sizeof(int) * (size_t)B);
   if (ws) {
     ws->part = reinterpret_cast<ChunkPartial*>(base + off);
@@ -129,30 +129,6 @@ __device__ __forceinline__ void arg_better(float& m, int& mi, float& md, float m
     mi = i2;
     md = d2;
   }
-}
-
-// e * g(w), g(w) = exp(-w) - 1 + w >= 0, to ~1e-7 relative for every w:
-//   |w| < 1: e u^2 h(u), u = -w, h(u) = (e^u - 1 - u)/u^2 by a degree-7
-//            near-minimax polynomial (Chebyshev fit on [-1,1]; 1.1e-7 relative
-//            in fp32 Horner, tools/fit_g.py) — no cancellation near w = 0;
-//   |w| >= 1: e exp(-w) - e + e w, with e exp(-w) = 2^(xt - w log2 e) formed in
-//            one exponent (= exp(d - (M - C)) <= e^64 by the choice of C), so no
-//            intermediate overflows; relative error <= ~4 ulp there.
-// xt = (t - M) log2 e and e = 2^xt.
-__device__ __forceinline__ float e_g(float e, float xt, float w) {
-  const float u = -w;
-  float p = 2.812654656736413e-06f;
-  p = fmaf(p, u, 2.5358644052175805e-05f);
-  p = fmaf(p, u, 1.9836986029986292e-04f);
-  p = fmaf(p, u, 1.3885394437238574e-03f);
-  p = fmaf(p, u, 8.33334494382143e-03f);
-  p = fmaf(p, u, 4.166673496365547e-02f);
-  p = fmaf(p, u, 1.666666716337204e-01f);
-  p = fmaf(p, u, 0.5f);
-  const float small = e * ((u * u) * p);
-  const float f = fast_exp2(fmaf(u, kLog2e, xt));
-  const float big = fmaf(e, w, f - e);
-  return fabsf(w) < 1.f ? small : big;
 }
 
 // w = (t - d) - C. For bf16 inputs t - d is exact in fp32 (8-bit significands,
@@ -450,14 +426,14 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
   }
 
   // ---------------- consumer warps ----------------
-  const float2 L2 = make_float2(kLog2e, kLog2e), nL2 = make_float2(-kLog2e, -kLog2e);
-  // h(-w) coefficients in powers of w (alternating signs of tools/fit_g.py's)
-  const float2 K7 = make_float2(-2.812654656736413e-06f, -2.812654656736413e-06f);
-  const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
-  const float2 K5 = make_float2(-1.9836986029986292e-04f, -1.9836986029986292e-04f);
-  const float2 K4 = make_float2(1.3885394437238574e-03f, 1.3885394437238574e-03f);
-  const float2 K3 = make_float2(-8.33334494382143e-03f, -8.33334494382143e-03f);
-  const float2 K2 = make_float2(4.166673496365547e-02f, 4.166673496365547e-02f);
+  const float2 L2 = make_float2(kLog2e, kLog2e);
+  // h(-w), h(u) = (e^u - 1 - u)/u^2, degree-5 Chebyshev fit on |u| <= 1/2
+  // (1.1e-7 relative in fp32 Horner; tools/fit_g.py --deg 5 --range 0.5), in
+  // powers of w (odd coefficients negated)
+  const float2 K5 = make_float2(-1.9962186343036592e-04f, -1.9962186343036592e-04f);
+  const float2 K4 = make_float2(1.3982197269797325e-03f, 1.3982197269797325e-03f);
+  const float2 K3 = make_float2(-8.333181962370872e-03f, -8.333181962370872e-03f);
+  const float2 K2 = make_float2(4.166579246520996e-02f, 4.166579246520996e-02f);
   const float2 K1 = make_float2(-1.666666716337204e-01f, -1.666666716337204e-01f);
   const float2 K0 = make_float2(0.5f, 0.5f);
   ItemCursor it;
@@ -483,18 +459,22 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&consumed[s]);
       if constexpr (sizeof(T) == 2) {
-        __nv_bfloat162 bt = *reinterpret_cast<const __nv_bfloat162*>(&rt[0].x);
-        __nv_bfloat162 bd = *reinterpret_cast<const __nv_bfloat162*>(&rd[0].x);
+        // two independent max chains per row (short dependency chains)
+        __nv_bfloat162 bt0 = *reinterpret_cast<const __nv_bfloat162*>(&rt[0].x), bt1 = bt0;
+        __nv_bfloat162 bd0 = *reinterpret_cast<const __nv_bfloat162*>(&rd[0].x), bd1 = bd0;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           const uint32_t wt[4] = {rt[v].x, rt[v].y, rt[v].z, rt[v].w};
           const uint32_t wd[4] = {rd[v].x, rd[v].y, rd[v].z, rd[v].w};
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            bt = __hmax2_nan(bt, *reinterpret_cast<const __nv_bfloat162*>(&wt[h]));  // NaN propagates
-            bd = __hmax2(bd, *reinterpret_cast<const __nv_bfloat162*>(&wd[h]));
+          for (int h = 0; h < 4; h += 2) {
+            bt0 = __hmax2_nan(bt0, *reinterpret_cast<const __nv_bfloat162*>(&wt[h]));  // NaN propagates
+            bt1 = __hmax2_nan(bt1, *reinterpret_cast<const __nv_bfloat162*>(&wt[h + 1]));
+            bd0 = __hmax2(bd0, *reinterpret_cast<const __nv_bfloat162*>(&wd[h]));
+            bd1 = __hmax2(bd1, *reinterpret_cast<const __nv_bfloat162*>(&wd[h + 1]));
           }
         }
+        const __nv_bfloat162 bt = __hmax2_nan(bt0, bt1), bd = __hmax2(bd0, bd1);
         const float lo = __low2float(bt), hi = __high2float(bt);
         mt = (lo != lo || hi != hi) ? NAN : fmaxf(lo, hi);
         md = fmaxf(__low2float(bd), __high2float(bd));
@@ -560,8 +540,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
       p.maxd = -INFINITY;
     } else {
       const float Cw = M - Dmax;
-      const float ML2 = M * kLog2e;
-      const float2 nML2 = make_float2(-ML2, -ML2);
+      const float ML2 = M * kLog2e, DL2 = Dmax * kLog2e;
+      const float2 nML2 = make_float2(-ML2, -ML2), nDL2 = make_float2(-DL2, -DL2);
       float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
 #pragma unroll
       for (int h = 0; h < E; h += 2) {
@@ -571,19 +551,17 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
         const float2 w = diff2<T>(tt, dd, Cw);
         S2 = __fadd2_rn(S2, e);
         A2 = __ffma2_rn(e, w, A2);
-        float2 pp = __ffma2_rn(K7, w, K6);
-        pp = __ffma2_rn(pp, w, K5);
-        pp = __ffma2_rn(pp, w, K4);
+        float2 pp = __ffma2_rn(K5, w, K4);
         pp = __ffma2_rn(pp, w, K3);
         pp = __ffma2_rn(pp, w, K2);
         pp = __ffma2_rn(pp, w, K1);
         pp = __ffma2_rn(pp, w, K0);
         const float2 sm = __fmul2_rn(__fmul2_rn(e, __fmul2_rn(w, w)), pp);
-        const float2 arg = __ffma2_rn(w, nL2, xt);  // (d - max d) log2 e <= 0
+        const float2 arg = __ffma2_rn(dd, L2, nDL2);  // (d - max d) log2 e <= 0
         const float2 f = make_float2(fast_exp2(arg.x), fast_exp2(arg.y));
         const float2 bg = __ffma2_rn(e, w, __fadd2_rn(f, make_float2(-e.x, -e.y)));
         const float2 term =
-            make_float2(fabsf(w.x) < 1.f ? sm.x : bg.x, fabsf(w.y) < 1.f ? sm.y : bg.y);
+            make_float2(fabsf(w.x) < 0.5f ? sm.x : bg.x, fabsf(w.y) < 0.5f ? sm.y : bg.y);
         D2 = __fadd2_rn(D2, term);
       }
       float S = S2.x + S2.y, A = A2.x + A2.y, D = D2.x + D2.y;
@@ -801,69 +779,67 @@ struct SampArgs {
   uint8_t* flags;
   float* cmax;
   int* counter;
+  int32_t* err;
 };
 
-__device__ __forceinline__ double block_sum(double v, double* s_w) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  v = warp_sum(v);
-  __syncthreads();
-  if (lane == 0) s_w[warp] = v;
-  __syncthreads();
-  double t = 0.0;
-#pragma unroll
-  for (int w = 0; w < kThreads / 32; ++w) t += s_w[w];
-  return t;
-}
 
 // ---------------------------------------------------------------------------
-// a4: one launch for every draw of the step. CTA (i, c) forms the draw weights
-// of chunk c of sequence i (E contiguous elements per thread, 128-bit loads)
-// and their mass; the last CTA of sequence i to finish (atomic counter +
-// threadfence) selects the token: fp64 prefix over the chunk masses, then a
-// shuffle-based block scan inside the crossing chunk (re-read from L2).
+// a4: one launch for every draw of the step, warp-granular (no block barrier).
+// Warp (i, u) forms the draw weights of sub-chunk u (SUB = 32*E elements,
+// lane-strided 16-byte vectors) of sequence i and their mass; the last warp of
+// sequence i to finish (atomic counter + threadfence) selects the token: an
+// fp64 warp scan over the sub-chunk masses, then a warp scan inside the
+// crossing sub-chunk (re-read from L2), in ascending token order (D7).
 //   residual: rho_v = e_v (1 - exp(-z_v)) for z_v > 0, else 0, with
 //             e_v = exp(t_v - M), z_v = w_v + lam, w_v = (t_v - d_v) - C exact,
 //             lam added as hi + lo floats; 1 - exp(-z) = z (1 - z h(-z)) for
 //             z < 1 (no cancellation), 1 - 2^(-z log2 e) otherwise;
-//   bonus:    p_v up to a scale: exp(t_v - m_t) about the thread's max m_t,
-//             threads rescaled by exp(m_t - M) in fp64 (one pass over the row).
-// Every per-thread value is recomputed bit-identically by the select pass.
+//   bonus:    p_v up to a scale: exp(t_v - m_u) about the warp max m_u,
+//             rescaled by exp(m_u - max_u m_u) in fp64 (one pass over the row).
+// Every per-lane value is recomputed bit-identically by the select pass.
 // ---------------------------------------------------------------------------
 template <typename T>
-__device__ __forceinline__ void load_contig(const T* row, int V, int e0, float (&x)[Traits<T>::VEC * Traits<T>::NV]) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV;
-  if (e0 + VEC * NV <= V) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(row + e0 + v * VEC);
-      unpack16<T>(raw, x + v * VEC);
-    }
+__host__ __device__ constexpr int sub_elems() {
+  return 32 * Traits<T>::VEC * Traits<T>::NV;
+}
+
+template <typename T>
+__device__ __forceinline__ void load_vec(const T* row, int V, int e0, float* x) {
+  constexpr int VEC = Traits<T>::VEC;
+  if (e0 + VEC <= V) {
+    unpack16<T>(*reinterpret_cast<const uint4*>(row + e0), x);
   } else {
 #pragma unroll
-    for (int e = 0; e < VEC * NV; ++e) x[e] = (e0 + e < V) ? load_logit<T>(row + e0 + e) : -INFINITY;
+    for (int e = 0; e < VEC; ++e) x[e] = (e0 + e < V) ? load_logit<T>(row + e0 + e) : -INFINITY;
   }
 }
 
-// Draw weights of the thread's elements of chunk c; returns the thread's
-// reference (residual: the row reference M; bonus: the thread max of t).
+// Draw weights of this lane's elements of sub-chunk u: w[v*VEC + e] for token
+// u*SUB + (v*32 + lane)*VEC + e. Returns the reference (residual: the row's M;
+// bonus: the warp max of t over the sub-chunk, -inf if all padding).
 template <typename T>
-__device__ __forceinline__ float draw_weights(const SampArgs& a, const SeqRec& r, bool resid, int c,
-                                              float (&w)[Traits<T>::VEC * Traits<T>::NV]) {
-  constexpr int E = Traits<T>::VEC * Traits<T>::NV;
-  const int e0 = c * chunk_elems<T>() + threadIdx.x * E;
+__device__ __forceinline__ float sub_weights(const SampArgs& a, const SeqRec& r, bool resid, int u,
+                                             float (&w)[Traits<T>::VEC * Traits<T>::NV]) {
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, E = VEC * NV;
+  const int lane = threadIdx.x & 31;
+  const int base = u * sub_elems<T>() + lane * VEC;
   float t[E];
-  load_contig<T>(reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t, a.V, e0, t);
+  const T* tp = reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) load_vec<T>(tp, a.V, base + v * 32 * VEC, t + v * VEC);
   if (resid) {
     float d[E];
-    load_contig<T>(reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d, a.V, e0, d);
+    const T* dp = reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) load_vec<T>(dp, a.V, base + v * 32 * VEC, d + v * VEC);
     const float Cf = (float)r.C;  // exact: r.C holds an fp32 value
     const float lhi = (float)r.lam, llo = (float)(r.lam - (double)lhi);
     const float ML2 = r.M * kLog2e;
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const float ev = fast_exp2(fmaf(t[e], kLog2e, -ML2));  // 0 for padding (-inf)
-      const float z = (diff_ref<T>(t[e], d[e], Cf) + lhi) + llo;
-      float pz = -2.812654656736413e-06f;  // h(-z), h as in e_g
+    for (int q = 0; q < E; ++q) {
+      const float ev = fast_exp2(fmaf(t[q], kLog2e, -ML2));  // 0 for padding (-inf)
+      const float z = (diff_ref<T>(t[q], d[q], Cf) + lhi) + llo;
+      float pz = -2.812654656736413e-06f;  // h(-z): tools/fit_g.py (degree 7, |u| <= 1)
       pz = fmaf(pz, z, 2.5358644052175805e-05f);
       pz = fmaf(pz, z, -1.9836986029986292e-04f);
       pz = fmaf(pz, z, 1.3885394437238574e-03f);
@@ -872,187 +848,213 @@ __device__ __forceinline__ float draw_weights(const SampArgs& a, const SeqRec& r
       pz = fmaf(pz, z, -1.666666716337204e-01f);
       pz = fmaf(pz, z, 0.5f);
       const float one_m = z < 1.f ? z * fmaf(-z, pz, 1.f) : 1.f - fast_exp2(-z * kLog2e);
-      w[e] = (z > 0.f && e0 + e < a.V) ? ev * one_m : 0.f;
+      w[q] = (z > 0.f && ev > 0.f) ? ev * one_m : 0.f;
     }
     return r.M;
   }
   float m = -INFINITY;
 #pragma unroll
-  for (int e = 0; e < E; ++e) m = fmaxf(m, t[e]);
+  for (int q = 0; q < E; ++q) m = max_nan(m, t[q]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(kFull, m, o));
   const float mL2 = m * kLog2e;
 #pragma unroll
-  for (int e = 0; e < E; ++e) w[e] = m == -INFINITY ? 0.f : fast_exp2(fmaf(t[e], kLog2e, -mL2));
+  for (int q = 0; q < E; ++q) w[q] = m == -INFINITY ? 0.f : fast_exp2(fmaf(t[q], kLog2e, -mL2));
   return m;
 }
 
-__device__ __forceinline__ float block_max(float v, float* s_f) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
-  __syncthreads();
-  if (lane == 0) s_f[warp] = v;
-  __syncthreads();
-  float m = s_f[0];
-#pragma unroll
-  for (int w = 1; w < kThreads / 32; ++w) m = fmaxf(m, s_f[w]);
-  return m;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kThreads) k_sample(SampArgs a) {
-  constexpr int E = Traits<T>::VEC * Traits<T>::NV;
-  const int i = blockIdx.x / a.nchunks, c = blockIdx.x % a.nchunks;
-  const SeqRec r = a.rec[i];
-  if (r.mode != MODE_RESIDUAL && r.mode != MODE_BONUS) return;
-  const bool resid = r.mode == MODE_RESIDUAL;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  __shared__ double s_w[kThreads / 32];
-  __shared__ float s_f[kThreads / 32];
-  __shared__ int s_last, s_cand, s_cs;
-  __shared__ double s_base, s_target, s_R, s_scale;
-  __shared__ float s_Mcs;
-
-  float w[E];
-  float mt = draw_weights<T>(a, r, resid, c, w);
-  float sum = 0.f;
-#pragma unroll
-  for (int e = 0; e < E; ++e) sum += w[e];
-  const float Mc = resid ? r.M : block_max(mt, s_f);
-  const double ft = (resid || mt == -INFINITY) ? (resid ? 1.0 : 0.0) : exp((double)mt - (double)Mc);
-  const double tot = block_sum(ft * (double)sum, s_w);
-  if (tid == 0) {
-    a.mass[(long long)i * a.nchunks + c] = tot;
-    a.cmax[(long long)i * a.nchunks + c] = Mc;
-    __threadfence();
-    const int done = atomicAdd(a.counter + i, 1);
-    s_last = done == a.nchunks - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-
-  // ---- last CTA of sequence i: select the token (D7) ----
-  uint8_t fl = 0;
-  if (tid == 0) {
-    const double* mass = a.mass + (long long)i * a.nchunks;
-    const float* cm = a.cmax + (long long)i * a.nchunks;
-    double Mg = -INFINITY;
-    if (!resid)
-      for (int cc = 0; cc < a.nchunks; ++cc) Mg = fmax(Mg, (double)__ldcg(cm + cc));
-    double R = 0.0;
-    for (int cc = 0; cc < a.nchunks; ++cc)
-      R += (resid ? 1.0 : exp((double)__ldcg(cm + cc) - Mg)) * __ldcg(mass + cc);
-    s_R = R;
-    const double target = r.u * R;
-    double cum = 0.0, base = 0.0;
-    int cs = -1;
-    for (int cc = 0; cc < a.nchunks; ++cc) {
-      const double sc = resid ? 1.0 : exp((double)__ldcg(cm + cc) - Mg);
-      const double m = sc * __ldcg(mass + cc);
-      if (m > 0.0) {
-        cs = cc;  // if no crossing is found: the last chunk with mass
-        base = cum;
-      }
-      if (m > 0.0 && cum + m > target) break;
-      cum += m;
-    }
-    s_cs = cs;
-    s_base = base;
-    s_target = target;
-    s_scale = (cs >= 0 && !resid) ? exp((double)__ldcg(cm + cs) - Mg) : 1.0;
-    s_Mcs = cs >= 0 ? __ldcg(cm + cs) : 0.f;
-    s_cand = 0x7fffffff;
-  }
-  __syncthreads();
-  const int cs = s_cs;
-  if (cs < 0) {
-    // D7 fallback: residual mass 0 (p <= q everywhere in fp32; a rejection needs
-    // p(x) < q(x), so only rounding reaches this): draw from p of the same
-    // target row, the slow way.
-    double R = 0.0;
-    SeqRec rb = r;
-    rb.mode = MODE_BONUS;
-    for (int cc = 0; cc < a.nchunks; ++cc) {
-      const float m2 = draw_weights<T>(a, rb, false, cc, w);
-      float s2 = 0.f;
-#pragma unroll
-      for (int e = 0; e < E; ++e) s2 += w[e];
-      R += block_sum(m2 == -INFINITY ? 0.0 : exp((double)m2 - (double)r.M) * (double)s2, s_w);
-    }
-    if (tid == 0) {
-      const double target = r.u * R;
-      double cum = 0.0;
-      int tok = 0;
-      for (int v = 0; v < a.V; ++v) {
-        const float tv = load_logit<T>(reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t + v);
-        const double wv = exp((double)tv - (double)r.M);
-        cum += wv;
-        if (wv > 0.0) tok = v;
-        if (wv > 0.0 && cum > target) break;
-      }
-      a.emitted[r.slot] = tok;
-      if (a.flags) a.flags[r.slot] |= DSDE_FLAG_FALLBACK;
-    }
-    return;
-  }
-  if (cs != c) mt = draw_weights<T>(a, r, resid, cs, w);
-  float ssum = 0.f;
-#pragma unroll
-  for (int e = 0; e < E; ++e) ssum += w[e];
-  // thread factor: chunk scale x thread scale (bonus), 1 (residual)
-  const double f = resid ? 1.0 : (mt == -INFINITY ? 0.0 : s_scale * exp((double)mt - (double)s_Mcs));
-  // exclusive block scan of f * ssum (fp64): warp shuffles + warp totals
-  double x = f * (double)ssum;
+__device__ __forceinline__ double warp_incl_scan(double x, int lane) {
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const double y = __shfl_up_sync(kFull, x, o);
     if (lane >= o) x += y;
   }
-  if (lane == 31) s_w[warp] = x;
-  __syncthreads();
-  double wbase = 0.0;
-  for (int ww = 0; ww < warp; ++ww) wbase += s_w[ww];
-  const double pre = s_base + wbase + x - f * (double)ssum;
-  const double target = s_target;
-  const int e0 = cs * chunk_elems<T>() + tid * E;
-  int cand = 0x7fffffff;
-  float run = 0.f;
+  return x;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_sample(SampArgs a) {
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, E = VEC * NV, SUB = sub_elems<T>();
+  const int lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const int nsub = (a.V + SUB - 1) / SUB;
+  if (gw >= (long long)a.B * nsub) return;
+  const int i = (int)(gw / nsub), u = (int)(gw - (long long)i * nsub);
+  const SeqRec r = a.rec[i];
+  if (r.mode != MODE_RESIDUAL && r.mode != MODE_BONUS) return;
+  const bool resid = r.mode == MODE_RESIDUAL;
+  double* wmass = a.mass + (long long)i * a.nchunks * kCWarps;
+  float* wmax = a.cmax + (long long)i * a.nchunks * kCWarps;
+
+  float w[E];
+  const float mu = sub_weights<T>(a, r, resid, u, w);
+  double m = 0.0;  // sub-chunk mass about its reference, in the select pass's order
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    run += w[e];
-    if (cand == 0x7fffffff && w[e] > 0.f && pre + f * (double)run > target) cand = e0 + e;
+  for (int v = 0; v < NV; ++v) {
+    float ls = 0.f;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) ls += w[v * VEC + e];
+    m += warp_sum_d((double)ls);
   }
-  if (cand != 0x7fffffff) atomicMin(&s_cand, cand);
-  __syncthreads();
-  int tok = s_cand;
-  if (tok == 0x7fffffff) {  // rounding corner: last positive-weight token of the chunk
-    int last = -1;
-#pragma unroll
-    for (int e = 0; e < E; ++e)
-      if (w[e] > 0.f) last = e0 + e;
-    __syncthreads();
-    if (tid == 0) s_cand = -1;
-    __syncthreads();
-    if (last >= 0) atomicMax(&s_cand, last);
-    __syncthreads();
-    tok = s_cand;
-    fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
+  int last = 0;
+  if (lane == 0) {
+    wmass[u] = m;
+    wmax[u] = mu;
+    __threadfence();
+    last = atomicAdd(a.counter + i, 1) == nsub - 1;
   }
-  if (tok >= e0 && tok < e0 + E) {
-    float run2 = 0.f;
-    double lo = pre, hi = pre;
+  if (!__shfl_sync(kFull, last, 0)) return;
+  __threadfence();
+
+  // ---- last warp of sequence i: select the token ----
+  float Mg = -INFINITY;
+  if (!resid) {
+    for (int s0 = lane; s0 < nsub; s0 += 32) Mg = max_nan(Mg, __ldcg(wmax + s0));
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const double before = pre + f * (double)run2;
-      run2 += w[e];
-      if (e0 + e == tok) {
-        lo = before;
-        hi = pre + f * (double)run2;
+    for (int o = 16; o > 0; o >>= 1) Mg = max_nan(Mg, __shfl_xor_sync(kFull, Mg, o));
+  }
+  auto scale_of = [&](int s0) -> double {  // sub-chunk mass scale to the common reference
+    if (resid) return 1.0;
+    const float ms = __ldcg(wmax + s0);
+    return ms == -INFINITY ? 0.0 : exp((double)ms - (double)Mg);
+  };
+  double R = 0.0;
+  for (int s0 = lane; s0 < nsub; s0 += 32) R += scale_of(s0) * __ldcg(wmass + s0);
+  R = warp_sum_d(R);
+  uint8_t fl = 0;
+  if (!(R > 0.0) || !isfinite(R)) {
+    if (lane == 0) {
+      // residual mass 0 (p <= q everywhere in fp32; D7 fallback) or a
+      // non-finite bonus row: no valid draw from these weights
+      if (resid && isfinite(R)) {
+        // D7: draw from p of the same target row (slow path, one lane)
+        const float M = r.M;
+        double tot = 0.0;
+        for (int v = 0; v < a.V; ++v)
+          tot += exp((double)load_logit<T>(reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t + v) - M);
+        const double target = r.u * tot;
+        double cum = 0.0;
+        int tok = 0;
+        for (int v = 0; v < a.V; ++v) {
+          const double wv = exp((double)load_logit<T>(reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t + v) - M);
+          cum += wv;
+          if (wv > 0.0) tok = v;
+          if (wv > 0.0 && cum > target) break;
+        }
+        a.emitted[r.slot] = tok;
+        if (a.flags) a.flags[r.slot] |= DSDE_FLAG_FALLBACK;
+      } else {
+        a.emitted[r.slot] = DSDE_PAD;
+        raise_device_error(a.err, DSDE_DERR_NONFINITE, i);
       }
     }
-    const double R = s_R;
+    return;
+  }
+  const double target = r.u * R;
+  // crossing sub-chunk: first u with prefix(u) > target (fallback: last with mass)
+  int us = -1, ulast = -1;
+  double base = 0.0, base_last = 0.0, cum = 0.0;
+  for (int g = 0; g < nsub; g += 32) {
+    const int s0 = g + lane;
+    const double ms = s0 < nsub ? scale_of(s0) * __ldcg(wmass + s0) : 0.0;
+    const double incl = warp_incl_scan(ms, lane);
+    const unsigned pos = __ballot_sync(kFull, ms > 0.0);
+    const unsigned cross = __ballot_sync(kFull, ms > 0.0 && cum + incl > target);
+    if (pos) {
+      const int lp = 31 - __clz(pos);
+      ulast = g + lp;
+      base_last = cum + __shfl_sync(kFull, incl - ms, lp);
+    }
+    if (cross) {
+      const int lc = __ffs(cross) - 1;
+      us = g + lc;
+      base = cum + __shfl_sync(kFull, incl - ms, lc);
+      break;
+    }
+    cum += __shfl_sync(kFull, incl, 31);
+  }
+  if (us < 0) {
+    us = ulast;
+    base = base_last;
+    fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
+  }
+  const double f = scale_of(us);
+  if (us != u) sub_weights<T>(a, r, resid, us, w);
+  int tok = -1;
+  double lo = 0.0, hi = 0.0;
+  int last_pos = -1;
+  double lp_lo = 0.0, lp_hi = 0.0;
+  double vbase = base;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    float ls = 0.f;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) ls += w[v * VEC + e];
+    const double incl = warp_incl_scan((double)ls, lane);
+    const double pre = vbase + f * (incl - (double)ls);
+    int cand = -1;
+    double clo = 0.0, chi = 0.0;
+    float run = 0.f;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const float before = run;
+      run += w[v * VEC + e];
+      const double cb = pre + f * (double)before, ca = pre + f * (double)run;
+      if (cand < 0 && w[v * VEC + e] > 0.f && ca > target) {
+        cand = e;
+        clo = cb;
+        chi = ca;
+      }
+    }
+    const unsigned bc = __ballot_sync(kFull, cand >= 0);
+    const int tok_base = us * SUB + v * 32 * VEC;
+    if (bc) {
+      const int lc = __ffs(bc) - 1;
+      tok = tok_base + lc * VEC + __shfl_sync(kFull, cand, lc);
+      lo = __shfl_sync(kFull, clo, lc);
+      hi = __shfl_sync(kFull, chi, lc);
+      break;
+    }
+    // remember the last positive-weight token for the rounding corner
+    int lpos = -1;
+    double llo = 0.0, lhi = 0.0;
+    {
+      float run2 = 0.f;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const float before = run2;
+        run2 += w[v * VEC + e];
+        if (w[v * VEC + e] > 0.f) {
+          lpos = e;
+          llo = pre + f * (double)before;
+          lhi = pre + f * (double)run2;
+        }
+      }
+    }
+    const unsigned bp = __ballot_sync(kFull, lpos >= 0);
+    if (bp) {
+      const int lp = 31 - __clz(bp);
+      last_pos = tok_base + lp * VEC + __shfl_sync(kFull, lpos, lp);
+      lp_lo = __shfl_sync(kFull, llo, lp);
+      lp_hi = __shfl_sync(kFull, lhi, lp);
+    }
+    vbase += f * __shfl_sync(kFull, incl, 31);
+  }
+  if (tok < 0) {  // rounding corner: u R within rounding of the sub-chunk total
+    tok = last_pos;
+    lo = lp_lo;
+    hi = lp_hi;
+    fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
+  }
+  if (lane == 0) {
     if (fabs(r.u - lo / R) < 1e-6 || fabs(r.u - hi / R) < 1e-6) fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
-    a.emitted[r.slot] = tok;
+    a.emitted[r.slot] = tok < 0 ? 0 : tok;
     if (a.flags) a.flags[r.slot] |= fl;
   }
 }
@@ -1082,8 +1084,9 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
              acc_len, emitted, kld, flags, ws.rec, ws.counter, err};
   k_finalize<T><<<(B + 3) / 4, 128, 0, s>>>(fa);
   SampArgs pa{B, V, nc, total, tl, ld_t, dl, ld_d, ws.part, ws.rec, ws.mass, emitted, flags,
-              ws.cmax, ws.counter};
-  k_sample<T><<<(unsigned)((long long)B * nc), kThreads, 0, s>>>(pa);
+              ws.cmax, ws.counter, err};
+  const long long warps = (long long)B * ((V + sub_elems<T>() - 1) / sub_elems<T>());
+  k_sample<T><<<(unsigned)((warps + kThreads / 32 - 1) / (kThreads / 32)), kThreads, 0, s>>>(pa);
   return cudaGetLastError();
 }
 

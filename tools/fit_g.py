@@ -1,7 +1,8 @@
-"""Fits the polynomial used by the verify kernel for g(w) = exp(-w) - 1 + w.
+"""Fits the polynomials used by the kernels for g(w) = exp(-w) - 1 + w.
 
-g(w) = u^2 h(u), u = -w, h(u) = (e^u - 1 - u) / u^2 on u in [-1, 1]. A degree-7
-Chebyshev interpolant (near-minimax) is converted to monomial form, rounded to
+g(w) = u^2 h(u), u = -w, h(u) = (e^u - 1 - u) / u^2 on |u| <= R. A Chebyshev
+interpolant (degree 5 on R = 1/2 for the stream kernel, degree 7 on R = 1 for
+the sampling kernel) (near-minimax) is converted to monomial form, rounded to
 fp32, and checked with fp32 Horner evaluation against an fp64 reference.
 Prints the coefficients (lowest degree first) and the max relative error.
 """
@@ -20,10 +21,11 @@ def h(u):
     return out
 
 
-def fit(deg=7, n=200):
-    x = np.cos(np.pi * (np.arange(n) + 0.5) / n)
-    mono = Ch.cheb2poly(Ch.chebfit(x, h(x), deg)).astype(np.float32)
-    xs = np.linspace(-1, 1, 200001)
+def fit(deg=7, R=1.0, n=200):
+    x = R * np.cos(np.pi * (np.arange(n) + 0.5) / n)
+    mono = Ch.cheb2poly(Ch.chebfit(x / R, h(x), deg))
+    mono = (mono / R ** np.arange(deg + 1)).astype(np.float32)
+    xs = np.linspace(-R, R, 200001)
     u = xs.astype(np.float32)
     p = np.float32(mono[-1])
     for c in mono[-2::-1]:
@@ -33,6 +35,11 @@ def fit(deg=7, n=200):
 
 
 if __name__ == "__main__":
-    mono, err = fit()
-    print("coefficients (u^0 .. u^7):", [repr(float(c)) for c in mono])
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--deg", type=int, default=7)
+    ap.add_argument("--range", type=float, default=1.0)
+    args = ap.parse_args()
+    mono, err = fit(args.deg, args.range)
+    print(f"coefficients (u^0 .. u^{args.deg}) on |u| <= {args.range}:", [repr(float(c)) for c in mono])
     print("max relative error (fp32 Horner):", err)
