@@ -225,6 +225,30 @@ __device__ __forceinline__ void unpack16<float>(uint4 raw, float* x) {
 }
 
 template <typename T>
+__device__ __forceinline__ T pad_bits();
+template <>
+__device__ __forceinline__ uint16_t pad_bits<uint16_t>() { return (uint16_t)0xF14Au; }  // bf16 ~ -1e30
+template <>
+__device__ __forceinline__ float pad_bits<float>() { return -1e30f; }
+
+// Elements h, h+1 (h even) of a lane's 4 x 16-byte vectors as an fp32 pair.
+template <typename T>
+__device__ __forceinline__ float2 pair_of(const uint4 (&r)[Traits<T>::NV], int h);
+template <>
+__device__ __forceinline__ float2 pair_of<uint16_t>(const uint4 (&r)[4], int h) {
+  const uint4 x = r[h >> 3];
+  const int k = (h & 7) >> 1;
+  const uint32_t w = k == 0 ? x.x : k == 1 ? x.y : k == 2 ? x.z : x.w;
+  return make_float2(bf16_lo(w), bf16_hi(w));
+}
+template <>
+__device__ __forceinline__ float2 pair_of<float>(const uint4 (&r)[4], int h) {
+  const uint4 x = r[h >> 2];
+  return (h & 3) == 0 ? make_float2(__uint_as_float(x.x), __uint_as_float(x.y))
+                      : make_float2(__uint_as_float(x.z), __uint_as_float(x.w));
+}
+
+template <typename T>
 __device__ __forceinline__ float2 diff2(float2 t, float2 d, float C);
 template <>
 __device__ __forceinline__ float2 diff2<uint16_t>(float2 t, float2 d, float C) {
@@ -453,50 +477,16 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
     mbar_wait(&full[s], round & 1u);
     const T* st = reinterpret_cast<const T*>(smem + s * 2 * ROWB);
     const T* sd = reinterpret_cast<const T*>(smem + s * 2 * ROWB + ROWB);
-    float t[E], d[E];
+    // the lane's 2 x 16 words (raw bf16 pairs / fp32) of the chunk; converted
+    // to fp32 pair by pair inside the statistics loop (low register pressure)
+    uint4 rt[NV], rd[NV];
     float mt = -INFINITY, md = -INFINITY;
     if (n_el == CH) {
-      uint4 rt[NV], rd[NV];
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const int e0 = warp * SL + (v * 32 + lane) * VEC;
         rt[v] = *reinterpret_cast<const uint4*>(st + e0);
         rd[v] = *reinterpret_cast<const uint4*>(sd + e0);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&consumed[s]);
-      if constexpr (sizeof(T) == 2) {
-        // two independent max chains per row (short dependency chains)
-        __nv_bfloat162 bt0 = *reinterpret_cast<const __nv_bfloat162*>(&rt[0].x), bt1 = bt0;
-        __nv_bfloat162 bd0 = *reinterpret_cast<const __nv_bfloat162*>(&rd[0].x), bd1 = bd0;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const uint32_t wt[4] = {rt[v].x, rt[v].y, rt[v].z, rt[v].w};
-          const uint32_t wd[4] = {rd[v].x, rd[v].y, rd[v].z, rd[v].w};
-#pragma unroll
-          for (int h = 0; h < 4; h += 2) {
-            bt0 = __hmax2_nan(bt0, *reinterpret_cast<const __nv_bfloat162*>(&wt[h]));  // NaN propagates
-            bt1 = __hmax2_nan(bt1, *reinterpret_cast<const __nv_bfloat162*>(&wt[h + 1]));
-            bd0 = __hmax2(bd0, *reinterpret_cast<const __nv_bfloat162*>(&wd[h]));
-            bd1 = __hmax2(bd1, *reinterpret_cast<const __nv_bfloat162*>(&wd[h + 1]));
-          }
-        }
-        const __nv_bfloat162 bt = __hmax2_nan(bt0, bt1), bd = __hmax2(bd0, bd1);
-        const float lo = __low2float(bt), hi = __high2float(bt);
-        mt = (lo != lo || hi != hi) ? NAN : fmaxf(lo, hi);
-        md = fmaxf(__low2float(bd), __high2float(bd));
-      }
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        unpack16<T>(rt[v], t + v * VEC);
-        unpack16<T>(rd[v], d + v * VEC);
-      }
-      if constexpr (sizeof(T) != 2) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          mt = max_nan(mt, t[e]);
-          md = fmaxf(md, d[e]);
-        }
       }
     } else {
       // last chunk of a row: bulk-copied part from shared memory, an unaligned
@@ -514,25 +504,57 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const int e0 = warp * SL + (v * 32 + lane) * VEC;
+        T tb[VEC], db[VEC];
 #pragma unroll
         for (int e = 0; e < VEC; ++e) {
           const int idx = e0 + e;
-          float tv = -1e30f, dv = -1e30f;
+          tb[e] = pad_bits<T>();
+          db[e] = pad_bits<T>();
           if (idx < bulk_el) {
-            tv = load_logit_smem(st + idx);
-            dv = load_logit_smem(sd + idx);
+            tb[e] = st[idx];
+            db[e] = sd[idx];
           } else if (idx < n_el) {
-            tv = load_logit<T>(reinterpret_cast<const T*>(a.tl) + trow * a.ld_t + c0 + idx);
-            dv = load_logit<T>(reinterpret_cast<const T*>(a.dl) + it.r * a.ld_d + c0 + idx);
+            tb[e] = reinterpret_cast<const T*>(a.tl)[trow * a.ld_t + c0 + idx];
+            db[e] = reinterpret_cast<const T*>(a.dl)[it.r * a.ld_d + c0 + idx];
           }
-          t[v * VEC + e] = tv;
-          d[v * VEC + e] = dv;
-          mt = max_nan(mt, tv);
-          md = fmaxf(md, dv);
+        }
+        rt[v] = *reinterpret_cast<const uint4*>(tb);
+        rd[v] = *reinterpret_cast<const uint4*>(db);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&consumed[s]);
+    if constexpr (sizeof(T) == 2) {
+      // two independent max chains per row (short dependency chains)
+      __nv_bfloat162 bt0 = *reinterpret_cast<const __nv_bfloat162*>(&rt[0].x), bt1 = bt0;
+      __nv_bfloat162 bd0 = *reinterpret_cast<const __nv_bfloat162*>(&rd[0].x), bd1 = bd0;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const uint32_t wt[4] = {rt[v].x, rt[v].y, rt[v].z, rt[v].w};
+        const uint32_t wd[4] = {rd[v].x, rd[v].y, rd[v].z, rd[v].w};
+#pragma unroll
+        for (int h = 0; h < 4; h += 2) {
+          bt0 = __hmax2_nan(bt0, *reinterpret_cast<const __nv_bfloat162*>(&wt[h]));  // NaN propagates
+          bt1 = __hmax2_nan(bt1, *reinterpret_cast<const __nv_bfloat162*>(&wt[h + 1]));
+          bd0 = __hmax2(bd0, *reinterpret_cast<const __nv_bfloat162*>(&wd[h]));
+          bd1 = __hmax2(bd1, *reinterpret_cast<const __nv_bfloat162*>(&wd[h + 1]));
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&consumed[s]);
+      const __nv_bfloat162 bt = __hmax2_nan(bt0, bt1), bd = __hmax2(bd0, bd1);
+      const float lo = __low2float(bt), hi = __high2float(bt);
+      mt = (lo != lo || hi != hi) ? NAN : fmaxf(lo, hi);
+      md = fmaxf(__low2float(bd), __high2float(bd));
+    } else {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const uint32_t wt[4] = {rt[v].x, rt[v].y, rt[v].z, rt[v].w};
+        const uint32_t wd[4] = {rd[v].x, rd[v].y, rd[v].z, rd[v].w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          mt = max_nan(mt, __uint_as_float(wt[h]));
+          md = fmaxf(md, __uint_as_float(wd[h]));
+        }
+      }
     }
     // warp reference: M = max t (NaN if any t is NaN), C = M - max d
     float M = warp_max(mt);
@@ -552,7 +574,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
       float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
 #pragma unroll
       for (int h = 0; h < E; h += 2) {
-        const float2 tt = make_float2(t[h], t[h + 1]), dd = make_float2(d[h], d[h + 1]);
+        const float2 tt = pair_of<T>(rt, h), dd = pair_of<T>(rd, h);
         const float2 xt = __ffma2_rn(tt, L2, nML2);
         const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
         const float2 w = diff2<T>(tt, dd, Cw);
