@@ -557,9 +557,23 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
       }
     }
     // warp reference: M = max t (NaN if any t is NaN), C = M - max d
-    float M = warp_max(mt);
+    float M, Dmax;
+    if constexpr (sizeof(T) == 2) {
+      // both maxima are bf16 values: one packed shuffle chain
+      __nv_bfloat162 pk = __floats2bfloat162_rn(mt, md);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t y = __shfl_xor_sync(kFull, *reinterpret_cast<const uint32_t*>(&pk), o);
+        pk = __hmax2_nan(pk, *reinterpret_cast<const __nv_bfloat162*>(&y));
+      }
+      M = __low2float(pk);
+      const float dh = __high2float(pk);
+      Dmax = dh == dh ? dh : warp_max(md);  // all-NaN d in some lane: NaN-ignoring max
+    } else {
+      M = warp_max(mt);
+      Dmax = warp_max(md);
+    }
     if (__any_sync(kFull, mt != mt)) M = NAN;
-    const float Dmax = warp_max(md);
     const uint32_t sb = round & 1u, su = round >> 1;  // slot set (s, sb), its su-th use
     WarpPartial p;
     if (M <= -1e30f) {  // slice beyond V (padding only): an empty partial (NaN is not empty)
@@ -576,20 +590,20 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
       for (int h = 0; h < E; h += 2) {
         const float2 tt = pair_of<T>(rt, h), dd = pair_of<T>(rd, h);
         const float2 xt = __ffma2_rn(tt, L2, nML2);
+        const float2 arg = __ffma2_rn(dd, L2, nDL2);  // (d - max d) log2 e <= 0
         const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
+        const float2 f = make_float2(fast_exp2(arg.x), fast_exp2(arg.y));
         const float2 w = diff2<T>(tt, dd, Cw);
+        // h(-w) by Estrin's scheme (dependency depth 4 instead of 7)
+        const float2 w2 = __fmul2_rn(w, w);
+        const float2 q01 = __ffma2_rn(K1, w, K0), q23 = __ffma2_rn(K3, w, K2);
+        const float2 q45 = __ffma2_rn(K5, w, K4), q67 = __ffma2_rn(K7, w, K6);
+        const float2 w4 = __fmul2_rn(w2, w2);
+        const float2 q03 = __ffma2_rn(q23, w2, q01), q47 = __ffma2_rn(q67, w2, q45);
+        const float2 pp = __ffma2_rn(q47, w4, q03);
         S2 = __fadd2_rn(S2, e);
         A2 = __ffma2_rn(e, w, A2);
-        float2 pp = __ffma2_rn(K7, w, K6);
-        pp = __ffma2_rn(pp, w, K5);
-        pp = __ffma2_rn(pp, w, K4);
-        pp = __ffma2_rn(pp, w, K3);
-        pp = __ffma2_rn(pp, w, K2);
-        pp = __ffma2_rn(pp, w, K1);
-        pp = __ffma2_rn(pp, w, K0);
-        const float2 sm = __fmul2_rn(__fmul2_rn(e, __fmul2_rn(w, w)), pp);
-        const float2 arg = __ffma2_rn(dd, L2, nDL2);  // (d - max d) log2 e <= 0
-        const float2 f = make_float2(fast_exp2(arg.x), fast_exp2(arg.y));
+        const float2 sm = __fmul2_rn(__fmul2_rn(e, w2), pp);
         const float2 bg = __ffma2_rn(e, w, __fadd2_rn(f, make_float2(-e.x, -e.y)));
         const float2 term =
             make_float2(fabsf(w.x) < 1.f ? sm.x : bg.x, fabsf(w.y) < 1.f ? sm.y : bg.y);
