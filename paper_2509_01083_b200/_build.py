@@ -60,6 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xptxas", "-v" if verbose else "-O3",
            f"-I{INCLUDE}", f"-I{CSRC}", f"-I{_nccl_include()}",
            "-Xlinker", f"--version-script={os.path.join(CSRC, 'exports.map')}",
+           *os.environ.get("DSDE_NVCC_FLAGS", "").split(),
            "-o", LIB + ".tmp", *sources(), "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

@@ -276,7 +276,14 @@ __device__ __forceinline__ float2 diff2<float>(float2 t, float2 d, float C) {
 // ---------------------------------------------------------------------------
 constexpr int kCWarps = 8;
 constexpr int kWsThreads = 32 * (kCWarps + 2);  // + TMA producer warp + merger warp
-constexpr int kWsStages = 3;
+#ifndef DSDE_WS_STAGES
+#define DSDE_WS_STAGES 3
+#endif
+#ifndef DSDE_WS_CTAS
+#define DSDE_WS_CTAS 2
+#endif
+constexpr int kWsStages = DSDE_WS_STAGES;  // stages per CTA
+constexpr int kWsCtas = DSDE_WS_CTAS;      // CTAs per SM
 
 struct WarpPartial {  // 24 bytes
   float S, A, D;      // about (M, C) of the warp slice
@@ -313,21 +320,29 @@ struct ItemCursor {
   }
 };
 
-template <typename T>
-__device__ __forceinline__ void issue_item(const StreamTmaArgs& a, long long r, int c, uint8_t* dst,
-                                           uint64_t* bar) {
-  constexpr int CH = chunk_elems<T>(), ROWB = stage_row_bytes<T>();
-  int lo = 0, hi = a.B - 1;  // sequence of draft row r
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(a.cu_sl + mid) <= r) lo = mid; else hi = mid - 1;
+// Sequence of draft row r, by a warp-cooperative forward scan from `seq`
+// (rows only move forward for a CTA): 32 cu_sl entries per round trip.
+__device__ __forceinline__ int seq_of_row(const int32_t* cu_sl, int B, int seq, long long r) {
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    const int j = seq + 1 + lane;
+    const bool le = j <= B - 1 && __ldg(cu_sl + j) <= r;  // sequence j starts at or before r
+    const unsigned m = __ballot_sync(kFull, le);
+    seq += __popc(m);
+    if (m != kFull) return seq;
   }
+}
+
+template <typename T>
+__device__ __forceinline__ void issue_item(const StreamTmaArgs& a, long long r, int c, int seq,
+                                           uint8_t* dst, uint64_t* bar) {
+  constexpr int CH = chunk_elems<T>(), ROWB = stage_row_bytes<T>();
   const int c0 = c * CH;
   const int n_el = min(CH, a.V - c0);
   const uint32_t bytes = (uint32_t)(n_el * (int)sizeof(T)) & ~15u;
   if (bytes) {
     mbar_arrive_expect_tx(bar, 2 * bytes);
-    bulk_g2s(dst, reinterpret_cast<const T*>(a.tl) + (r + lo) * a.ld_t + c0, bytes, bar);
+    bulk_g2s(dst, reinterpret_cast<const T*>(a.tl) + (r + seq) * a.ld_t + c0, bytes, bar);
     bulk_g2s(dst + ROWB, reinterpret_cast<const T*>(a.dl) + r * a.ld_d + c0, bytes, bar);
   } else {
     mbar_arrive(bar);
@@ -335,7 +350,7 @@ __device__ __forceinline__ void issue_item(const StreamTmaArgs& a, long long r, 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
+__global__ void __launch_bounds__(kWsThreads, kWsCtas) k_stream_ws(StreamTmaArgs a) {
   constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, E = VEC * NV, CH = chunk_elems<T>();
   constexpr int ROWB = stage_row_bytes<T>();
   constexpr int SL = CH / kCWarps;  // elements of a chunk owned by one consumer warp
@@ -364,25 +379,30 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
 
   if (warp == kCWarps) {
     // ---------------- TMA producer: refill a stage once it is consumed ----------------
-    if (lane == 0) {
-      ItemCursor it;
-      it.init(blockIdx.x, a.nchunks);
-      long long q = blockIdx.x;
-      for (int s = 0; s < kWsStages && q < n_items; ++s, q += G) {
-        issue_item<T>(a, it.r, it.c, smem + s * 2 * ROWB, &full[s]);
-        it.advance(dr, dc, a.nchunks);
-      }
-      int s = 0;
-      uint32_t round = 0;
-      for (; q < n_items; q += G) {
-        mbar_wait(&consumed[s], round & 1u);
+    // (the whole warp tracks the row -> sequence cursor; lane 0 issues the copies;
+    // the next item's addresses are resolved before waiting for its stage)
+    ItemCursor it;
+    it.init(blockIdx.x, a.nchunks);
+    int seq = 0;
+    long long q = blockIdx.x;
+    for (int s = 0; s < kWsStages && q < n_items; ++s, q += G) {
+      seq = seq_of_row(a.cu_sl, a.B, seq, it.r);
+      if (lane == 0) issue_item<T>(a, it.r, it.c, seq, smem + s * 2 * ROWB, &full[s]);
+      it.advance(dr, dc, a.nchunks);
+    }
+    int s = 0;
+    uint32_t round = 0;
+    for (; q < n_items; q += G) {
+      seq = seq_of_row(a.cu_sl, a.B, seq, it.r);
+      mbar_wait(&consumed[s], round & 1u);
+      if (lane == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_item<T>(a, it.r, it.c, smem + s * 2 * ROWB, &full[s]);
-        it.advance(dr, dc, a.nchunks);
-        if (++s == kWsStages) {
-          s = 0;
-          ++round;
-        }
+        issue_item<T>(a, it.r, it.c, seq, smem + s * 2 * ROWB, &full[s]);
+      }
+      it.advance(dr, dc, a.nchunks);
+      if (++s == kWsStages) {
+        s = 0;
+        ++round;
       }
     }
     return;
@@ -586,6 +606,14 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
       const float ML2 = M * kLog2e, DL2 = Dmax * kLog2e;
       const float2 nML2 = make_float2(-ML2, -ML2), nDL2 = make_float2(-DL2, -DL2);
       float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
+#ifdef DSDE_STREAM_LITE  // measurement experiment only: memory pipeline with minimal math
+#pragma unroll
+      for (int h = 0; h < E; h += 2) {
+        const float2 tt = pair_of<T>(rt, h), dd = pair_of<T>(rd, h);
+        S2 = __fadd2_rn(S2, tt);
+        A2 = __fadd2_rn(A2, dd);
+      }
+#else
 #pragma unroll
       for (int h = 0; h < E; h += 2) {
         const float2 tt = pair_of<T>(rt, h), dd = pair_of<T>(rd, h);
@@ -609,6 +637,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_stream_ws(StreamTmaArgs a) {
             make_float2(fabsf(w.x) < 1.f ? sm.x : bg.x, fabsf(w.y) < 1.f ? sm.y : bg.y);
         D2 = __fadd2_rn(D2, term);
       }
+#endif
       float S = S2.x + S2.y, A = A2.x + A2.y, D = D2.x + D2.y;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1121,7 +1150,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long long items = (long long)total * nc;
-    const int grid = (int)std::min<long long>(items, 2LL * sms);
+    const int grid = (int)std::min<long long>(items, (long long)kWsCtas * sms);
     StreamTmaArgs ta{tl, ld_t, dl, ld_d, cu_sl, B, V, nc, total, ws.part};
     k_stream_ws<T><<<grid, kWsThreads, smem, s>>>(ta);
   }
