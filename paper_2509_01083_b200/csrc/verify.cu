@@ -24,6 +24,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 
 #include <cuda_bf16.h>
 
@@ -83,7 +85,7 @@ struct VerifyWs {
   SeqRec* rec;         // [B]
   double* mass;        // [B * nchunks * 8] draw-weight mass per warp sub-chunk
   float* cmax;         // [B * nchunks * 8] reference of each sub-chunk mass (bonus)
-  int* counter;        // [B] chunks done per sequence (last-block election)
+  int* counter;        // [3 * B] per-sequence counters / flags (zeroed per call)
 };
 
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -100,7 +102,7 @@ inline size_t ws_layout(int B, int total, int V, dsde_dtype dt, VerifyWs* ws, ch
   const size_t r_bytes = align256(sizeof(SeqRec) * (size_t)B);
   const size_t m_bytes = align256(sizeof(double) * (size_t)B * nc * 8);  // per warp sub-chunk
   const size_t x_bytes = align256(sizeof(float) * (size_t)B * nc * 8);
-  const size_t c_bytes = align256(sizeof(int) * (size_t)B);
+  const size_t c_bytes = align256(sizeof(int) * (size_t)B * 3);
   if (ws) {
     ws->part = reinterpret_cast<ChunkPartial*>(base + off);
     ws->rec = reinterpret_cast<SeqRec*>(base + off + p_bytes);
@@ -1133,12 +1135,39 @@ __global__ void __launch_bounds__(kThreads) k_sample(SampArgs a) {
   }
 }
 
+#include "verify_fused.cuh"
+
 template <typename T>
 cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const int32_t* tokens,
                           const void* tl, int64_t ld_t, const void* dl, int64_t ld_d,
                           const uint64_t* seeds, int32_t* acc_len, int32_t* emitted, float* kld,
                           uint8_t* flags, const VerifyWs& ws, int32_t* err, cudaStream_t s) {
   const int nc = (V + chunk_elems<T>() - 1) / chunk_elems<T>();
+  if (getenv("DSDE_LEGACY_VERIFY") == nullptr) {
+    // one persistent, cooperative launch for a1-a4 (verify_fused.cuh)
+    constexpr int smem = fused_smem<T>();
+    static int grid_per_dev[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& grid = grid_per_dev[dev & 63];
+    if (grid == 0) {
+      cudaFuncSetAttribute(k_verify_fused<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      int sms = 148, per_sm = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_verify_fused<T>, kWsThreads, smem);
+      grid = std::max(1, std::min(per_sm, kWsCtas)) * sms;
+    }
+    const double rows_per_seq = std::max(1.0, (double)total / B);
+    int lag = (int)std::ceil(2.0 * grid * kWsStages / (nc * (rows_per_seq + 1.0)));
+    lag = std::max(1, std::min(lag, B));
+    cudaMemsetAsync(ws.counter, 0, sizeof(int) * 3 * (size_t)B, s);
+    FusedArgs fa{B, V, nc, total, lag, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, acc_len, emitted,
+                 kld, flags, ws.part, ws.rec, ws.mass, ws.cmax, ws.counter, err};
+    void* args[] = {&fa};
+    return cudaLaunchCooperativeKernel((const void*)k_verify_fused<T>, dim3(grid), dim3(kWsThreads),
+                                       args, smem, s);
+  }
+  // legacy three-launch path (kept for A/B measurements)
   if (total > 0) {
     static bool attr_set = false;
     constexpr int smem = stream_ws_smem<T>();
