@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include <cuda_bf16.h>
@@ -102,7 +103,7 @@ inline size_t ws_layout(int B, int total, int V, dsde_dtype dt, VerifyWs* ws, ch
   const size_t r_bytes = align256(sizeof(SeqRec) * (size_t)B);
   const size_t m_bytes = align256(sizeof(double) * (size_t)B * nc * 8);  // per warp sub-chunk
   const size_t x_bytes = align256(sizeof(float) * (size_t)B * nc * 8);
-  const size_t c_bytes = align256(sizeof(int) * (size_t)B * 3);
+  const size_t c_bytes = align256(sizeof(int) * ((size_t)B * 5 + 8));  // counters + event queue
   if (ws) {
     ws->part = reinterpret_cast<ChunkPartial*>(base + off);
     ws->rec = reinterpret_cast<SeqRec*>(base + off + p_bytes);
@@ -168,20 +169,19 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
-// Blocking wait on an mbarrier phase. The suspend-time hint lets the warp sleep
-// in hardware until the phase completes instead of re-issuing the probe, so
-// waiting producer / merger / consumer warps do not steal issue slots.
+// Blocking wait on an mbarrier phase (try_wait blocks in hardware for a
+// system-defined time before returning false; the loop re-probes).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
       "@P1 bra DONE;\n"
       "bra LAB_WAIT;\n"
       "DONE:\n"
       "}\n" ::"r"(smem_addr(bar)),
-      "r"(parity), "r"(0x100000u)
+      "r"(parity)
       : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -398,7 +398,6 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtas) k_stream_ws(StreamTmaArgs
       seq = seq_of_row(a.cu_sl, a.B, seq, it.r);
       mbar_wait(&consumed[s], round & 1u);
       if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue_item<T>(a, it.r, it.c, seq, smem + s * 2 * ROWB, &full[s]);
       }
       it.advance(dr, dc, a.nchunks);
@@ -1154,17 +1153,22 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
       cudaFuncSetAttribute(k_verify_fused<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       int sms = 148, per_sm = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_verify_fused<T>, kWsThreads, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_verify_fused<T>, kFzThreads, smem);
       grid = std::max(1, std::min(per_sm, kWsCtas)) * sms;
     }
-    const double rows_per_seq = std::max(1.0, (double)total / B);
-    int lag = (int)std::ceil(2.0 * grid * kWsStages / (nc * (rows_per_seq + 1.0)));
+    // draw items of a sequence are placed `lag` sequence blocks after its
+    // stream items (all at the end by default: no pipeline waits on finalize)
+    int lag = B;
+    if (const char* e = getenv("DSDE_LAG")) lag = atoi(e) > 0 ? atoi(e) : B;
     lag = std::max(1, std::min(lag, B));
-    cudaMemsetAsync(ws.counter, 0, sizeof(int) * 3 * (size_t)B, s);
-    FusedArgs fa{B, V, nc, total, lag, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, acc_len, emitted,
-                 kld, flags, ws.part, ws.rec, ws.mass, ws.cmax, ws.counter, err};
+    cudaMemsetAsync(ws.counter, 0, sizeof(int) * (3 * (size_t)B + 2), s);
+    cudaMemsetAsync(ws.counter + 3 * (size_t)B + 2, 0xff, sizeof(int) * 2 * (size_t)B, s);
+    const int exp_flags = getenv("DSDE_EXP_FLAGS") ? atoi(getenv("DSDE_EXP_FLAGS")) : 0;
+    FusedArgs fa{B, V, nc, total, lag, exp_flags, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, acc_len, emitted,
+                 kld, flags, ws.part, ws.rec, ws.mass, ws.cmax, ws.counter,
+                 ws.counter + 3 * (size_t)B + 2, err};
     void* args[] = {&fa};
-    return cudaLaunchCooperativeKernel((const void*)k_verify_fused<T>, dim3(grid), dim3(kWsThreads),
+    return cudaLaunchCooperativeKernel((const void*)k_verify_fused<T>, dim3(grid), dim3(kFzThreads),
                                        args, smem, s);
   }
   // legacy three-launch path (kept for A/B measurements)

@@ -25,7 +25,7 @@
 enum { IT_STREAM = 0, IT_RESID = 1, IT_BONUS = 2, IT_NONE = 3 };
 
 struct FusedArgs {
-  int B, V, nchunks, total, lag;
+  int B, V, nchunks, total, lag, exp_flags;
   const int32_t* cu_sl;
   const int32_t* tokens;
   const void* tl;
@@ -41,9 +41,20 @@ struct FusedArgs {
   SeqRec* rec;         // [B]
   double* smass;       // [B * nc * 8] draw mass per warp sub-chunk
   float* sref;         // [B * nc * 8] its reference (bonus)
-  int* counters;       // [3 * B]: stream chunks done, draw chunks done, record published
+  int* counters;       // [3 * B + 2]: stream chunks done, draw chunks done, record published,
+                       //   event-queue tail, head
+  int* evq;            // [2 * B] finisher events (seq << 1 | kind), -1 = not yet written
   int32_t* err;
 };
+
+constexpr int kFzThreads = 32 * (kCWarps + 2);  // + producer warp, merger/finisher warp
+
+// push a finisher event (kind 0 = finalize, 1 = select) onto the global queue
+__device__ __forceinline__ void push_event(const FusedArgs& a, int seq, int kind) {
+  const int pos = atomicAdd(a.counters + 3 * a.B, 1);
+  __threadfence();
+  atomicExch(a.evq + pos, (seq << 1) | kind);
+}
 
 struct DrawSlot {  // 16 bytes
   double m;
@@ -530,11 +541,61 @@ __device__ void select_seq(const FusedArgs& a, int i) {
   }
 }
 
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Takes one published finisher event, if any, and processes it (warp-wide).
+// Events are finalize (a2-a3) or select (a4) of a sequence; any idle merger of
+// any CTA can take any event, so a CTA that completes a sequence is not stalled
+// by that sequence's finalize. Returns false if no event was available.
+template <typename T>
+__device__ bool take_event(const FusedArgs& a) {
+  const int lane = threadIdx.x & 31;
+  int got = -1;
+  if (lane == 0) {
+    volatile const int* ctl = a.counters + 3 * a.B;
+    const int h = ctl[1], t = ctl[0];
+    if (h < t && atomicCAS(a.counters + 3 * a.B + 1, h, h + 1) == h) got = h;
+  }
+  got = __shfl_sync(kFull, got, 0);
+  if (got < 0) return false;
+  int ev = -1;
+  if (lane == 0)
+    while ((ev = *reinterpret_cast<volatile const int*>(a.evq + got)) < 0) __nanosleep(64);
+  ev = __shfl_sync(kFull, ev, 0);
+  __threadfence();
+  const int seq = ev >> 1;
+  if ((ev & 1) == 0) {
+    finalize_seq<T>(a, seq);
+  } else if (__ldcg(&a.rec[seq].mode) != MODE_ERROR) {
+    select_seq<T>(a, seq);
+  }
+  return true;
+}
+
 // ---------------------------------------------------------------------------
 // the persistent kernel
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(kWsThreads, kWsCtas) k_verify_fused(FusedArgs a) {
+__global__ void __launch_bounds__(kFzThreads, kWsCtas) k_verify_fused(FusedArgs a) {
   constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, E = VEC * NV, CH = chunk_elems<T>();
   constexpr int ROWB = stage_row_bytes<T>();
   constexpr int SL = CH / kCWarps;
@@ -592,15 +653,21 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtas) k_verify_fused(FusedArgs 
         drow = (long long)__ldg(a.cu_sl + it.seq) + it.j;
         trow = drow + it.seq;
       } else {
+        // wait until the record is published: a relaxed volatile poll (an
+        // ld.acquire.gpu would invalidate this SM's L1 on every probe), then
+        // one fence for acquire ordering
         if (lane == 0)
-          while (ld_acquire(a.counters + 2 * a.B + it.seq) == 0) __nanosleep(256);
+          while (*reinterpret_cast<volatile const int*>(a.counters + 2 * a.B + it.seq) == 0)
+            __nanosleep(128);
         __syncwarp();
+        __threadfence();
         const int mode = __ldcg(&a.rec[it.seq].mode);
         it.type = mode == MODE_RESIDUAL ? IT_RESID : mode == MODE_BONUS ? IT_BONUS : IT_NONE;
         trow = __ldcg(&a.rec[it.seq].trow);
         drow = __ldcg(&a.rec[it.seq].drow);
       }
       if (round > 0) mbar_wait(&consumed[s], (round - 1) & 1u);
+
       if (lane == 0) {
         StageDesc dsc;
         dsc.type = it.type;
@@ -608,7 +675,6 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtas) k_verify_fused(FusedArgs 
         dsc.c = it.c;
         dsc.j = it.j;
         sdesc[s] = dsc;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         const int c0 = it.c * CH;
         const int n_el = min(CH, a.V - c0);
         const uint32_t bytes = (uint32_t)(n_el * (int)sizeof(T)) & ~15u;
@@ -632,12 +698,28 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtas) k_verify_fused(FusedArgs 
 
   if (warp == kCWarps + 1) {
     // ---------------- merger / finisher ----------------
+#ifdef DSDE_DEBUG_TIMING
+    const unsigned long long t_start = gtimer();
+    unsigned long long t_stream_done = 0, t_ev = 0;
+    int n_ev = 0;
+    bool in_stream = true;
+#endif
     int blk = 0, s = 0;
     uint32_t round = 0;
     for (long long q = blockIdx.x; q < n_items; q += G) {
       const ItemInfo it = decode_item(a, q, blk);
       const uint32_t b = round & 1u, u = round >> 1;
-      mbar_wait(&ready[2 * s + b], u & 1u);
+#ifdef DSDE_DEBUG_TIMING
+      if (in_stream && it.type != IT_STREAM) { t_stream_done = gtimer(); in_stream = false; }
+#endif
+      while (!mbar_test(&ready[2 * s + b], u & 1u)) {
+#ifdef DSDE_DEBUG_TIMING
+        const unsigned long long te = gtimer();
+        if (take_event<T>(a)) { t_ev += gtimer() - te; ++n_ev; } else __nanosleep(32);
+#else
+        if (!take_event<T>(a)) __nanosleep(32);
+#endif
+      }
       if (it.type == IT_STREAM) {
         const WarpPartial* wp = slots + (s * 2 + b) * kCWarps;
         float Mr = -INFINITY, Dx = -INFINITY;
@@ -694,37 +776,46 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtas) k_verify_fused(FusedArgs 
           const int k = __ldg(a.cu_sl + it.seq + 1) - __ldg(a.cu_sl + it.seq);
           last = atomicAdd(a.counters + it.seq, 1) == k * nc - 1;
         }
-        if (__shfl_sync(kFull, last, 0)) {
-          __threadfence();
-          finalize_seq<T>(a, it.seq);
-        }
+        if (lane == 0 && last) push_event(a, it.seq, 0);
       } else {
         const DrawSlot* ds = dslots + (s * 2 + b) * kCWarps;
         const int ity = ds[0].pad;  // item type posted by the consumers
         const DrawSlot p = ds[lane < kCWarps ? lane : 0];
         __syncwarp();
         if (lane == 0) mbar_arrive(&freeb[2 * s + b]);
-        if (ity != IT_NONE) {
+        if (ity != IT_NONE && lane < kCWarps) {
           const long long base = ((long long)it.seq * nc + it.c) * kCWarps;
-          if (lane < kCWarps) {
-            a.smass[base + lane] = p.m;
-            a.sref[base + lane] = p.ref;
-          }
-          __threadfence();
-          __syncwarp();
-          int last = 0;
-          if (lane == 0) last = atomicAdd(a.counters + a.B + it.seq, 1) == nc - 1;
-          if (__shfl_sync(kFull, last, 0)) {
-            __threadfence();
-            select_seq<T>(a, it.seq);
-          }
+          a.smass[base + lane] = p.m;
+          a.sref[base + lane] = p.ref;
         }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0 && atomicAdd(a.counters + a.B + it.seq, 1) == nc - 1) push_event(a, it.seq, 1);
       }
       if (++s == kWsStages) {
         s = 0;
         ++round;
       }
     }
+    // all own items merged: help with the remaining finisher events
+#ifdef DSDE_DEBUG_TIMING
+    const unsigned long long t_items = gtimer();
+#endif
+    while (true) {
+#ifdef DSDE_DEBUG_TIMING
+      const unsigned long long te = gtimer();
+      if (take_event<T>(a)) { t_ev += gtimer() - te; ++n_ev; continue; }
+#else
+      if (take_event<T>(a)) continue;
+#endif
+      if (*reinterpret_cast<volatile const int*>(a.counters + 3 * a.B + 1) >= 2 * a.B) break;
+      __nanosleep(128);
+    }
+#ifdef DSDE_DEBUG_TIMING
+    if (lane == 0)
+      printf("T cta=%d start=%llu stream_done=%llu items_done=%llu end=%llu ev_ns=%llu n_ev=%d\n", blockIdx.x,
+             t_start, t_stream_done, t_items, gtimer(), t_ev, n_ev);
+#endif
     return;
   }
 
@@ -743,6 +834,7 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtas) k_verify_fused(FusedArgs 
   for (long long q = blockIdx.x; q < n_items; q += G) {
     mbar_wait(&full[s], round & 1u);
     const StageDesc dsc = sdesc[s];
+
     const T* st = reinterpret_cast<const T*>(smem + s * 2 * ROWB);
     const T* sd = reinterpret_cast<const T*>(smem + s * 2 * ROWB + ROWB);
     const int c0 = dsc.c * CH;
