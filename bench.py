@@ -254,7 +254,8 @@ def run(args):
         bonus = int(np.sum(acc == k))
         rows = 2 * n + bonus
         vbytes = rows * V * 2 + n * 4 + (n + B) * 8 + n * 4 + (n + B) * 5 + B * 4
-        rec.append(dict(inp=inp, n=n, k=k.copy(), rows=rows, vbytes=vbytes, next=nx))
+        sbytes = 2 * n * V * 2  # k_stream_ws: target + draft row of every draft position
+        rec.append(dict(inp=inp, n=n, k=k.copy(), rows=rows, vbytes=vbytes, sbytes=sbytes, next=nx))
         stats["pos"] += n
         stats["acc"] += int(acc.sum())
         stats["bonus"] += bonus
@@ -281,6 +282,8 @@ def run(args):
         dist.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
+    state.profile_read()  # drop anything recorded before the timed region
+    state.profile(True)
     with sampler:
         t_start.record(stream)
         for j in range(args.steps):
@@ -292,24 +295,29 @@ def run(args):
             step.signal_and_cap(i.cu_sl)
         t_end.record(stream)
         torch.cuda.synchronize()
+    state.profile(False)
+    phase_ms, phase_calls = state.profile_read()
     if ws > 1:
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
     verify_ms = sum(a.elapsed_time(b) for a, b in ev)
+    stream_ms = phase_ms["stream"]
     positions = sum(rec[(args.warmup + j) % R]["n"] for j in range(args.steps))
     vbytes = sum(rec[(args.warmup + j) % R]["vbytes"] for j in range(args.steps))
+    sbytes = sum(rec[(args.warmup + j) % R]["sbytes"] for j in range(args.steps))
     code, _ = state.device_error()
     if code != 0:
         raise SystemExit(f"device error {code} during the bench")
 
-    t = torch.tensor([elapsed_ms, verify_ms, float(positions), float(vbytes)], dtype=torch.float64, device=dev)
+    t = torch.tensor([elapsed_ms, verify_ms, stream_ms, float(positions), float(vbytes), float(sbytes)],
+                     dtype=torch.float64, device=dev)
     if ws > 1:
-        mx = t[:2].clone()
+        mx = t[:3].clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        tot = t[2:].clone()
+        tot = t[3:].clone()
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-        elapsed_ms, verify_ms = float(mx[0]), float(mx[1])
-        positions, vbytes = float(tot[0]), float(tot[1])
+        elapsed_ms, verify_ms, stream_ms = float(mx[0]), float(mx[1]), float(mx[2])
+        positions, vbytes, sbytes = float(tot[0]), float(tot[1]), float(tot[2])
     value = positions / (elapsed_ms / 1e3)
 
     # ---- e2e through the public API from pinned host buffers (rank-local, max over ranks)
@@ -322,22 +330,29 @@ def run(args):
 
     if rank == 0:
         peak, peak_kind = _peaks()
-        ach = (vbytes / ws) / (verify_ms / 1e3) / 1e9 if verify_ms > 0 else None
+        # dominant kernel: k_stream_ws (a1), timed by the library's per-launch events
+        ach = (sbytes / ws) / (stream_ms / 1e3) / 1e9 if stream_ms > 0 else None
+        vach = (vbytes / ws) / (verify_ms / 1e3) / 1e9 if verify_ms > 0 else None
         traffic = _traffic_record(f"cfg{args.config}")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": _config_dict(args, cfg, ws),
-            "roofline": {"bound": "hbm", "kernel": "dsde_verify (verify pass: k_stream + finalize + sample)",
+            "roofline": {"bound": "hbm", "kernel": "k_stream_ws (a1: target + draft row of every draft position)",
                          "achieved": ach, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": (ach / peak) if ach else None,
                          "traffic": traffic,
-                         "algorithmic_bytes_per_launch": vbytes / ws / args.steps,
-                         "avg_launch_ms": verify_ms / args.steps},
+                         "algorithmic_bytes_per_launch": sbytes / ws / args.steps,
+                         "avg_launch_ms": stream_ms / args.steps},
+            "verify_pass": {"kernels": list(phase_ms), "ms_per_step": {k: v / args.steps for k, v in phase_ms.items()},
+                            "event_ms_per_step": verify_ms / args.steps,
+                            "algorithmic_bytes_per_step": vbytes / ws / args.steps,
+                            "achieved_gbs": vach, "frac": (vach / peak) if vach else None},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * (6 + (1 if ws == 1 else 2)),
+            # per step: dsde_verify 4 kernels, dsde_update_signal 1, dsde_next_sl 1 (2 with NCCL)
+            "gpu_launches": args.steps * (4 + 1 + (1 if ws == 1 else 2)),
             "clocks": sampler.summary(),
             "verify_ms_per_step": verify_ms / args.steps,
             "rows_per_s": None,
@@ -444,7 +459,7 @@ def main():
     ap.add_argument("--preroll", type=int, default=32)
     ap.add_argument("--record", type=int, default=24)
     ap.add_argument("--e2e-steps", type=int, default=4)
-    ap.add_argument("--cpu-seqs", type=int, default=64)
+    ap.add_argument("--cpu-seqs", type=int, default=128)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seqs", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -200,6 +200,19 @@ dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_draft_rows,
                         int32_t* emitted_tokens, float* kld, uint8_t* flags,
                         void* workspace, size_t ws_bytes, dsde_state st, void* stream);
 
+/* Kernel timing of dsde_verify (instrumentation; off by default). While
+ * enabled, every dsde_verify call on this state records CUDA events on its
+ * stream before its first launch and after each of its DSDE_VERIFY_PHASES
+ * launches (a1 stream, a2-a3 finalize, a4 draw mass, a4 select).
+ * dsde_profile_read blocks until the last recorded event completes, writes
+ * the summed milliseconds of each phase over the calls recorded since the
+ * previous read to ms[DSDE_VERIFY_PHASES] (host memory) and the call count to
+ * *calls (may be NULL), then forgets them. Host functions; not thread-safe
+ * per state. */
+#define DSDE_VERIFY_PHASES 4
+dsde_status dsde_profile_enable(dsde_state st, int enable);
+dsde_status dsde_profile_read(dsde_state st, float* ms, int* calls);
+
 /* ---------------------------------------------------------------------- */
 /* Signal + SL prediction: §8(a) steps a5-a6                               */
 /* ---------------------------------------------------------------------- */

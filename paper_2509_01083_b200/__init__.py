@@ -35,7 +35,9 @@ EXPORTS = (
     "dsde_state_import", "dsde_get_device_error", "dsde_clear_device_error",
     "dsde_verify_workspace_size", "dsde_verify", "dsde_update_signal", "dsde_next_sl",
     "dsde_cap_value", "dsde_comm_unique_id", "dsde_comm_init", "dsde_comm_destroy",
+    "dsde_profile_enable", "dsde_profile_read",
 )
+VERIFY_PHASES = ("stream", "finalize", "draw", "select")
 
 
 class DsdeError(RuntimeError):
@@ -97,6 +99,8 @@ def lib() -> C.CDLL:
         L.dsde_comm_unique_id.argtypes = [P]
         L.dsde_comm_init.argtypes = [P, I, I, P]
         L.dsde_comm_destroy.argtypes = [P]
+        L.dsde_profile_enable.argtypes = [P, I]
+        L.dsde_profile_read.argtypes = [P, P, P]
         _lib = L
     return _lib
 
@@ -173,6 +177,17 @@ class State:
 
     def clear_error(self, stream=None):
         _check(lib().dsde_clear_device_error(self.h, _stream(stream)), "dsde_clear_device_error")
+
+    def profile(self, enable: bool = True):
+        """Turns on/off per-kernel CUDA-event timing of dsde_verify calls on this state."""
+        _check(lib().dsde_profile_enable(self.h, int(enable)), "dsde_profile_enable")
+
+    def profile_read(self) -> tuple[dict, int]:
+        """Summed ms per verify phase since the last read, and the call count."""
+        ms = (C.c_float * len(VERIFY_PHASES))()
+        calls = C.c_int()
+        _check(lib().dsde_profile_read(self.h, ms, C.byref(calls)), "dsde_profile_read")
+        return dict(zip(VERIFY_PHASES, (float(x) for x in ms))), calls.value
 
 
 class Comm:

@@ -152,7 +152,37 @@ dsde_status dsde_state_destroy(dsde_state st) {
   cudaFree(st->seq);
   cudaFree(st->err);
   cudaFree(st->scratch);
+  delete st->prof;
   free(st);
+  return DSDE_OK;
+}
+
+dsde_status dsde_profile_enable(dsde_state st, int enable) {
+  if (!st) return DSDE_ERR_ARG;
+  if (!st->prof) st->prof = new dsde::Profiler();
+  st->prof->on = enable != 0;
+  return DSDE_OK;
+}
+
+dsde_status dsde_profile_read(dsde_state st, float* ms, int* calls) {
+  if (!st || !ms) return DSDE_ERR_ARG;
+  constexpr int P = DSDE_VERIFY_PHASES;
+  for (int k = 0; k < P; ++k) ms[k] = 0.f;
+  int n = 0;
+  if (st->prof && st->prof->used > 0) {
+    dsde::Profiler& pr = *st->prof;
+    if (cudaEventSynchronize(pr.ev[pr.used - 1]) != cudaSuccess) return DSDE_ERR_CUDA;
+    n = (int)(pr.used / (P + 1));
+    for (int c = 0; c < n; ++c)
+      for (int k = 0; k < P; ++k) {
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, pr.ev[c * (P + 1) + k], pr.ev[c * (P + 1) + k + 1]) != cudaSuccess)
+          return DSDE_ERR_CUDA;
+        ms[k] += t;
+      }
+    pr.used = 0;
+  }
+  if (calls) *calls = n;
   return DSDE_OK;
 }
 

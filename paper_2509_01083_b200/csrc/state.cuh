@@ -1,7 +1,10 @@
 // state.cuh — layout of dsde_state (device side) and the verify workspace.
 #pragma once
 
+#include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <vector>
 
 #include "dsde.h"
 
@@ -26,6 +29,26 @@ struct SeqState {
 };
 static_assert(sizeof(SeqState) % 16 == 0, "SeqState must stay 16-byte sized");
 
+// Optional kernel timing of dsde_verify (dsde_profile_enable/read): events
+// recorded before the first and after each launch of every call, reused
+// across reads.
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;  // (DSDE_VERIFY_PHASES + 1) per recorded call
+  size_t used = 0;
+  cudaEvent_t next() {
+    if (used == ev.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+    return ev[used++];
+  }
+  ~Profiler() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
+};
+
 }  // namespace dsde
 
 struct dsde_state_s {
@@ -35,6 +58,7 @@ struct dsde_state_s {
   dsde::SeqState* seq;   // [max_seqs]
   int32_t* err;          // [2]: code, sequence
   long long* scratch;    // [8]: cap partials (sum, n, max) for dsde_next_sl
+  dsde::Profiler* prof;  // kernel timing (host side), created by dsde_profile_enable
 };
 
 struct dsde_comm_s {

@@ -1,16 +1,16 @@
 // verify.cu — dsde_verify: the fused speculative-verification pass (§8(a) a1-a4).
 //
-// Pipeline (all on the caller's stream, no host synchronisation; 3 launches):
-//   1. k_stream_tma   persistent CTAs, TMA-bulk ring: one streaming read of every
-//                     (draft position row, vocab chunk) of the target and draft
-//                     logits; chunk max/argmax, then S = sum e_v, A = sum e_v w_v,
-//                     D = sum e_v g(w_v) about the chunk reference (a1).
-//   2. k_finalize     one warp per sequence, one lane per position: fp64 merge of
-//                     the chunk partials about the row reference, KL, log p/q, the
-//                     Philox accept test, the first rejection a_i, token layout (a2-a3).
-//   3. k_sample       per (sequence, chunk): draw-weight mass of the residual
-//                     max(0, p - q) (row a_i) or of p (bonus row k_i); the last CTA
-//                     of each sequence selects the smallest token with C_v > u R (a4, D7).
+// Pipeline (all on the caller's stream, no host synchronisation; 4 launches):
+//   1. k_stream_ws   persistent warp-specialised CTAs, TMA-bulk ring: one streaming
+//                    read of every (draft position row, vocab chunk) of the target
+//                    and draft logits; S = sum e_v, A = sum e_v w_v, D = sum e_v g(w_v)
+//                    about the chunk reference (a1).
+//   2. k_finalize    one CTA per sequence, one warp per position: fp64 merge of the
+//                    chunk partials, KL, log p/q; the Philox accept test, the first
+//                    rejection a_i, token layout, the draw record (a2-a3).
+//   3. k_draw_ws     same TMA ring over (sequence, chunk) of the drawn row: the mass
+//                    of max(0, p - q) (row a_i) or of p (bonus row k_i) per sub-chunk.
+//   4. k_select      one warp per sequence: the smallest token with C_v > u R (a4, D7).
 //
 // Numerics: with e_v = exp(t_v - M), w_v = (t_v - d_v) - C, C = t - d at
 // the argmax of t, and g(w) = exp(-w) - 1 + w >= 0:
@@ -666,534 +666,53 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtas) k_stream_ws(StreamTmaArgs
   }
 }
 
-// Merged statistics of one row about the row argmax.
-struct RowStats {
-  double M, C, S, A, D;
-  int flags;
-};
-
-// fp64 merge of chunk partials in chunk order about the row reference
-// M = max_c M_c and C = fp32(M - max_v d_v) (so every merged term
-// e^{t-M} e^{-w} = e^{d - max d} <= 1; C is an fp32 value so the sampling
-// pass can rebuild w exactly). Chunk c's w is shifted by Delta = C_c - C; with
-// s = e^(M_c - M) and E1 = s e^-Delta:
-//   S += s S_c,   A += s (A_c + S_c Delta),
-//   D += E1 D_c - A_c s expm1(-Delta) + S_c s g(Delta),  g(x) = expm1(-x) + x.
-__device__ RowStats merge_row(const ChunkPartial* P, int nchunks, bool pair) {
-  float Mref = P[0].M, maxd = P[0].maxd;
-  for (int c = 1; c < nchunks; ++c) {
-    Mref = max_nan(Mref, P[c].M);
-    maxd = fmaxf(maxd, P[c].maxd);
-  }
-  RowStats r;
-  r.M = (double)Mref;
-  r.C = pair ? (double)(Mref - maxd) : 0.0;
-  r.S = r.A = r.D = 0.0;
-  r.flags = 0;
-  for (int c = 0; c < nchunks; ++c) {
-    const ChunkPartial q = P[c];
-    const double ls = (double)q.M - r.M;
-    const double s = exp(ls);
-    r.S += s * q.S;
-    r.flags |= q.flags;
-    if (pair) {
-      const double dl = (double)q.C - r.C;
-      double sem, sg, E1;  // s expm1(-dl), s g(dl), s e^-dl
-      if (fabs(dl) < 1.0) {
-        const double em = expm1(-dl);
-        sem = s * em;
-        sg = s * (em + dl);
-        E1 = s + sem;
-      } else {
-        E1 = exp(ls - dl);
-        sem = E1 - s;
-        sg = sem + s * dl;
-      }
-      r.A += s * q.A + s * q.S * dl;
-      r.D += E1 * q.D - q.A * sem + q.S * sg;
-    }
-  }
-  return r;
-}
-
-struct FinArgs {
-  int B, V, total, nchunks;
-  const int32_t* cu_sl;
-  const int32_t* tokens;
-  const void* tl;
-  long long ld_t;
-  const void* dl;
-  long long ld_d;
-  const uint64_t* seeds;
-  const ChunkPartial* part;
-  int32_t* acc_len;
-  int32_t* emitted;
-  float* kld;
-  uint8_t* flags;
-  SeqRec* rec;
-  int* counter;
-  int32_t* err;
-};
-
-// a2 + a3: one warp per sequence, lane j = draft position j (k_i <= 16 < 32);
-// lane k_i also draws the uniforms of the bonus slot.
-template <typename T>
-__global__ void __launch_bounds__(128) k_finalize(FinArgs a) {
-  const int i = blockIdx.x * 4 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (i >= a.B) return;
-  const int c0 = __ldg(a.cu_sl + i), c1 = __ldg(a.cu_sl + i + 1);
-  const int k = c1 - c0;
-  const bool range_ok = c0 >= 0 && k >= 1 && k <= DSDE_MAX_SL && c1 <= a.total;
-  const bool rows_ok = (i != a.B - 1) || (c1 == a.total);
-  if (!range_ok || !rows_ok) {
-    if (lane == 0) {
-      a.acc_len[i] = -1;
-      a.rec[i].mode = MODE_ERROR;
-      raise_device_error(a.err, range_ok ? DSDE_DERR_ROWS : DSDE_DERR_BAD_SL, i);
-    }
-    return;
-  }
-  const long long slot0 = (long long)c0 + i;
-  double kl = 0.0, lr = 0.0, C = 0.0, lam = 0.0, M = 0.0;
-  bool acc = false, near = false, bad_tok = false, nonfin = false;
-  int rflags = 0;
-  Uniforms u = {0.0, 0.0};
-  if (lane <= k) u = philox_uniforms(__ldg(a.seeds + slot0 + lane));
-  if (lane < k) {
-    const long long drow = (long long)c0 + lane;
-    const int x = __ldg(a.tokens + drow);
-    bad_tok = x < 0 || x >= a.V;
-    const RowStats r = merge_row(a.part + drow * a.nchunks, a.nchunks, true);
-    rflags = r.flags;
-    nonfin = !(isfinite(r.S) && isfinite(r.A) && isfinite(r.D) && r.S > 0.0 && isfinite(r.M) &&
-               isfinite(r.C));
-    // y = E_p[exp(-w)] - 1. KL = D/S + (log1p(y) - y) has no cancellation for
-    // small KL; when y > 1 (the draft puts far more mass away from the
-    // reference, e.g. disjoint supports) the equal form A/S + log1p(y) is used.
-    const double y = (r.D - r.A) / r.S;
-    lam = log1p(y);
-    kl = fmax(0.0, y <= 1.0 ? r.D / r.S + (lam - y) : r.A / r.S + lam);
-    C = r.C;
-    M = r.M;
-    if (!bad_tok) {
-      const T* tp = reinterpret_cast<const T*>(a.tl) + (drow + i) * a.ld_t;
-      const T* dp = reinterpret_cast<const T*>(a.dl) + drow * a.ld_d;
-      const double tx = (double)load_logit<T>(tp + x), dx = (double)load_logit<T>(dp + x);
-      lr = (tx - dx) - C + lam;
-      nonfin |= !isfinite(lr);
-    }
-    const double pacc = lr >= 0.0 ? 1.0 : exp(lr);
-    acc = u.acc < pacc;
-    near = fabs(u.acc - pacc) < 1e-6;
-  }
-  const unsigned bt = __ballot_sync(kFull, bad_tok);
-  const unsigned nf = __ballot_sync(kFull, nonfin);
-  const unsigned am = __ballot_sync(kFull, acc);
-  if (bt | nf) {
-    if (lane < k) a.kld[c0 + lane] = NAN;
-    if (lane <= k) {
-      a.emitted[slot0 + lane] = DSDE_PAD;
-      if (a.flags) a.flags[slot0 + lane] = 0;
-    }
-    if (lane == 0) {
-      a.acc_len[i] = -1;
-      a.rec[i].mode = MODE_ERROR;
-      raise_device_error(a.err, bt ? DSDE_DERR_BAD_TOKEN : DSDE_DERR_NONFINITE, i);
-    }
-    return;
-  }
-  const int acc_run = __ffs(~am) - 1;  // first rejected lane (lanes >= k never accept)
-  const int aa = acc_run < k ? acc_run : k;
-  if (lane < k) a.kld[c0 + lane] = (float)kl;
-  if (lane <= k) {
-    a.emitted[slot0 + lane] = lane < aa ? __ldg(a.tokens + c0 + lane) : DSDE_PAD;
-    if (a.flags) {
-      uint8_t f = (uint8_t)(rflags & DSDE_FLAG_OVERFLOW);
-      if (near && lane <= aa && lane < k) f |= DSDE_FLAG_ACCEPT_NEAR_TIE;
-      a.flags[slot0 + lane] = f;
-    }
-  }
-  if (lane == 0) {
-    a.acc_len[i] = aa;
-    a.counter[i] = 0;
-  }
-  if (lane == aa) {
-    SeqRec r;
-    r.slot = (int)(slot0 + aa);
-    r.trow = slot0 + aa;
-    r.u = u.smp;
-    r.pad0 = 0;
-    if (aa < k) {
-      r.mode = MODE_RESIDUAL;
-      r.drow = (long long)c0 + aa;
-      r.M = (float)M;
-      r.C = C;
-      r.lam = lam;
-    } else {
-      r.mode = MODE_BONUS;
-      r.drow = -1;
-      r.M = 0.f;
-      r.C = 0.0;
-      r.lam = 0.0;
-    }
-    a.rec[i] = r;
-  }
-}
-
-struct SampArgs {
-  int B, V, nchunks, total;
-  const void* tl;
-  long long ld_t;
-  const void* dl;
-  long long ld_d;
-  const ChunkPartial* part;
-  const SeqRec* rec;
-  double* mass;
-  int32_t* emitted;
-  uint8_t* flags;
-  float* cmax;
-  int* counter;
-  int32_t* err;
-};
-
-
-// ---------------------------------------------------------------------------
-// a4: one launch for every draw of the step, warp-granular (no block barrier).
-// Warp (i, u) forms the draw weights of sub-chunk u (SUB = 32*E elements,
-// lane-strided 16-byte vectors) of sequence i and their mass; the last warp of
-// sequence i to finish (atomic counter + threadfence) selects the token: an
-// fp64 warp scan over the sub-chunk masses, then a warp scan inside the
-// crossing sub-chunk (re-read from L2), in ascending token order (D7).
-//   residual: rho_v = e_v (1 - exp(-z_v)) for z_v > 0, else 0, with
-//             e_v = exp(t_v - M), z_v = w_v + lam, w_v = (t_v - d_v) - C exact,
-//             lam added as hi + lo floats; 1 - exp(-z) = z (1 - z h(-z)) for
-//             z < 1 (no cancellation), 1 - 2^(-z log2 e) otherwise;
-//   bonus:    p_v up to a scale: exp(t_v - m_u) about the warp max m_u,
-//             rescaled by exp(m_u - max_u m_u) in fp64 (one pass over the row).
-// Every per-lane value is recomputed bit-identically by the select pass.
-// ---------------------------------------------------------------------------
-template <typename T>
-__host__ __device__ constexpr int sub_elems() {
-  return 32 * Traits<T>::VEC * Traits<T>::NV;
-}
-
-template <typename T>
-__device__ __forceinline__ void load_vec(const T* row, int V, int e0, float* x) {
-  constexpr int VEC = Traits<T>::VEC;
-  if (e0 + VEC <= V) {
-    unpack16<T>(*reinterpret_cast<const uint4*>(row + e0), x);
-  } else {
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) x[e] = (e0 + e < V) ? load_logit<T>(row + e0 + e) : -INFINITY;
-  }
-}
-
-// Draw weights of this lane's elements of sub-chunk u: w[v*VEC + e] for token
-// u*SUB + (v*32 + lane)*VEC + e. Returns the reference (residual: the row's M;
-// bonus: the warp max of t over the sub-chunk, -inf if all padding).
-template <typename T>
-__device__ __forceinline__ float sub_weights(const SampArgs& a, const SeqRec& r, bool resid, int u,
-                                             float (&w)[Traits<T>::VEC * Traits<T>::NV]) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, E = VEC * NV;
-  const int lane = threadIdx.x & 31;
-  const int base = u * sub_elems<T>() + lane * VEC;
-  float t[E];
-  const T* tp = reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) load_vec<T>(tp, a.V, base + v * 32 * VEC, t + v * VEC);
-  if (resid) {
-    float d[E];
-    const T* dp = reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) load_vec<T>(dp, a.V, base + v * 32 * VEC, d + v * VEC);
-    const float Cf = (float)r.C;  // exact: r.C holds an fp32 value
-    const float lhi = (float)r.lam, llo = (float)(r.lam - (double)lhi);
-    const float ML2 = r.M * kLog2e;
-#pragma unroll
-    for (int q = 0; q < E; ++q) {
-      const float ev = fast_exp2(fmaf(t[q], kLog2e, -ML2));  // 0 for padding (-inf)
-      const float z = (diff_ref<T>(t[q], d[q], Cf) + lhi) + llo;
-      float pz = -2.812654656736413e-06f;  // h(-z): tools/fit_g.py (degree 7, |u| <= 1)
-      pz = fmaf(pz, z, 2.5358644052175805e-05f);
-      pz = fmaf(pz, z, -1.9836986029986292e-04f);
-      pz = fmaf(pz, z, 1.3885394437238574e-03f);
-      pz = fmaf(pz, z, -8.33334494382143e-03f);
-      pz = fmaf(pz, z, 4.166673496365547e-02f);
-      pz = fmaf(pz, z, -1.666666716337204e-01f);
-      pz = fmaf(pz, z, 0.5f);
-      const float one_m = z < 1.f ? z * fmaf(-z, pz, 1.f) : 1.f - fast_exp2(-z * kLog2e);
-      w[q] = (z > 0.f && ev > 0.f) ? ev * one_m : 0.f;
-    }
-    return r.M;
-  }
-  float m = -INFINITY;
-#pragma unroll
-  for (int q = 0; q < E; ++q) m = max_nan(m, t[q]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(kFull, m, o));
-  const float mL2 = m * kLog2e;
-#pragma unroll
-  for (int q = 0; q < E; ++q) w[q] = m == -INFINITY ? 0.f : fast_exp2(fmaf(t[q], kLog2e, -mL2));
-  return m;
-}
-
-__device__ __forceinline__ double warp_sum_d(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  return v;
-}
-
-__device__ __forceinline__ double warp_incl_scan(double x, int lane) {
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double y = __shfl_up_sync(kFull, x, o);
-    if (lane >= o) x += y;
-  }
-  return x;
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kThreads) k_sample(SampArgs a) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, E = VEC * NV, SUB = sub_elems<T>();
-  const int lane = threadIdx.x & 31;
-  const long long gw = (long long)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-  const int nsub = (a.V + SUB - 1) / SUB;
-  if (gw >= (long long)a.B * nsub) return;
-  const int i = (int)(gw / nsub), u = (int)(gw - (long long)i * nsub);
-  const SeqRec r = a.rec[i];
-  if (r.mode != MODE_RESIDUAL && r.mode != MODE_BONUS) return;
-  const bool resid = r.mode == MODE_RESIDUAL;
-  double* wmass = a.mass + (long long)i * a.nchunks * kCWarps;
-  float* wmax = a.cmax + (long long)i * a.nchunks * kCWarps;
-
-  float w[E];
-  const float mu = sub_weights<T>(a, r, resid, u, w);
-  double m = 0.0;  // sub-chunk mass about its reference, in the select pass's order
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    float ls = 0.f;
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) ls += w[v * VEC + e];
-    m += warp_sum_d((double)ls);
-  }
-  int last = 0;
-  if (lane == 0) {
-    wmass[u] = m;
-    wmax[u] = mu;
-    __threadfence();
-    last = atomicAdd(a.counter + i, 1) == nsub - 1;
-  }
-  if (!__shfl_sync(kFull, last, 0)) return;
-  __threadfence();
-
-  // ---- last warp of sequence i: select the token ----
-  float Mg = -INFINITY;
-  if (!resid) {
-    for (int s0 = lane; s0 < nsub; s0 += 32) Mg = max_nan(Mg, __ldcg(wmax + s0));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) Mg = max_nan(Mg, __shfl_xor_sync(kFull, Mg, o));
-  }
-  auto scale_of = [&](int s0) -> double {  // sub-chunk mass scale to the common reference
-    if (resid) return 1.0;
-    const float ms = __ldcg(wmax + s0);
-    return ms == -INFINITY ? 0.0 : exp((double)ms - (double)Mg);
-  };
-  double R = 0.0;
-  for (int s0 = lane; s0 < nsub; s0 += 32) R += scale_of(s0) * __ldcg(wmass + s0);
-  R = warp_sum_d(R);
-  uint8_t fl = 0;
-  if (!(R > 0.0) || !isfinite(R)) {
-    if (lane == 0) {
-      // residual mass 0 (p <= q everywhere in fp32; D7 fallback) or a
-      // non-finite bonus row: no valid draw from these weights
-      if (resid && isfinite(R)) {
-        // D7: draw from p of the same target row (slow path, one lane)
-        const float M = r.M;
-        double tot = 0.0;
-        for (int v = 0; v < a.V; ++v)
-          tot += exp((double)load_logit<T>(reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t + v) - M);
-        const double target = r.u * tot;
-        double cum = 0.0;
-        int tok = 0;
-        for (int v = 0; v < a.V; ++v) {
-          const double wv = exp((double)load_logit<T>(reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t + v) - M);
-          cum += wv;
-          if (wv > 0.0) tok = v;
-          if (wv > 0.0 && cum > target) break;
-        }
-        a.emitted[r.slot] = tok;
-        if (a.flags) a.flags[r.slot] |= DSDE_FLAG_FALLBACK;
-      } else {
-        a.emitted[r.slot] = DSDE_PAD;
-        raise_device_error(a.err, DSDE_DERR_NONFINITE, i);
-      }
-    }
-    return;
-  }
-  const double target = r.u * R;
-  // crossing sub-chunk: first u with prefix(u) > target (fallback: last with mass)
-  int us = -1, ulast = -1;
-  double base = 0.0, base_last = 0.0, cum = 0.0;
-  for (int g = 0; g < nsub; g += 32) {
-    const int s0 = g + lane;
-    const double ms = s0 < nsub ? scale_of(s0) * __ldcg(wmass + s0) : 0.0;
-    const double incl = warp_incl_scan(ms, lane);
-    const unsigned pos = __ballot_sync(kFull, ms > 0.0);
-    const unsigned cross = __ballot_sync(kFull, ms > 0.0 && cum + incl > target);
-    if (pos) {
-      const int lp = 31 - __clz(pos);
-      ulast = g + lp;
-      base_last = cum + __shfl_sync(kFull, incl - ms, lp);
-    }
-    if (cross) {
-      const int lc = __ffs(cross) - 1;
-      us = g + lc;
-      base = cum + __shfl_sync(kFull, incl - ms, lc);
-      break;
-    }
-    cum += __shfl_sync(kFull, incl, 31);
-  }
-  if (us < 0) {
-    us = ulast;
-    base = base_last;
-    fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
-  }
-  const double f = scale_of(us);
-  if (us != u) sub_weights<T>(a, r, resid, us, w);
-  int tok = -1;
-  double lo = 0.0, hi = 0.0;
-  int last_pos = -1;
-  double lp_lo = 0.0, lp_hi = 0.0;
-  double vbase = base;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    float ls = 0.f;
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) ls += w[v * VEC + e];
-    const double incl = warp_incl_scan((double)ls, lane);
-    const double pre = vbase + f * (incl - (double)ls);
-    int cand = -1;
-    double clo = 0.0, chi = 0.0;
-    float run = 0.f;
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      const float before = run;
-      run += w[v * VEC + e];
-      const double cb = pre + f * (double)before, ca = pre + f * (double)run;
-      if (cand < 0 && w[v * VEC + e] > 0.f && ca > target) {
-        cand = e;
-        clo = cb;
-        chi = ca;
-      }
-    }
-    const unsigned bc = __ballot_sync(kFull, cand >= 0);
-    const int tok_base = us * SUB + v * 32 * VEC;
-    if (bc) {
-      const int lc = __ffs(bc) - 1;
-      tok = tok_base + lc * VEC + __shfl_sync(kFull, cand, lc);
-      lo = __shfl_sync(kFull, clo, lc);
-      hi = __shfl_sync(kFull, chi, lc);
-      break;
-    }
-    // remember the last positive-weight token for the rounding corner
-    int lpos = -1;
-    double llo = 0.0, lhi = 0.0;
-    {
-      float run2 = 0.f;
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) {
-        const float before = run2;
-        run2 += w[v * VEC + e];
-        if (w[v * VEC + e] > 0.f) {
-          lpos = e;
-          llo = pre + f * (double)before;
-          lhi = pre + f * (double)run2;
-        }
-      }
-    }
-    const unsigned bp = __ballot_sync(kFull, lpos >= 0);
-    if (bp) {
-      const int lp = 31 - __clz(bp);
-      last_pos = tok_base + lp * VEC + __shfl_sync(kFull, lpos, lp);
-      lp_lo = __shfl_sync(kFull, llo, lp);
-      lp_hi = __shfl_sync(kFull, lhi, lp);
-    }
-    vbase += f * __shfl_sync(kFull, incl, 31);
-  }
-  if (tok < 0) {  // rounding corner: u R within rounding of the sub-chunk total
-    tok = last_pos;
-    lo = lp_lo;
-    hi = lp_hi;
-    fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
-  }
-  if (lane == 0) {
-    if (fabs(r.u - lo / R) < 1e-6 || fabs(r.u - hi / R) < 1e-6) fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
-    a.emitted[r.slot] = tok < 0 ? 0 : tok;
-    if (a.flags) a.flags[r.slot] |= fl;
-  }
-}
-
-#include "verify_fused.cuh"
+#include "verify_draw.cuh"
 
 template <typename T>
 cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const int32_t* tokens,
                           const void* tl, int64_t ld_t, const void* dl, int64_t ld_d,
                           const uint64_t* seeds, int32_t* acc_len, int32_t* emitted, float* kld,
-                          uint8_t* flags, const VerifyWs& ws, int32_t* err, cudaStream_t s) {
+                          uint8_t* flags, const VerifyWs& ws, int32_t* err, Profiler* prof,
+                          cudaStream_t s) {
+  const bool pr = prof != nullptr && prof->on;
+  auto mark = [&]() {
+    if (pr) cudaEventRecord(prof->next(), s);
+  };
+  mark();
   const int nc = (V + chunk_elems<T>() - 1) / chunk_elems<T>();
-  if (getenv("DSDE_LEGACY_VERIFY") == nullptr) {
-    // one persistent, cooperative launch for a1-a4 (verify_fused.cuh)
-    constexpr int smem = fused_smem<T>();
-    static int grid_per_dev[64] = {0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int& grid = grid_per_dev[dev & 63];
-    if (grid == 0) {
-      cudaFuncSetAttribute(k_verify_fused<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      int sms = 148, per_sm = 0;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_verify_fused<T>, kFzThreads, smem);
-      grid = std::max(1, std::min(per_sm, kWsCtas)) * sms;
-    }
-    // draw items of a sequence are placed `lag` sequence blocks after its
-    // stream items (all at the end by default: no pipeline waits on finalize)
-    int lag = B;
-    if (const char* e = getenv("DSDE_LAG")) lag = atoi(e) > 0 ? atoi(e) : B;
-    lag = std::max(1, std::min(lag, B));
-    cudaMemsetAsync(ws.counter, 0, sizeof(int) * (3 * (size_t)B + 2), s);
-    cudaMemsetAsync(ws.counter + 3 * (size_t)B + 2, 0xff, sizeof(int) * 2 * (size_t)B, s);
-    const int exp_flags = getenv("DSDE_EXP_FLAGS") ? atoi(getenv("DSDE_EXP_FLAGS")) : 0;
-    FusedArgs fa{B, V, nc, total, lag, exp_flags, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, acc_len, emitted,
-                 kld, flags, ws.part, ws.rec, ws.mass, ws.cmax, ws.counter,
-                 ws.counter + 3 * (size_t)B + 2, err};
-    void* args[] = {&fa};
-    return cudaLaunchCooperativeKernel((const void*)k_verify_fused<T>, dim3(grid), dim3(kFzThreads),
-                                       args, smem, s);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static bool attr_set[64] = {false};
+  if (!attr_set[dev & 63]) {
+    cudaFuncSetAttribute(k_stream_ws<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_ws_smem<T>());
+    cudaFuncSetAttribute(k_draw_ws<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, draw_ws_smem<T>());
+    attr_set[dev & 63] = true;
   }
-  // legacy three-launch path (kept for A/B measurements)
+  // a1: statistics of every (draft row, vocab chunk)
   if (total > 0) {
-    static bool attr_set = false;
-    constexpr int smem = stream_ws_smem<T>();
-    if (!attr_set) {
-      cudaFuncSetAttribute(k_stream_ws<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr_set = true;
-    }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long long items = (long long)total * nc;
     const int grid = (int)std::min<long long>(items, (long long)kWsCtas * sms);
     StreamTmaArgs ta{tl, ld_t, dl, ld_d, cu_sl, B, V, nc, total, ws.part};
-    k_stream_ws<T><<<grid, kWsThreads, smem, s>>>(ta);
+    k_stream_ws<T><<<grid, kWsThreads, stream_ws_smem<T>(), s>>>(ta);
   }
+  mark();
+  // a2-a3: row merge, KL, accept test, layout, draw record
   FinArgs fa{B, V, total, nc, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, ws.part,
-             acc_len, emitted, kld, flags, ws.rec, ws.counter, err};
-  k_finalize<T><<<(B + 3) / 4, 128, 0, s>>>(fa);
-  SampArgs pa{B, V, nc, total, tl, ld_t, dl, ld_d, ws.part, ws.rec, ws.mass, emitted, flags,
-              ws.cmax, ws.counter, err};
-  const long long warps = (long long)B * ((V + sub_elems<T>() - 1) / sub_elems<T>());
-  k_sample<T><<<(unsigned)((warps + kThreads / 32 - 1) / (kThreads / 32)), kThreads, 0, s>>>(pa);
+             acc_len, emitted, kld, flags, ws.rec, err};
+  k_finalize<T><<<B, kFinThreads, 0, s>>>(fa);
+  mark();
+  // a4: draw-weight masses of the drawn rows, then the inverse-CDF select
+  {
+    const long long items = (long long)B * nc;
+    const int grid = (int)std::min<long long>(items, (long long)kWsCtas * sms);
+    DrawArgs da{B, V, nc, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.cmax};
+    k_draw_ws<T><<<grid, kDrawThreads, draw_ws_smem<T>(), s>>>(da);
+  }
+  mark();
+  SelArgs sa{B, V, nc, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.cmax, emitted, flags, err};
+  k_select<T><<<(B + 3) / 4, 128, 0, s>>>(sa);
+  mark();
   return cudaGetLastError();
 }
 
@@ -1235,10 +754,10 @@ extern "C" dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_dra
   if (dtype == DSDE_BF16)
     e = launch_verify<uint16_t>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                                 draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld,
-                                flags, ws, st->err, s);
+                                flags, ws, st->err, st->prof, s);
   else
     e = launch_verify<float>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                              draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld, flags,
-                             ws, st->err, s);
+                             ws, st->err, st->prof, s);
   return e == cudaSuccess ? DSDE_OK : DSDE_ERR_CUDA;
 }
