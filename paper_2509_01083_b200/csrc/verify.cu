@@ -1,24 +1,30 @@
-// verify.cu — dsde_verify: the fused speculative-verification pass (§8(a) a1-a4).
+// verify.cu — dsde_verify: the speculative-verification pass (§8(a) a1-a4).
 //
 // Pipeline (all on the caller's stream, no host synchronisation; 4 launches):
-//   1. k_stream_ws   persistent warp-specialised CTAs, TMA-bulk ring: one streaming
-//                    read of every (draft position row, vocab chunk) of the target
-//                    and draft logits; S = sum e_v, A = sum e_v w_v, D = sum e_v g(w_v)
-//                    about the chunk reference (a1).
+//   1. k_stream_*    one streaming read of every (draft position row, vocab slice)
+//                    of the target and draft logits; per 1024-token (bf16) /
+//                    512-token (fp32) slice: S = sum e_v, A = sum e_v w_v,
+//                    D = sum e_v g(w_v) about the slice reference (a1).
 //   2. k_finalize    one CTA per sequence, one warp per position: fp64 merge of the
-//                    chunk partials, KL, log p/q; the Philox accept test, the first
+//                    slice partials, KL, log p/q; the Philox accept test, the first
 //                    rejection a_i, token layout, the draw record (a2-a3).
-//   3. k_draw_ws     same TMA ring over (sequence, chunk) of the drawn row: the mass
-//                    of max(0, p - q) (row a_i) or of p (bonus row k_i) per sub-chunk.
+//   3. k_draw_*      the mass of max(0, p - q) (row a_i) or of p (bonus row k_i)
+//                    per slice of the drawn row.
 //   4. k_select      one warp per sequence: the smallest token with C_v > u R (a4, D7).
+// Two variants of the streaming kernels (1, 3), selected by DSDE_STREAM at run
+// time for A/B measurements: "ldg" (default; persistent warps, 128-bit
+// non-allocating loads, next slice prefetched into registers) and "tma"
+// (warp-specialised CTAs: a TMA bulk-copy producer warp filling a shared-memory
+// ring, 8 consumer warps).
 //
-// Numerics: with e_v = exp(t_v - M), w_v = (t_v - d_v) - C, C = t - d at
-// the argmax of t, and g(w) = exp(-w) - 1 + w >= 0:
+// Numerics: with e_v = exp(t_v - M), w_v = (t_v - d_v) - C, C = M - max d
+// (an fp32 value), and g(w) = exp(-w) - 1 + w >= 0:
 //   KL(p||q) = D/S + (log1p(y) - y),  y = (D - A)/S = E_p[exp(-w)] - 1,
 //   log p(x)/q(x) = (t_x - d_x) - C + log1p(y),
 //   q_v / p_v = exp(-(w_v + log1p(y))).
 // D sums non-negative terms, so the small-KL regime has no cancellation (the naive
 // E_p[t - d] - LSE_t + LSE_d form loses ~1e-3 relative at KL ~ 1e-3).
+// e_v e^{-w_v} = e^{d_v - max d} <= 1, so no term overflows for any finite input.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -27,6 +33,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include <cuda_bf16.h>
 
@@ -35,35 +42,51 @@
 
 namespace dsde {
 
-constexpr int kThreads = 256;
-
 template <typename T>
 struct Traits;
+#ifndef DSDE_NV_BF16
+#define DSDE_NV_BF16 6
+#endif
+#ifndef DSDE_NVD_BF16
+#define DSDE_NVD_BF16 4
+#endif
 template <>
-struct Traits<uint16_t> {      // bf16 bit patterns
-  static constexpr int VEC = 8;  // elements per 16-byte vector
-  static constexpr int NV = 4;   // vectors per thread per row
+struct Traits<uint16_t> {                  // bf16 bit patterns
+  static constexpr int VEC = 8;            // elements per 16-byte vector
+  static constexpr int NV = DSDE_NV_BF16;  // vectors per lane per row slice, a1 stream
+  static constexpr int NVD = DSDE_NVD_BF16;  // the same for the a4 draw pass
 };
 template <>
 struct Traits<float> {
   static constexpr int VEC = 4;
   static constexpr int NV = 4;
+  static constexpr int NVD = 4;
 };
+// one warp's slice of a row: 32 lanes x NV vectors x VEC elements (stream),
+// 32 x NVD x VEC (draw)
+template <typename T>
+__host__ __device__ constexpr int sub_elems() {
+  return 32 * Traits<T>::VEC * Traits<T>::NV;
+}
+template <typename T>
+__host__ __device__ constexpr int sub_elems_d() {
+  return 32 * Traits<T>::VEC * Traits<T>::NVD;
+}
+constexpr int kCWarps = 8;  // TMA variant: consumer warps per CTA = slices per stage
 template <typename T>
 __host__ __device__ constexpr int chunk_elems() {
-  return kThreads * Traits<T>::VEC * Traits<T>::NV;
+  return kCWarps * sub_elems<T>();
 }
 
-struct ChunkPartial {  // 48 bytes
-  double S, A, D;      // about (M, C) of this chunk
-  float M;             // chunk max of t
-  float C;             // t - d at the chunk argmax (fp32, as used for w)
-  int idx;             // chunk argmax (smallest index among ties)
-  int flags;           // DSDE_FLAG_OVERFLOW
-  float maxd;          // max of d over the chunk (overflow-safe reference bound)
-  int pad;
+// statistics of one row slice about its own reference (32 bytes)
+struct SubPartial {
+  float S, A, D;  // sum e, sum e w, sum e g(w), e = exp(t - M), w = (t - d) - C
+  float M;        // slice max of t (-inf: padding only; NaN if any t is NaN)
+  float C;        // M - maxd
+  float maxd;     // slice max of d
+  float pad0, pad1;
 };
-static_assert(sizeof(ChunkPartial) == 48, "ChunkPartial layout");
+static_assert(sizeof(SubPartial) == 32, "SubPartial layout");
 
 enum { MODE_NONE = 0, MODE_RESIDUAL = 1, MODE_BONUS = 2, MODE_ERROR = 3 };
 
@@ -82,56 +105,48 @@ struct SeqRec {  // 64 bytes
 static_assert(sizeof(SeqRec) == 64, "SeqRec layout");
 
 struct VerifyWs {
-  ChunkPartial* part;  // [(total + B) * nchunks]
-  SeqRec* rec;         // [B]
-  double* mass;        // [B * nchunks * 8] draw-weight mass per warp sub-chunk
-  float* cmax;         // [B * nchunks * 8] reference of each sub-chunk mass (bonus)
-  int* counter;        // [3 * B] per-sequence counters / flags (zeroed per call)
+  SubPartial* part;  // [total * nsub] slice statistics of every draft row
+  SeqRec* rec;       // [B]
+  double* mass;      // [B * nsub_d] draw-weight mass per draw slice of the drawn row
+  float* ref;        // [B * nsub_d] reference of each slice mass (bonus)
 };
 
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-inline int n_chunks(int V, dsde_dtype dt) {
-  const int ch = dt == DSDE_BF16 ? chunk_elems<uint16_t>() : chunk_elems<float>();
-  return (V + ch - 1) / ch;
+inline int n_subs(int V, dsde_dtype dt) {
+  const int se = dt == DSDE_BF16 ? sub_elems<uint16_t>() : sub_elems<float>();
+  // rounded up to whole TMA chunks so both stream variants share the layout
+  const int ce = kCWarps * se;
+  return (V + ce - 1) / ce * kCWarps;
+}
+
+inline int n_subs_d(int V, dsde_dtype dt) {
+  const int se = dt == DSDE_BF16 ? sub_elems_d<uint16_t>() : sub_elems_d<float>();
+  return (V + se - 1) / se;
 }
 
 inline size_t ws_layout(int B, int total, int V, dsde_dtype dt, VerifyWs* ws, char* base) {
-  const int nc = n_chunks(V, dt);
-  size_t off = 0;
-  const size_t p_bytes = align256(sizeof(ChunkPartial) * (size_t)(total + B) * nc);
+  const int ns = n_subs(V, dt), nd = n_subs_d(V, dt);
+  const size_t p_bytes = align256(sizeof(SubPartial) * (size_t)total * ns);
   const size_t r_bytes = align256(sizeof(SeqRec) * (size_t)B);
-  const size_t m_bytes = align256(sizeof(double) * (size_t)B * nc * 8);  // per warp sub-chunk
-  const size_t x_bytes = align256(sizeof(float) * (size_t)B * nc * 8);
-  const size_t c_bytes = align256(sizeof(int) * ((size_t)B * 5 + 8));  // counters + event queue
+  const size_t m_bytes = align256(sizeof(double) * (size_t)B * nd);
+  const size_t x_bytes = align256(sizeof(float) * (size_t)B * nd);
   if (ws) {
-    ws->part = reinterpret_cast<ChunkPartial*>(base + off);
-    ws->rec = reinterpret_cast<SeqRec*>(base + off + p_bytes);
-    ws->mass = reinterpret_cast<double*>(base + off + p_bytes + r_bytes);
-    ws->cmax = reinterpret_cast<float*>(base + off + p_bytes + r_bytes + m_bytes);
-    ws->counter = reinterpret_cast<int*>(base + off + p_bytes + r_bytes + m_bytes + x_bytes);
+    ws->part = reinterpret_cast<SubPartial*>(base);
+    ws->rec = reinterpret_cast<SeqRec*>(base + p_bytes);
+    ws->mass = reinterpret_cast<double*>(base + p_bytes + r_bytes);
+    ws->ref = reinterpret_cast<float*>(base + p_bytes + r_bytes + m_bytes);
   }
-  return p_bytes + r_bytes + m_bytes + x_bytes + c_bytes;
-}
-
-template <typename T>
-__device__ __forceinline__ float load_logit_smem(const T* p);
-template <>
-__device__ __forceinline__ float load_logit_smem<float>(const float* p) { return *p; }
-template <>
-__device__ __forceinline__ float load_logit_smem<uint16_t>(const uint16_t* p) {
-  return bf16_bits_to_float(*p);
+  return p_bytes + r_bytes + m_bytes + x_bytes;
 }
 
 // max that propagates NaN (a NaN logit must reach the non-finite check)
 __device__ __forceinline__ float max_nan(float a, float b) { return (b > a || b != b) ? b : a; }
 
-__device__ __forceinline__ void arg_better(float& m, int& mi, float& md, float m2, int i2, float d2) {
-  if (m2 > m || (m2 == m && i2 < mi)) {
-    m = m2;
-    mi = i2;
-    md = d2;
-  }
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+  return v;
 }
 
 // w = (t - d) - C. For bf16 inputs t - d is exact in fp32 (8-bit significands,
@@ -151,10 +166,336 @@ __device__ __forceinline__ float diff_ref<float>(float t, float d, float C) {
   return __fadd_rn(__fsub_rn(hi, C), lo);
 }
 
-// ---------------------------------------------------------------------------
-// mbarrier / TMA bulk-copy primitives (PTX), packed element helpers
-// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T pad_bits();
+template <>
+__device__ __forceinline__ uint16_t pad_bits<uint16_t>() { return (uint16_t)0xF14Au; }  // bf16 ~ -1e30
+template <>
+__device__ __forceinline__ float pad_bits<float>() { return -1e30f; }
 
+// Elements h, h+1 (h even) of a lane's N x 16-byte vectors as an fp32 pair.
+template <typename T, int N>
+__device__ __forceinline__ float2 pair_of(const uint4 (&r)[N], int h) {
+  if constexpr (sizeof(T) == 2) {
+    const uint4 x = r[h >> 3];
+    const int k = (h & 7) >> 1;
+    const uint32_t w = k == 0 ? x.x : k == 1 ? x.y : k == 2 ? x.z : x.w;
+    return make_float2(bf16_lo(w), bf16_hi(w));
+  } else {
+    const uint4 x = r[h >> 2];
+    return (h & 3) == 0 ? make_float2(__uint_as_float(x.x), __uint_as_float(x.y))
+                        : make_float2(__uint_as_float(x.z), __uint_as_float(x.w));
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ float2 diff2(float2 t, float2 d, float C);
+template <>
+__device__ __forceinline__ float2 diff2<uint16_t>(float2 t, float2 d, float C) {
+  return __fadd2_rn(__fadd2_rn(t, make_float2(-d.x, -d.y)), make_float2(-C, -C));
+}
+template <>
+__device__ __forceinline__ float2 diff2<float>(float2 t, float2 d, float C) {
+  return make_float2(diff_ref<float>(t.x, d.x, C), diff_ref<float>(t.y, d.y, C));
+}
+
+// ---------------------------------------------------------------------------
+// Loading a lane's words of row slice u: token u*SUB + (v*32 + lane)*VEC + e.
+// Full slices use 128-bit loads; the last slice of a row pads past V with a
+// value whose weights are exactly 0.
+// ---------------------------------------------------------------------------
+template <typename T, int NV>
+__device__ __forceinline__ void load_slice(const T* row, int V, int u, uint4 (&r)[NV]) {
+  constexpr int VEC = Traits<T>::VEC, SUB = 32 * VEC * NV;
+  const int lane = threadIdx.x & 31;
+  if ((u + 1) * SUB <= V) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) r[v] = ld_stream_v4(row + u * SUB + (v * 32 + lane) * VEC);
+  } else {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int e0 = u * SUB + (v * 32 + lane) * VEC;
+      if (e0 + VEC <= V) {
+        r[v] = ld_stream_v4(row + e0);
+      } else {
+        T b[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) b[e] = (e0 + e < V) ? row[e0 + e] : pad_bits<T>();
+        r[v] = *reinterpret_cast<const uint4*>(b);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a1 per warp slice: reference M = max t (NaN if any t is NaN), C = M - max d,
+// then S, A, D with packed FFMA2 math. g(w) for |w| < 1 is w^2 h(-w) with
+// h(u) = (e^u - 1 - u)/u^2 as a degree-6 Chebyshev fit on |u| <= 1 (2.0e-7
+// relative in fp32 Horner; `tools/fit_g.py --deg 6`) in powers of w (odd
+// coefficients negated; DSDE_POLY_DEG7 selects the 1.1e-7 degree-7 fit);
+// for |w| >= 1 it is f - e + e w with f = e^{d - max d} from MUFU.EX2, whose
+// relative error 2^-21 e^|w| / g(w) stays below ~1e-6 there (a cut at 1/2 was
+// measured to push single-position KL errors to 1e-5).
+// ---------------------------------------------------------------------------
+template <typename T, int NV>
+__device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const uint4 (&rd)[NV]) {
+  constexpr int E = Traits<T>::VEC * NV;
+  float mt = -INFINITY, md = -INFINITY;
+  if constexpr (sizeof(T) == 2) {
+    // two independent packed max chains per row (short dependency chains)
+    __nv_bfloat162 bt0 = *reinterpret_cast<const __nv_bfloat162*>(&rt[0].x), bt1 = bt0;
+    __nv_bfloat162 bd0 = *reinterpret_cast<const __nv_bfloat162*>(&rd[0].x), bd1 = bd0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const uint32_t wt[4] = {rt[v].x, rt[v].y, rt[v].z, rt[v].w};
+      const uint32_t wd[4] = {rd[v].x, rd[v].y, rd[v].z, rd[v].w};
+#pragma unroll
+      for (int h = 0; h < 4; h += 2) {
+        bt0 = __hmax2_nan(bt0, *reinterpret_cast<const __nv_bfloat162*>(&wt[h]));  // NaN propagates
+        bt1 = __hmax2_nan(bt1, *reinterpret_cast<const __nv_bfloat162*>(&wt[h + 1]));
+        bd0 = __hmax2(bd0, *reinterpret_cast<const __nv_bfloat162*>(&wd[h]));
+        bd1 = __hmax2(bd1, *reinterpret_cast<const __nv_bfloat162*>(&wd[h + 1]));
+      }
+    }
+    const __nv_bfloat162 bt = __hmax2_nan(bt0, bt1), bd = __hmax2(bd0, bd1);
+    const float lo = __low2float(bt), hi = __high2float(bt);
+    mt = (lo != lo || hi != hi) ? NAN : fmaxf(lo, hi);
+    md = fmaxf(__low2float(bd), __high2float(bd));
+  } else {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const uint32_t wt[4] = {rt[v].x, rt[v].y, rt[v].z, rt[v].w};
+      const uint32_t wd[4] = {rd[v].x, rd[v].y, rd[v].z, rd[v].w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        mt = max_nan(mt, __uint_as_float(wt[h]));
+        md = fmaxf(md, __uint_as_float(wd[h]));
+      }
+    }
+  }
+  float M, Dmax;
+  if constexpr (sizeof(T) == 2) {
+    // both maxima are bf16 values: one packed shuffle chain
+    __nv_bfloat162 pk = __floats2bfloat162_rn(mt, md);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint32_t y = __shfl_xor_sync(kFull, *reinterpret_cast<const uint32_t*>(&pk), o);
+      pk = __hmax2_nan(pk, *reinterpret_cast<const __nv_bfloat162*>(&y));
+    }
+    M = __low2float(pk);
+    const float dh = __high2float(pk);
+    Dmax = dh == dh ? dh : warp_max(md);  // all-NaN d in some lane: NaN-ignoring max
+  } else {
+    M = warp_max(mt);
+    Dmax = warp_max(md);
+  }
+  if (__any_sync(kFull, mt != mt)) M = NAN;
+  SubPartial p;
+  p.pad0 = p.pad1 = 0.f;
+  if (M <= -1e30f) {  // slice beyond V (padding only): an empty partial (NaN is not empty)
+    p.S = p.A = p.D = 0.f;
+    p.M = -INFINITY;
+    p.C = 0.f;
+    p.maxd = -INFINITY;
+    return p;
+  }
+  const float2 L2 = make_float2(kLog2e, kLog2e);
+#ifndef DSDE_POLY_DEG7
+  const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
+  const float2 K5 = make_float2(-2.0329201652202755e-04f, -2.0329201652202755e-04f);
+  const float2 K4 = make_float2(1.3885394437238574e-03f, 1.3885394437238574e-03f);
+  const float2 K3 = make_float2(-8.330884389579296e-03f, -8.330884389579296e-03f);
+  const float2 K2 = make_float2(4.166673496365547e-02f, 4.166673496365547e-02f);
+  const float2 K1 = make_float2(-1.6666696965694427e-01f, -1.6666696965694427e-01f);
+  const float2 K0 = make_float2(0.5f, 0.5f);
+#else
+  const float2 K7 = make_float2(-2.812654656736413e-06f, -2.812654656736413e-06f);
+  const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
+  const float2 K5 = make_float2(-1.9836986029986292e-04f, -1.9836986029986292e-04f);
+  const float2 K4 = make_float2(1.3885394437238574e-03f, 1.3885394437238574e-03f);
+  const float2 K3 = make_float2(-8.33334494382143e-03f, -8.33334494382143e-03f);
+  const float2 K2 = make_float2(4.166673496365547e-02f, 4.166673496365547e-02f);
+  const float2 K1 = make_float2(-1.666666716337204e-01f, -1.666666716337204e-01f);
+  const float2 K0 = make_float2(0.5f, 0.5f);
+#endif
+  const float Cw = M - Dmax;
+  const float ML2 = M * kLog2e, DL2 = Dmax * kLog2e;
+  const float2 nML2 = make_float2(-ML2, -ML2), nDL2 = make_float2(-DL2, -DL2);
+#ifdef DSDE_DUAL_ACC
+  constexpr int NA = 2;  // independent accumulator sets (shorter add chains)
+#else
+  constexpr int NA = 1;
+#endif
+  float2 S2[NA], A2[NA], D2[NA];
+#pragma unroll
+  for (int k = 0; k < NA; ++k) S2[k] = A2[k] = D2[k] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int h = 0; h < E; h += 2) {
+    const int k = (h >> 1) % NA;
+    const float2 tt = pair_of<T>(rt, h), dd = pair_of<T>(rd, h);
+    const float2 xt = __ffma2_rn(tt, L2, nML2);
+    const float2 arg = __ffma2_rn(dd, L2, nDL2);  // (d - max d) log2 e <= 0
+    const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
+    const float2 f = make_float2(fast_exp2(arg.x), fast_exp2(arg.y));
+    const float2 w = diff2<T>(tt, dd, Cw);
+    const float2 w2 = __fmul2_rn(w, w);
+#if defined(DSDE_ESTRIN) && defined(DSDE_POLY_DEG7)
+    const float2 q01 = __ffma2_rn(K1, w, K0), q23 = __ffma2_rn(K3, w, K2);
+    const float2 q45 = __ffma2_rn(K5, w, K4), q67 = __ffma2_rn(K7, w, K6);
+    const float2 w4 = __fmul2_rn(w2, w2);
+    const float2 pp = __ffma2_rn(__ffma2_rn(q67, w2, q45), w4, __ffma2_rn(q23, w2, q01));
+#else
+#ifndef DSDE_POLY_DEG7
+    float2 pp = __ffma2_rn(K6, w, K5);
+#else
+    float2 pp = __ffma2_rn(K7, w, K6);
+    pp = __ffma2_rn(pp, w, K5);
+#endif
+    pp = __ffma2_rn(pp, w, K4);
+    pp = __ffma2_rn(pp, w, K3);
+    pp = __ffma2_rn(pp, w, K2);
+    pp = __ffma2_rn(pp, w, K1);
+    pp = __ffma2_rn(pp, w, K0);
+#endif
+    S2[k] = __fadd2_rn(S2[k], e);
+    A2[k] = __ffma2_rn(e, w, A2[k]);
+    const float2 sm = __fmul2_rn(__fmul2_rn(e, w2), pp);
+    const float2 bg = __ffma2_rn(e, w, __fadd2_rn(f, make_float2(-e.x, -e.y)));
+    const float2 term = make_float2(fabsf(w.x) < 1.f ? sm.x : bg.x, fabsf(w.y) < 1.f ? sm.y : bg.y);
+    D2[k] = __fadd2_rn(D2[k], term);
+  }
+#pragma unroll
+  for (int k = 1; k < NA; ++k) {
+    S2[0] = __fadd2_rn(S2[0], S2[k]);
+    A2[0] = __fadd2_rn(A2[0], A2[k]);
+    D2[0] = __fadd2_rn(D2[0], D2[k]);
+  }
+  float S = S2[0].x + S2[0].y, A = A2[0].x + A2[0].y, D = D2[0].x + D2[0].y;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    S += __shfl_xor_sync(kFull, S, o);
+    A += __shfl_xor_sync(kFull, A, o);
+    D += __shfl_xor_sync(kFull, D, o);
+  }
+  p.S = S;
+  p.A = A;
+  p.D = D;
+  p.M = M;
+  p.C = Cw;
+  p.maxd = Dmax;
+  return p;
+}
+
+__device__ __forceinline__ void store_partial(SubPartial* dst, const SubPartial& p) {
+  const int lane = threadIdx.x & 31;
+  if (lane < 2) {
+    const float4 v = lane == 0 ? make_float4(p.S, p.A, p.D, p.M) : make_float4(p.C, p.maxd, 0.f, 0.f);
+    reinterpret_cast<float4*>(dst)[lane] = v;
+  }
+}
+
+// Sequence of draft row r, by a warp-cooperative forward scan from `seq`
+// (rows only move forward for a warp): 32 cu_sl entries per round trip.
+__device__ __forceinline__ int seq_of_row(const int32_t* cu_sl, int B, int seq, long long r) {
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    const int j = seq + 1 + lane;
+    const bool le = j <= B - 1 && __ldg(cu_sl + j) <= r;  // sequence j starts at or before r
+    const unsigned m = __ballot_sync(kFull, le);
+    seq += __popc(m);
+    if (m != kFull) return seq;
+  }
+}
+
+struct StreamArgs {
+  const void* tl;
+  long long ld_t;
+  const void* dl;
+  long long ld_d;
+  const int32_t* cu_sl;
+  int B, V, nsub, total;
+  SubPartial* part;
+};
+
+// ---------------------------------------------------------------------------
+// a1, "ldg" variant: persistent warps over the units q = (draft row r, slice u),
+// q = global warp + j * (total warps). Each lane keeps the NEXT unit's 2 x 4
+// 16-byte vectors in flight while it computes the current one (ping-pong
+// register buffers, no shared memory, no block barriers).
+// ---------------------------------------------------------------------------
+constexpr int kLdgThreads = 256;
+#ifndef DSDE_LDG_MINB
+#define DSDE_LDG_MINB 3
+#endif
+#ifndef DSDE_LDG_PREFETCH
+#define DSDE_LDG_PREFETCH 0
+#endif
+#ifndef DSDE_EXPERIMENT
+#define DSDE_EXPERIMENT 0
+#endif
+
+template <typename T>
+__device__ __forceinline__ void stream_unit_load(const StreamArgs& a, long long q, int& seq,
+                                                 uint4 (&rt)[Traits<T>::NV], uint4 (&rd)[Traits<T>::NV]) {
+  const int r = (int)((unsigned)q / (unsigned)a.nsub);  // units < 2^31 (checked by dsde_verify)
+  const int u = (int)q - r * a.nsub;
+  seq = seq_of_row(a.cu_sl, a.B, seq, r);
+  load_slice<T>(reinterpret_cast<const T*>(a.tl) + (long long)(r + seq) * a.ld_t, a.V, u, rt);
+  load_slice<T>(reinterpret_cast<const T*>(a.dl) + (long long)r * a.ld_d, a.V, u, rd);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(StreamArgs a) {
+  constexpr int NV = Traits<T>::NV;
+  const long long n_units = (long long)a.total * a.nsub;
+  const long long W = (long long)gridDim.x * (kLdgThreads / 32);
+  long long q = (long long)blockIdx.x * (kLdgThreads / 32) + (threadIdx.x >> 5);
+  if (q >= n_units) return;
+  int seq = 0;
+#if !DSDE_LDG_PREFETCH
+  for (; q < n_units; q += W) {
+    uint4 rt[NV], rd[NV];
+#if DSDE_EXPERIMENT == 2  // measurement only: math without the loads
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const uint32_t x = 0x3f803f80u ^ ((uint32_t)q * 2654435761u + v * 40503u + threadIdx.x) & 0x007f007fu;
+      rt[v] = make_uint4(x, x ^ 0x10001u, x ^ 0x20002u, x ^ 0x30003u);
+      rd[v] = make_uint4(x ^ 0x40004u, x ^ 0x50005u, x, x ^ 0x60006u);
+    }
+#else
+    stream_unit_load<T>(a, q, seq, rt, rd);
+#endif
+#if DSDE_EXPERIMENT == 1  // measurement only: the loads without the math
+    uint32_t acc = 0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc ^= rt[v].x ^ rt[v].y ^ rt[v].z ^ rt[v].w ^ rd[v].x ^ rd[v].y ^ rd[v].z ^ rd[v].w;
+    SubPartial p{};
+    p.S = __uint_as_float(acc);
+    store_partial(a.part + q, p);
+#else
+    store_partial(a.part + q, slice_stats<T>(rt, rd));
+#endif
+  }
+  return;
+#endif
+  uint4 at[NV], ad[NV], bt[NV], bd[NV];
+  stream_unit_load<T>(a, q, seq, at, ad);
+  while (true) {
+    const long long qb = q + W;
+    if (qb < n_units) stream_unit_load<T>(a, qb, seq, bt, bd);
+    store_partial(a.part + q, slice_stats<T>(at, ad));
+    if (qb >= n_units) return;
+    const long long qa = qb + W;
+    if (qa < n_units) stream_unit_load<T>(a, qa, seq, at, ad);
+    store_partial(a.part + qb, slice_stats<T>(bt, bd));
+    if (qa >= n_units) return;
+    q = qa;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier / TMA bulk-copy primitives (PTX)
+// ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -192,280 +533,98 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-struct StreamTmaArgs {
-  const void* tl;
-  long long ld_t;
-  const void* dl;
-  long long ld_d;
-  const int32_t* cu_sl;
-  int B, V, nchunks, total;
-  ChunkPartial* part;
-};
+// ---------------------------------------------------------------------------
+// a1, "tma" variant: per CTA 1 TMA producer warp + 8 consumer warps, 2 CTAs per
+// SM, a kTmaStages ring of (target, draft) chunk stages filled by 1-D bulk
+// copies. Items q = (draft row r, chunk c) are swept q = blockIdx.x + j*grid;
+// consumer warp w takes slice u = c*8 + w of the staged chunk, releases the
+// stage, and writes its slice partial.
+// ---------------------------------------------------------------------------
+constexpr int kTmaThreads = 32 * (kCWarps + 1);
+constexpr int kTmaStages = 3;
+constexpr int kTmaCtas = 2;
 
 template <typename T>
 __host__ __device__ constexpr int stage_row_bytes() {
   return chunk_elems<T>() * (int)sizeof(T);
 }
-
 template <typename T>
-__device__ __forceinline__ void unpack16(uint4 raw, float* x);
-template <>
-__device__ __forceinline__ void unpack16<uint16_t>(uint4 raw, float* x) {
-  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+__host__ __device__ constexpr int tma_smem() {
+  return kTmaStages * 2 * stage_row_bytes<T>() + 16 * kTmaStages + 2 * kTmaStages * 8;
+}
+
+// Consumer side of a staged chunk: the lane's words of slice `warp`, with the
+// unaligned tail (V * sizeof(T) not a multiple of 16) from global and padding
+// after V.
+template <typename T>
+__device__ __forceinline__ void stage_slice(const T* st, const T* grow, int n_el, int c0,
+                                            uint4 (&r)[Traits<T>::NV]) {
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, CH = chunk_elems<T>(), SL = sub_elems<T>();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (n_el == CH) {
 #pragma unroll
-  for (int h = 0; h < 4; ++h) {
-    x[2 * h] = bf16_lo(w[h]);
-    x[2 * h + 1] = bf16_hi(w[h]);
+    for (int v = 0; v < NV; ++v) r[v] = *reinterpret_cast<const uint4*>(st + warp * SL + (v * 32 + lane) * VEC);
+    return;
   }
-}
-template <>
-__device__ __forceinline__ void unpack16<float>(uint4 raw, float* x) {
-  x[0] = __uint_as_float(raw.x);
-  x[1] = __uint_as_float(raw.y);
-  x[2] = __uint_as_float(raw.z);
-  x[3] = __uint_as_float(raw.w);
-}
-
-template <typename T>
-__device__ __forceinline__ T pad_bits();
-template <>
-__device__ __forceinline__ uint16_t pad_bits<uint16_t>() { return (uint16_t)0xF14Au; }  // bf16 ~ -1e30
-template <>
-__device__ __forceinline__ float pad_bits<float>() { return -1e30f; }
-
-// Elements h, h+1 (h even) of a lane's 4 x 16-byte vectors as an fp32 pair.
-template <typename T>
-__device__ __forceinline__ float2 pair_of(const uint4 (&r)[Traits<T>::NV], int h);
-template <>
-__device__ __forceinline__ float2 pair_of<uint16_t>(const uint4 (&r)[4], int h) {
-  const uint4 x = r[h >> 3];
-  const int k = (h & 7) >> 1;
-  const uint32_t w = k == 0 ? x.x : k == 1 ? x.y : k == 2 ? x.z : x.w;
-  return make_float2(bf16_lo(w), bf16_hi(w));
-}
-template <>
-__device__ __forceinline__ float2 pair_of<float>(const uint4 (&r)[4], int h) {
-  const uint4 x = r[h >> 2];
-  return (h & 3) == 0 ? make_float2(__uint_as_float(x.x), __uint_as_float(x.y))
-                      : make_float2(__uint_as_float(x.z), __uint_as_float(x.w));
-}
-
-template <typename T>
-__device__ __forceinline__ float2 diff2(float2 t, float2 d, float C);
-template <>
-__device__ __forceinline__ float2 diff2<uint16_t>(float2 t, float2 d, float C) {
-  return __fadd2_rn(__fadd2_rn(t, make_float2(-d.x, -d.y)), make_float2(-C, -C));
-}
-template <>
-__device__ __forceinline__ float2 diff2<float>(float2 t, float2 d, float C) {
-  return make_float2(diff_ref<float>(t.x, d.x, C), diff_ref<float>(t.y, d.y, C));
-}
-
-// ---------------------------------------------------------------------------
-// a1, warp-specialised stream (the launched path). Per CTA: 8 consumer warps,
-// 1 TMA producer warp, 1 merger warp; 2 CTAs per SM; a 3-stage ring of 32 KB
-// stages filled by 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx).
-// Items q = (draft row r, chunk c) are swept in order, q = blockIdx.x + j*grid.
-// No CTA-wide barrier in the loop:
-//   * a consumer warp lifts its 1/8 of the chunk (t and d) into registers,
-//     releases the stage (mbarrier `consumed`), takes its own reference
-//     M = max t, C = M - max d (so e^{t-M} e^{-w} = e^{d - max d} <= 1: no
-//     overflow for any input), accumulates S, A, D with packed FFMA2 math and
-//     posts a warp partial (mbarriers `ready` / `freeb` guard the slot sets);
-//   * the producer refills a stage as soon as it is consumed;
-//   * the merger folds the 8 warp partials into the chunk partial in fp64
-//     (same re-referencing as merge_row).
-// ---------------------------------------------------------------------------
-constexpr int kCWarps = 8;
-constexpr int kWsThreads = 32 * (kCWarps + 2);  // + TMA producer warp + merger warp
-#ifndef DSDE_WS_STAGES
-#define DSDE_WS_STAGES 3
-#endif
-#ifndef DSDE_WS_CTAS
-#define DSDE_WS_CTAS 2
-#endif
-constexpr int kWsStages = DSDE_WS_STAGES;  // stages per CTA
-constexpr int kWsCtas = DSDE_WS_CTAS;      // CTAs per SM
-
-struct WarpPartial {  // 24 bytes
-  float S, A, D;      // about (M, C) of the warp slice
-  float M, C, maxd;
-};
-
-template <typename T>
-__host__ __device__ constexpr int stream_ws_smem() {
-  return kWsStages * 2 * stage_row_bytes<T>() + kWsStages * 2 * kCWarps * (int)sizeof(WarpPartial) +
-         6 * kWsStages * 8;
-}
-
-__device__ __forceinline__ float warp_max(float v) {
+  const int bulk_el = (int)(((uint32_t)(n_el * (int)sizeof(T)) & ~15u) / sizeof(T));
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
-  return v;
-}
-
-// q -> (draft row r, chunk c), advanced by the grid stride without divisions
-struct ItemCursor {
-  long long r;
-  int c;
-  __device__ void init(long long q, int nchunks) {
-    r = q / nchunks;
-    c = (int)(q - r * nchunks);
-  }
-  __device__ void advance(int dr, int dc, int nchunks) {
-    r += dr;
-    c += dc;
-    if (c >= nchunks) {
-      c -= nchunks;
-      r += 1;
+  for (int v = 0; v < NV; ++v) {
+    const int e0 = warp * SL + (v * 32 + lane) * VEC;
+    T b[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const int idx = e0 + e;
+      b[e] = idx < bulk_el ? st[idx] : idx < n_el ? grow[c0 + idx] : pad_bits<T>();
     }
-  }
-};
-
-// Sequence of draft row r, by a warp-cooperative forward scan from `seq`
-// (rows only move forward for a CTA): 32 cu_sl entries per round trip.
-__device__ __forceinline__ int seq_of_row(const int32_t* cu_sl, int B, int seq, long long r) {
-  const int lane = threadIdx.x & 31;
-  while (true) {
-    const int j = seq + 1 + lane;
-    const bool le = j <= B - 1 && __ldg(cu_sl + j) <= r;  // sequence j starts at or before r
-    const unsigned m = __ballot_sync(kFull, le);
-    seq += __popc(m);
-    if (m != kFull) return seq;
+    r[v] = *reinterpret_cast<const uint4*>(b);
   }
 }
 
 template <typename T>
-__device__ __forceinline__ void issue_item(const StreamTmaArgs& a, long long r, int c, int seq,
-                                           uint8_t* dst, uint64_t* bar) {
-  constexpr int CH = chunk_elems<T>(), ROWB = stage_row_bytes<T>();
-  const int c0 = c * CH;
-  const int n_el = min(CH, a.V - c0);
-  const uint32_t bytes = (uint32_t)(n_el * (int)sizeof(T)) & ~15u;
-  if (bytes) {
-    mbar_arrive_expect_tx(bar, 2 * bytes);
-    bulk_g2s(dst, reinterpret_cast<const T*>(a.tl) + (r + seq) * a.ld_t + c0, bytes, bar);
-    bulk_g2s(dst + ROWB, reinterpret_cast<const T*>(a.dl) + r * a.ld_d + c0, bytes, bar);
-  } else {
-    mbar_arrive(bar);
-  }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kWsThreads, kWsCtas) k_stream_ws(StreamTmaArgs a) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, E = VEC * NV, CH = chunk_elems<T>();
-  constexpr int ROWB = stage_row_bytes<T>();
-  constexpr int SL = CH / kCWarps;  // elements of a chunk owned by one consumer warp
+__global__ void __launch_bounds__(kTmaThreads, kTmaCtas) k_stream_tma(StreamArgs a) {
+  constexpr int CH = chunk_elems<T>(), ROWB = stage_row_bytes<T>(), NV = Traits<T>::NV;
   extern __shared__ __align__(128) uint8_t smem[];
-  WarpPartial* slots = reinterpret_cast<WarpPartial*>(smem + kWsStages * 2 * ROWB);
-  uint64_t* full = reinterpret_cast<uint64_t*>(slots + kWsStages * 2 * kCWarps);
-  uint64_t* consumed = full + kWsStages;
-  uint64_t* ready = consumed + kWsStages;   // [stage][2]: 8 warp partials posted
-  uint64_t* freeb = ready + 2 * kWsStages;  // [stage][2]: merger done with the slot set
-  const long long n_items = (long long)a.total * a.nchunks;
+  int4* sdesc = reinterpret_cast<int4*>(smem + kTmaStages * 2 * ROWB);  // (trow lo, trow hi, c, -)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sdesc + kTmaStages);
+  uint64_t* consumed = full + kTmaStages;
+  const int nc = a.nsub / kCWarps;
+  const long long n_items = (long long)a.total * nc;
   const int G = gridDim.x;
-  const int dr = G / a.nchunks, dc = G % a.nchunks;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kWsStages; ++s) {
+    for (int s = 0; s < kTmaStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&consumed[s], kCWarps);
-      for (int b = 0; b < 2; ++b) {
-        mbar_init(&ready[2 * s + b], kCWarps);
-        mbar_init(&freeb[2 * s + b], 1);
-      }
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
   if (warp == kCWarps) {
-    // ---------------- TMA producer: refill a stage once it is consumed ----------------
-    // (the whole warp tracks the row -> sequence cursor; lane 0 issues the copies;
-    // the next item's addresses are resolved before waiting for its stage)
-    ItemCursor it;
-    it.init(blockIdx.x, a.nchunks);
-    int seq = 0;
-    long long q = blockIdx.x;
-    for (int s = 0; s < kWsStages && q < n_items; ++s, q += G) {
-      seq = seq_of_row(a.cu_sl, a.B, seq, it.r);
-      if (lane == 0) issue_item<T>(a, it.r, it.c, seq, smem + s * 2 * ROWB, &full[s]);
-      it.advance(dr, dc, a.nchunks);
-    }
-    int s = 0;
-    uint32_t round = 0;
-    for (; q < n_items; q += G) {
-      seq = seq_of_row(a.cu_sl, a.B, seq, it.r);
-      mbar_wait(&consumed[s], round & 1u);
-      if (lane == 0) {
-        issue_item<T>(a, it.r, it.c, seq, smem + s * 2 * ROWB, &full[s]);
-      }
-      it.advance(dr, dc, a.nchunks);
-      if (++s == kWsStages) {
-        s = 0;
-        ++round;
-      }
-    }
-    return;
-  }
-  if (warp == kCWarps + 1) {
-    // ---------------- merger: 8 warp partials -> chunk partial (fp64) ----------------
-    int s = 0;
+    // ---------------- TMA producer (whole warp tracks the row cursor) ----------------
+    int seq = 0, s = 0;
     uint32_t round = 0;
     for (long long q = blockIdx.x; q < n_items; q += G) {
-      const uint32_t b = round & 1u, u = round >> 1;  // slot set (s, b), its u-th use
-      mbar_wait(&ready[2 * s + b], u & 1u);
-      const WarpPartial* wp = slots + (s * 2 + b) * kCWarps;
-      float Mr = -INFINITY, Dx = -INFINITY;
-#pragma unroll
-      for (int w = 0; w < kCWarps; ++w) {
-        Mr = fmaxf(Mr, wp[w].M);
-        Dx = fmaxf(Dx, wp[w].maxd);
-      }
-      const WarpPartial p = wp[lane < kCWarps ? lane : 0];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&freeb[2 * s + b]);  // slot set reusable
-      const float Cc = Mr - Dx;
-      double S = 0.0, A = 0.0, D = 0.0;
-      if (lane < kCWarps) {
-        const double ls = (double)p.M - (double)Mr;  // -inf for an empty slice
-        const double sc = exp(ls);
-        const double dl = (double)p.C - (double)Cc;
-        double sem, sg, E1;
-        if (fabs(dl) < 1.0) {
-          const double em = expm1(-dl);
-          sem = sc * em;
-          sg = sc * (em + dl);
-          E1 = sc + sem;
-        } else {
-          E1 = exp(ls - dl);
-          sem = E1 - sc;
-          sg = sem + sc * dl;
-        }
-        S = sc * (double)p.S;
-        A = sc * (double)p.A + sc * (double)p.S * dl;
-        D = E1 * (double)p.D - (double)p.A * sem + (double)p.S * sg;
-      }
-#pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
-        S += __shfl_xor_sync(kFull, S, o);
-        A += __shfl_xor_sync(kFull, A, o);
-        D += __shfl_xor_sync(kFull, D, o);
-      }
+      const long long r = q / nc;
+      const int c = (int)(q - r * nc);
+      seq = seq_of_row(a.cu_sl, a.B, seq, r);
+      if (round > 0) mbar_wait(&consumed[s], (round - 1) & 1u);
       if (lane == 0) {
-        ChunkPartial cp;
-        cp.S = S;
-        cp.A = A;
-        cp.D = D;
-        cp.M = Mr;
-        cp.C = Cc;
-        cp.idx = 0;
-        cp.flags = 0;
-        cp.maxd = Dx;
-        cp.pad = 0;
-        a.part[q] = cp;
+        const long long trow = r + seq;
+        sdesc[s] = make_int4((int)(trow & 0xffffffff), (int)(trow >> 32), c, 0);
+        const int c0 = c * CH;
+        const int n_el = min(CH, a.V - c0);
+        const uint32_t bytes = n_el > 0 ? (uint32_t)(n_el * (int)sizeof(T)) & ~15u : 0u;
+        uint8_t* dst = smem + s * 2 * ROWB;
+        if (bytes) {
+          mbar_arrive_expect_tx(&full[s], 2 * bytes);
+          bulk_g2s(dst, reinterpret_cast<const T*>(a.tl) + trow * a.ld_t + c0, bytes, &full[s]);
+          bulk_g2s(dst + ROWB, reinterpret_cast<const T*>(a.dl) + r * a.ld_d + c0, bytes, &full[s]);
+        } else {
+          mbar_arrive(&full[s]);
+        }
       }
-      if (++s == kWsStages) {
+      if (++s == kTmaStages) {
         s = 0;
         ++round;
       }
@@ -474,199 +633,48 @@ __global__ void __launch_bounds__(kWsThreads, kWsCtas) k_stream_ws(StreamTmaArgs
   }
 
   // ---------------- consumer warps ----------------
-  const float2 L2 = make_float2(kLog2e, kLog2e);
-  // h(-w), h(u) = (e^u - 1 - u)/u^2, degree-7 Chebyshev fit on |u| <= 1
-  // (1.1e-7 relative in fp32 Horner; tools/fit_g.py), in powers of w (odd
-  // coefficients negated). The MUFU form is used only for |w| >= 1, where its
-  // relative error 2^-21 e^|w| / g(w) stays below ~1e-6; a cut at 1/2 was
-  // measured to push single-position KL errors to 1e-5.
-  const float2 K7 = make_float2(-2.812654656736413e-06f, -2.812654656736413e-06f);
-  const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
-  const float2 K5 = make_float2(-1.9836986029986292e-04f, -1.9836986029986292e-04f);
-  const float2 K4 = make_float2(1.3885394437238574e-03f, 1.3885394437238574e-03f);
-  const float2 K3 = make_float2(-8.33334494382143e-03f, -8.33334494382143e-03f);
-  const float2 K2 = make_float2(4.166673496365547e-02f, 4.166673496365547e-02f);
-  const float2 K1 = make_float2(-1.666666716337204e-01f, -1.666666716337204e-01f);
-  const float2 K0 = make_float2(0.5f, 0.5f);
-  ItemCursor it;
-  it.init(blockIdx.x, a.nchunks);
   int s = 0;
   uint32_t round = 0;
   for (long long q = blockIdx.x; q < n_items; q += G) {
-    const int c0 = it.c * CH;
-    const int n_el = min(CH, a.V - c0);
+    const long long r = q / nc;
     mbar_wait(&full[s], round & 1u);
+    const int4 dsc = sdesc[s];
+    const int c = dsc.z;
+    const long long trow = (long long)(uint32_t)dsc.x | ((long long)dsc.y << 32);
+    const int c0 = c * CH;
+    const int n_el = max(0, min(CH, a.V - c0));
     const T* st = reinterpret_cast<const T*>(smem + s * 2 * ROWB);
-    const T* sd = reinterpret_cast<const T*>(smem + s * 2 * ROWB + ROWB);
-    // the lane's 2 x 16 words (raw bf16 pairs / fp32) of the chunk; converted
-    // to fp32 pair by pair inside the statistics loop (low register pressure)
     uint4 rt[NV], rd[NV];
-    float mt = -INFINITY, md = -INFINITY;
-    if (n_el == CH) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int e0 = warp * SL + (v * 32 + lane) * VEC;
-        rt[v] = *reinterpret_cast<const uint4*>(st + e0);
-        rd[v] = *reinterpret_cast<const uint4*>(sd + e0);
-      }
-    } else {
-      // last chunk of a row: bulk-copied part from shared memory, an unaligned
-      // tail (V * sizeof(T) not a multiple of 16) from global, padding after V
-      const int bulk_el = (int)(((uint32_t)(n_el * (int)sizeof(T)) & ~15u) / sizeof(T));
-      long long trow = 0;
-      if (bulk_el < n_el) {
-        int lo = 0, hi = a.B - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (__ldg(a.cu_sl + mid) <= it.r) lo = mid; else hi = mid - 1;
-        }
-        trow = it.r + lo;
-      }
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int e0 = warp * SL + (v * 32 + lane) * VEC;
-        T tb[VEC], db[VEC];
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const int idx = e0 + e;
-          tb[e] = pad_bits<T>();
-          db[e] = pad_bits<T>();
-          if (idx < bulk_el) {
-            tb[e] = st[idx];
-            db[e] = sd[idx];
-          } else if (idx < n_el) {
-            tb[e] = reinterpret_cast<const T*>(a.tl)[trow * a.ld_t + c0 + idx];
-            db[e] = reinterpret_cast<const T*>(a.dl)[it.r * a.ld_d + c0 + idx];
-          }
-        }
-        rt[v] = *reinterpret_cast<const uint4*>(tb);
-        rd[v] = *reinterpret_cast<const uint4*>(db);
-      }
-    }
+    stage_slice<T>(st, reinterpret_cast<const T*>(a.tl) + trow * a.ld_t, n_el, c0, rt);
+    stage_slice<T>(st + CH, reinterpret_cast<const T*>(a.dl) + r * a.ld_d, n_el, c0, rd);
     __syncwarp();
     if (lane == 0) mbar_arrive(&consumed[s]);
-    if constexpr (sizeof(T) == 2) {
-      // two independent max chains per row (short dependency chains)
-      __nv_bfloat162 bt0 = *reinterpret_cast<const __nv_bfloat162*>(&rt[0].x), bt1 = bt0;
-      __nv_bfloat162 bd0 = *reinterpret_cast<const __nv_bfloat162*>(&rd[0].x), bd1 = bd0;
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const uint32_t wt[4] = {rt[v].x, rt[v].y, rt[v].z, rt[v].w};
-        const uint32_t wd[4] = {rd[v].x, rd[v].y, rd[v].z, rd[v].w};
-#pragma unroll
-        for (int h = 0; h < 4; h += 2) {
-          bt0 = __hmax2_nan(bt0, *reinterpret_cast<const __nv_bfloat162*>(&wt[h]));  // NaN propagates
-          bt1 = __hmax2_nan(bt1, *reinterpret_cast<const __nv_bfloat162*>(&wt[h + 1]));
-          bd0 = __hmax2(bd0, *reinterpret_cast<const __nv_bfloat162*>(&wd[h]));
-          bd1 = __hmax2(bd1, *reinterpret_cast<const __nv_bfloat162*>(&wd[h + 1]));
-        }
-      }
-      const __nv_bfloat162 bt = __hmax2_nan(bt0, bt1), bd = __hmax2(bd0, bd1);
-      const float lo = __low2float(bt), hi = __high2float(bt);
-      mt = (lo != lo || hi != hi) ? NAN : fmaxf(lo, hi);
-      md = fmaxf(__low2float(bd), __high2float(bd));
-    } else {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const uint32_t wt[4] = {rt[v].x, rt[v].y, rt[v].z, rt[v].w};
-        const uint32_t wd[4] = {rd[v].x, rd[v].y, rd[v].z, rd[v].w};
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          mt = max_nan(mt, __uint_as_float(wt[h]));
-          md = fmaxf(md, __uint_as_float(wd[h]));
-        }
-      }
-    }
-    // warp reference: M = max t (NaN if any t is NaN), C = M - max d
-    float M, Dmax;
-    if constexpr (sizeof(T) == 2) {
-      // both maxima are bf16 values: one packed shuffle chain
-      __nv_bfloat162 pk = __floats2bfloat162_rn(mt, md);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint32_t y = __shfl_xor_sync(kFull, *reinterpret_cast<const uint32_t*>(&pk), o);
-        pk = __hmax2_nan(pk, *reinterpret_cast<const __nv_bfloat162*>(&y));
-      }
-      M = __low2float(pk);
-      const float dh = __high2float(pk);
-      Dmax = dh == dh ? dh : warp_max(md);  // all-NaN d in some lane: NaN-ignoring max
-    } else {
-      M = warp_max(mt);
-      Dmax = warp_max(md);
-    }
-    if (__any_sync(kFull, mt != mt)) M = NAN;
-    const uint32_t sb = round & 1u, su = round >> 1;  // slot set (s, sb), its su-th use
-    WarpPartial p;
-    if (M <= -1e30f) {  // slice beyond V (padding only): an empty partial (NaN is not empty)
-      p.S = p.A = p.D = 0.f;
-      p.M = -INFINITY;
-      p.C = 0.f;
-      p.maxd = -INFINITY;
-    } else {
-      const float Cw = M - Dmax;
-      const float ML2 = M * kLog2e, DL2 = Dmax * kLog2e;
-      const float2 nML2 = make_float2(-ML2, -ML2), nDL2 = make_float2(-DL2, -DL2);
-      float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
-#ifdef DSDE_STREAM_LITE  // measurement experiment only: memory pipeline with minimal math
-#pragma unroll
-      for (int h = 0; h < E; h += 2) {
-        const float2 tt = pair_of<T>(rt, h), dd = pair_of<T>(rd, h);
-        S2 = __fadd2_rn(S2, tt);
-        A2 = __fadd2_rn(A2, dd);
-      }
-#else
-#pragma unroll
-      for (int h = 0; h < E; h += 2) {
-        const float2 tt = pair_of<T>(rt, h), dd = pair_of<T>(rd, h);
-        const float2 xt = __ffma2_rn(tt, L2, nML2);
-        const float2 arg = __ffma2_rn(dd, L2, nDL2);  // (d - max d) log2 e <= 0
-        const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
-        const float2 f = make_float2(fast_exp2(arg.x), fast_exp2(arg.y));
-        const float2 w = diff2<T>(tt, dd, Cw);
-        // h(-w) by Estrin's scheme (dependency depth 4 instead of 7)
-        const float2 w2 = __fmul2_rn(w, w);
-        const float2 q01 = __ffma2_rn(K1, w, K0), q23 = __ffma2_rn(K3, w, K2);
-        const float2 q45 = __ffma2_rn(K5, w, K4), q67 = __ffma2_rn(K7, w, K6);
-        const float2 w4 = __fmul2_rn(w2, w2);
-        const float2 q03 = __ffma2_rn(q23, w2, q01), q47 = __ffma2_rn(q67, w2, q45);
-        const float2 pp = __ffma2_rn(q47, w4, q03);
-        S2 = __fadd2_rn(S2, e);
-        A2 = __ffma2_rn(e, w, A2);
-        const float2 sm = __fmul2_rn(__fmul2_rn(e, w2), pp);
-        const float2 bg = __ffma2_rn(e, w, __fadd2_rn(f, make_float2(-e.x, -e.y)));
-        const float2 term =
-            make_float2(fabsf(w.x) < 1.f ? sm.x : bg.x, fabsf(w.y) < 1.f ? sm.y : bg.y);
-        D2 = __fadd2_rn(D2, term);
-      }
-#endif
-      float S = S2.x + S2.y, A = A2.x + A2.y, D = D2.x + D2.y;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        S += __shfl_xor_sync(kFull, S, o);
-        A += __shfl_xor_sync(kFull, A, o);
-        D += __shfl_xor_sync(kFull, D, o);
-      }
-      p.S = S;
-      p.A = A;
-      p.D = D;
-      p.M = M;
-      p.C = Cw;
-      p.maxd = Dmax;
-    }
-    if (lane == 0) {
-      if (su > 0) mbar_wait(&freeb[2 * s + sb], (su - 1) & 1u);
-      slots[(s * 2 + sb) * kCWarps + warp] = p;
-      mbar_arrive(&ready[2 * s + sb]);
-    }
-    it.advance(dr, dc, a.nchunks);
-    if (++s == kWsStages) {
+    if (++s == kTmaStages) {
       s = 0;
       ++round;
     }
+    store_partial(a.part + r * a.nsub + c * kCWarps + warp, slice_stats<T>(rt, rd));
   }
 }
 
-#include "verify_draw.cuh"
+#include "verify_draw.cuh"  // a2-a4 kernels (inside namespace dsde)
+
+static int stream_variant() {  // 0 = ldg (default), 1 = tma
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DSDE_STREAM");
+    v = (e && strcmp(e, "tma") == 0) ? 1 : 0;
+  }
+  return v;
+}
+
+template <typename KernelT>
+static int resident_grid(KernelT k, int threads, int smem, int sms, int cap_per_sm) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
+  per_sm = std::max(1, cap_per_sm > 0 ? std::min(per_sm, cap_per_sm) : per_sm);
+  return per_sm * sms;
+}
 
 template <typename T>
 cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const int32_t* tokens,
@@ -678,40 +686,52 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   auto mark = [&]() {
     if (pr) cudaEventRecord(prof->next(), s);
   };
-  mark();
-  const int nc = (V + chunk_elems<T>() - 1) / chunk_elems<T>();
-  int dev = 0, sms = 148;
+  const int ns = n_subs(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32);
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  static bool attr_set[64] = {false};
-  if (!attr_set[dev & 63]) {
-    cudaFuncSetAttribute(k_stream_ws<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_ws_smem<T>());
-    cudaFuncSetAttribute(k_draw_ws<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, draw_ws_smem<T>());
-    attr_set[dev & 63] = true;
+  struct Grids {
+    int sms = 0, ldg = 0, tma = 0, draw = 0;
+  };
+  static Grids grids[64];
+  Grids& g = grids[dev & 63];
+  if (g.sms == 0) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_stream_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem<T>());
+    g.ldg = resident_grid(k_stream_ldg<T>, kLdgThreads, 0, sms, 0);
+    g.tma = resident_grid(k_stream_tma<T>, kTmaThreads, tma_smem<T>(), sms, kTmaCtas);
+    g.draw = resident_grid(k_draw_ldg<T>, kLdgThreads, 0, sms, 0);
+    g.sms = sms;
   }
-  // a1: statistics of every (draft row, vocab chunk)
-  if (total > 0) {
-    const long long items = (long long)total * nc;
-    const int grid = (int)std::min<long long>(items, (long long)kWsCtas * sms);
-    StreamTmaArgs ta{tl, ld_t, dl, ld_d, cu_sl, B, V, nc, total, ws.part};
-    k_stream_ws<T><<<grid, kWsThreads, stream_ws_smem<T>(), s>>>(ta);
+  const bool tma = stream_variant() == 1;
+  mark();
+  // a1: statistics of every (draft row, vocab slice)
+  StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, ns, total, ws.part};
+  if (tma) {
+    const long long items = (long long)total * (ns / kCWarps);
+    k_stream_tma<T><<<(int)std::min<long long>(items, g.tma), kTmaThreads, tma_smem<T>(), s>>>(sa);
+  } else {
+    const long long units = (long long)total * ns;
+    const long long blocks = (units + kLdgThreads / 32 - 1) / (kLdgThreads / 32);
+    k_stream_ldg<T><<<(int)std::min<long long>(blocks, g.ldg), kLdgThreads, 0, s>>>(sa);
   }
   mark();
   // a2-a3: row merge, KL, accept test, layout, draw record
-  FinArgs fa{B, V, total, nc, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, ws.part,
+  FinArgs fa{B, V, total, ns, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, ws.part,
              acc_len, emitted, kld, flags, ws.rec, err};
   k_finalize<T><<<B, kFinThreads, 0, s>>>(fa);
   mark();
   // a4: draw-weight masses of the drawn rows, then the inverse-CDF select
+  const int nd = n_subs_d(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32);
+  DrawArgs da{B, V, nd, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.ref};
   {
-    const long long items = (long long)B * nc;
-    const int grid = (int)std::min<long long>(items, (long long)kWsCtas * sms);
-    DrawArgs da{B, V, nc, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.cmax};
-    k_draw_ws<T><<<grid, kDrawThreads, draw_ws_smem<T>(), s>>>(da);
+    const long long units = (long long)B * nd;
+    const long long blocks = (units + kLdgThreads / 32 - 1) / (kLdgThreads / 32);
+    k_draw_ldg<T><<<(int)std::min<long long>(blocks, g.draw), kLdgThreads, 0, s>>>(da);
   }
   mark();
-  SelArgs sa{B, V, nc, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.cmax, emitted, flags, err};
-  k_select<T><<<(B + 3) / 4, 128, 0, s>>>(sa);
+  SelArgs sel{B, V, nd, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.ref, emitted, flags, err};
+  k_select<T><<<(B + 3) / 4, 128, 0, s>>>(sel);
   mark();
   return cudaGetLastError();
 }
@@ -722,6 +742,7 @@ using namespace dsde;
 
 extern "C" size_t dsde_verify_workspace_size(int B, int total_draft_rows, int V, dsde_dtype dtype) {
   if (B < 1 || V < 2 || total_draft_rows < 0) return 0;
+  if (dtype != DSDE_F32 && dtype != DSDE_BF16) return 0;
   return ws_layout(B, total_draft_rows, V, dtype, nullptr, nullptr);
 }
 
@@ -745,8 +766,7 @@ extern "C" dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_dra
   if (((uintptr_t)workspace) & 255) return DSDE_ERR_ARG;
   const size_t need = ws_layout(B, total_draft_rows, V, dtype, nullptr, nullptr);
   if (ws_bytes < need) return DSDE_ERR_ARG;
-  const int nc = n_chunks(V, dtype);
-  if ((long long)(total_draft_rows + B) * nc > 0x7fffffffLL) return DSDE_ERR_ARG;
+  if ((long long)(total_draft_rows + B) * n_subs(V, dtype) > 0x7fffffffLL) return DSDE_ERR_ARG;
   VerifyWs ws;
   ws_layout(B, total_draft_rows, V, dtype, &ws, reinterpret_cast<char*>(workspace));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -2,22 +2,21 @@
 // verify.cu inside namespace dsde; uses its helpers).
 //
 //   k_finalize  one CTA per sequence, one warp per draft position: fp64 merge of
-//               the row's chunk partials (lanes over chunks), KL, log p/q; then
+//               the row's slice partials (lanes over slices), KL, log p/q; then
 //               warp 0 runs the Philox accept test of every position, finds the
 //               first rejection a_i, lays out the emitted tokens and publishes
 //               the draw record (residual row a_i, or the bonus row k_i) (a2-a3).
-//   k_draw_ws   persistent CTAs with the same TMA ring as k_stream_ws over the
-//               items (sequence, vocab chunk) of the draw rows: every consumer
-//               warp forms the draw weights of its 1024-token (bf16) / 512-token
-//               (fp32) sub-chunk and writes their mass (a4, first pass).
-//   k_select    one warp per sequence: the inverse CDF over the sub-chunk
-//               masses, then inside the crossing sub-chunk (re-read from L2)
+//   k_draw_*    every warp forms the draw weights of one 1024-token (bf16) /
+//               512-token (fp32) slice of the drawn row and writes their mass
+//               (a4, first pass); persistent warps as k_stream_ldg.
+//   k_select    one warp per sequence: the inverse CDF over the slice masses,
+//               then inside the crossing slice (re-read from L2)
 //               in ascending token order (a4, D7).
 
 enum { IT_RESID = 1, IT_BONUS = 2, IT_NONE = 3 };
 
 struct FinArgs {
-  int B, V, total, nchunks;
+  int B, V, total, nsub;
   const int32_t* cu_sl;
   const int32_t* tokens;
   const void* tl;
@@ -25,7 +24,7 @@ struct FinArgs {
   const void* dl;
   long long ld_d;
   const uint64_t* seeds;
-  const ChunkPartial* part;
+  const SubPartial* part;
   int32_t* acc_len;
   int32_t* emitted;
   float* kld;
@@ -55,13 +54,14 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs a) {
     }
     return;
   }
-  const int nc = a.nchunks;
+  const int nc = a.nsub;
   if (warp < k) {
-    // ---- row j = warp: fp64 merge about M = max_c M_c, C = fp32(M - max d) ----
-    // Chunk c's w is shifted by Delta = C_c - C; with s = e^(M_c - M), E1 = s e^-Delta:
+    // ---- row j = warp: fp64 merge of the slice partials (lanes over slices c)
+    // about M = max_c M_c, C = fp32(M - max d). Slice c's w is shifted by
+    // Delta = C_c - C; with s = e^(M_c - M), E1 = s e^-Delta:
     //   S += s S_c,  A += s (A_c + S_c Delta),
     //   D += E1 D_c - A_c s expm1(-Delta) + S_c s g(Delta),  g(x) = expm1(-x) + x.
-    const ChunkPartial* P = a.part + ((long long)c0 + warp) * nc;
+    const SubPartial* P = a.part + ((long long)c0 + warp) * nc;
     float Ml = -INFINITY, Dl = -INFINITY;
     for (int c = lane; c < nc; c += 32) {
       Ml = max_nan(Ml, P[c].M);
@@ -75,10 +75,12 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs a) {
     const double M = (double)Ml, C = (double)(Ml - Dl);  // C is an fp32 value
     double S = 0.0, A = 0.0, D = 0.0;
     for (int c = lane; c < nc; c += 32) {
-      const ChunkPartial q = P[c];
-      const double ls = (double)q.M - M;
+      const float4 q0 = __ldg(reinterpret_cast<const float4*>(P + c));
+      const float4 q1 = __ldg(reinterpret_cast<const float4*>(P + c) + 1);
+      const double qS = q0.x, qA = q0.y, qD = q0.z, qM = q0.w, qC = q1.x;
+      const double ls = qM - M;
       const double s = exp(ls);
-      const double dl = (double)q.C - C;
+      const double dl = qC - C;
       double sem, sg, E1;
       if (fabs(dl) < 1.0) {
         const double em = expm1(-dl);
@@ -90,9 +92,9 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs a) {
         sem = E1 - s;
         sg = sem + s * dl;
       }
-      S += s * q.S;
-      A += s * q.A + s * q.S * dl;
-      D += E1 * q.D - q.A * sem + q.S * sg;
+      S += s * qS;
+      A += s * qA + s * qS * dl;
+      D += E1 * qD - qA * sem + qS * sg;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -205,34 +207,52 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs a) {
 //             rescaled by exp(m_u - max_u m_u) in fp64 by k_select.
 // k_select recomputes every weight bit-identically from the same words.
 // ---------------------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ float draw_weights_raw(const uint4 (&rt)[Traits<T>::NV],
-                                                  const uint4 (&rd)[Traits<T>::NV], bool resid,
+template <typename T, int NV>
+__device__ __forceinline__ float draw_weights_raw(const uint4 (&rt)[NV], const uint4 (&rd)[NV], bool resid,
                                                   float M, float Cf, double lam,
-                                                  float (&w)[Traits<T>::VEC * Traits<T>::NV]) {
-  constexpr int E = Traits<T>::VEC * Traits<T>::NV;
+                                                  float (&w)[Traits<T>::VEC * NV]) {
+  constexpr int E = Traits<T>::VEC * NV;
   if (resid) {
+    // packed (FFMA2) element pairs; h(-z) as in slice_stats (tools/fit_g.py, degree 7)
     const float lhi = (float)lam, llo = (float)(lam - (double)lhi);
     const float ML2 = M * kLog2e;
+    const float2 L2 = make_float2(kLog2e, kLog2e), nL2 = make_float2(-kLog2e, -kLog2e);
+    const float2 nML2 = make_float2(-ML2, -ML2), nC = make_float2(-Cf, -Cf);
+    const float2 LH = make_float2(lhi, lhi), LL = make_float2(llo, llo), ONE = make_float2(1.f, 1.f);
+    const float2 K7 = make_float2(-2.812654656736413e-06f, -2.812654656736413e-06f);
+    const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
+    const float2 K5 = make_float2(-1.9836986029986292e-04f, -1.9836986029986292e-04f);
+    const float2 K4 = make_float2(1.3885394437238574e-03f, 1.3885394437238574e-03f);
+    const float2 K3 = make_float2(-8.33334494382143e-03f, -8.33334494382143e-03f);
+    const float2 K2 = make_float2(4.166673496365547e-02f, 4.166673496365547e-02f);
+    const float2 K1 = make_float2(-1.666666716337204e-01f, -1.666666716337204e-01f);
+    const float2 K0 = make_float2(0.5f, 0.5f);
 #pragma unroll
     for (int h = 0; h < E; h += 2) {
       const float2 tt = pair_of<T>(rt, h), dd = pair_of<T>(rd, h);
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const float tv = q ? tt.y : tt.x, dv = q ? dd.y : dd.x;
-        const float ev = fast_exp2(fmaf(tv, kLog2e, -ML2));  // 0 for padding
-        const float z = (diff_ref<T>(tv, dv, Cf) + lhi) + llo;
-        float pz = -2.812654656736413e-06f;  // h(-z): tools/fit_g.py (degree 7, |u| <= 1)
-        pz = fmaf(pz, z, 2.5358644052175805e-05f);
-        pz = fmaf(pz, z, -1.9836986029986292e-04f);
-        pz = fmaf(pz, z, 1.3885394437238574e-03f);
-        pz = fmaf(pz, z, -8.33334494382143e-03f);
-        pz = fmaf(pz, z, 4.166673496365547e-02f);
-        pz = fmaf(pz, z, -1.666666716337204e-01f);
-        pz = fmaf(pz, z, 0.5f);
-        const float one_m = z < 1.f ? z * fmaf(-z, pz, 1.f) : 1.f - fast_exp2(-z * kLog2e);
-        w[h + q] = (z > 0.f && ev > 0.f) ? ev * one_m : 0.f;
+      const float2 xt = __ffma2_rn(tt, L2, nML2);
+      const float2 ev = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));  // 0 for padding
+      float2 z;
+      if constexpr (sizeof(T) == 2) {
+        z = __fadd2_rn(__fadd2_rn(tt, make_float2(-dd.x, -dd.y)), nC);  // t - d exact
+      } else {
+        z = make_float2(diff_ref<T>(tt.x, dd.x, Cf), diff_ref<T>(tt.y, dd.y, Cf));
       }
+      z = __fadd2_rn(__fadd2_rn(z, LH), LL);
+      float2 pz = __ffma2_rn(K7, z, K6);
+      pz = __ffma2_rn(pz, z, K5);
+      pz = __ffma2_rn(pz, z, K4);
+      pz = __ffma2_rn(pz, z, K3);
+      pz = __ffma2_rn(pz, z, K2);
+      pz = __ffma2_rn(pz, z, K1);
+      pz = __ffma2_rn(pz, z, K0);
+      const float2 sm = __fmul2_rn(z, __ffma2_rn(make_float2(-z.x, -z.y), pz, ONE));  // z (1 - z h(-z))
+      const float2 xz = __fmul2_rn(z, nL2);
+      const float2 bg = __fadd2_rn(ONE, make_float2(-fast_exp2(xz.x), -fast_exp2(xz.y)));  // 1 - e^-z
+      const float2 om = make_float2(z.x < 1.f ? sm.x : bg.x, z.y < 1.f ? sm.y : bg.y);
+      const float2 r = __fmul2_rn(ev, om);
+      w[h] = (z.x > 0.f && ev.x > 0.f) ? r.x : 0.f;
+      w[h + 1] = (z.y > 0.f && ev.y > 0.f) ? r.y : 0.f;
     }
     return M;
   }
@@ -245,19 +265,20 @@ __device__ __forceinline__ float draw_weights_raw(const uint4 (&rt)[Traits<T>::N
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(kFull, m, o));
   const float mL2 = m * kLog2e;
+  const float2 L2 = make_float2(kLog2e, kLog2e), nmL2 = make_float2(-mL2, -mL2);
 #pragma unroll
   for (int h = 0; h < E; h += 2) {
-    const float2 tt = pair_of<T>(rt, h);
-    w[h] = m <= -1e30f ? 0.f : fast_exp2(fmaf(tt.x, kLog2e, -mL2));
-    w[h + 1] = m <= -1e30f ? 0.f : fast_exp2(fmaf(tt.y, kLog2e, -mL2));
+    const float2 x = __ffma2_rn(pair_of<T>(rt, h), L2, nmL2);
+    w[h] = m <= -1e30f ? 0.f : fast_exp2(x.x);
+    w[h + 1] = m <= -1e30f ? 0.f : fast_exp2(x.y);
   }
   return m <= -1e30f ? -INFINITY : m;
 }
 
 // raw words of sub-chunk u of a row, from global memory (select pass)
-template <typename T>
-__device__ __forceinline__ void load_sub_raw(const T* row, int V, int u, uint4 (&r)[Traits<T>::NV]) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, SUB = 32 * VEC * NV;
+template <typename T, int NV>
+__device__ __forceinline__ void load_sub_raw(const T* row, int V, int u, uint4 (&r)[NV]) {
+  constexpr int VEC = Traits<T>::VEC, SUB = 32 * VEC * NV;
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
@@ -290,9 +311,9 @@ __device__ __forceinline__ double wscan_d(double x, int lane) {
 
 // mass of a lane's draw weights in the select pass's order: per vector, an
 // fp32 lane sum, then an fp64 warp sum
-template <typename T>
-__device__ __forceinline__ double draw_mass(const float (&w)[Traits<T>::VEC * Traits<T>::NV]) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV;
+template <typename T, int E>
+__device__ __forceinline__ double draw_mass(const float (&w)[E]) {
+  constexpr int VEC = Traits<T>::VEC, NV = E / VEC;
   double m = 0.0;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
@@ -305,153 +326,95 @@ __device__ __forceinline__ double draw_mass(const float (&w)[Traits<T>::VEC * Tr
 }
 
 // ---------------------------------------------------------------------------
-// k_draw_ws: items q = (sequence i, vocab chunk c), q = i * nc + c, swept by
-// persistent CTAs (q = blockIdx.x + j * grid). 1 TMA producer warp + 8
-// consumer warps per CTA, a kWsStages ring of 2 x 16 KB (bf16) stages. The
-// consumers write their sub-chunk mass and reference straight to global.
+// a4 first pass: units q = (sequence i, slice u), q = i * nsub + u. Each warp
+// writes the mass of its slice's draw weights and the slice reference.
 // ---------------------------------------------------------------------------
 struct DrawArgs {
-  int B, V, nchunks;
+  int B, V, nsub;
   const void* tl;
   long long ld_t;
   const void* dl;
   long long ld_d;
   const SeqRec* rec;
-  double* smass;  // [B * nc * 8]
-  float* sref;    // [B * nc * 8]
+  double* smass;  // [B * nsub]
+  float* sref;    // [B * nsub]
 };
 
-constexpr int kDrawThreads = 32 * (kCWarps + 1);
+struct DrawUnit {
+  int type;  // IT_RESID / IT_BONUS / IT_NONE
+  float M, Cf;
+  double lam;
+};
 
 template <typename T>
-__host__ __device__ constexpr int draw_ws_smem() {
-  return kWsStages * 2 * stage_row_bytes<T>() + kWsStages * 16 + 2 * kWsStages * 8;
+__device__ __forceinline__ DrawUnit draw_unit_load(const DrawArgs& a, long long q, uint4 (&rt)[Traits<T>::NVD],
+                                                   uint4 (&rd)[Traits<T>::NVD]) {
+  const int i = (int)(q / a.nsub), u = (int)(q - (long long)i * a.nsub);
+  const SeqRec* r = a.rec + i;
+  const int mode = __ldg(&r->mode);
+  DrawUnit d;
+  d.type = mode == MODE_RESIDUAL ? IT_RESID : mode == MODE_BONUS ? IT_BONUS : IT_NONE;
+  d.M = 0.f;
+  d.Cf = 0.f;
+  d.lam = 0.0;
+  if (d.type == IT_NONE) return d;
+  load_slice<T>(reinterpret_cast<const T*>(a.tl) + __ldg(&r->trow) * a.ld_t, a.V, u, rt);
+  if (d.type == IT_RESID) {
+    load_slice<T>(reinterpret_cast<const T*>(a.dl) + __ldg(&r->drow) * a.ld_d, a.V, u, rd);
+    d.M = __ldg(&r->M);
+    d.Cf = (float)__ldg(&r->C);
+    d.lam = __ldg(&r->lam);
+  }
+  return d;
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kDrawThreads, kWsCtas) k_draw_ws(DrawArgs a) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, E = VEC * NV, CH = chunk_elems<T>();
-  constexpr int ROWB = stage_row_bytes<T>();
-  constexpr int SL = CH / kCWarps;
-  extern __shared__ __align__(128) uint8_t smem[];
-  int4* sdesc = reinterpret_cast<int4*>(smem + kWsStages * 2 * ROWB);  // (type, seq, c, -)
-  uint64_t* full = reinterpret_cast<uint64_t*>(sdesc + kWsStages);
-  uint64_t* consumed = full + kWsStages;
-  const int nc = a.nchunks;
-  const long long n_items = (long long)a.B * nc;
-  const int G = gridDim.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kWsStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&consumed[s], kCWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+__device__ __forceinline__ void draw_unit_finish(const DrawArgs& a, long long q, const DrawUnit& d,
+                                                 const uint4 (&rt)[Traits<T>::NVD],
+                                                 const uint4 (&rd)[Traits<T>::NVD]) {
+  constexpr int E = Traits<T>::VEC * Traits<T>::NVD;
+  if (d.type == IT_NONE) return;
+  float w[E];
+  const float ref = draw_weights_raw<T>(rt, rd, d.type == IT_RESID, d.M, d.Cf, d.lam, w);
+  const double m = draw_mass<T>(w);
+  if ((threadIdx.x & 31) == 0) {
+    a.smass[q] = m;
+    a.sref[q] = ref;
   }
-  __syncthreads();
+}
 
-  if (warp == kCWarps) {
-    // ---------------- TMA producer ----------------
-    if (lane != 0) return;
-    int s = 0;
-    uint32_t round = 0;
-    for (long long q = blockIdx.x; q < n_items; q += G) {
-      const int i = (int)(q / nc), c = (int)(q - (long long)i * nc);
-      const SeqRec* r = a.rec + i;
-      const int mode = __ldg(&r->mode);
-      const int type = mode == MODE_RESIDUAL ? IT_RESID : mode == MODE_BONUS ? IT_BONUS : IT_NONE;
-      const long long trow = __ldg(&r->trow), drow = __ldg(&r->drow);
-      if (round > 0) mbar_wait(&consumed[s], (round - 1) & 1u);
-      sdesc[s] = make_int4(type, i, c, 0);
-      const int c0 = c * CH;
-      const int n_el = min(CH, a.V - c0);
-      const uint32_t bytes = (uint32_t)(n_el * (int)sizeof(T)) & ~15u;
-      uint8_t* dst = smem + s * 2 * ROWB;
-      if (type == IT_NONE || bytes == 0) {
-        mbar_arrive(&full[s]);
-      } else {
-        const bool two = type == IT_RESID;
-        mbar_arrive_expect_tx(&full[s], (two ? 2 : 1) * bytes);
-        bulk_g2s(dst, reinterpret_cast<const T*>(a.tl) + trow * a.ld_t + c0, bytes, &full[s]);
-        if (two) bulk_g2s(dst + ROWB, reinterpret_cast<const T*>(a.dl) + drow * a.ld_d + c0, bytes, &full[s]);
-      }
-      if (++s == kWsStages) {
-        s = 0;
-        ++round;
-      }
-    }
-    return;
-  }
-
-  // ---------------- consumers ----------------
-  int s = 0;
-  uint32_t round = 0;
-  for (long long q = blockIdx.x; q < n_items; q += G) {
-    mbar_wait(&full[s], round & 1u);
-    const int4 dsc = sdesc[s];
-    const int type = dsc.x, i = dsc.y, c = dsc.z;
-    const T* st = reinterpret_cast<const T*>(smem + s * 2 * ROWB);
-    const T* sd = reinterpret_cast<const T*>(smem + s * 2 * ROWB + ROWB);
-    const int c0 = c * CH;
-    const int n_el = min(CH, a.V - c0);
-    const bool resid = type == IT_RESID;
+// "ldg" variant: persistent warps, the next unit's vectors in flight while the
+// current one is computed (as k_stream_ldg).
+#ifndef DSDE_DRAW_MINB
+#define DSDE_DRAW_MINB 3
+#endif
+template <typename T>
+__global__ void __launch_bounds__(kLdgThreads, DSDE_DRAW_MINB) k_draw_ldg(DrawArgs a) {
+  constexpr int NV = Traits<T>::NVD;
+  const long long n_units = (long long)a.B * a.nsub;
+  const long long W = (long long)gridDim.x * (kLdgThreads / 32);
+  long long q = (long long)blockIdx.x * (kLdgThreads / 32) + (threadIdx.x >> 5);
+  if (q >= n_units) return;
+#if !DSDE_LDG_PREFETCH
+  for (; q < n_units; q += W) {
     uint4 rt[NV], rd[NV];
-    if (type != IT_NONE) {
-      if (n_el == CH) {
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const int e0 = warp * SL + (v * 32 + lane) * VEC;
-          rt[v] = *reinterpret_cast<const uint4*>(st + e0);
-          rd[v] = resid ? *reinterpret_cast<const uint4*>(sd + e0) : rt[v];
-        }
-      } else {
-        // last chunk: bulk-copied part, an unaligned tail from global, padding after V
-        const int bulk_el = (int)(((uint32_t)(n_el * (int)sizeof(T)) & ~15u) / sizeof(T));
-        const long long trow = __ldg(&a.rec[i].trow), drow = __ldg(&a.rec[i].drow);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const int e0 = warp * SL + (v * 32 + lane) * VEC;
-          T tb[VEC], db[VEC];
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            const int idx = e0 + e;
-            tb[e] = pad_bits<T>();
-            db[e] = pad_bits<T>();
-            if (idx < bulk_el) {
-              tb[e] = st[idx];
-              if (resid) db[e] = sd[idx];
-            } else if (idx < n_el) {
-              tb[e] = reinterpret_cast<const T*>(a.tl)[trow * a.ld_t + c0 + idx];
-              if (resid) db[e] = reinterpret_cast<const T*>(a.dl)[drow * a.ld_d + c0 + idx];
-            }
-          }
-          rt[v] = *reinterpret_cast<const uint4*>(tb);
-          rd[v] = *reinterpret_cast<const uint4*>(db);
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&consumed[s]);
-    if (++s == kWsStages) {
-      s = 0;
-      ++round;
-    }
-    if (type == IT_NONE) continue;
-    float Mr = 0.f, Cf = 0.f;
-    double lam = 0.0;
-    if (resid) {
-      Mr = __ldg(&a.rec[i].M);
-      Cf = (float)__ldg(&a.rec[i].C);
-      lam = __ldg(&a.rec[i].lam);
-    }
-    float w[E];
-    const float ref = draw_weights_raw<T>(rt, rd, resid, Mr, Cf, lam, w);
-    const double m = draw_mass<T>(w);
-    if (lane == 0) {
-      const long long o = ((long long)i * nc + c) * kCWarps + warp;
-      a.smass[o] = m;
-      a.sref[o] = ref;
-    }
+    const DrawUnit d = draw_unit_load<T>(a, q, rt, rd);
+    draw_unit_finish<T>(a, q, d, rt, rd);
+  }
+  return;
+#endif
+  uint4 at[NV], ad[NV], bt[NV], bd[NV];
+  DrawUnit da = draw_unit_load<T>(a, q, at, ad), db;
+  while (true) {
+    const long long qb = q + W;
+    if (qb < n_units) db = draw_unit_load<T>(a, qb, bt, bd);
+    draw_unit_finish<T>(a, q, da, at, ad);
+    if (qb >= n_units) return;
+    const long long qa = qb + W;
+    if (qa < n_units) da = draw_unit_load<T>(a, qa, at, ad);
+    draw_unit_finish<T>(a, qb, db, bt, bd);
+    if (qa >= n_units) return;
+    q = qa;
   }
 }
 
@@ -459,7 +422,7 @@ __global__ void __launch_bounds__(kDrawThreads, kWsCtas) k_draw_ws(DrawArgs a) {
 // k_select: one warp per sequence (4 per CTA).
 // ---------------------------------------------------------------------------
 struct SelArgs {
-  int B, V, nchunks;
+  int B, V, nsub;
   const void* tl;
   long long ld_t;
   const void* dl;
@@ -474,14 +437,14 @@ struct SelArgs {
 
 template <typename T>
 __global__ void __launch_bounds__(128) k_select(SelArgs a) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, E = VEC * NV, SUB = 32 * VEC * NV;
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NVD, E = VEC * NV, SUB = 32 * VEC * NV;
   const int i = blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= a.B) return;
   const SeqRec r = a.rec[i];
   if (r.mode != MODE_RESIDUAL && r.mode != MODE_BONUS) return;
   const bool resid = r.mode == MODE_RESIDUAL;
-  const int nsub = a.nchunks * kCWarps;
+  const int nsub = a.nsub;
   const double* wmass = a.smass + (long long)i * nsub;
   const float* wref = a.sref + (long long)i * nsub;
   float Mg = -INFINITY;
