@@ -42,6 +42,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "verify positions/s and HBM GB/s vs peak at V=128256, 1/2/4/8 B200"
 UNIT = "positions/s"
+STREAM_KERNEL = {"tma": "k_stream_tma", "wt": "k_stream_wt", "wt2": "k_stream_wt2"}.get(
+    os.environ.get("DSDE_STREAM", ""), "k_stream_ldg")
 
 CONFIGS = {
     # BASELINE.json configs[2]: the N=1 workload (and the per-rank shard at N>1)
@@ -254,7 +256,7 @@ def run(args):
         bonus = int(np.sum(acc == k))
         rows = 2 * n + bonus
         vbytes = rows * V * 2 + n * 4 + (n + B) * 8 + n * 4 + (n + B) * 5 + B * 4
-        sbytes = 2 * n * V * 2  # k_stream_ws: target + draft row of every draft position
+        sbytes = 2 * n * V * 2  # a1 stream kernel: target + draft row of every draft position
         rec.append(dict(inp=inp, n=n, k=k.copy(), rows=rows, vbytes=vbytes, sbytes=sbytes, next=nx))
         stats["pos"] += n
         stats["acc"] += int(acc.sum())
@@ -290,9 +292,13 @@ def run(args):
             e = rec[(args.warmup + j) % R]
             i = e["inp"]
             ev[j][0].record(stream)
-            step.verify(i.cu_sl, i.draft_tokens, i.target, i.draft, i.seeds, e["n"])
-            ev[j][1].record(stream)
-            step.signal_and_cap(i.cu_sl)
+            if args.split_calls:
+                step.verify(i.cu_sl, i.draft_tokens, i.target, i.draft, i.seeds, e["n"])
+                ev[j][1].record(stream)
+                step.signal_and_cap(i.cu_sl)
+            else:  # one dsde_step call: the whole hot path (verify + signal + cap)
+                step(i.cu_sl, i.draft_tokens, i.target, i.draft, i.seeds, e["n"])
+                ev[j][1].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize()
     state.profile(False)
@@ -330,7 +336,7 @@ def run(args):
 
     if rank == 0:
         peak, peak_kind = _peaks()
-        # dominant kernel: k_stream_ws (a1), timed by the library's per-launch events
+        # dominant kernel: the a1 stream kernel, timed by the library's per-launch events
         ach = (sbytes / ws) / (stream_ms / 1e3) / 1e9 if stream_ms > 0 else None
         vach = (vbytes / ws) / (verify_ms / 1e3) / 1e9 if verify_ms > 0 else None
         traffic = _traffic_record(f"cfg{args.config}")
@@ -339,7 +345,7 @@ def run(args):
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": _config_dict(args, cfg, ws),
-            "roofline": {"bound": "hbm", "kernel": "k_stream_ws (a1: target + draft row of every draft position)",
+            "roofline": {"bound": "hbm", "kernel": f"{STREAM_KERNEL} (a1: target + draft row of every draft position)",
                          "achieved": ach, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": (ach / peak) if ach else None,
                          "traffic": traffic,
@@ -351,8 +357,11 @@ def run(args):
                             "achieved_gbs": vach, "frac": (vach / peak) if vach else None},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            # per step: dsde_verify 4 kernels, dsde_update_signal 1, dsde_next_sl 1 (2 with NCCL)
-            "gpu_launches": args.steps * (4 + 1 + (1 if ws == 1 else 2)),
+            # per step: dsde_step = stream + tail (+ cap partial/apply around NCCL at N > 1);
+            # split calls: dsde_verify 2 (4 with DSDE_TAIL=split), update_signal 1, next_sl 1 (2 with NCCL)
+            "gpu_launches": args.steps * ((2 + (0 if ws == 1 else 2)) if not args.split_calls else
+                                          ((4 if os.environ.get("DSDE_TAIL") == "split" else 2) + 1 +
+                                           (1 if ws == 1 else 2))),
             "clocks": sampler.summary(),
             "verify_ms_per_step": verify_ms / args.steps,
             "rows_per_s": None,
@@ -405,8 +414,7 @@ def _e2e(args, m, step, rec, R, dev, ws, B):
         dt[:n + B].copy_(h["t"], non_blocking=True)
         dd[:n].copy_(h["d"], non_blocking=True)
         dseed[:n + B].copy_(h["s"], non_blocking=True)
-        step.verify(dcu, dtok[:n], dt[:n + B], dd[:n], dseed[:n + B], n)
-        step.signal_and_cap(dcu)
+        step(dcu, dtok[:n], dt[:n + B], dd[:n], dseed[:n + B], n)
         o_acc.copy_(step.accepted_len, non_blocking=True)
         o_em[:n + B].copy_(step.emitted[:n + B], non_blocking=True)
         o_nx.copy_(step.next_sl, non_blocking=True)
@@ -463,6 +471,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seqs", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--split-calls", action="store_true",
+                    help="time dsde_verify + dsde_update_signal + dsde_next_sl instead of one dsde_step")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -265,6 +265,32 @@ dsde_status dsde_next_sl(dsde_state st, int B, const int32_t* slots, const int32
                          const int32_t* budget, int32_t* next_sl, int32_t* cap,
                          dsde_comm comm, void* stream);
 
+/* ---------------------------------------------------------------------- */
+/* Whole step: §8(a) steps a1-a7 in one call                               */
+/* ---------------------------------------------------------------------- */
+
+/* One DSDE decoding step of the batch: exactly
+ *   dsde_verify(B, V, dtype, total_draft_rows, cu_sl, draft_tokens, ...);
+ *   dsde_update_signal(st, B, slots, cu_sl, kld, accepted_len, sl_hat, diag);
+ *   dsde_next_sl(st, B, slots, sl_hat, budget, next_sl, cap, comm);
+ * with the same arguments, results, state updates and errors as those three
+ * calls made in that order on `stream` (bit-identical outputs), but launched as
+ * two kernels on one GPU: the row stream (a1) and one tail kernel per batch
+ * that finalizes each sequence (a2-a3), draws its token (a4), updates its
+ * signal and predicts SL^ (a5-a6) in the same CTA, the CTA finishing last
+ * applying the cap (a7). With a communicator the cap's exact partial is
+ * all-reduced over NCCL in between (two more launches + the collective).
+ * The workspace is the one dsde_verify takes. Errors: the union of the three
+ * calls' synchronous checks (DSDE_ERR_ARG / DSDE_ERR_STATE) and
+ * DSDE_ERR_CUDA / DSDE_ERR_NCCL. Calls on one state must be serialised. */
+dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, int total_draft_rows,
+                      const int32_t* slots, const int32_t* cu_sl, const int32_t* draft_tokens,
+                      const void* target_logits, int64_t ld_t, const void* draft_logits,
+                      int64_t ld_d, const uint64_t* seeds, const int32_t* budget,
+                      int32_t* accepted_len, int32_t* emitted_tokens, float* kld, uint8_t* flags,
+                      int32_t* sl_hat, double* diag, int32_t* next_sl, int32_t* cap,
+                      void* workspace, size_t ws_bytes, dsde_comm comm, void* stream);
+
 /* Host-callable form of the cap rule used by dsde_next_sl (same code): the
  * cap from the global exact partial (sum of SL^, N, max SL^). Lets callers
  * that all-reduce the partial themselves (and the CPU tests) apply it. */

@@ -33,11 +33,13 @@ EXPORTS = (
     "dsde_config_default", "dsde_status_string", "dsde_abi_version", "dsde_state_create",
     "dsde_state_reset", "dsde_state_destroy", "dsde_state_bytes", "dsde_state_export",
     "dsde_state_import", "dsde_get_device_error", "dsde_clear_device_error",
-    "dsde_verify_workspace_size", "dsde_verify", "dsde_update_signal", "dsde_next_sl",
+    "dsde_verify_workspace_size", "dsde_verify", "dsde_update_signal", "dsde_next_sl", "dsde_step",
     "dsde_cap_value", "dsde_comm_unique_id", "dsde_comm_init", "dsde_comm_destroy",
     "dsde_profile_enable", "dsde_profile_read",
 )
 VERIFY_PHASES = ("stream", "finalize", "draw", "select")
+# default launch sequence: the stream kernel, then k_tail (finalize + draw + select)
+VERIFY_PHASES_FUSED = ("stream", "tail", "", "")
 
 
 class DsdeError(RuntimeError):
@@ -93,6 +95,8 @@ def lib() -> C.CDLL:
         L.dsde_verify_workspace_size.restype = S
         L.dsde_verify.argtypes = [I, I, I, I, P, P, P, I64, P, I64, P, P, P, P, P, P, S, P, P]
         L.dsde_update_signal.argtypes = [P, I, P, P, P, P, P, P, P]
+        L.dsde_step.argtypes = [P, I, I, I, I, P, P, P, P, I64, P, I64, P, P, P, P, P, P, P, P, P, P,
+                                P, S, P, P]
         L.dsde_next_sl.argtypes = [P, I, P, P, P, P, P, P, P]
         L.dsde_cap_value.argtypes = [P, I64, I64, I64]
         L.dsde_cap_value.restype = C.c_int32
@@ -187,7 +191,9 @@ class State:
         ms = (C.c_float * len(VERIFY_PHASES))()
         calls = C.c_int()
         _check(lib().dsde_profile_read(self.h, ms, C.byref(calls)), "dsde_profile_read")
-        return dict(zip(VERIFY_PHASES, (float(x) for x in ms))), calls.value
+        names = VERIFY_PHASES if os.environ.get("DSDE_TAIL") == "split" else VERIFY_PHASES_FUSED
+        out = {n: float(x) for n, x in zip(names, ms) if n}
+        return out, calls.value
 
 
 class Comm:
@@ -238,6 +244,19 @@ def dsde_next_sl(state: State, slots, sl_hat, budget, next_sl, cap, comm: Comm |
                               _stream(stream)), "dsde_next_sl")
 
 
+def dsde_step(state: State, V: int, total_draft_rows: int, slots, cu_sl, draft_tokens, target_logits,
+              draft_logits, seeds, budget, accepted_len, emitted_tokens, kld, flags, sl_hat, diag, next_sl,
+              cap, workspace, comm: Comm | None = None, stream=None):
+    """dsde_step (include/dsde.h): verify -> update_signal -> next_sl in one call."""
+    B = cu_sl.numel() - 1
+    _check(lib().dsde_step(
+        state.h, B, int(V), dtype_code(target_logits.dtype), int(total_draft_rows), _ptr(slots), _ptr(cu_sl),
+        _ptr(draft_tokens), _ptr(target_logits), target_logits.stride(0), _ptr(draft_logits),
+        draft_logits.stride(0), _ptr(seeds), _ptr(budget), _ptr(accepted_len), _ptr(emitted_tokens), _ptr(kld),
+        _ptr(flags), _ptr(sl_hat), _ptr(diag), _ptr(next_sl), _ptr(cap), _ptr(workspace), workspace.numel(),
+        comm.h if comm is not None else None, _stream(stream)), "dsde_step")
+
+
 @dataclass
 class StepOut:
     accepted_len: torch.Tensor   # int32 [B]
@@ -286,9 +305,14 @@ class Step:
         dsde_next_sl(self.state, self.slots, self.sl_hat, budget, self.next_sl, self.cap, self.comm, stream)
 
     def __call__(self, cu_sl, draft_tokens, target, draft, seeds, total_draft_rows: int, budget=None,
-                 stream=None) -> StepOut:
-        self.verify(cu_sl, draft_tokens, target, draft, seeds, total_draft_rows, stream)
-        self.signal_and_cap(cu_sl, budget, stream)
+                 stream=None, fused: bool = True) -> StepOut:
         n = total_draft_rows
+        if fused:  # one dsde_step call: stream kernel + tail kernel (+ the NCCL cap at N > 1)
+            dsde_step(self.state, self.V, n, self.slots, cu_sl, draft_tokens, target, draft, seeds, budget,
+                      self.accepted_len, self.emitted[: n + self.B], self.kld[:n], self.flags[: n + self.B],
+                      self.sl_hat, self.diag, self.next_sl, self.cap, self.ws, self.comm, stream)
+        else:
+            self.verify(cu_sl, draft_tokens, target, draft, seeds, total_draft_rows, stream)
+            self.signal_and_cap(cu_sl, budget, stream)
         return StepOut(self.accepted_len, self.emitted[: n + self.B], self.kld[:n], self.flags[: n + self.B],
                        self.sl_hat, self.next_sl, self.cap, self.diag)

@@ -39,6 +39,7 @@
 
 #include "common.cuh"
 #include "state.cuh"
+#include "signal.cuh"
 
 namespace dsde {
 
@@ -237,18 +238,24 @@ __device__ __forceinline__ void load_slice(const T* row, int V, int u, uint4 (&r
 // relative error 2^-21 e^|w| / g(w) stays below ~1e-6 there (a cut at 1/2 was
 // measured to push single-position KL errors to 1e-5).
 // ---------------------------------------------------------------------------
-template <typename T, int NV>
-__device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const uint4 (&rd)[NV]) {
-  constexpr int E = Traits<T>::VEC * NV;
-  float mt = -INFINITY, md = -INFINITY;
-  if constexpr (sizeof(T) == 2) {
-    // two independent packed max chains per row (short dependency chains)
-    __nv_bfloat162 bt0 = *reinterpret_cast<const __nv_bfloat162*>(&rt[0].x), bt1 = bt0;
-    __nv_bfloat162 bd0 = *reinterpret_cast<const __nv_bfloat162*>(&rd[0].x), bd1 = bd0;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const uint32_t wt[4] = {rt[v].x, rt[v].y, rt[v].z, rt[v].w};
-      const uint32_t wd[4] = {rd[v].x, rd[v].y, rd[v].z, rd[v].w};
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// Lane-level running maxima of t (NaN-propagating) and d over 16-byte vectors.
+template <typename T>
+struct LaneMax {
+  __nv_bfloat162 bt0, bt1, bd0, bd1;  // bf16: two packed chains per row
+  float mt, md;                       // fp32
+  __device__ __forceinline__ void init() {
+    const __nv_bfloat162 ninf = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+    bt0 = bt1 = bd0 = bd1 = ninf;
+    mt = md = -INFINITY;
+  }
+  __device__ __forceinline__ void add(const uint4& t, const uint4& d) {
+    const uint32_t wt[4] = {t.x, t.y, t.z, t.w};
+    const uint32_t wd[4] = {d.x, d.y, d.z, d.w};
+    if constexpr (sizeof(T) == 2) {
 #pragma unroll
       for (int h = 0; h < 4; h += 2) {
         bt0 = __hmax2_nan(bt0, *reinterpret_cast<const __nv_bfloat162*>(&wt[h]));  // NaN propagates
@@ -256,16 +263,7 @@ __device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const u
         bd0 = __hmax2(bd0, *reinterpret_cast<const __nv_bfloat162*>(&wd[h]));
         bd1 = __hmax2(bd1, *reinterpret_cast<const __nv_bfloat162*>(&wd[h + 1]));
       }
-    }
-    const __nv_bfloat162 bt = __hmax2_nan(bt0, bt1), bd = __hmax2(bd0, bd1);
-    const float lo = __low2float(bt), hi = __high2float(bt);
-    mt = (lo != lo || hi != hi) ? NAN : fmaxf(lo, hi);
-    md = fmaxf(__low2float(bd), __high2float(bd));
-  } else {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const uint32_t wt[4] = {rt[v].x, rt[v].y, rt[v].z, rt[v].w};
-      const uint32_t wd[4] = {rd[v].x, rd[v].y, rd[v].z, rd[v].w};
+    } else {
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         mt = max_nan(mt, __uint_as_float(wt[h]));
@@ -273,32 +271,48 @@ __device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const u
       }
     }
   }
-  float M, Dmax;
-  if constexpr (sizeof(T) == 2) {
-    // both maxima are bf16 values: one packed shuffle chain
-    __nv_bfloat162 pk = __floats2bfloat162_rn(mt, md);
+  // warp-wide slice reference: M = max t (NaN if any t is NaN), Dmax = max d
+  __device__ __forceinline__ void reduce(float& M, float& Dmax) {
+    if constexpr (sizeof(T) == 2) {
+      const __nv_bfloat162 bt = __hmax2_nan(bt0, bt1), bd = __hmax2(bd0, bd1);
+      const float lo = __low2float(bt), hi = __high2float(bt);
+      mt = (lo != lo || hi != hi) ? NAN : fmaxf(lo, hi);
+      md = fmaxf(__low2float(bd), __high2float(bd));
+      // both maxima are bf16 values: one packed shuffle chain
+      __nv_bfloat162 pk = __floats2bfloat162_rn(mt, md);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint32_t y = __shfl_xor_sync(kFull, *reinterpret_cast<const uint32_t*>(&pk), o);
-      pk = __hmax2_nan(pk, *reinterpret_cast<const __nv_bfloat162*>(&y));
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t y = __shfl_xor_sync(kFull, *reinterpret_cast<const uint32_t*>(&pk), o);
+        pk = __hmax2_nan(pk, *reinterpret_cast<const __nv_bfloat162*>(&y));
+      }
+      M = __low2float(pk);
+      const float dh = __high2float(pk);
+      Dmax = dh == dh ? dh : warp_max(md);  // all-NaN d in some lane: NaN-ignoring max
+    } else {
+      M = warp_max(mt);
+      Dmax = warp_max(md);
     }
-    M = __low2float(pk);
-    const float dh = __high2float(pk);
-    Dmax = dh == dh ? dh : warp_max(md);  // all-NaN d in some lane: NaN-ignoring max
-  } else {
-    M = warp_max(mt);
-    Dmax = warp_max(md);
+    if (__any_sync(kFull, mt != mt)) M = NAN;
   }
-  if (__any_sync(kFull, mt != mt)) M = NAN;
-  SubPartial p;
-  p.pad0 = p.pad1 = 0.f;
-  if (M <= -1e30f) {  // slice beyond V (padding only): an empty partial (NaN is not empty)
-    p.S = p.A = p.D = 0.f;
-    p.M = -INFINITY;
-    p.C = 0.f;
-    p.maxd = -INFINITY;
-    return p;
+};
+
+// Per-slice constants of the a1 sums about the reference (M, C = M - max d).
+struct SumRef {
+  float2 nML2, nDL2;
+  float Cw;
+  __device__ __forceinline__ SumRef(float M, float Dmax) {
+    Cw = M - Dmax;
+    const float ML2 = M * kLog2e, DL2 = Dmax * kLog2e;
+    nML2 = make_float2(-ML2, -ML2);
+    nDL2 = make_float2(-DL2, -DL2);
   }
+};
+
+// a1 accumulation of one element pair (packed FFMA2 math, two MUFU.EX2 per
+// element): S += e, A += e w, D += e g(w).
+template <typename T>
+__device__ __forceinline__ void pair_accum(float2 tt, float2 dd, const SumRef& R, float2& S2, float2& A2,
+                                           float2& D2) {
   const float2 L2 = make_float2(kLog2e, kLog2e);
 #ifndef DSDE_POLY_DEG7
   const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
@@ -318,65 +332,61 @@ __device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const u
   const float2 K1 = make_float2(-1.666666716337204e-01f, -1.666666716337204e-01f);
   const float2 K0 = make_float2(0.5f, 0.5f);
 #endif
-  const float Cw = M - Dmax;
-  const float ML2 = M * kLog2e, DL2 = Dmax * kLog2e;
-  const float2 nML2 = make_float2(-ML2, -ML2), nDL2 = make_float2(-DL2, -DL2);
-#ifdef DSDE_DUAL_ACC
-  constexpr int NA = 2;  // independent accumulator sets (shorter add chains)
-#else
-  constexpr int NA = 1;
-#endif
-  float2 S2[NA], A2[NA], D2[NA];
-#pragma unroll
-  for (int k = 0; k < NA; ++k) S2[k] = A2[k] = D2[k] = make_float2(0.f, 0.f);
-#pragma unroll
-  for (int h = 0; h < E; h += 2) {
-    const int k = (h >> 1) % NA;
-    const float2 tt = pair_of<T>(rt, h), dd = pair_of<T>(rd, h);
-    const float2 xt = __ffma2_rn(tt, L2, nML2);
-    const float2 arg = __ffma2_rn(dd, L2, nDL2);  // (d - max d) log2 e <= 0
-    const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
-    const float2 f = make_float2(fast_exp2(arg.x), fast_exp2(arg.y));
-    const float2 w = diff2<T>(tt, dd, Cw);
-    const float2 w2 = __fmul2_rn(w, w);
-#if defined(DSDE_ESTRIN) && defined(DSDE_POLY_DEG7)
-    const float2 q01 = __ffma2_rn(K1, w, K0), q23 = __ffma2_rn(K3, w, K2);
-    const float2 q45 = __ffma2_rn(K5, w, K4), q67 = __ffma2_rn(K7, w, K6);
-    const float2 w4 = __fmul2_rn(w2, w2);
-    const float2 pp = __ffma2_rn(__ffma2_rn(q67, w2, q45), w4, __ffma2_rn(q23, w2, q01));
-#else
+  const float2 xt = __ffma2_rn(tt, L2, R.nML2);
+  const float2 arg = __ffma2_rn(dd, L2, R.nDL2);  // (d - max d) log2 e <= 0
+  const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
+  const float2 f = make_float2(fast_exp2(arg.x), fast_exp2(arg.y));
+  const float2 w = diff2<T>(tt, dd, R.Cw);
+  const float2 w2 = __fmul2_rn(w, w);
 #ifndef DSDE_POLY_DEG7
-    float2 pp = __ffma2_rn(K6, w, K5);
+  float2 pp = __ffma2_rn(K6, w, K5);
 #else
-    float2 pp = __ffma2_rn(K7, w, K6);
-    pp = __ffma2_rn(pp, w, K5);
+  float2 pp = __ffma2_rn(K7, w, K6);
+  pp = __ffma2_rn(pp, w, K5);
 #endif
-    pp = __ffma2_rn(pp, w, K4);
-    pp = __ffma2_rn(pp, w, K3);
-    pp = __ffma2_rn(pp, w, K2);
-    pp = __ffma2_rn(pp, w, K1);
-    pp = __ffma2_rn(pp, w, K0);
-#endif
-    S2[k] = __fadd2_rn(S2[k], e);
-    A2[k] = __ffma2_rn(e, w, A2[k]);
-    const float2 sm = __fmul2_rn(__fmul2_rn(e, w2), pp);
-    const float2 bg = __ffma2_rn(e, w, __fadd2_rn(f, make_float2(-e.x, -e.y)));
-    const float2 term = make_float2(fabsf(w.x) < 1.f ? sm.x : bg.x, fabsf(w.y) < 1.f ? sm.y : bg.y);
-    D2[k] = __fadd2_rn(D2[k], term);
-  }
+  pp = __ffma2_rn(pp, w, K4);
+  pp = __ffma2_rn(pp, w, K3);
+  pp = __ffma2_rn(pp, w, K2);
+  pp = __ffma2_rn(pp, w, K1);
+  pp = __ffma2_rn(pp, w, K0);
+  S2 = __fadd2_rn(S2, e);
+  A2 = __ffma2_rn(e, w, A2);
+  const float2 sm = __fmul2_rn(__fmul2_rn(e, w2), pp);
+  const float2 bg = __ffma2_rn(e, w, __fadd2_rn(f, make_float2(-e.x, -e.y)));
+  const float2 term = make_float2(fabsf(w.x) < 1.f ? sm.x : bg.x, fabsf(w.y) < 1.f ? sm.y : bg.y);
+  D2 = __fadd2_rn(D2, term);
+}
+
+// the sums of one 16-byte vector pair
+template <typename T>
+__device__ __forceinline__ void vec_accum(const uint4& t, const uint4& d, const SumRef& R, float2& S2,
+                                          float2& A2, float2& D2) {
+  const uint4 rt[1] = {t}, rd[1] = {d};
 #pragma unroll
-  for (int k = 1; k < NA; ++k) {
-    S2[0] = __fadd2_rn(S2[0], S2[k]);
-    A2[0] = __fadd2_rn(A2[0], A2[k]);
-    D2[0] = __fadd2_rn(D2[0], D2[k]);
-  }
-  float S = S2[0].x + S2[0].y, A = A2[0].x + A2[0].y, D = D2[0].x + D2[0].y;
+  for (int h = 0; h < Traits<T>::VEC; h += 2) pair_accum<T>(pair_of<T>(rt, h), pair_of<T>(rd, h), R, S2, A2, D2);
+}
+
+__device__ __forceinline__ SubPartial empty_partial() {
+  SubPartial p;
+  p.pad0 = p.pad1 = 0.f;
+  p.S = p.A = p.D = 0.f;
+  p.M = -INFINITY;
+  p.C = 0.f;
+  p.maxd = -INFINITY;
+  return p;
+}
+
+__device__ __forceinline__ SubPartial finish_partial(float2 S2, float2 A2, float2 D2, float M, float Dmax,
+                                                     float Cw) {
+  float S = S2.x + S2.y, A = A2.x + A2.y, D = D2.x + D2.y;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     S += __shfl_xor_sync(kFull, S, o);
     A += __shfl_xor_sync(kFull, A, o);
     D += __shfl_xor_sync(kFull, D, o);
   }
+  SubPartial p;
+  p.pad0 = p.pad1 = 0.f;
   p.S = S;
   p.A = A;
   p.D = D;
@@ -384,6 +394,26 @@ __device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const u
   p.C = Cw;
   p.maxd = Dmax;
   return p;
+}
+
+// `after_max` runs (warp-uniformly) once the slice maxima are reduced over the
+// warp, i.e. once every lane's words have been consumed.
+template <typename T, int NV, typename Hook = NoHook>
+__device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const uint4 (&rd)[NV],
+                                                  Hook after_max = Hook()) {
+  LaneMax<T> mx;
+  mx.init();
+#pragma unroll
+  for (int v = 0; v < NV; ++v) mx.add(rt[v], rd[v]);
+  float M, Dmax;
+  mx.reduce(M, Dmax);
+  after_max();
+  if (M <= -1e30f) return empty_partial();  // slice beyond V (padding only; NaN is not empty)
+  const SumRef R(M, Dmax);
+  float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) vec_accum<T>(rt[v], rd[v], R, S2, A2, D2);
+  return finish_partial(S2, A2, D2, M, Dmax, R.Cw);
 }
 
 __device__ __forceinline__ void store_partial(SubPartial* dst, const SubPartial& p) {
@@ -657,13 +687,292 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtas) k_stream_tma(StreamArgs
   }
 }
 
+// ---------------------------------------------------------------------------
+// a1, "wt" variant (warp-private bulk-copy rings): every warp owns a
+// DSDE_WT_STAGES-deep ring of (target, draft) slice stages in shared memory and
+// its own mbarriers. Lane 0 refills a stage with two 1-D bulk copies
+// (cp.async.bulk, the TMA engine) as soon as the warp has lifted it into
+// registers, so each warp keeps DSDE_WT_STAGES units of HBM reads in flight
+// while it computes, at no register cost and with no coupling between warps
+// (no producer warp, no CTA barrier in the loop). Units q = (draft row r,
+// slice u) are swept q = global warp + j * (total warps), as k_stream_ldg.
+// ---------------------------------------------------------------------------
+#ifndef DSDE_WT_STAGES
+#define DSDE_WT_STAGES 3
+#endif
+#ifndef DSDE_WT_WARPS
+#define DSDE_WT_WARPS 8
+#endif
+#ifndef DSDE_WT_MINB
+#define DSDE_WT_MINB 2
+#endif
+constexpr int kWtWarps = DSDE_WT_WARPS;
+constexpr int kWtStages = DSDE_WT_STAGES;
+
+template <typename T>
+__host__ __device__ constexpr int wt_row_bytes() {
+  return sub_elems<T>() * (int)sizeof(T);
+}
+template <typename T>
+__host__ __device__ constexpr int wt_smem() {
+  return kWtWarps * kWtStages * (2 * wt_row_bytes<T>() + 16);  // stages + (mbarrier, seq) per stage
+}
+
+// Lane words of a staged slice: 128-bit shared loads (consecutive lanes,
+// consecutive 16 bytes: conflict-free); the unaligned tail (V * sizeof(T) not a
+// multiple of 16) from global, padding after V.
+template <typename T>
+__device__ __forceinline__ void wt_lift(const T* st, const T* grow, int n_el, int e_base,
+                                        uint4 (&r)[Traits<T>::NV]) {
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, SUB = sub_elems<T>();
+  const int lane = threadIdx.x & 31;
+  if (n_el == SUB) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) r[v] = *reinterpret_cast<const uint4*>(st + (v * 32 + lane) * VEC);
+    return;
+  }
+  const int bulk_el = (int)(((uint32_t)(n_el * (int)sizeof(T)) & ~15u) / sizeof(T));
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int e0 = (v * 32 + lane) * VEC;
+    if (e0 + VEC <= bulk_el) {
+      r[v] = *reinterpret_cast<const uint4*>(st + e0);
+    } else {
+      T b[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const int idx = e0 + e;
+        b[e] = idx < bulk_el ? st[idx] : idx < n_el ? grow[e_base + idx] : pad_bits<T>();
+      }
+      r[v] = *reinterpret_cast<const uint4*>(b);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kWtWarps * 32, DSDE_WT_MINB) k_stream_wt(StreamArgs a) {
+  constexpr int NV = Traits<T>::NV, SUB = sub_elems<T>(), ROWB = wt_row_bytes<T>(), ST = kWtStages;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * ST * 2 * ROWB;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kWtWarps * ST * 2 * ROWB) + warp * ST;
+  int* sseq = reinterpret_cast<int*>(smem + kWtWarps * ST * 2 * ROWB + kWtWarps * ST * 8) + warp * ST;
+  const long long n_units = (long long)a.total * a.nsub;
+  const long long W = (long long)gridDim.x * kWtWarps;
+  const long long q0 = (long long)blockIdx.x * kWtWarps + warp;
+  if (q0 >= n_units) return;
+  if (lane == 0) {
+    for (int s = 0; s < ST; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const T* tl = reinterpret_cast<const T*>(a.tl);
+  const T* dl = reinterpret_cast<const T*>(a.dl);
+  int seq_issue = 0;
+  // warp-wide: locate unit q's rows, then lane 0 starts the two bulk copies
+  auto issue = [&](long long q, int s) {
+    const int r = (int)((unsigned)q / (unsigned)a.nsub);
+    const int u = (int)q - r * a.nsub;
+    seq_issue = seq_of_row(a.cu_sl, a.B, seq_issue, r);
+    if (lane == 0) {
+      sseq[s] = seq_issue;
+      const int e0 = u * SUB;
+      const int n_el = max(0, min(SUB, a.V - e0));
+      const uint32_t bytes = (uint32_t)(n_el * (int)sizeof(T)) & ~15u;
+      uint8_t* dst = ring + s * 2 * ROWB;
+      if (bytes) {
+        mbar_arrive_expect_tx(&bar[s], 2 * bytes);
+        bulk_g2s(dst, tl + (long long)(r + seq_issue) * a.ld_t + e0, bytes, &bar[s]);
+        bulk_g2s(dst + ROWB, dl + (long long)r * a.ld_d + e0, bytes, &bar[s]);
+      } else {
+        mbar_arrive(&bar[s]);
+      }
+    }
+  };
+#pragma unroll 1
+  for (int s = 0; s < ST; ++s) {
+    const long long q = q0 + s * W;
+    if (q < n_units) issue(q, s);
+  }
+  int s = 0;
+  uint32_t phase = 0;
+#pragma unroll 1
+  for (long long q = q0; q < n_units; q += W) {
+    mbar_wait(&bar[s], phase);
+    const int r = (int)((unsigned)q / (unsigned)a.nsub);
+    const int u = (int)q - r * a.nsub;
+    const int e0 = u * SUB;
+    const int n_el = max(0, min(SUB, a.V - e0));
+    const T* st = reinterpret_cast<const T*>(ring + s * 2 * ROWB);
+    uint4 rt[NV], rd[NV];
+    if (n_el == SUB) {
+      wt_lift<T>(st, nullptr, SUB, 0, rt);
+      wt_lift<T>(st + SUB, nullptr, SUB, 0, rd);
+    } else {
+      const int sq = sseq[s];
+      wt_lift<T>(st, tl + (long long)(r + sq) * a.ld_t, n_el, e0, rt);
+      wt_lift<T>(st + SUB, dl + (long long)r * a.ld_d, n_el, e0, rd);
+    }
+    const long long qn = q + ST * W;
+    const int sn = s;
+    // the stage is refilled once every lane's words are in registers (the
+    // warp-wide max reduction inside slice_stats consumes all of them)
+    const SubPartial p = slice_stats<T>(rt, rd, [&]() {
+      if (qn < n_units) issue(qn, sn);
+    });
+    store_partial(a.part + q, p);
+    if (++s == ST) {
+      s = 0;
+      phase ^= 1u;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a1, "wt2" variant: warp-private bulk-copy rings as "wt", but the staged
+// slice is read from shared memory twice (pass 1: the slice maxima, pass 2:
+// the sums) instead of being lifted into registers, so the registers go to
+// instruction-level parallelism of the math instead of holding raw words.
+// The stage is refilled after pass 2.
+// ---------------------------------------------------------------------------
+#ifndef DSDE_W2_STAGES
+#define DSDE_W2_STAGES 3
+#endif
+#ifndef DSDE_W2_WARPS
+#define DSDE_W2_WARPS 4
+#endif
+#ifndef DSDE_W2_MINB
+#define DSDE_W2_MINB 2
+#endif
+constexpr int kW2Warps = DSDE_W2_WARPS;
+constexpr int kW2Stages = DSDE_W2_STAGES;
+
+template <typename T>
+__host__ __device__ constexpr int w2_smem() {
+  return kW2Warps * kW2Stages * (2 * wt_row_bytes<T>() + 16);
+}
+
+// vector v of a lane from a staged slice holding n_el valid elements (bulk
+// part in shared memory, unaligned tail from global, padding after V)
+template <typename T>
+__device__ __forceinline__ uint4 stage_vec(const T* st, const T* grow, bool full, int n_el, int bulk_el,
+                                           int e_base, int v) {
+  constexpr int VEC = Traits<T>::VEC;
+  const int e0 = (v * 32 + (threadIdx.x & 31)) * VEC;
+  if (full || e0 + VEC <= bulk_el) return *reinterpret_cast<const uint4*>(st + e0);
+  T b[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    const int idx = e0 + e;
+    b[e] = idx < bulk_el ? st[idx] : idx < n_el ? grow[e_base + idx] : pad_bits<T>();
+  }
+  return *reinterpret_cast<const uint4*>(b);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kW2Warps * 32, DSDE_W2_MINB) k_stream_wt2(StreamArgs a) {
+  constexpr int NV = Traits<T>::NV, SUB = sub_elems<T>(), ROWB = wt_row_bytes<T>(), ST = kW2Stages;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * ST * 2 * ROWB;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kW2Warps * ST * 2 * ROWB) + warp * ST;
+  int* sseq = reinterpret_cast<int*>(smem + kW2Warps * ST * 2 * ROWB + kW2Warps * ST * 8) + warp * ST;
+  const long long n_units = (long long)a.total * a.nsub;
+  const long long W = (long long)gridDim.x * kW2Warps;
+  const long long q0 = (long long)blockIdx.x * kW2Warps + warp;
+  if (q0 >= n_units) return;
+  if (lane == 0) {
+    for (int s = 0; s < ST; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const T* tl = reinterpret_cast<const T*>(a.tl);
+  const T* dl = reinterpret_cast<const T*>(a.dl);
+  int seq_issue = 0;
+  auto issue = [&](long long q, int s) {
+    const int r = (int)((unsigned)q / (unsigned)a.nsub);
+    const int u = (int)q - r * a.nsub;
+    seq_issue = seq_of_row(a.cu_sl, a.B, seq_issue, r);
+    if (lane == 0) {
+      sseq[s] = seq_issue;
+      const int e0 = u * SUB;
+      const int n_el = max(0, min(SUB, a.V - e0));
+      const uint32_t bytes = (uint32_t)(n_el * (int)sizeof(T)) & ~15u;
+      uint8_t* dst = ring + s * 2 * ROWB;
+      if (bytes) {
+        mbar_arrive_expect_tx(&bar[s], 2 * bytes);
+        bulk_g2s(dst, tl + (long long)(r + seq_issue) * a.ld_t + e0, bytes, &bar[s]);
+        bulk_g2s(dst + ROWB, dl + (long long)r * a.ld_d + e0, bytes, &bar[s]);
+      } else {
+        mbar_arrive(&bar[s]);
+      }
+    }
+  };
+#pragma unroll 1
+  for (int s = 0; s < ST; ++s) {
+    const long long q = q0 + s * W;
+    if (q < n_units) issue(q, s);
+  }
+  int s = 0;
+  uint32_t phase = 0;
+#pragma unroll 1
+  for (long long q = q0; q < n_units; q += W) {
+    mbar_wait(&bar[s], phase);
+    const int r = (int)((unsigned)q / (unsigned)a.nsub);
+    const int u = (int)q - r * a.nsub;
+    const int e0 = u * SUB;
+    const int n_el = max(0, min(SUB, a.V - e0));
+    const bool full = n_el == SUB;
+    const int bulk_el = (int)(((uint32_t)(n_el * (int)sizeof(T)) & ~15u) / sizeof(T));
+    const T* st = reinterpret_cast<const T*>(ring + s * 2 * ROWB);
+    const T* gt = full ? nullptr : tl + (long long)(r + sseq[s]) * a.ld_t;
+    const T* gd = full ? nullptr : dl + (long long)r * a.ld_d;
+    LaneMax<T> mx;
+    mx.init();
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      mx.add(stage_vec<T>(st, gt, full, n_el, bulk_el, e0, v), stage_vec<T>(st + SUB, gd, full, n_el, bulk_el, e0, v));
+    float M, Dmax;
+    mx.reduce(M, Dmax);
+    SubPartial p;
+    if (M <= -1e30f) {
+      p = empty_partial();
+    } else {
+      const SumRef R(M, Dmax);
+      float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        vec_accum<T>(stage_vec<T>(st, gt, full, n_el, bulk_el, e0, v),
+                     stage_vec<T>(st + SUB, gd, full, n_el, bulk_el, e0, v), R, S2, A2, D2);
+      p = finish_partial(S2, A2, D2, M, Dmax, R.Cw);
+    }
+    __syncwarp();
+    const long long qn = q + ST * W;
+    if (qn < n_units) issue(qn, s);
+    store_partial(a.part + q, p);
+    if (++s == ST) {
+      s = 0;
+      phase ^= 1u;
+    }
+  }
+}
+
 #include "verify_draw.cuh"  // a2-a4 kernels (inside namespace dsde)
 
-static int stream_variant() {  // 0 = ldg (default), 1 = tma
+static int tail_variant() {  // 0 = fused k_tail (default), 1 = split finalize/draw/select
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DSDE_TAIL");
+    v = (e && strcmp(e, "split") == 0) ? 1 : 0;
+  }
+  return v;
+}
+
+static int stream_variant() {  // 0 = ldg (default), 1 = tma, 2 = wt, 3 = wt2
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("DSDE_STREAM");
-    v = (e && strcmp(e, "tma") == 0) ? 1 : 0;
+    v = !e ? 0 : strcmp(e, "tma") == 0 ? 1 : strcmp(e, "wt") == 0 ? 2 : strcmp(e, "wt2") == 0 ? 3 : 0;
   }
   return v;
 }
@@ -676,12 +985,14 @@ static int resident_grid(KernelT k, int threads, int smem, int sms, int cap_per_
   return per_sm * sms;
 }
 
+// step != nullptr: the whole-step launch (dsde_step) with the signal (and, if
+// step->fuse_cap, the cap) fused into the tail kernel.
 template <typename T>
 cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const int32_t* tokens,
                           const void* tl, int64_t ld_t, const void* dl, int64_t ld_d,
                           const uint64_t* seeds, int32_t* acc_len, int32_t* emitted, float* kld,
                           uint8_t* flags, const VerifyWs& ws, int32_t* err, Profiler* prof,
-                          cudaStream_t s) {
+                          cudaStream_t s, const StepExtra* step = nullptr) {
   const bool pr = prof != nullptr && prof->on;
   auto mark = [&]() {
     if (pr) cudaEventRecord(prof->next(), s);
@@ -690,7 +1001,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   int dev = 0;
   cudaGetDevice(&dev);
   struct Grids {
-    int sms = 0, ldg = 0, tma = 0, draw = 0;
+    int sms = 0, ldg = 0, tma = 0, wt = 0, wt2 = 0, draw = 0;
   };
   static Grids grids[64];
   Grids& g = grids[dev & 63];
@@ -698,16 +1009,28 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_stream_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem<T>());
+    cudaFuncSetAttribute(k_stream_wt<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, wt_smem<T>());
     g.ldg = resident_grid(k_stream_ldg<T>, kLdgThreads, 0, sms, 0);
+    g.wt = resident_grid(k_stream_wt<T>, kWtWarps * 32, wt_smem<T>(), sms, 0);
+    cudaFuncSetAttribute(k_stream_wt2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, w2_smem<T>());
+    g.wt2 = resident_grid(k_stream_wt2<T>, kW2Warps * 32, w2_smem<T>(), sms, 0);
     g.tma = resident_grid(k_stream_tma<T>, kTmaThreads, tma_smem<T>(), sms, kTmaCtas);
     g.draw = resident_grid(k_draw_ldg<T>, kLdgThreads, 0, sms, 0);
     g.sms = sms;
   }
-  const bool tma = stream_variant() == 1;
+  const int variant = stream_variant();
   mark();
   // a1: statistics of every (draft row, vocab slice)
   StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, ns, total, ws.part};
-  if (tma) {
+  if (variant == 3) {
+    const long long units = (long long)total * ns;
+    const long long blocks = (units + kW2Warps - 1) / kW2Warps;
+    k_stream_wt2<T><<<(int)std::min<long long>(blocks, g.wt2), kW2Warps * 32, w2_smem<T>(), s>>>(sa);
+  } else if (variant == 2) {
+    const long long units = (long long)total * ns;
+    const long long blocks = (units + kWtWarps - 1) / kWtWarps;
+    k_stream_wt<T><<<(int)std::min<long long>(blocks, g.wt), kWtWarps * 32, wt_smem<T>(), s>>>(sa);
+  } else if (variant == 1) {
     const long long items = (long long)total * (ns / kCWarps);
     k_stream_tma<T><<<(int)std::min<long long>(items, g.tma), kTmaThreads, tma_smem<T>(), s>>>(sa);
   } else {
@@ -719,18 +1042,33 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   // a2-a3: row merge, KL, accept test, layout, draw record
   FinArgs fa{B, V, total, ns, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, ws.part,
              acc_len, emitted, kld, flags, ws.rec, err};
+  const int nd = n_subs_d(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32);
+  DrawArgs da{B, V, nd, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.ref};
+  SelArgs sel{B, V, nd, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.ref, emitted, flags, err};
+  if (step) {
+    k_tail<T, true><<<B, kFinThreads, 0, s>>>(fa, da, sel, *step);
+    mark();
+    mark();
+    mark();
+    return cudaGetLastError();
+  }
+  if (tail_variant() == 0) {
+    // a2-a4 fused: one CTA per sequence (the profiler's later phases read 0)
+    k_tail<T, false><<<B, kFinThreads, 0, s>>>(fa, da, sel, StepExtra{});
+    mark();
+    mark();
+    mark();
+    return cudaGetLastError();
+  }
   k_finalize<T><<<B, kFinThreads, 0, s>>>(fa);
   mark();
   // a4: draw-weight masses of the drawn rows, then the inverse-CDF select
-  const int nd = n_subs_d(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32);
-  DrawArgs da{B, V, nd, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.ref};
   {
     const long long units = (long long)B * nd;
     const long long blocks = (units + kLdgThreads / 32 - 1) / (kLdgThreads / 32);
     k_draw_ldg<T><<<(int)std::min<long long>(blocks, g.draw), kLdgThreads, 0, s>>>(da);
   }
   mark();
-  SelArgs sel{B, V, nd, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.ref, emitted, flags, err};
   k_select<T><<<(B + 3) / 4, 128, 0, s>>>(sel);
   mark();
   return cudaGetLastError();
@@ -779,5 +1117,61 @@ extern "C" dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_dra
     e = launch_verify<float>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                              draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld, flags,
                              ws, st->err, st->prof, s);
+  return e == cudaSuccess ? DSDE_OK : DSDE_ERR_CUDA;
+}
+
+// Implemented in api.cu / signal.cu.
+dsde_status dsde_comm_allreduce_i64(dsde_comm comm, long long* buf, int n_sum, int max_at,
+                                    cudaStream_t s);
+namespace dsde {
+cudaError_t launch_cap_multi(const CapArgs& a, dsde_comm comm, cudaStream_t s, dsde_status* st);
+}
+
+extern "C" dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, int total_draft_rows,
+                                 const int32_t* slots, const int32_t* cu_sl,
+                                 const int32_t* draft_tokens, const void* target_logits,
+                                 int64_t ld_t, const void* draft_logits, int64_t ld_d,
+                                 const uint64_t* seeds, const int32_t* budget,
+                                 int32_t* accepted_len, int32_t* emitted_tokens, float* kld,
+                                 uint8_t* flags, int32_t* sl_hat, double* diag, int32_t* next_sl,
+                                 int32_t* cap, void* workspace, size_t ws_bytes, dsde_comm comm,
+                                 void* stream) {
+  if (!st || !slots || !sl_hat || !next_sl || !cap || !cu_sl || !draft_tokens || !target_logits ||
+      !draft_logits || !seeds || !accepted_len || !emitted_tokens || !kld || !workspace)
+    return DSDE_ERR_ARG;
+  if (B < 1 || V < 2 || total_draft_rows < B || total_draft_rows > B * DSDE_MAX_SL)
+    return DSDE_ERR_ARG;
+  if (B > st->max_seqs) return DSDE_ERR_STATE;
+  if (dtype != DSDE_F32 && dtype != DSDE_BF16) return DSDE_ERR_ARG;
+  if (ld_t < V || ld_d < V) return DSDE_ERR_ARG;
+  const size_t esz = dtype == DSDE_BF16 ? 2 : 4;
+  if ((((uintptr_t)target_logits) | ((uintptr_t)draft_logits)) & 15) return DSDE_ERR_ARG;
+  if (((size_t)ld_t * esz) % 16 || ((size_t)ld_d * esz) % 16) return DSDE_ERR_ARG;
+  if (((uintptr_t)workspace) & 255) return DSDE_ERR_ARG;
+  if (ws_bytes < ws_layout(B, total_draft_rows, V, dtype, nullptr, nullptr)) return DSDE_ERR_ARG;
+  if ((long long)(total_draft_rows + B) * n_subs(V, dtype) > 0x7fffffffLL) return DSDE_ERR_ARG;
+  VerifyWs ws;
+  ws_layout(B, total_draft_rows, V, dtype, &ws, reinterpret_cast<char*>(workspace));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  StepExtra x;
+  x.sig = SignalArgs{st->cfg, B, st->max_seqs, slots, cu_sl, kld, accepted_len, sl_hat, diag,
+                     st->seq, st->err};
+  x.cap = CapArgs{st->cfg, B, st->max_seqs, slots, sl_hat, budget, next_sl, cap, st->seq, st->scratch};
+  x.fuse_cap = comm == nullptr;
+  x.counter = reinterpret_cast<unsigned*>(st->scratch + 4);
+  cudaError_t e;
+  if (dtype == DSDE_BF16)
+    e = launch_verify<uint16_t>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
+                                draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld,
+                                flags, ws, st->err, st->prof, s, &x);
+  else
+    e = launch_verify<float>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
+                             draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld, flags,
+                             ws, st->err, st->prof, s, &x);
+  if (e != cudaSuccess) return DSDE_ERR_CUDA;
+  if (!comm) return DSDE_OK;
+  dsde_status rs = DSDE_OK;
+  e = launch_cap_multi(x.cap, comm, s, &rs);
+  if (rs != DSDE_OK) return rs;
   return e == cudaSuccess ? DSDE_OK : DSDE_ERR_CUDA;
 }

@@ -35,12 +35,13 @@ struct FinArgs {
 
 constexpr int kFinThreads = 32 * DSDE_MAX_SL;
 
+// One CTA (kFinThreads) per sequence i; the draw record goes to *out (global
+// or shared; written by one lane of warp 0, visible to the CTA after a barrier).
 template <typename T>
-__global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs a) {
+__device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* out) {
   __shared__ double s_kl[DSDE_MAX_SL], s_lam[DSDE_MAX_SL], s_C[DSDE_MAX_SL];
   __shared__ float s_M[DSDE_MAX_SL];
   __shared__ int s_fin[DSDE_MAX_SL];
-  const int i = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = __ldg(a.cu_sl + i), c1 = __ldg(a.cu_sl + i + 1);
   const int k = c1 - c0;
@@ -49,7 +50,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs a) {
   if (!range_ok || !rows_ok) {
     if (threadIdx.x == 0) {
       a.acc_len[i] = -1;
-      a.rec[i].mode = MODE_ERROR;
+      out->mode = MODE_ERROR;
       raise_device_error(a.err, range_ok ? DSDE_DERR_ROWS : DSDE_DERR_BAD_SL, i);
     }
     return;
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs a) {
       r.drow = -1;
       r.M = 0.f;
       r.C = r.lam = r.u = 0.0;
-      a.rec[i] = r;
+      *out = r;
     }
     return;
   }
@@ -191,8 +192,13 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs a) {
       r.C = 0.0;
       r.lam = 0.0;
     }
-    a.rec[i] = r;
+    *out = r;
   }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs a) {
+  finalize_seq<T>(a, blockIdx.x, a.rec + blockIdx.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -347,25 +353,40 @@ struct DrawUnit {
 };
 
 template <typename T>
-__device__ __forceinline__ DrawUnit draw_unit_load(const DrawArgs& a, long long q, uint4 (&rt)[Traits<T>::NVD],
-                                                   uint4 (&rd)[Traits<T>::NVD]) {
+__device__ __forceinline__ DrawUnit draw_unit_load(const DrawArgs& a, long long q, const SeqRec& r,
+                                                   uint4 (&rt)[Traits<T>::NVD], uint4 (&rd)[Traits<T>::NVD]) {
   const int i = (int)(q / a.nsub), u = (int)(q - (long long)i * a.nsub);
-  const SeqRec* r = a.rec + i;
-  const int mode = __ldg(&r->mode);
+  const int mode = r.mode;
   DrawUnit d;
   d.type = mode == MODE_RESIDUAL ? IT_RESID : mode == MODE_BONUS ? IT_BONUS : IT_NONE;
   d.M = 0.f;
   d.Cf = 0.f;
   d.lam = 0.0;
   if (d.type == IT_NONE) return d;
-  load_slice<T>(reinterpret_cast<const T*>(a.tl) + __ldg(&r->trow) * a.ld_t, a.V, u, rt);
+  load_slice<T>(reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t, a.V, u, rt);
   if (d.type == IT_RESID) {
-    load_slice<T>(reinterpret_cast<const T*>(a.dl) + __ldg(&r->drow) * a.ld_d, a.V, u, rd);
-    d.M = __ldg(&r->M);
-    d.Cf = (float)__ldg(&r->C);
-    d.lam = __ldg(&r->lam);
+    load_slice<T>(reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d, a.V, u, rd);
+    d.M = r.M;
+    d.Cf = (float)r.C;
+    d.lam = r.lam;
   }
   return d;
+}
+
+template <typename T>
+__device__ __forceinline__ DrawUnit draw_unit_load(const DrawArgs& a, long long q, uint4 (&rt)[Traits<T>::NVD],
+                                                   uint4 (&rd)[Traits<T>::NVD]) {
+  const SeqRec* rp = a.rec + (int)(q / a.nsub);
+  SeqRec r;
+  r.mode = __ldg(&rp->mode);
+  if (r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS) {
+    r.trow = __ldg(&rp->trow);
+    r.drow = __ldg(&rp->drow);
+    r.M = __ldg(&rp->M);
+    r.C = __ldg(&rp->C);
+    r.lam = __ldg(&rp->lam);
+  }
+  return draw_unit_load<T>(a, q, r, rt, rd);
 }
 
 template <typename T>
@@ -435,13 +456,11 @@ struct SelArgs {
   int32_t* err;
 };
 
+// One warp: the inverse-CDF select of sequence i from its slice masses.
 template <typename T>
-__global__ void __launch_bounds__(128) k_select(SelArgs a) {
+__device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec& r) {
   constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NVD, E = VEC * NV, SUB = 32 * VEC * NV;
-  const int i = blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (i >= a.B) return;
-  const SeqRec r = a.rec[i];
   if (r.mode != MODE_RESIDUAL && r.mode != MODE_BONUS) return;
   const bool resid = r.mode == MODE_RESIDUAL;
   const int nsub = a.nsub;
@@ -580,4 +599,70 @@ __global__ void __launch_bounds__(128) k_select(SelArgs a) {
     a.emitted[r.slot] = tok < 0 ? 0 : tok;
     if (a.flags) a.flags[r.slot] |= fl;
   }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_select(SelArgs a) {
+  const int i = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (i >= a.B) return;
+  const SeqRec r = a.rec[i];
+  select_seq<T>(a, i, r);
+}
+
+// ---------------------------------------------------------------------------
+// k_tail: a2-a4 fused, one CTA (kFinThreads) per sequence: finalize (warp per
+// position), then every warp forms the draw-weight masses of its slices of the
+// drawn row (a4 first pass), then warp 0 selects the token. The drawn row is
+// read by the CTA that decided it, so no launch boundary separates the steps.
+// ---------------------------------------------------------------------------
+// Extra arguments of the fused whole-step launch (dsde_step): the signal of
+// every sequence (a5-a6) runs on the CTA's last warp as soon as its KLDs and
+// a_i exist, and the CTA that finishes last computes the batch cap and next SLs
+// (a7, single GPU; `counter` is zero before the launch and reset by that CTA).
+struct StepExtra {
+  SignalArgs sig;
+  CapArgs cap;
+  int fuse_cap;
+  unsigned* counter;
+};
+
+template <typename T, bool STEP>
+__global__ void __launch_bounds__(kFinThreads, 2) k_tail(FinArgs fa, DrawArgs da, SelArgs sa, StepExtra sx) {
+  constexpr int NVD = Traits<T>::NVD, NW = kFinThreads / 32;
+  __shared__ SeqRec s_rec;
+  __shared__ int s_last;
+  const int i = blockIdx.x;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_rec.mode = MODE_NONE;
+  __syncthreads();
+  finalize_seq<T>(fa, i, &s_rec);
+  __syncthreads();
+  const SeqRec r = s_rec;
+  const bool draw = r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS;
+  if (STEP && warp == NW - 1) {
+    signal_seq(sx.sig, i);
+    __threadfence();  // sl_hat / state visible to the CTA that applies the cap
+  }
+  if (draw) {
+    const long long q0 = (long long)i * da.nsub;
+    for (int u = warp; u < da.nsub; u += NW) {
+      uint4 rt[NVD], rd[NVD];
+      const DrawUnit d = draw_unit_load<T>(da, q0 + u, r, rt, rd);
+      draw_unit_finish<T>(da, q0 + u, d, rt, rd);
+    }
+  }
+  __syncthreads();
+  if (draw && warp == 0) select_seq<T>(sa, i, r);
+  if (!STEP || !sx.fuse_cap) return;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(sx.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  long long sum, n, mx;
+  cap_partial_block(sx.cap, sum, n, mx);
+  apply_cap(sx.cap, cap_rule(sx.cap.cfg, sum, n, mx));
+  if (threadIdx.x == 0) *sx.counter = 0u;
 }

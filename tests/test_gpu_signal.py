@@ -105,10 +105,13 @@ def test_state_export_import_replay(m):
     assert out[0] == gc.calib_sl
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["dsde_step", "three_calls"])
 @pytest.mark.parametrize("cfg_id", [1, 2])
-def test_closed_loop_parity(m, cfg_id):
+def test_closed_loop_parity(m, cfg_id, fused):
     """Configs 1-2: the full DSDE step for 64 steps; each side computes its own
-    KLDs; the oracle's next SL is teacher-forced into both (D16)."""
+    KLDs; the oracle's next SL is teacher-forced into both (D16). Run through
+    the fused dsde_step call and through dsde_verify / dsde_update_signal /
+    dsde_next_sl."""
     if cfg_id == 1:
         B, V, dtype, profiles, ceiling, steps = 4, 32000, torch.float32, ("code",), 4, 64
     else:
@@ -125,7 +128,7 @@ def test_closed_loop_parity(m, cfg_id):
     for s in range(steps):
         inp = synth.generate_step(w, s, k, device="cuda")
         host = inp.host_arrays()
-        out = stepper(inp.cu_sl, inp.draft_tokens, inp.target, inp.draft, inp.seeds, int(k.sum()))
+        out = stepper(inp.cu_sl, inp.draft_tokens, inp.target, inp.draft, inp.seeds, int(k.sum()), fused=fused)
         torch.cuda.synchronize()
         o = oracle_verify(host)
         rep = parity.compare_verify(host["cu_sl"], out.accepted_len.cpu().numpy(), out.emitted.cpu().numpy(),
@@ -149,3 +152,26 @@ def test_closed_loop_parity(m, cfg_id):
             assert np.array_equal(out.next_sl.cpu().numpy(), nx_o)
         k = nx_o.astype(np.int64)
     print(f"cfg{cfg_id}: {total} sl_ties={sl_ties}")
+
+
+def test_step_matches_three_calls(m):
+    """dsde_step (stream + fused tail/signal/cap) and the three separate calls
+    give bit-identical results and state, step after step (config-2 shapes)."""
+    B, V, dtype = 64, 32000, torch.bfloat16
+    gc, _ = _cfg_pair(m, sl_ceiling=8, calib_sl=4)
+    sa, sb = m.State(gc, B), m.State(gc, B)
+    pa, pb = m.Step(sa, B, V, dtype, with_diag=True), m.Step(sb, B, V, dtype, with_diag=True)
+    w = synth.Workload(B=B, V=V, dtype=dtype, profiles=("code", "low"), seed=77)
+    k = np.full(B, 4)
+    for s in range(12):
+        inp = synth.generate_step(w, s, k, device="cuda")
+        n = int(k.sum())
+        oa = pa(inp.cu_sl, inp.draft_tokens, inp.target, inp.draft, inp.seeds, n, fused=True)
+        ob = pb(inp.cu_sl, inp.draft_tokens, inp.target, inp.draft, inp.seeds, n, fused=False)
+        torch.cuda.synchronize()
+        for f in ("accepted_len", "emitted", "kld", "sl_hat", "next_sl", "cap"):
+            x, y = getattr(oa, f).cpu(), getattr(ob, f).cpu()
+            assert torch.equal(x, y), (s, f)
+        assert torch.equal(oa.diag.cpu().nan_to_num(-7.0), ob.diag.cpu().nan_to_num(-7.0)), s
+        k = oa.next_sl.cpu().numpy().astype(np.int64)
+    assert sa.device_error() == (0, -1) and sb.device_error() == (0, -1)
