@@ -68,6 +68,7 @@ typedef enum { DSDE_F32 = 0, DSDE_BF16 = 1 } dsde_dtype;
 #define DSDE_DERR_NONFINITE 3     /* non-finite logits in a row                          */
 #define DSDE_DERR_ROWS 4          /* cu_sl[B] != total_draft_rows                         */
 #define DSDE_DERR_BAD_SLOT 5      /* state slot outside [0, max_seqs)                     */
+#define DSDE_DERR_STALL 6         /* internal: a fused-kernel wait timed out (bug guard)  */
 
 /* Per-slot bits of the optional `flags` output of dsde_verify. */
 #define DSDE_FLAG_ACCEPT_NEAR_TIE 1  /* |u_acc - min(1, p/q)| < 1e-6 at this position      */

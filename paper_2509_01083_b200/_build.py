@@ -56,7 +56,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [_nvcc(), *ARCH, "-O3", "-std=c++17", "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
+    cmd = [_nvcc(), *ARCH, "-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-v" if verbose else "-O3",
            f"-I{INCLUDE}", f"-I{CSRC}", f"-I{_nccl_include()}",
            "-Xlinker", f"--version-script={os.path.join(CSRC, 'exports.map')}",

@@ -46,7 +46,7 @@ namespace dsde {
 template <typename T>
 struct Traits;
 #ifndef DSDE_NV_BF16
-#define DSDE_NV_BF16 6
+#define DSDE_NV_BF16 8
 #endif
 #ifndef DSDE_NVD_BF16
 #define DSDE_NVD_BF16 4
@@ -110,9 +110,14 @@ struct VerifyWs {
   SeqRec* rec;       // [B]
   double* mass;      // [B * nsub_d] draw-weight mass per draw slice of the drawn row
   float* ref;        // [B * nsub_d] reference of each slice mass (bonus)
+  void* rowres;      // [total] per-row results of the fused kernel (48 B each)
+  int* counters;     // fused kernel: ctl[8], row_cnt[total], seq_cnt/draw_cnt/fin/queue[B]
+  size_t counter_bytes;
 };
 
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+constexpr int kCtlInts = 128;  // the fused kernel's control block (FusedCtl), ints
 
 inline int n_subs(int V, dsde_dtype dt) {
   const int se = dt == DSDE_BF16 ? sub_elems<uint16_t>() : sub_elems<float>();
@@ -132,13 +137,18 @@ inline size_t ws_layout(int B, int total, int V, dsde_dtype dt, VerifyWs* ws, ch
   const size_t r_bytes = align256(sizeof(SeqRec) * (size_t)B);
   const size_t m_bytes = align256(sizeof(double) * (size_t)B * nd);
   const size_t x_bytes = align256(sizeof(float) * (size_t)B * nd);
+  const size_t rr_bytes = align256((size_t)48 * total);
+  const size_t c_bytes = align256(sizeof(int) * (kCtlInts + (size_t)total + 4 * (size_t)B));
   if (ws) {
     ws->part = reinterpret_cast<SubPartial*>(base);
     ws->rec = reinterpret_cast<SeqRec*>(base + p_bytes);
     ws->mass = reinterpret_cast<double*>(base + p_bytes + r_bytes);
     ws->ref = reinterpret_cast<float*>(base + p_bytes + r_bytes + m_bytes);
+    ws->rowres = base + p_bytes + r_bytes + m_bytes + x_bytes;
+    ws->counters = reinterpret_cast<int*>(base + p_bytes + r_bytes + m_bytes + x_bytes + rr_bytes);
+    ws->counter_bytes = sizeof(int) * (kCtlInts + (size_t)total + 4 * (size_t)B);
   }
-  return p_bytes + r_bytes + m_bytes + x_bytes;
+  return p_bytes + r_bytes + m_bytes + x_bytes + rr_bytes + c_bytes;
 }
 
 // max that propagates NaN (a NaN logit must reach the non-finite check)
@@ -416,11 +426,11 @@ __device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const u
   return finish_partial(S2, A2, D2, M, Dmax, R.Cw);
 }
 
+// lane 0 writes the whole 32-byte partial (so a release by lane 0 covers it)
 __device__ __forceinline__ void store_partial(SubPartial* dst, const SubPartial& p) {
-  const int lane = threadIdx.x & 31;
-  if (lane < 2) {
-    const float4 v = lane == 0 ? make_float4(p.S, p.A, p.D, p.M) : make_float4(p.C, p.maxd, 0.f, 0.f);
-    reinterpret_cast<float4*>(dst)[lane] = v;
+  if ((threadIdx.x & 31) == 0) {
+    reinterpret_cast<float4*>(dst)[0] = make_float4(p.S, p.A, p.D, p.M);
+    reinterpret_cast<float4*>(dst)[1] = make_float4(p.C, p.maxd, 0.f, 0.f);
   }
 }
 
@@ -483,28 +493,40 @@ __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(Strea
   if (q >= n_units) return;
   int seq = 0;
 #if !DSDE_LDG_PREFETCH
-  for (; q < n_units; q += W) {
+  // (row r, slice u) of unit q advanced incrementally by W units per step
+  int r = (int)((unsigned)q / (unsigned)a.nsub), u = (int)q - r * a.nsub;
+  const int dr = (int)((unsigned long long)W / (unsigned)a.nsub), du = (int)(W - (long long)dr * a.nsub);
+  while (r < a.total) {
     uint4 rt[NV], rd[NV];
 #if DSDE_EXPERIMENT == 2  // measurement only: math without the loads
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      const uint32_t x = 0x3f803f80u ^ ((uint32_t)q * 2654435761u + v * 40503u + threadIdx.x) & 0x007f007fu;
+      const uint32_t x = 0x3f803f80u ^ ((uint32_t)(r * 977 + u) * 2654435761u + v * 40503u + threadIdx.x) & 0x007f007fu;
       rt[v] = make_uint4(x, x ^ 0x10001u, x ^ 0x20002u, x ^ 0x30003u);
       rd[v] = make_uint4(x ^ 0x40004u, x ^ 0x50005u, x, x ^ 0x60006u);
     }
 #else
-    stream_unit_load<T>(a, q, seq, rt, rd);
+    seq = seq_of_row(a.cu_sl, a.B, seq, r);
+    load_slice<T>(reinterpret_cast<const T*>(a.tl) + (long long)(r + seq) * a.ld_t, a.V, u, rt);
+    load_slice<T>(reinterpret_cast<const T*>(a.dl) + (long long)r * a.ld_d, a.V, u, rd);
 #endif
+    SubPartial* dst = a.part + ((long long)r * a.nsub + u);
 #if DSDE_EXPERIMENT == 1  // measurement only: the loads without the math
     uint32_t acc = 0;
 #pragma unroll
     for (int v = 0; v < NV; ++v) acc ^= rt[v].x ^ rt[v].y ^ rt[v].z ^ rt[v].w ^ rd[v].x ^ rd[v].y ^ rd[v].z ^ rd[v].w;
     SubPartial p{};
     p.S = __uint_as_float(acc);
-    store_partial(a.part + q, p);
+    store_partial(dst, p);
 #else
-    store_partial(a.part + q, slice_stats<T>(rt, rd));
+    store_partial(dst, slice_stats<T>(rt, rd));
 #endif
+    u += du;
+    r += dr;
+    if (u >= a.nsub) {
+      u -= a.nsub;
+      ++r;
+    }
   }
   return;
 #endif
@@ -957,13 +979,16 @@ __global__ void __launch_bounds__(kW2Warps * 32, DSDE_W2_MINB) k_stream_wt2(Stre
   }
 }
 
-#include "verify_draw.cuh"  // a2-a4 kernels (inside namespace dsde)
+#include "verify_draw.cuh"   // a2-a4 kernels (inside namespace dsde)
+#include "verify_fused.cuh"  // the whole step in one persistent kernel
 
-static int tail_variant() {  // 0 = fused k_tail (default), 1 = split finalize/draw/select
+// 0 = stream kernel + k_tail (default), 1 = stream kernel + split finalize /
+// draw / select, 2 = one persistent kernel k_fused (DSDE_TAIL=tail|split|fused)
+static int tail_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("DSDE_TAIL");
-    v = (e && strcmp(e, "split") == 0) ? 1 : 0;
+    v = !e ? 0 : strcmp(e, "split") == 0 ? 1 : strcmp(e, "fused") == 0 ? 2 : 0;
   }
   return v;
 }
@@ -1019,6 +1044,63 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
     g.sms = sms;
   }
   const int variant = stream_variant();
+  const int tv = tail_variant();
+  if (tv == 2) {
+    static int fused_grid[64] = {0};
+    int& fg = fused_grid[dev & 63];
+    if (fg == 0) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused<T>, kFusedThreads, 0);
+      fg = std::max(1, per_sm) * g.sms;
+    }
+    mark();
+    FusedArgs fa2{};
+    fa2.B = B;
+    fa2.V = V;
+    fa2.total = total;
+    fa2.nsub = ns;
+    fa2.nd = n_subs_d(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32);
+    fa2.cu_sl = cu_sl;
+    fa2.tokens = tokens;
+    fa2.tl = tl;
+    fa2.ld_t = ld_t;
+    fa2.dl = dl;
+    fa2.ld_d = ld_d;
+    fa2.seeds = seeds;
+    fa2.part = ws.part;
+    fa2.rowres = reinterpret_cast<RowRes*>(ws.rowres);
+    fa2.rec = ws.rec;
+    fa2.smass = ws.mass;
+    fa2.sref = ws.ref;
+    fa2.acc_len = acc_len;
+    fa2.emitted = emitted;
+    fa2.kld = kld;
+    fa2.flags = flags;
+    fa2.err = err;
+    fa2.ctl = reinterpret_cast<FusedCtl*>(ws.counters);
+    fa2.row_cnt = ws.counters + kCtlInts;
+    fa2.seq_cnt = fa2.row_cnt + total;
+    fa2.draw_cnt = fa2.seq_cnt + B;
+    fa2.fin = fa2.draw_cnt + B;
+    fa2.queue = fa2.fin + B;
+    fa2.step = step != nullptr;
+    fa2.fuse_cap = step != nullptr && step->fuse_cap;
+    if (step) {
+      fa2.sig = step->sig;
+      fa2.cap = step->cap;
+    }
+    cudaError_t e = cudaMemsetAsync(ws.counters, 0, ws.counter_bytes, s);
+    if (e != cudaSuccess) return e;
+    const long long units = (long long)total * ns;
+    const int grid = (int)std::min<long long>(fg, std::max<long long>(1, (units + 7) / 8));
+    void* args[] = {&fa2};
+    e = cudaLaunchCooperativeKernel((const void*)k_fused<T>, dim3(grid), dim3(kFusedThreads), args, 0, s);
+    mark();
+    mark();
+    mark();
+    mark();
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
   mark();
   // a1: statistics of every (draft row, vocab slice)
   StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, ns, total, ws.part};
@@ -1052,7 +1134,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
     mark();
     return cudaGetLastError();
   }
-  if (tail_variant() == 0) {
+  if (tv == 0) {
     // a2-a4 fused: one CTA per sequence (the profiler's later phases read 0)
     k_tail<T, false><<<B, kFinThreads, 0, s>>>(fa, da, sel, StepExtra{});
     mark();

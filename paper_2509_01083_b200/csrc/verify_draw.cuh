@@ -468,17 +468,17 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   const float* wref = a.sref + (long long)i * nsub;
   float Mg = -INFINITY;
   if (!resid) {
-    for (int s0 = lane; s0 < nsub; s0 += 32) Mg = max_nan(Mg, wref[s0]);
+    for (int s0 = lane; s0 < nsub; s0 += 32) Mg = max_nan(Mg, __ldcg(wref + s0));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) Mg = max_nan(Mg, __shfl_xor_sync(kFull, Mg, o));
   }
   auto scale_of = [&](int s0) -> double {  // sub-chunk mass scale to the common reference
     if (resid) return 1.0;
-    const float ms = wref[s0];
+    const float ms = __ldcg(wref + s0);
     return ms == -INFINITY ? 0.0 : exp((double)ms - (double)Mg);
   };
   double R = 0.0;
-  for (int s0 = lane; s0 < nsub; s0 += 32) R += scale_of(s0) * wmass[s0];
+  for (int s0 = lane; s0 < nsub; s0 += 32) R += scale_of(s0) * __ldcg(wmass + s0);
   R = wsum_d(R);
   uint8_t fl = 0;
   const T* tp = reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t;
@@ -513,7 +513,7 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   double base = 0.0, base_last = 0.0, cum = 0.0;
   for (int g = 0; g < nsub; g += 32) {
     const int s0 = g + lane;
-    const double ms = s0 < nsub ? scale_of(s0) * wmass[s0] : 0.0;
+    const double ms = s0 < nsub ? scale_of(s0) * __ldcg(wmass + s0) : 0.0;
     const double incl = wscan_d(ms, lane);
     const unsigned pos = __ballot_sync(kFull, ms > 0.0);
     const unsigned cross = __ballot_sync(kFull, ms > 0.0 && cum + incl > target);

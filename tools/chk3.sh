@@ -1,0 +1,14 @@
+timeout 150 python -m pytest tests/test_gpu_signal.py -m gpu -x -q -k "three_calls" 2>&1 | grep -E "Error|assert|^E " | head -20
+timeout 150 python -m pytest tests -m gpu -q 2>&1 | tail -4
+for v in fused tail; do DSDE_TAIL=$v timeout 150 python bench.py --steps 50 --warmup 5 --no-cpu-baseline --e2e-steps 1 > gpurun_out/b_$v.json 2>gpurun_out/b_$v.err; done
+DSDE_NVCC_FLAGS="-DDSDE_FUSED_MINB=2" python paper_2509_01083_b200/_build.py --force > /dev/null 2>&1
+DSDE_TAIL=fused timeout 150 python bench.py --steps 50 --warmup 5 --no-cpu-baseline --e2e-steps 1 > gpurun_out/b_fm2.json 2>gpurun_out/b_fm2.err
+python - <<'PY'
+import json
+for v in ["fused","tail","fm2"]:
+    try:
+        d = json.loads(open(f"gpurun_out/b_{v}.json").read().strip().splitlines()[-1])
+        print(v, round(d["value"]), round(d["ms_per_step"], 4), {k: round(x * 1e3, 1) for k, x in d["verify_pass"]["ms_per_step"].items()}, round(d["roofline"]["frac"], 3))
+    except Exception as e:
+        print(v, "bench failed", e, open(f"gpurun_out/b_{v}.err").read()[-1500:])
+PY
