@@ -1,28 +1,33 @@
 // verify_fused.cuh — the whole verification step as ONE persistent kernel
 // (included by verify.cu inside namespace dsde, after verify_draw.cuh).
 //
-// k_fused: every warp sweeps the a1 stream units (draft row r, slice u) as
-// k_stream_ldg does, and the work that depends on them is done by whichever
-// warp completes its inputs, so no launch boundary or idle tail separates the
-// steps:
+// EXPERIMENTAL (DSDE_TAIL=fused; parity-green, NOT the default): measured
+// ~360 us per cfg3 step against ~212 us for the stream kernel + k_tail, because
+// the dependent latency chains of the tail work (row merge, finalize, draw,
+// select) run inside a memory system saturated by the stream and slow the
+// warps that carry them.
+//
+// k_fused: warps claim the a1 stream units (draft row r, slice u) in
+// increasing order from a global counter, and the work that depends on them is
+// done by whichever warp completes its inputs:
 //   * the warp that writes the last slice partial of row r merges the row
 //     (fp64), computes KL, log p/q and the Philox accept test (a2);
 //   * the warp that merges the last row of sequence i finds a_i, writes the
-//     KLDs and tokens, the draw record (a3) and, in the whole-step launch,
-//     updates the signal and SL^ (a5-a6); the warp that completes the last
-//     signal applies the batch cap and next SLs (a7, single GPU);
-//   * it then enqueues sequence i's draw task: nd slice units of the drawn row
-//     (residual row a_i, still in L2, or the bonus row), claimed one at a time
-//     between stream units by any warp; the warp completing the last unit of a
-//     task selects the token (a4).
+//     KLDs and tokens, the draw record (a3), publishes a ready flag and, in the
+//     whole-step launch, updates the signal and SL^ (a5-a6); the warp that
+//     completes the last signal applies the batch cap and next SLs (a7);
+//   * draw units (sequence i, slice u) are assigned statically to warps, in
+//     sequence order; a warp takes its next one between stream units once the
+//     sequence is ready; the warp completing the last unit of a sequence
+//     selects the token (a4).
 // Ordering: producers write with plain stores and bump a counter with a
 // release atomic (atom.add.release.gpu: MEMBAR.ALL.GPU, no SC fence, no L1
 // invalidation); the consumer that sees the final count issues an acquire
-// fence and reads with ld.global.cg. The grid is launched cooperatively (all CTAs
-// co-resident), so warps that wait for published tasks cannot starve the
-// warps that produce them. A bad cu_sl cannot hang the kernel: the warp that
+// fence and reads with ld.global.cg. Stream units are claimed dynamically, so
+// a warp waiting for a ready flag never holds work that flag depends on (no
+// co-residency requirement). A bad cu_sl cannot hang the kernel: the warp that
 // merges the last row finalizes every sequence that did not complete as a
-// data error.
+// data error, and a wait that never ends raises DSDE_DERR_STALL after ~2 s.
 
 struct RowRes {  // 48 bytes, per draft row
   double kl, lam, C;

@@ -1,0 +1,14 @@
+timeout 200 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for pf in 1 2 3; do
+  DSDE_NVCC_FLAGS="-DDSDE_TAIL_PF=$pf" python paper_2509_01083_b200/_build.py --force > /dev/null 2>&1
+  DSDE_TAIL=tail timeout 150 python bench.py --steps 50 --warmup 5 --no-cpu-baseline --e2e-steps 1 > gpurun_out/b_pf$pf.json 2>gpurun_out/b_pf$pf.err
+done
+python - <<'PY'
+import json
+for v in ["pf1","pf2","pf3"]:
+    try:
+        d = json.loads(open(f"gpurun_out/b_{v}.json").read().strip().splitlines()[-1])
+        print(v, round(d["value"]), round(d["ms_per_step"], 4), {k: round(x * 1e3, 1) for k, x in d["verify_pass"]["ms_per_step"].items()}, round(d["roofline"]["frac"], 3))
+    except Exception as e:
+        print(v, "bench failed", e, open(f"gpurun_out/b_{v}.err").read()[-1500:])
+PY
