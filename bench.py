@@ -339,7 +339,11 @@ def run(args):
         # dominant kernel: the a1 stream kernel, timed by the library's per-launch events
         ach = (sbytes / ws) / (stream_ms / 1e3) / 1e9 if stream_ms > 0 else None
         vach = (vbytes / ws) / (verify_ms / 1e3) / 1e9 if verify_ms > 0 else None
-        traffic = _traffic_record(f"cfg{args.config}")
+        # DRAM read+write bytes per launch of the stream kernel: the ratio to the
+        # algorithmic bytes measured on one ncu --set full launch (profiles/),
+        # scaled to this run's per-launch algorithmic bytes
+        trec = _traffic_record(f"cfg{args.config}")
+        traffic = (trec["ratio"] * sbytes / ws / args.steps) if trec else None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
@@ -349,6 +353,7 @@ def run(args):
                          "achieved": ach, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": (ach / peak) if ach else None,
                          "traffic": traffic,
+                         "traffic_source": trec["source"] if trec else None,
                          "algorithmic_bytes_per_launch": sbytes / ws / args.steps,
                          "avg_launch_ms": stream_ms / args.steps},
             "verify_pass": {"kernels": list(phase_ms), "ms_per_step": {k: v / args.steps for k, v in phase_ms.items()},
