@@ -101,7 +101,7 @@ struct SeqRec {  // 64 bytes
   double C;          // reference t - d (residual)
   double lam;        // log1p(y) = log(sum_v p_v exp(-w_v)) (residual)
   double u;          // u_smp of the slot
-  double pad1;
+  double S;          // sum_v exp(t_v - M) of the drawn row (residual)
 };
 static_assert(sizeof(SeqRec) == 64, "SeqRec layout");
 

@@ -39,7 +39,7 @@ constexpr int kFinThreads = 32 * DSDE_MAX_SL;
 // or shared; written by one lane of warp 0, visible to the CTA after a barrier).
 template <typename T>
 __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* out) {
-  __shared__ double s_kl[DSDE_MAX_SL], s_lam[DSDE_MAX_SL], s_C[DSDE_MAX_SL];
+  __shared__ double s_kl[DSDE_MAX_SL], s_lam[DSDE_MAX_SL], s_C[DSDE_MAX_SL], s_S[DSDE_MAX_SL];
   __shared__ float s_M[DSDE_MAX_SL];
   __shared__ int s_fin[DSDE_MAX_SL];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -114,6 +114,7 @@ __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* ou
       s_lam[warp] = lam;
       s_C[warp] = C;
       s_M[warp] = Ml;
+      s_S[warp] = S;
       s_fin[warp] = isfinite(S) && isfinite(A) && isfinite(D) && S > 0.0 && isfinite(M) &&
                     isfinite(C) && isfinite(kl);
     }
@@ -147,7 +148,7 @@ __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* ou
   const unsigned am = __ballot_sync(kFull, acc);
   SeqRec r;
   r.pad0 = 0;
-  r.pad1 = 0.0;
+  r.S = 0.0;
   if (bt | nf) {
     if (lane < k) a.kld[c0 + lane] = NAN;
     if (lane <= k) {
@@ -185,6 +186,7 @@ __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* ou
       r.M = s_M[aa];
       r.C = s_C[aa];
       r.lam = s_lam[aa];
+      r.S = s_S[aa];
     } else {
       r.mode = MODE_BONUS;
       r.drow = -1;
@@ -211,74 +213,108 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs a) {
 //             z < 1 (no cancellation), 1 - 2^(-z log2 e) otherwise;
 //   bonus:    p_v up to a scale: exp(t_v - m_u) about the warp max m_u,
 //             rescaled by exp(m_u - max_u m_u) in fp64 by k_select.
-// k_select recomputes every weight bit-identically from the same words.
+// The select recomputes every weight bit-identically from the same words.
 // ---------------------------------------------------------------------------
+// residual weights of one element pair (see above)
+template <typename T>
+__device__ __forceinline__ float2 resid_pair_exact(float2 tt, float2 dd, float2 nML2, float Cf, float lhi,
+                                                   float llo) {
+  const float2 L2 = make_float2(kLog2e, kLog2e), nL2 = make_float2(-kLog2e, -kLog2e);
+  const float2 nC = make_float2(-Cf, -Cf);
+  const float2 LH = make_float2(lhi, lhi), LL = make_float2(llo, llo), ONE = make_float2(1.f, 1.f);
+  const float2 K7 = make_float2(-2.812654656736413e-06f, -2.812654656736413e-06f);
+  const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
+  const float2 K5 = make_float2(-1.9836986029986292e-04f, -1.9836986029986292e-04f);
+  const float2 K4 = make_float2(1.3885394437238574e-03f, 1.3885394437238574e-03f);
+  const float2 K3 = make_float2(-8.33334494382143e-03f, -8.33334494382143e-03f);
+  const float2 K2 = make_float2(4.166673496365547e-02f, 4.166673496365547e-02f);
+  const float2 K1 = make_float2(-1.666666716337204e-01f, -1.666666716337204e-01f);
+  const float2 K0 = make_float2(0.5f, 0.5f);
+  const float2 xt = __ffma2_rn(tt, L2, nML2);
+  const float2 ev = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));  // 0 for padding
+  float2 z;
+  if constexpr (sizeof(T) == 2) {
+    z = __fadd2_rn(__fadd2_rn(tt, make_float2(-dd.x, -dd.y)), nC);  // t - d exact
+  } else {
+    z = make_float2(diff_ref<T>(tt.x, dd.x, Cf), diff_ref<T>(tt.y, dd.y, Cf));
+  }
+  z = __fadd2_rn(__fadd2_rn(z, LH), LL);
+  float2 pz = __ffma2_rn(K7, z, K6);
+  pz = __ffma2_rn(pz, z, K5);
+  pz = __ffma2_rn(pz, z, K4);
+  pz = __ffma2_rn(pz, z, K3);
+  pz = __ffma2_rn(pz, z, K2);
+  pz = __ffma2_rn(pz, z, K1);
+  pz = __ffma2_rn(pz, z, K0);
+  const float2 sm = __fmul2_rn(z, __ffma2_rn(make_float2(-z.x, -z.y), pz, ONE));  // z (1 - z h(-z))
+  const float2 xz = __fmul2_rn(z, nL2);
+  const float2 bg = __fadd2_rn(ONE, make_float2(-fast_exp2(xz.x), -fast_exp2(xz.y)));  // 1 - e^-z
+  const float2 om = make_float2(z.x < 1.f ? sm.x : bg.x, z.y < 1.f ? sm.y : bg.y);
+  const float2 r = __fmul2_rn(ev, om);
+  return make_float2((z.x > 0.f && ev.x > 0.f) ? r.x : 0.f, (z.y > 0.f && ev.y > 0.f) ? r.y : 0.f);
+}
+
+// Per-slice constants of the draw weights.
+struct DrawRef {
+  bool resid;
+  float M, Cf, lhi, llo;  // residual: row reference, lam = lhi + llo
+  float m;                // bonus: the slice's warp max of t (reference)
+};
+
+// Slice constants; for the bonus row the warp-wide max of t over the slice.
 template <typename T, int NV>
-__device__ __forceinline__ float draw_weights_raw(const uint4 (&rt)[NV], const uint4 (&rd)[NV], bool resid,
-                                                  float M, float Cf, double lam,
-                                                  float (&w)[Traits<T>::VEC * NV]) {
-  constexpr int E = Traits<T>::VEC * NV;
-  if (resid) {
-    // packed (FFMA2) element pairs; h(-z) as in slice_stats (tools/fit_g.py, degree 7)
-    const float lhi = (float)lam, llo = (float)(lam - (double)lhi);
-    const float ML2 = M * kLog2e;
-    const float2 L2 = make_float2(kLog2e, kLog2e), nL2 = make_float2(-kLog2e, -kLog2e);
-    const float2 nML2 = make_float2(-ML2, -ML2), nC = make_float2(-Cf, -Cf);
-    const float2 LH = make_float2(lhi, lhi), LL = make_float2(llo, llo), ONE = make_float2(1.f, 1.f);
-    const float2 K7 = make_float2(-2.812654656736413e-06f, -2.812654656736413e-06f);
-    const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
-    const float2 K5 = make_float2(-1.9836986029986292e-04f, -1.9836986029986292e-04f);
-    const float2 K4 = make_float2(1.3885394437238574e-03f, 1.3885394437238574e-03f);
-    const float2 K3 = make_float2(-8.33334494382143e-03f, -8.33334494382143e-03f);
-    const float2 K2 = make_float2(4.166673496365547e-02f, 4.166673496365547e-02f);
-    const float2 K1 = make_float2(-1.666666716337204e-01f, -1.666666716337204e-01f);
-    const float2 K0 = make_float2(0.5f, 0.5f);
+__device__ __forceinline__ DrawRef draw_ref(const uint4 (&rt)[NV], bool resid, float M, float Cf, double lam) {
+  DrawRef R;
+  R.resid = resid;
+  R.M = M;
+  R.Cf = Cf;
+  R.lhi = (float)lam;
+  R.llo = (float)(lam - (double)R.lhi);
+  R.m = 0.f;
+  if (!resid) {
+    float m = -INFINITY;
 #pragma unroll
-    for (int h = 0; h < E; h += 2) {
-      const float2 tt = pair_of<T>(rt, h), dd = pair_of<T>(rd, h);
-      const float2 xt = __ffma2_rn(tt, L2, nML2);
-      const float2 ev = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));  // 0 for padding
-      float2 z;
-      if constexpr (sizeof(T) == 2) {
-        z = __fadd2_rn(__fadd2_rn(tt, make_float2(-dd.x, -dd.y)), nC);  // t - d exact
-      } else {
-        z = make_float2(diff_ref<T>(tt.x, dd.x, Cf), diff_ref<T>(tt.y, dd.y, Cf));
+    for (int v = 0; v < NV; ++v) {
+      const uint4 x[1] = {rt[v]};
+#pragma unroll
+      for (int h = 0; h < Traits<T>::VEC; h += 2) {
+        const float2 tt = pair_of<T>(x, h);
+        m = max_nan(m, max_nan(tt.x, tt.y));
       }
-      z = __fadd2_rn(__fadd2_rn(z, LH), LL);
-      float2 pz = __ffma2_rn(K7, z, K6);
-      pz = __ffma2_rn(pz, z, K5);
-      pz = __ffma2_rn(pz, z, K4);
-      pz = __ffma2_rn(pz, z, K3);
-      pz = __ffma2_rn(pz, z, K2);
-      pz = __ffma2_rn(pz, z, K1);
-      pz = __ffma2_rn(pz, z, K0);
-      const float2 sm = __fmul2_rn(z, __ffma2_rn(make_float2(-z.x, -z.y), pz, ONE));  // z (1 - z h(-z))
-      const float2 xz = __fmul2_rn(z, nL2);
-      const float2 bg = __fadd2_rn(ONE, make_float2(-fast_exp2(xz.x), -fast_exp2(xz.y)));  // 1 - e^-z
-      const float2 om = make_float2(z.x < 1.f ? sm.x : bg.x, z.y < 1.f ? sm.y : bg.y);
-      const float2 r = __fmul2_rn(ev, om);
-      w[h] = (z.x > 0.f && ev.x > 0.f) ? r.x : 0.f;
-      w[h + 1] = (z.y > 0.f && ev.y > 0.f) ? r.y : 0.f;
     }
-    return M;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(kFull, m, o));
+    R.m = m;
   }
-  float m = -INFINITY;
+  return R;
+}
+
+// Draw weights of the VEC tokens of one lane vector.
+template <typename T>
+__device__ __forceinline__ void vec_weights(const uint4& t4, const uint4& d4, const DrawRef& R,
+                                            float (&w)[Traits<T>::VEC]) {
+  constexpr int VEC = Traits<T>::VEC;
+  const uint4 rt[1] = {t4}, rd[1] = {d4};
+  const float2 L2 = make_float2(kLog2e, kLog2e);
+  if (R.resid) {
+    const float ML2 = R.M * kLog2e;
+    const float2 nML2 = make_float2(-ML2, -ML2);
 #pragma unroll
-  for (int h = 0; h < E; h += 2) {
-    const float2 tt = pair_of<T>(rt, h);
-    m = max_nan(m, max_nan(tt.x, tt.y));
+    for (int h = 0; h < VEC; h += 2) {
+      const float2 r = resid_pair_exact<T>(pair_of<T>(rt, h), pair_of<T>(rd, h), nML2, R.Cf, R.lhi, R.llo);
+      w[h] = r.x;
+      w[h + 1] = r.y;
+    }
+    return;
   }
+  const float mL2 = R.m * kLog2e;
+  const float2 nmL2 = make_float2(-mL2, -mL2);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(kFull, m, o));
-  const float mL2 = m * kLog2e;
-  const float2 L2 = make_float2(kLog2e, kLog2e), nmL2 = make_float2(-mL2, -mL2);
-#pragma unroll
-  for (int h = 0; h < E; h += 2) {
+  for (int h = 0; h < VEC; h += 2) {
     const float2 x = __ffma2_rn(pair_of<T>(rt, h), L2, nmL2);
-    w[h] = m <= -1e30f ? 0.f : fast_exp2(x.x);
-    w[h + 1] = m <= -1e30f ? 0.f : fast_exp2(x.y);
+    w[h] = R.m <= -1e30f ? 0.f : fast_exp2(x.x);
+    w[h + 1] = R.m <= -1e30f ? 0.f : fast_exp2(x.y);
   }
-  return m <= -1e30f ? -INFINITY : m;
 }
 
 // raw words of sub-chunk u of a row, from global memory (select pass)
@@ -313,22 +349,6 @@ __device__ __forceinline__ double wscan_d(double x, int lane) {
     if (lane >= o) x += y;
   }
   return x;
-}
-
-// mass of a lane's draw weights in the select pass's order: per vector, an
-// fp32 lane sum, then an fp64 warp sum
-template <typename T, int E>
-__device__ __forceinline__ double draw_mass(const float (&w)[E]) {
-  constexpr int VEC = Traits<T>::VEC, NV = E / VEC;
-  double m = 0.0;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    float ls = 0.f;
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) ls += w[v * VEC + e];
-    m += wsum_d((double)ls);
-  }
-  return m;
 }
 
 // ---------------------------------------------------------------------------
@@ -393,14 +413,23 @@ template <typename T>
 __device__ __forceinline__ void draw_unit_finish(const DrawArgs& a, long long q, const DrawUnit& d,
                                                  const uint4 (&rt)[Traits<T>::NVD],
                                                  const uint4 (&rd)[Traits<T>::NVD]) {
-  constexpr int E = Traits<T>::VEC * Traits<T>::NVD;
+  constexpr int VEC = Traits<T>::VEC, NVD = Traits<T>::NVD;
   if (d.type == IT_NONE) return;
-  float w[E];
-  const float ref = draw_weights_raw<T>(rt, rd, d.type == IT_RESID, d.M, d.Cf, d.lam, w);
-  const double m = draw_mass<T>(w);
+  const DrawRef R = draw_ref<T>(rt, d.type == IT_RESID, d.M, d.Cf, d.lam);
+  // mass in the select pass's order: per vector an fp32 lane sum, then an fp64 warp sum
+  double m = 0.0;
+#pragma unroll
+  for (int v = 0; v < NVD; ++v) {
+    float w[VEC];
+    vec_weights<T>(rt[v], rd[v], R, w);
+    float ls = 0.f;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) ls += w[e];
+    m += wsum_d((double)ls);
+  }
   if ((threadIdx.x & 31) == 0) {
     a.smass[q] = m;
-    a.sref[q] = ref;
+    a.sref[q] = R.resid ? R.M : (R.m <= -1e30f ? -INFINITY : R.m);
   }
 }
 
@@ -539,15 +568,16 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   uint4 rt[NV], rd[NV];
   load_sub_raw<T>(tp, a.V, us, rt);
   if (resid) load_sub_raw<T>(reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d, a.V, us, rd);
-  float w[E];
-  draw_weights_raw<T>(rt, rd, resid, r.M, (float)r.C, r.lam, w);
+  const DrawRef DR = draw_ref<T>(rt, resid, r.M, (float)r.C, r.lam);
   int tok = -1, last_pos = -1;
   double lo = 0.0, hi = 0.0, lp_lo = 0.0, lp_hi = 0.0, vbase = base;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
+    float wv[VEC];
+    vec_weights<T>(rt[v], rd[v], DR, wv);
     float ls = 0.f;
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) ls += w[v * VEC + e];
+    for (int e = 0; e < VEC; ++e) ls += wv[e];
     const double incl = wscan_d((double)ls, lane);
     const double pre = vbase + f * (incl - (double)ls);
     int cand = -1, lpos = -1;
@@ -556,14 +586,14 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
       const float before = run;
-      run += w[v * VEC + e];
+      run += wv[e];
       const double cb = pre + f * (double)before, ca = pre + f * (double)run;
-      if (cand < 0 && w[v * VEC + e] > 0.f && ca > target) {
+      if (cand < 0 && wv[e] > 0.f && ca > target) {
         cand = e;
         clo = cb;
         chi = ca;
       }
-      if (w[v * VEC + e] > 0.f) {
+      if (wv[e] > 0.f) {
         lpos = e;
         llo = cb;
         lhi = ca;

@@ -263,7 +263,7 @@ __device__ __noinline__ void finalize_seq_fused(const FusedArgs& a, int i) {
   const unsigned am = __ballot_sync(kFull, lane < k && (rr.flags & RR_ACCEPT));
   SeqRec r;
   r.pad0 = 0;
-  r.pad1 = 0.0;
+  r.S = 0.0;
   if (bt | nf) {
     if (lane < k) a.kld[c0 + lane] = NAN;
     if (lane <= k) {
@@ -334,7 +334,7 @@ __device__ __noinline__ void finalize_seq_error(const FusedArgs& a, int i) {
     r.M = 0.f;
     r.C = r.lam = r.u = 0.0;
     r.pad0 = 0;
-    r.pad1 = 0.0;
+    r.S = 0.0;
     a.rec[i] = r;
   }
   seq_epilogue(a, i);
