@@ -266,4 +266,34 @@ __device__ __forceinline__ void apply_cap(const CapArgs& a, int32_t cap) {
   if (threadIdx.x == 0) *a.cap = cap;
 }
 
+// a7 by one warp: exact int64 partial over the batch (lanes stride over
+// sequences), the Eq.11 rule (D14), next SLs. Values written by other warps of
+// this launch are read with ld.global.cg (is_calibrating / sl_hat).
+__device__ __forceinline__ void cap_warp(const CapArgs& a) {
+  const int lane = threadIdx.x & 31;
+  long long ls = 0, ln = 0, lm = 0;
+  for (int i = lane; i < a.B; i += 32) {
+    if (is_calibrating(a, i)) continue;
+    const long long v = __ldcg(a.sl_hat + i);
+    ls += v;
+    ln += 1;
+    lm = v > lm ? v : lm;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ls += __shfl_xor_sync(kFull, ls, o);
+    ln += __shfl_xor_sync(kFull, ln, o);
+    const long long m2 = __shfl_xor_sync(kFull, lm, o);
+    lm = m2 > lm ? m2 : lm;
+  }
+  const int32_t cap = cap_rule(a.cfg, ls, ln, lm);
+  for (int i = lane; i < a.B; i += 32) {
+    const int sh = __ldcg(a.sl_hat + i);
+    int v = is_calibrating(a, i) ? a.cfg.calib_sl : (sh < cap ? sh : cap);
+    if (a.budget && a.budget[i] < v) v = a.budget[i];
+    a.next_sl[i] = v;
+  }
+  if (lane == 0) *a.cap = cap;
+}
+
 }  // namespace dsde

@@ -46,7 +46,7 @@ namespace dsde {
 template <typename T>
 struct Traits;
 #ifndef DSDE_NV_BF16
-#define DSDE_NV_BF16 8
+#define DSDE_NV_BF16 7
 #endif
 #ifndef DSDE_NVD_BF16
 #define DSDE_NVD_BF16 4
@@ -119,9 +119,11 @@ __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~(size
 
 constexpr int kCtlInts = 128;  // the fused kernel's control block (FusedCtl), ints
 
-inline int n_subs(int V, dsde_dtype dt) {
+// slices per row: exact for the warp-per-slice kernels; rounded up to whole
+// 8-slice chunks for the TMA variant (the workspace is sized for the latter)
+inline int n_subs(int V, dsde_dtype dt, bool chunked = true) {
   const int se = dt == DSDE_BF16 ? sub_elems<uint16_t>() : sub_elems<float>();
-  // rounded up to whole TMA chunks so both stream variants share the layout
+  if (!chunked) return (V + se - 1) / se;
   const int ce = kCWarps * se;
   return (V + ce - 1) / ce * kCWarps;
 }
@@ -1022,7 +1024,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   auto mark = [&]() {
     if (pr) cudaEventRecord(prof->next(), s);
   };
-  const int ns = n_subs(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32);
+  const int ns = n_subs(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32, stream_variant() == 1);
   int dev = 0;
   cudaGetDevice(&dev);
   struct Grids {
@@ -1130,7 +1132,12 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   DrawArgs da{B, V, nd, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.ref};
   SelArgs sel{B, V, nd, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.ref, emitted, flags, err};
   if (step) {
-    k_tail<T, true><<<B, kFinThreads, 0, s>>>(fa, da, sel, *step);
+    // 16-warp CTAs while every sequence gets a resident CTA (2 per SM), 8-warp
+    // CTAs (4 per SM) for larger batches so the tail stays one wave longer
+    if (B <= 2 * g.sms)
+      k_tail<T, true, 16><<<B, 512, 0, s>>>(fa, da, sel, *step);
+    else
+      k_tail<T, true, 8><<<B, 256, 0, s>>>(fa, da, sel, *step);
     mark();
     mark();
     mark();
@@ -1138,7 +1145,10 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   }
   if (tv == 0) {
     // a2-a4 fused: one CTA per sequence (the profiler's later phases read 0)
-    k_tail<T, false><<<B, kFinThreads, 0, s>>>(fa, da, sel, StepExtra{});
+    if (B <= 2 * g.sms)
+      k_tail<T, false, 16><<<B, 512, 0, s>>>(fa, da, sel, StepExtra{});
+    else
+      k_tail<T, false, 8><<<B, 256, 0, s>>>(fa, da, sel, StepExtra{});
     mark();
     mark();
     mark();

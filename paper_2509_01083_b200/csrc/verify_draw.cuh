@@ -56,13 +56,14 @@ __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* ou
     return;
   }
   const int nc = a.nsub;
-  if (warp < k) {
-    // ---- row j = warp: fp64 merge of the slice partials (lanes over slices c)
+  const int nwarps = blockDim.x >> 5;
+  for (int j = warp; j < k; j += nwarps) {
+    // ---- row j: fp64 merge of the slice partials (lanes over slices c)
     // about M = max_c M_c, C = fp32(M - max d). Slice c's w is shifted by
     // Delta = C_c - C; with s = e^(M_c - M), E1 = s e^-Delta:
     //   S += s S_c,  A += s (A_c + S_c Delta),
     //   D += E1 D_c - A_c s expm1(-Delta) + S_c s g(Delta),  g(x) = expm1(-x) + x.
-    const SubPartial* P = a.part + ((long long)c0 + warp) * nc;
+    const SubPartial* P = a.part + ((long long)c0 + j) * nc;
     float Ml = -INFINITY, Dl = -INFINITY;
     for (int c = lane; c < nc; c += 32) {
       Ml = max_nan(Ml, P[c].M);
@@ -110,12 +111,12 @@ __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* ou
       const double y = (D - A) / S;
       const double lam = log1p(y);
       const double kl = fmax(0.0, y <= 1.0 ? D / S + (lam - y) : A / S + lam);
-      s_kl[warp] = kl;
-      s_lam[warp] = lam;
-      s_C[warp] = C;
-      s_M[warp] = Ml;
-      s_S[warp] = S;
-      s_fin[warp] = isfinite(S) && isfinite(A) && isfinite(D) && S > 0.0 && isfinite(M) &&
+      s_kl[j] = kl;
+      s_lam[j] = lam;
+      s_C[j] = C;
+      s_M[j] = Ml;
+      s_S[j] = S;
+      s_fin[j] = isfinite(S) && isfinite(A) && isfinite(D) && S > 0.0 && isfinite(M) &&
                     isfinite(C) && isfinite(kl);
     }
   }
@@ -656,11 +657,11 @@ struct StepExtra {
   unsigned* counter;
 };
 
-template <typename T, bool STEP>
-__global__ void __launch_bounds__(kFinThreads, 2) k_tail(FinArgs fa, DrawArgs da, SelArgs sa, StepExtra sx) {
-  constexpr int NVD = Traits<T>::NVD, NW = kFinThreads / 32;
+template <typename T, bool STEP, int NW>
+__global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(FinArgs fa, DrawArgs da, SelArgs sa,
+                                                                   StepExtra sx) {
+  constexpr int NVD = Traits<T>::NVD;
   __shared__ SeqRec s_rec;
-  __shared__ int s_last;
   const int i = blockIdx.x;
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_rec.mode = MODE_NONE;
@@ -671,7 +672,20 @@ __global__ void __launch_bounds__(kFinThreads, 2) k_tail(FinArgs fa, DrawArgs da
   const bool draw = r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS;
   if (STEP && warp == NW - 1) {
     signal_seq(sx.sig, i);
-    __threadfence();  // sl_hat / state visible to the CTA that applies the cap
+    if (sx.fuse_cap) {
+      // release ticket: this warp's sl_hat / state writes before the count; the
+      // warp drawing the last ticket acquires and applies the cap (a7), without
+      // waiting for any CTA's draw or select
+      __syncwarp();
+      unsigned old = 0;
+      if ((threadIdx.x & 31) == 0)
+        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(sx.counter) : "memory");
+      if (__shfl_sync(kFull, old, 0) == gridDim.x - 1) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        cap_warp(sx.cap);
+        if ((threadIdx.x & 31) == 0) *sx.counter = 0u;
+      }
+    }
   }
   if (draw) {
     const long long q0 = (long long)i * da.nsub;
@@ -683,16 +697,4 @@ __global__ void __launch_bounds__(kFinThreads, 2) k_tail(FinArgs fa, DrawArgs da
   }
   __syncthreads();
   if (draw && warp == 0) select_seq<T>(sa, i, r);
-  if (!STEP || !sx.fuse_cap) return;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(sx.counter, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  long long sum, n, mx;
-  cap_partial_block(sx.cap, sum, n, mx);
-  apply_cap(sx.cap, cap_rule(sx.cap.cfg, sum, n, mx));
-  if (threadIdx.x == 0) *sx.counter = 0u;
 }

@@ -98,36 +98,6 @@ __device__ __forceinline__ int atomic_add_release(int* p, int v) {
 // Acquire side after observing a final count (reads then use ld.global.cg).
 __device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
-// a7 by one warp: exact int64 partial over the batch (lanes stride over
-// sequences), the Eq.11 rule (D14), next SLs. Values written by other warps of
-// this launch are read with ld.global.cg (is_calibrating / sl_hat).
-__device__ __forceinline__ void cap_warp(const CapArgs& a) {
-  const int lane = threadIdx.x & 31;
-  long long ls = 0, ln = 0, lm = 0;
-  for (int i = lane; i < a.B; i += 32) {
-    if (is_calibrating(a, i)) continue;
-    const long long v = __ldcg(a.sl_hat + i);
-    ls += v;
-    ln += 1;
-    lm = v > lm ? v : lm;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    ls += __shfl_xor_sync(kFull, ls, o);
-    ln += __shfl_xor_sync(kFull, ln, o);
-    const long long m2 = __shfl_xor_sync(kFull, lm, o);
-    lm = m2 > lm ? m2 : lm;
-  }
-  const int32_t cap = cap_rule(a.cfg, ls, ln, lm);
-  for (int i = lane; i < a.B; i += 32) {
-    const int sh = __ldcg(a.sl_hat + i);
-    int v = is_calibrating(a, i) ? a.cfg.calib_sl : (sh < cap ? sh : cap);
-    if (a.budget && a.budget[i] < v) v = a.budget[i];
-    a.next_sl[i] = v;
-  }
-  if (lane == 0) *a.cap = cap;
-}
-
 // the sequence range of i, and whether it is well formed (as finalize_seq)
 __device__ __forceinline__ bool seq_range(const FusedArgs& a, int i, int& c0, int& k) {
   c0 = __ldg(a.cu_sl + i);

@@ -53,6 +53,15 @@ def test_verify_parity(m, state, V, dtype, kmax, B):
         _check(m, state, host, dtype)
 
 
+def test_verify_large_batch_tail_variant(m, state):
+    """B beyond two resident 16-warp tail CTAs per SM (k_tail switches to 8-warp
+    CTAs): parity on every sequence of a 400-sequence batch, both profiles."""
+    B = 400
+    k = synth.random_k(B, 8, 17)
+    host = make_host_batch(4096, k, seed=41, profiles=("code", "low"))
+    _check(m, state, host, torch.bfloat16)
+
+
 def test_verify_ld_padding(m, state):
     k = synth.random_k(6, 8, 3)
     host = make_host_batch(20000, k, seed=5)
