@@ -323,8 +323,8 @@ struct SumRef {
 // a1 accumulation of one element pair (packed FFMA2 math, two MUFU.EX2 per
 // element): S += e, A += e w, D += e g(w).
 template <typename T>
-__device__ __forceinline__ void pair_accum(float2 tt, float2 dd, const SumRef& R, float2& S2, float2& A2,
-                                           float2& D2) {
+__device__ __forceinline__ void pair_accum_w(float2 tt, float2 dd, float2 w, const SumRef& R, float2& S2,
+                                             float2& A2, float2& D2) {
   const float2 L2 = make_float2(kLog2e, kLog2e);
 #ifndef DSDE_POLY_DEG7
   const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
@@ -348,7 +348,6 @@ __device__ __forceinline__ void pair_accum(float2 tt, float2 dd, const SumRef& R
   const float2 arg = __ffma2_rn(dd, L2, R.nDL2);  // (d - max d) log2 e <= 0
   const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
   const float2 f = make_float2(fast_exp2(arg.x), fast_exp2(arg.y));
-  const float2 w = diff2<T>(tt, dd, R.Cw);
   const float2 w2 = __fmul2_rn(w, w);
 #ifndef DSDE_POLY_DEG7
   float2 pp = __ffma2_rn(K6, w, K5);
@@ -369,13 +368,80 @@ __device__ __forceinline__ void pair_accum(float2 tt, float2 dd, const SumRef& R
   D2 = __fadd2_rn(D2, term);
 }
 
-// the sums of one 16-byte vector pair
+template <typename T>
+__device__ __forceinline__ void pair_accum(float2 tt, float2 dd, const SumRef& R, float2& S2, float2& A2,
+                                           float2& D2) {
+  pair_accum_w<T>(tt, dd, diff2<T>(tt, dd, R.Cw), R, S2, A2, D2);
+}
+
+// The sums of one 16-byte vector pair. When every |w| of the vector is below 2
+// in every lane of the warp (the common case once the draft tracks the target),
+// g(w) = w^2 h(-w) is a single degree-8 polynomial (Chebyshev fit of h on
+// |u| <= 2, 3.3e-7 relative in fp32 Horner, `tools/fit_g.py --deg 8 --range 2`)
+// and the e^{d - max d} exponential, the big-|w| form and the per-element
+// select are skipped; otherwise every pair takes pair_accum (the test costs one
+// FMNMX3 per pair; a slice-level "stop testing after a failure" flag and a
+// separate untested path both measured slower on cfg3, faster only on cfg4).
+#ifndef DSDE_WIDE_POLY
+#define DSDE_WIDE_POLY 1
+#endif
 template <typename T>
 __device__ __forceinline__ void vec_accum(const uint4& t, const uint4& d, const SumRef& R, float2& S2,
                                           float2& A2, float2& D2) {
+  constexpr int P = Traits<T>::VEC / 2;
   const uint4 rt[1] = {t}, rd[1] = {d};
+#if DSDE_WIDE_POLY
+  float2 tt[P], w[P];
+  float am = 0.f;
+#pragma unroll
+  for (int h = 0; h < P; ++h) {
+    tt[h] = pair_of<T>(rt, 2 * h);
+    w[h] = diff2<T>(tt[h], pair_of<T>(rd, 2 * h), R.Cw);
+    am = fmaxf(am, fmaxf(fabsf(w[h].x), fabsf(w[h].y)));
+  }
+  if (__all_sync(kFull, am < 2.f)) {
+    const float2 L2 = make_float2(kLog2e, kLog2e);
+    // coefficients of h(-w) in powers of w (odd ones negated)
+    const float2 Q7 = make_float2(-2.990256007251446e-06f, -2.990256007251446e-06f);
+    const float2 Q6 = make_float2(2.47248935920652e-05f, 2.47248935920652e-05f);
+    const float2 Q5 = make_float2(-1.9769996288232505e-04f, -1.9769996288232505e-04f);
+    const float2 Q4 = make_float2(1.388999167829752e-03f, 1.388999167829752e-03f);
+    const float2 Q3 = make_float2(-8.334130048751831e-03f, -8.334130048751831e-03f);
+    const float2 Q2 = make_float2(4.166661202907562e-02f, 4.166661202907562e-02f);
+    const float2 Q1 = make_float2(-1.666664332151413e-01f, -1.666664332151413e-01f);
+    const float2 Q0 = make_float2(0.5f, 0.5f);
+    const float2 Q8 = make_float2(2.972247159505059e-07f, 2.972247159505059e-07f);
+#pragma unroll
+    for (int h = 0; h < P; ++h) {
+      const float2 xt = __ffma2_rn(tt[h], L2, R.nML2);
+      const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
+      const float2 ww = w[h];
+      const float2 w2 = __fmul2_rn(ww, ww);
+      float2 pp = __ffma2_rn(Q8, ww, Q7);
+      pp = __ffma2_rn(pp, ww, Q6);
+      pp = __ffma2_rn(pp, ww, Q5);
+      pp = __ffma2_rn(pp, ww, Q4);
+      pp = __ffma2_rn(pp, ww, Q3);
+      pp = __ffma2_rn(pp, ww, Q2);
+      pp = __ffma2_rn(pp, ww, Q1);
+      pp = __ffma2_rn(pp, ww, Q0);
+      S2 = __fadd2_rn(S2, e);
+      A2 = __ffma2_rn(e, ww, A2);
+      D2 = __fadd2_rn(D2, __fmul2_rn(__fmul2_rn(e, w2), pp));
+    }
+    return;
+  }
+#ifdef DSDE_WIDE_RECOMPUTE
 #pragma unroll
   for (int h = 0; h < Traits<T>::VEC; h += 2) pair_accum<T>(pair_of<T>(rt, h), pair_of<T>(rd, h), R, S2, A2, D2);
+#else
+#pragma unroll
+  for (int h = 0; h < P; ++h) pair_accum_w<T>(tt[h], pair_of<T>(rd, 2 * h), w[h], R, S2, A2, D2);
+#endif
+#else
+#pragma unroll
+  for (int h = 0; h < Traits<T>::VEC; h += 2) pair_accum<T>(pair_of<T>(rt, h), pair_of<T>(rd, h), R, S2, A2, D2);
+#endif
 }
 
 __device__ __forceinline__ SubPartial empty_partial() {
