@@ -399,35 +399,63 @@ __device__ __forceinline__ void vec_accum(const uint4& t, const uint4& d, const 
     w[h] = diff2<T>(tt[h], pair_of<T>(rd, 2 * h), R.Cw);
     am = fmaxf(am, fmaxf(fabsf(w[h].x), fabsf(w[h].y)));
   }
-  if (__all_sync(kFull, am < 2.f)) {
+#ifndef DSDE_WIDE_R
+#define DSDE_WIDE_R 2
+#endif
+#if DSDE_WIDE_R == 2
+  constexpr float kWideR = 2.f;
+#elif DSDE_WIDE_R == 25
+  constexpr float kWideR = 2.5f;
+#else
+  constexpr float kWideR = 3.f;
+#endif
+  if (__all_sync(kFull, am < kWideR)) {
     const float2 L2 = make_float2(kLog2e, kLog2e);
-    // coefficients of h(-w) in powers of w (odd ones negated)
-    const float2 Q7 = make_float2(-2.990256007251446e-06f, -2.990256007251446e-06f);
-    const float2 Q6 = make_float2(2.47248935920652e-05f, 2.47248935920652e-05f);
-    const float2 Q5 = make_float2(-1.9769996288232505e-04f, -1.9769996288232505e-04f);
-    const float2 Q4 = make_float2(1.388999167829752e-03f, 1.388999167829752e-03f);
-    const float2 Q3 = make_float2(-8.334130048751831e-03f, -8.334130048751831e-03f);
-    const float2 Q2 = make_float2(4.166661202907562e-02f, 4.166661202907562e-02f);
-    const float2 Q1 = make_float2(-1.666664332151413e-01f, -1.666664332151413e-01f);
-    const float2 Q0 = make_float2(0.5f, 0.5f);
-    const float2 Q8 = make_float2(2.972247159505059e-07f, 2.972247159505059e-07f);
 #pragma unroll
     for (int h = 0; h < P; ++h) {
       const float2 xt = __ffma2_rn(tt[h], L2, R.nML2);
       const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
       const float2 ww = w[h];
-      const float2 w2 = __fmul2_rn(ww, ww);
-      float2 pp = __ffma2_rn(Q8, ww, Q7);
-      pp = __ffma2_rn(pp, ww, Q6);
-      pp = __ffma2_rn(pp, ww, Q5);
-      pp = __ffma2_rn(pp, ww, Q4);
-      pp = __ffma2_rn(pp, ww, Q3);
-      pp = __ffma2_rn(pp, ww, Q2);
-      pp = __ffma2_rn(pp, ww, Q1);
-      pp = __ffma2_rn(pp, ww, Q0);
+      // h(-w) in powers of w (odd coefficients negated), Chebyshev fits of
+      // tools/fit_g.py: deg 8 on |u|<=2 (3.3e-7), deg 9 on 2.5 (3.3e-7), deg 10 on 3 (4.0e-7)
+#if DSDE_WIDE_R == 2
+      float2 pp = __ffma2_rn(make_float2(2.972247159505059e-07f, 2.972247159505059e-07f), ww,
+                             make_float2(-2.990256007251446e-06f, -2.990256007251446e-06f));
+      pp = __ffma2_rn(pp, ww, make_float2(2.47248935920652e-05f, 2.47248935920652e-05f));
+      pp = __ffma2_rn(pp, ww, make_float2(-1.9769996288232505e-04f, -1.9769996288232505e-04f));
+      pp = __ffma2_rn(pp, ww, make_float2(1.388999167829752e-03f, 1.388999167829752e-03f));
+      pp = __ffma2_rn(pp, ww, make_float2(-8.334130048751831e-03f, -8.334130048751831e-03f));
+      pp = __ffma2_rn(pp, ww, make_float2(4.166661202907562e-02f, 4.166661202907562e-02f));
+      pp = __ffma2_rn(pp, ww, make_float2(-1.666664332151413e-01f, -1.666664332151413e-01f));
+      pp = __ffma2_rn(pp, ww, make_float2(0.5f, 0.5f));
+#elif DSDE_WIDE_R == 25
+      float2 pp = __ffma2_rn(make_float2(-2.79628800115006e-08f, -2.79628800115006e-08f), ww,
+                             make_float2(3.10109527390523e-07f, 3.10109527390523e-07f));
+      pp = __ffma2_rn(pp, ww, make_float2(-2.73722048405034e-06f, -2.73722048405034e-06f));
+      pp = __ffma2_rn(pp, ww, make_float2(2.4609160391264595e-05f, 2.4609160391264595e-05f));
+      pp = __ffma2_rn(pp, ww, make_float2(-1.9846374925691634e-04f, -1.9846374925691634e-04f));
+      pp = __ffma2_rn(pp, ww, make_float2(1.3893224531784654e-03f, 1.3893224531784654e-03f));
+      pp = __ffma2_rn(pp, ww, make_float2(-8.333276025950909e-03f, -8.333276025950909e-03f));
+      pp = __ffma2_rn(pp, ww, make_float2(4.166632518172264e-02f, 4.166632518172264e-02f));
+      pp = __ffma2_rn(pp, ww, make_float2(-1.666666865348816e-01f, -1.666666865348816e-01f));
+      pp = __ffma2_rn(pp, ww, make_float2(0.5000000596046448f, 0.5000000596046448f));
+#else
+      float2 pp = __ffma2_rn(make_float2(2.4204336313005115e-09f, 2.4204336313005115e-09f), ww,
+                             make_float2(-2.934377540952937e-08f, -2.934377540952937e-08f));
+      pp = __ffma2_rn(pp, ww, make_float2(2.721244527492672e-07f, 2.721244527492672e-07f));
+      pp = __ffma2_rn(pp, ww, make_float2(-2.7161327125213575e-06f, -2.7161327125213575e-06f));
+      pp = __ffma2_rn(pp, ww, make_float2(2.4817869416438043e-05f, 2.4817869416438043e-05f));
+      pp = __ffma2_rn(pp, ww, make_float2(-1.9857056031469256e-04f, -1.9857056031469256e-04f));
+      pp = __ffma2_rn(pp, ww, make_float2(1.3888543471693993e-03f, 1.3888543471693993e-03f));
+      pp = __ffma2_rn(pp, ww, make_float2(-8.333077654242516e-03f, -8.333077654242516e-03f));
+      pp = __ffma2_rn(pp, ww, make_float2(4.166669398546219e-02f, 4.166669398546219e-02f));
+      pp = __ffma2_rn(pp, ww, make_float2(-1.6666677594184875e-01f, -1.6666677594184875e-01f));
+      pp = __ffma2_rn(pp, ww, make_float2(0.5f, 0.5f));
+#endif
+      const float2 ew = __fmul2_rn(e, ww);
       S2 = __fadd2_rn(S2, e);
-      A2 = __ffma2_rn(e, ww, A2);
-      D2 = __fadd2_rn(D2, __fmul2_rn(__fmul2_rn(e, w2), pp));
+      A2 = __fadd2_rn(A2, ew);
+      D2 = __ffma2_rn(ew, __fmul2_rn(ww, pp), D2);  // e w^2 h(-w)
     }
     return;
   }
