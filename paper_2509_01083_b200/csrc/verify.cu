@@ -46,7 +46,7 @@ namespace dsde {
 template <typename T>
 struct Traits;
 #ifndef DSDE_NV_BF16
-#define DSDE_NV_BF16 7
+#define DSDE_NV_BF16 8
 #endif
 #ifndef DSDE_NVD_BF16
 #define DSDE_NVD_BF16 4

@@ -489,7 +489,7 @@ struct SelArgs {
 // One warp: the inverse-CDF select of sequence i from its slice masses.
 template <typename T>
 __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec& r) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NVD, E = VEC * NV, SUB = 32 * VEC * NV;
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NVD, SUB = 32 * VEC * NV;
   const int lane = threadIdx.x & 31;
   if (r.mode != MODE_RESIDUAL && r.mode != MODE_BONUS) return;
   const bool resid = r.mode == MODE_RESIDUAL;

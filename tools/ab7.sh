@@ -1,4 +1,4 @@
-for f in "" "-DDSDE_WIDE_R=25" "-DDSDE_WIDE_R=3"; do
+for f in "" "-DDSDE_L2PF=0"; do
   DSDE_NVCC_FLAGS="$f" python paper_2509_01083_b200/_build.py --force > /dev/null 2>&1
   for c in 3 4; do
   timeout 150 python bench.py --config $c --steps 40 --warmup 5 --no-cpu-baseline --e2e-steps 1 > gpurun_out/b_x.json 2>gpurun_out/b_x.err
