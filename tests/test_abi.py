@@ -67,5 +67,8 @@ def test_invalid_args_rejected_without_launch(dsde):
     assert L.dsde_state_create(C.byref(bad), 4, C.byref(h)) == dsde.DSDE_ERR_ARG
     assert L.dsde_verify(0, 10, 1, 0, None, None, None, 10, None, 10, None, None, None, None,
                          None, None, 0, None, None) == dsde.DSDE_ERR_ARG
+    # dsde_step: the union of the three calls' synchronous checks (null state / pointers)
+    assert L.dsde_step(None, 4, 10, 1, 4, None, None, None, None, 10, None, 10, None, None, None, None,
+                       None, None, None, None, None, None, None, 0, None, None) == dsde.DSDE_ERR_ARG
     assert L.dsde_verify_workspace_size(0, 1, 10, 1) == 0
     assert L.dsde_verify_workspace_size(4, 16, 128256, 1) > 0
