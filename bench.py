@@ -42,7 +42,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "verify positions/s and HBM GB/s vs peak at V=128256, 1/2/4/8 B200"
 UNIT = "positions/s"
-STREAM_KERNEL = {"tma": "k_stream_tma", "wt": "k_stream_wt", "wt2": "k_stream_wt2"}.get(
+STREAM_KERNEL = {"tma": "k_stream_tma"}.get(
     os.environ.get("DSDE_STREAM", ""), "k_stream_ldg")
 
 CONFIGS = {

@@ -1,21 +1,22 @@
-// verify.cu — dsde_verify: the speculative-verification pass (§8(a) a1-a4).
+// verify.cu — dsde_verify / dsde_step: the speculative-verification pass
+// (§8(a) a1-a4; with dsde_step also a5-a7).
 //
-// Pipeline (all on the caller's stream, no host synchronisation; 4 launches):
-//   1. k_stream_*    one streaming read of every (draft position row, vocab slice)
-//                    of the target and draft logits; per 1024-token (bf16) /
+// Default pipeline (all on the caller's stream, no host synchronisation; 2 launches):
+//   1. k_stream_ldg  one streaming read of every (draft position row, vocab slice)
+//                    of the target and draft logits; per 2048-token (bf16) /
 //                    512-token (fp32) slice: S = sum e_v, A = sum e_v w_v,
 //                    D = sum e_v g(w_v) about the slice reference (a1).
-//   2. k_finalize    one CTA per sequence, one warp per position: fp64 merge of the
-//                    slice partials, KL, log p/q; the Philox accept test, the first
-//                    rejection a_i, token layout, the draw record (a2-a3).
-//   3. k_draw_*      the mass of max(0, p - q) (row a_i) or of p (bonus row k_i)
-//                    per slice of the drawn row.
-//   4. k_select      one warp per sequence: the smallest token with C_v > u R (a4, D7).
-// Two variants of the streaming kernels (1, 3), selected by DSDE_STREAM at run
-// time for A/B measurements: "ldg" (default; persistent warps, 128-bit
-// non-allocating loads, next slice prefetched into registers) and "tma"
-// (warp-specialised CTAs: a TMA bulk-copy producer warp filling a shared-memory
-// ring, 8 consumer warps).
+//   2. k_tail        one CTA per sequence (verify_draw.cuh): fp64 merge of the
+//                    slice partials, KL, log p/q, the Philox accept test, the
+//                    first rejection a_i and token layout (a2-a3); the draw-weight
+//                    masses of the drawn row (residual row a_i or bonus row k_i)
+//                    and the inverse-CDF select (a4); in dsde_step also the
+//                    signal / SL^ (a5-a6) and the batch cap (a7).
+// Variants kept for A/B measurement (env, read once per process):
+// DSDE_STREAM=tma (TMA producer warp + 8 consumer warps, CTA shared-memory
+// ring), DSDE_TAIL=split (k_finalize, k_draw_ldg, k_select) and DSDE_TAIL=fused
+// (one persistent kernel for the whole step, verify_fused.cuh). DESIGN.md §8
+// lists their measurements.
 //
 // Numerics: with e_v = exp(t_v - M), w_v = (t_v - d_v) - C, C = M - max d
 // (an fp32 value), and g(w) = exp(-w) - 1 + w >= 0:
@@ -805,276 +806,6 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtas) k_stream_tma(StreamArgs
   }
 }
 
-// ---------------------------------------------------------------------------
-// a1, "wt" variant (warp-private bulk-copy rings): every warp owns a
-// DSDE_WT_STAGES-deep ring of (target, draft) slice stages in shared memory and
-// its own mbarriers. Lane 0 refills a stage with two 1-D bulk copies
-// (cp.async.bulk, the TMA engine) as soon as the warp has lifted it into
-// registers, so each warp keeps DSDE_WT_STAGES units of HBM reads in flight
-// while it computes, at no register cost and with no coupling between warps
-// (no producer warp, no CTA barrier in the loop). Units q = (draft row r,
-// slice u) are swept q = global warp + j * (total warps), as k_stream_ldg.
-// ---------------------------------------------------------------------------
-#ifndef DSDE_WT_STAGES
-#define DSDE_WT_STAGES 3
-#endif
-#ifndef DSDE_WT_WARPS
-#define DSDE_WT_WARPS 8
-#endif
-#ifndef DSDE_WT_MINB
-#define DSDE_WT_MINB 2
-#endif
-constexpr int kWtWarps = DSDE_WT_WARPS;
-constexpr int kWtStages = DSDE_WT_STAGES;
-
-template <typename T>
-__host__ __device__ constexpr int wt_row_bytes() {
-  return sub_elems<T>() * (int)sizeof(T);
-}
-template <typename T>
-__host__ __device__ constexpr int wt_smem() {
-  return kWtWarps * kWtStages * (2 * wt_row_bytes<T>() + 16);  // stages + (mbarrier, seq) per stage
-}
-
-// Lane words of a staged slice: 128-bit shared loads (consecutive lanes,
-// consecutive 16 bytes: conflict-free); the unaligned tail (V * sizeof(T) not a
-// multiple of 16) from global, padding after V.
-template <typename T>
-__device__ __forceinline__ void wt_lift(const T* st, const T* grow, int n_el, int e_base,
-                                        uint4 (&r)[Traits<T>::NV]) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, SUB = sub_elems<T>();
-  const int lane = threadIdx.x & 31;
-  if (n_el == SUB) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) r[v] = *reinterpret_cast<const uint4*>(st + (v * 32 + lane) * VEC);
-    return;
-  }
-  const int bulk_el = (int)(((uint32_t)(n_el * (int)sizeof(T)) & ~15u) / sizeof(T));
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    const int e0 = (v * 32 + lane) * VEC;
-    if (e0 + VEC <= bulk_el) {
-      r[v] = *reinterpret_cast<const uint4*>(st + e0);
-    } else {
-      T b[VEC];
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) {
-        const int idx = e0 + e;
-        b[e] = idx < bulk_el ? st[idx] : idx < n_el ? grow[e_base + idx] : pad_bits<T>();
-      }
-      r[v] = *reinterpret_cast<const uint4*>(b);
-    }
-  }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kWtWarps * 32, DSDE_WT_MINB) k_stream_wt(StreamArgs a) {
-  constexpr int NV = Traits<T>::NV, SUB = sub_elems<T>(), ROWB = wt_row_bytes<T>(), ST = kWtStages;
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* ring = smem + warp * ST * 2 * ROWB;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kWtWarps * ST * 2 * ROWB) + warp * ST;
-  int* sseq = reinterpret_cast<int*>(smem + kWtWarps * ST * 2 * ROWB + kWtWarps * ST * 8) + warp * ST;
-  const long long n_units = (long long)a.total * a.nsub;
-  const long long W = (long long)gridDim.x * kWtWarps;
-  const long long q0 = (long long)blockIdx.x * kWtWarps + warp;
-  if (q0 >= n_units) return;
-  if (lane == 0) {
-    for (int s = 0; s < ST; ++s) mbar_init(&bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  const T* tl = reinterpret_cast<const T*>(a.tl);
-  const T* dl = reinterpret_cast<const T*>(a.dl);
-  int seq_issue = 0;
-  // warp-wide: locate unit q's rows, then lane 0 starts the two bulk copies
-  auto issue = [&](long long q, int s) {
-    const int r = (int)((unsigned)q / (unsigned)a.nsub);
-    const int u = (int)q - r * a.nsub;
-    seq_issue = seq_of_row(a.cu_sl, a.B, seq_issue, r);
-    if (lane == 0) {
-      sseq[s] = seq_issue;
-      const int e0 = u * SUB;
-      const int n_el = max(0, min(SUB, a.V - e0));
-      const uint32_t bytes = (uint32_t)(n_el * (int)sizeof(T)) & ~15u;
-      uint8_t* dst = ring + s * 2 * ROWB;
-      if (bytes) {
-        mbar_arrive_expect_tx(&bar[s], 2 * bytes);
-        bulk_g2s(dst, tl + (long long)(r + seq_issue) * a.ld_t + e0, bytes, &bar[s]);
-        bulk_g2s(dst + ROWB, dl + (long long)r * a.ld_d + e0, bytes, &bar[s]);
-      } else {
-        mbar_arrive(&bar[s]);
-      }
-    }
-  };
-#pragma unroll 1
-  for (int s = 0; s < ST; ++s) {
-    const long long q = q0 + s * W;
-    if (q < n_units) issue(q, s);
-  }
-  int s = 0;
-  uint32_t phase = 0;
-#pragma unroll 1
-  for (long long q = q0; q < n_units; q += W) {
-    mbar_wait(&bar[s], phase);
-    const int r = (int)((unsigned)q / (unsigned)a.nsub);
-    const int u = (int)q - r * a.nsub;
-    const int e0 = u * SUB;
-    const int n_el = max(0, min(SUB, a.V - e0));
-    const T* st = reinterpret_cast<const T*>(ring + s * 2 * ROWB);
-    uint4 rt[NV], rd[NV];
-    if (n_el == SUB) {
-      wt_lift<T>(st, nullptr, SUB, 0, rt);
-      wt_lift<T>(st + SUB, nullptr, SUB, 0, rd);
-    } else {
-      const int sq = sseq[s];
-      wt_lift<T>(st, tl + (long long)(r + sq) * a.ld_t, n_el, e0, rt);
-      wt_lift<T>(st + SUB, dl + (long long)r * a.ld_d, n_el, e0, rd);
-    }
-    const long long qn = q + ST * W;
-    const int sn = s;
-    // the stage is refilled once every lane's words are in registers (the
-    // warp-wide max reduction inside slice_stats consumes all of them)
-    const SubPartial p = slice_stats<T>(rt, rd, [&]() {
-      if (qn < n_units) issue(qn, sn);
-    });
-    store_partial(a.part + q, p);
-    if (++s == ST) {
-      s = 0;
-      phase ^= 1u;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// a1, "wt2" variant: warp-private bulk-copy rings as "wt", but the staged
-// slice is read from shared memory twice (pass 1: the slice maxima, pass 2:
-// the sums) instead of being lifted into registers, so the registers go to
-// instruction-level parallelism of the math instead of holding raw words.
-// The stage is refilled after pass 2.
-// ---------------------------------------------------------------------------
-#ifndef DSDE_W2_STAGES
-#define DSDE_W2_STAGES 3
-#endif
-#ifndef DSDE_W2_WARPS
-#define DSDE_W2_WARPS 4
-#endif
-#ifndef DSDE_W2_MINB
-#define DSDE_W2_MINB 2
-#endif
-constexpr int kW2Warps = DSDE_W2_WARPS;
-constexpr int kW2Stages = DSDE_W2_STAGES;
-
-template <typename T>
-__host__ __device__ constexpr int w2_smem() {
-  return kW2Warps * kW2Stages * (2 * wt_row_bytes<T>() + 16);
-}
-
-// vector v of a lane from a staged slice holding n_el valid elements (bulk
-// part in shared memory, unaligned tail from global, padding after V)
-template <typename T>
-__device__ __forceinline__ uint4 stage_vec(const T* st, const T* grow, bool full, int n_el, int bulk_el,
-                                           int e_base, int v) {
-  constexpr int VEC = Traits<T>::VEC;
-  const int e0 = (v * 32 + (threadIdx.x & 31)) * VEC;
-  if (full || e0 + VEC <= bulk_el) return *reinterpret_cast<const uint4*>(st + e0);
-  T b[VEC];
-#pragma unroll
-  for (int e = 0; e < VEC; ++e) {
-    const int idx = e0 + e;
-    b[e] = idx < bulk_el ? st[idx] : idx < n_el ? grow[e_base + idx] : pad_bits<T>();
-  }
-  return *reinterpret_cast<const uint4*>(b);
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kW2Warps * 32, DSDE_W2_MINB) k_stream_wt2(StreamArgs a) {
-  constexpr int NV = Traits<T>::NV, SUB = sub_elems<T>(), ROWB = wt_row_bytes<T>(), ST = kW2Stages;
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* ring = smem + warp * ST * 2 * ROWB;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kW2Warps * ST * 2 * ROWB) + warp * ST;
-  int* sseq = reinterpret_cast<int*>(smem + kW2Warps * ST * 2 * ROWB + kW2Warps * ST * 8) + warp * ST;
-  const long long n_units = (long long)a.total * a.nsub;
-  const long long W = (long long)gridDim.x * kW2Warps;
-  const long long q0 = (long long)blockIdx.x * kW2Warps + warp;
-  if (q0 >= n_units) return;
-  if (lane == 0) {
-    for (int s = 0; s < ST; ++s) mbar_init(&bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  const T* tl = reinterpret_cast<const T*>(a.tl);
-  const T* dl = reinterpret_cast<const T*>(a.dl);
-  int seq_issue = 0;
-  auto issue = [&](long long q, int s) {
-    const int r = (int)((unsigned)q / (unsigned)a.nsub);
-    const int u = (int)q - r * a.nsub;
-    seq_issue = seq_of_row(a.cu_sl, a.B, seq_issue, r);
-    if (lane == 0) {
-      sseq[s] = seq_issue;
-      const int e0 = u * SUB;
-      const int n_el = max(0, min(SUB, a.V - e0));
-      const uint32_t bytes = (uint32_t)(n_el * (int)sizeof(T)) & ~15u;
-      uint8_t* dst = ring + s * 2 * ROWB;
-      if (bytes) {
-        mbar_arrive_expect_tx(&bar[s], 2 * bytes);
-        bulk_g2s(dst, tl + (long long)(r + seq_issue) * a.ld_t + e0, bytes, &bar[s]);
-        bulk_g2s(dst + ROWB, dl + (long long)r * a.ld_d + e0, bytes, &bar[s]);
-      } else {
-        mbar_arrive(&bar[s]);
-      }
-    }
-  };
-#pragma unroll 1
-  for (int s = 0; s < ST; ++s) {
-    const long long q = q0 + s * W;
-    if (q < n_units) issue(q, s);
-  }
-  int s = 0;
-  uint32_t phase = 0;
-#pragma unroll 1
-  for (long long q = q0; q < n_units; q += W) {
-    mbar_wait(&bar[s], phase);
-    const int r = (int)((unsigned)q / (unsigned)a.nsub);
-    const int u = (int)q - r * a.nsub;
-    const int e0 = u * SUB;
-    const int n_el = max(0, min(SUB, a.V - e0));
-    const bool full = n_el == SUB;
-    const int bulk_el = (int)(((uint32_t)(n_el * (int)sizeof(T)) & ~15u) / sizeof(T));
-    const T* st = reinterpret_cast<const T*>(ring + s * 2 * ROWB);
-    const T* gt = full ? nullptr : tl + (long long)(r + sseq[s]) * a.ld_t;
-    const T* gd = full ? nullptr : dl + (long long)r * a.ld_d;
-    LaneMax<T> mx;
-    mx.init();
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-      mx.add(stage_vec<T>(st, gt, full, n_el, bulk_el, e0, v), stage_vec<T>(st + SUB, gd, full, n_el, bulk_el, e0, v));
-    float M, Dmax;
-    mx.reduce(M, Dmax);
-    SubPartial p;
-    if (M <= -1e30f) {
-      p = empty_partial();
-    } else {
-      const SumRef R(M, Dmax);
-      float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-        vec_accum<T>(stage_vec<T>(st, gt, full, n_el, bulk_el, e0, v),
-                     stage_vec<T>(st + SUB, gd, full, n_el, bulk_el, e0, v), R, S2, A2, D2);
-      p = finish_partial(S2, A2, D2, M, Dmax, R.Cw);
-    }
-    __syncwarp();
-    const long long qn = q + ST * W;
-    if (qn < n_units) issue(qn, s);
-    store_partial(a.part + q, p);
-    if (++s == ST) {
-      s = 0;
-      phase ^= 1u;
-    }
-  }
-}
-
 #include "verify_draw.cuh"   // a2-a4 kernels (inside namespace dsde)
 #include "verify_fused.cuh"  // the whole step in one persistent kernel
 
@@ -1089,11 +820,11 @@ static int tail_variant() {
   return v;
 }
 
-static int stream_variant() {  // 0 = ldg (default), 1 = tma, 2 = wt, 3 = wt2
+static int stream_variant() {  // 0 = ldg (default), 1 = tma (DSDE_STREAM=tma)
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("DSDE_STREAM");
-    v = !e ? 0 : strcmp(e, "tma") == 0 ? 1 : strcmp(e, "wt") == 0 ? 2 : strcmp(e, "wt2") == 0 ? 3 : 0;
+    v = (e && strcmp(e, "tma") == 0) ? 1 : 0;
   }
   return v;
 }
@@ -1122,7 +853,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   int dev = 0;
   cudaGetDevice(&dev);
   struct Grids {
-    int sms = 0, ldg = 0, tma = 0, wt = 0, wt2 = 0, draw = 0;
+    int sms = 0, ldg = 0, tma = 0, draw = 0;
   };
   static Grids grids[64];
   Grids& g = grids[dev & 63];
@@ -1130,11 +861,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_stream_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem<T>());
-    cudaFuncSetAttribute(k_stream_wt<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, wt_smem<T>());
     g.ldg = resident_grid(k_stream_ldg<T>, kLdgThreads, 0, sms, 0);
-    g.wt = resident_grid(k_stream_wt<T>, kWtWarps * 32, wt_smem<T>(), sms, 0);
-    cudaFuncSetAttribute(k_stream_wt2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, w2_smem<T>());
-    g.wt2 = resident_grid(k_stream_wt2<T>, kW2Warps * 32, w2_smem<T>(), sms, 0);
     g.tma = resident_grid(k_stream_tma<T>, kTmaThreads, tma_smem<T>(), sms, kTmaCtas);
     g.draw = resident_grid(k_draw_ldg<T>, kLdgThreads, 0, sms, 0);
     g.sms = sms;
@@ -1202,15 +929,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   mark();
   // a1: statistics of every (draft row, vocab slice)
   StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, ns, total, ws.part};
-  if (variant == 3) {
-    const long long units = (long long)total * ns;
-    const long long blocks = (units + kW2Warps - 1) / kW2Warps;
-    k_stream_wt2<T><<<(int)std::min<long long>(blocks, g.wt2), kW2Warps * 32, w2_smem<T>(), s>>>(sa);
-  } else if (variant == 2) {
-    const long long units = (long long)total * ns;
-    const long long blocks = (units + kWtWarps - 1) / kWtWarps;
-    k_stream_wt<T><<<(int)std::min<long long>(blocks, g.wt), kWtWarps * 32, wt_smem<T>(), s>>>(sa);
-  } else if (variant == 1) {
+  if (variant == 1) {
     const long long items = (long long)total * (ns / kCWarps);
     k_stream_tma<T><<<(int)std::min<long long>(items, g.tma), kTmaThreads, tma_smem<T>(), s>>>(sa);
   } else {
