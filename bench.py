@@ -18,8 +18,10 @@ Measurement:
     steps run, then K timed steps replay the recorded steps in order (cyclically
     if K + W > R), bracketed by barrier + synchronize, CUDA events on the
     launching stream, max over ranks;
-  * roofline: algorithmic bytes of dsde_verify / its own CUDA-event
-    time inside the timed region, against MEASURED_PEAKS.json hbm_gbs;
+  * roofline: algorithmic bytes of the stream kernel / its own
+    CUDA-event time, measured in a second replay of the same steps with the
+    library's per-launch events (they cost ~14 us per step, so the headline
+    pass has none), against MEASURED_PEAKS.json hbm_gbs;
   * e2e: the same metric through the public Python API from pinned host buffers
     (H2D of the step inputs and D2H of the results inside the timed region);
   * cpu_baseline: the fp64 oracle (oracle/, test infrastructure) on a bounded
@@ -273,39 +275,57 @@ def run(args):
         step.verify(i.cu_sl, i.draft_tokens, i.target, i.draft, i.seeds, e["n"])
         step.signal_and_cap(i.cu_sl)
 
-    # ---- warm-up + timed replay from the recorded start state
+    def run_step(j):
+        e = rec[(args.warmup + j) % R]
+        i = e["inp"]
+        if args.split_calls:
+            step.verify(i.cu_sl, i.draft_tokens, i.target, i.draft, i.seeds, e["n"])
+            step.signal_and_cap(i.cu_sl)
+        else:  # one dsde_step call: the whole hot path (verify + signal + cap)
+            step(i.cu_sl, i.draft_tokens, i.target, i.draft, i.seeds, e["n"])
+
+    # ---- pass 1 (the headline): warm-up + K timed steps replayed from the
+    # recorded start state, nothing but the two bracketing events in the region
     state.load(snap)
     for wi in range(args.warmup):
         replay(wi)
-    n_ev = args.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_ev)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
-    state.profile_read()  # drop anything recorded before the timed region
-    state.profile(True)
     with sampler:
         t_start.record(stream)
         for j in range(args.steps):
-            e = rec[(args.warmup + j) % R]
-            i = e["inp"]
-            ev[j][0].record(stream)
-            if args.split_calls:
-                step.verify(i.cu_sl, i.draft_tokens, i.target, i.draft, i.seeds, e["n"])
-                ev[j][1].record(stream)
-                step.signal_and_cap(i.cu_sl)
-            else:  # one dsde_step call: the whole hot path (verify + signal + cap)
-                step(i.cu_sl, i.draft_tokens, i.target, i.draft, i.seeds, e["n"])
-                ev[j][1].record(stream)
+            run_step(j)
         t_end.record(stream)
         torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    elapsed_ms = t_start.elapsed_time(t_end)
+
+    # ---- pass 2 (kernel times for the roofline): the same replay with the
+    # library's per-launch events (dsde_profile_*) and per-step events on the
+    # launching stream; events cost ~14 us per step, so they stay out of pass 1
+    K2 = args.steps
+    state.load(snap)
+    for wi in range(args.warmup):
+        replay(wi)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K2)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    state.profile_read()  # drop anything recorded before the timed region
+    state.profile(True)
+    for j in range(K2):
+        ev[j][0].record(stream)
+        run_step(j)
+        ev[j][1].record(stream)
+    torch.cuda.synchronize()
     state.profile(False)
     phase_ms, phase_calls = state.profile_read()
     if ws > 1:
         dist.barrier()
-    elapsed_ms = t_start.elapsed_time(t_end)
     verify_ms = sum(a.elapsed_time(b) for a, b in ev)
     stream_ms = phase_ms["stream"]
     positions = sum(rec[(args.warmup + j) % R]["n"] for j in range(args.steps))
@@ -356,6 +376,8 @@ def run(args):
                          "traffic_source": trec["source"] if trec else None,
                          "algorithmic_bytes_per_launch": sbytes / ws / args.steps,
                          "avg_launch_ms": stream_ms / args.steps},
+            "timing": "value / ms_per_step: pass 1, only the two bracketing events in the region; roofline and "
+                      "verify_pass: pass 2, the same replay with per-launch CUDA events on the launching stream",
             "verify_pass": {"kernels": list(phase_ms), "ms_per_step": {k: v / args.steps for k, v in phase_ms.items()},
                             "event_ms_per_step": verify_ms / args.steps,
                             "algorithmic_bytes_per_step": vbytes / ws / args.steps,
