@@ -587,6 +587,9 @@ __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(Strea
   const long long n_units = (long long)a.total * a.nsub;
   const long long W = (long long)gridDim.x * (kLdgThreads / 32);
   long long q = (long long)blockIdx.x * (kLdgThreads / 32) + (threadIdx.x >> 5);
+  // let the tail kernel launch (programmatic dependent launch) and become
+  // resident on SMs as this grid drains; it waits for our completion
+  asm volatile("griddepcontrol.launch_dependents;");
   if (q >= n_units) return;
   int seq = 0;
 #if !DSDE_LDG_PREFETCH
@@ -820,6 +823,30 @@ static int tail_variant() {
   return v;
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while the previous kernel on the stream drains and must call
+// griddepcontrol.wait before touching that kernel's results. DSDE_PDL=0
+// launches it plainly (griddepcontrol.wait is then a no-op).
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
+  static int use = -1;
+  if (use < 0) {
+    const char* e = getenv("DSDE_PDL");
+    use = (e && strcmp(e, "0") == 0) ? 0 : 1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = use ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 static int stream_variant() {  // 0 = ldg (default), 1 = tma (DSDE_STREAM=tma)
   static int v = -1;
   if (v < 0) {
@@ -948,9 +975,9 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
     // 16-warp CTAs while every sequence gets a resident CTA (2 per SM), 8-warp
     // CTAs (4 per SM) for larger batches so the tail stays one wave longer
     if (B <= 2 * g.sms)
-      k_tail<T, true, 16><<<B, 512, 0, s>>>(fa, da, sel, *step);
+      launch_pdl(k_tail<T, true, 16>, B, 512, s, fa, da, sel, *step);
     else
-      k_tail<T, true, 8><<<B, 256, 0, s>>>(fa, da, sel, *step);
+      launch_pdl(k_tail<T, true, 8>, B, 256, s, fa, da, sel, *step);
     mark();
     mark();
     mark();
@@ -959,9 +986,9 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   if (tv == 0) {
     // a2-a4 fused: one CTA per sequence (the profiler's later phases read 0)
     if (B <= 2 * g.sms)
-      k_tail<T, false, 16><<<B, 512, 0, s>>>(fa, da, sel, StepExtra{});
+      launch_pdl(k_tail<T, false, 16>, B, 512, s, fa, da, sel, StepExtra{});
     else
-      k_tail<T, false, 8><<<B, 256, 0, s>>>(fa, da, sel, StepExtra{});
+      launch_pdl(k_tail<T, false, 8>, B, 256, s, fa, da, sel, StepExtra{});
     mark();
     mark();
     mark();

@@ -665,6 +665,9 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(FinArgs fa, 
   const int i = blockIdx.x;
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_rec.mode = MODE_NONE;
+  // programmatic dependent launch: the CTA may be resident before the stream
+  // kernel has finished; wait for its completion (and memory) here
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   finalize_seq<T>(fa, i, &s_rec);
   __syncthreads();
