@@ -66,6 +66,8 @@ def lib():
         L.oracle_verify.argtypes = [C.c_int, C.c_int, C.c_int, P, P, P, C.c_int64, P, C.c_int64,
                                     P, P, P, P, P, P, P, P, P, C.c_int]
         L.oracle_verify.restype = C.c_int
+        L.oracle_verify_mode.argtypes = list(L.oracle_verify.argtypes) + [C.c_int]
+        L.oracle_verify_mode.restype = C.c_int
         L.oracle_weighted_variance.argtypes = [P, C.c_int, C.c_double]
         L.oracle_weighted_variance.restype = C.c_double
         L.oracle_scale_factor.argtypes = [C.c_double]
@@ -140,9 +142,11 @@ class VerifyResult:
 
 
 def verify(cu_sl, draft_tokens, target_logits, draft_logits, seeds, dtype: int,
-           nthreads: int = 1) -> VerifyResult:
+           nthreads: int = 1, greedy: bool = False) -> VerifyResult:
     """Batched verification. ``target_logits`` / ``draft_logits`` are 2-D numpy
-    arrays of float32 (dtype=F32) or uint16 bf16 bit patterns (dtype=BF16)."""
+    arrays of float32 (dtype=F32) or uint16 bf16 bit patterns (dtype=BF16).
+    greedy=True: T = 0 verification (accept iff x_j = argmax t_j, emit the
+    target argmax)."""
     cu_sl = np.ascontiguousarray(cu_sl, dtype=np.int32)
     toks = np.ascontiguousarray(draft_tokens, dtype=np.int32)
     tl = np.ascontiguousarray(target_logits)
@@ -159,10 +163,10 @@ def verify(cu_sl, draft_tokens, target_logits, draft_logits, seeds, dtype: int,
         kld=np.zeros(nk, np.float64), log_ratio=np.zeros(nk, np.float64),
         u_acc=np.zeros(nk + B, np.float64), u_smp=np.zeros(nk + B, np.float64),
         samp_diag=np.zeros((B, 3), np.float64), flags=np.zeros(nk + B, np.int32))
-    rc = lib().oracle_verify(B, V, dtype, _p(cu_sl), _p(toks), _p(tl), tl.shape[1], _p(dl),
-                             dl.shape[1], _p(seeds), _p(r.accepted_len), _p(r.emitted), _p(r.kld),
-                             _p(r.log_ratio), _p(r.u_acc), _p(r.u_smp), _p(r.samp_diag),
-                             _p(r.flags), int(nthreads))
+    rc = lib().oracle_verify_mode(B, V, dtype, _p(cu_sl), _p(toks), _p(tl), tl.shape[1], _p(dl),
+                                  dl.shape[1], _p(seeds), _p(r.accepted_len), _p(r.emitted), _p(r.kld),
+                                  _p(r.log_ratio), _p(r.u_acc), _p(r.u_smp), _p(r.samp_diag),
+                                  _p(r.flags), int(nthreads), int(bool(greedy)))
     if rc != 0:
         raise ValueError(f"oracle_verify failed: {rc}")
     return r

@@ -199,9 +199,18 @@ typedef struct {
     double* u_smp;           /* [sum k + B] */
     double* samp_diag;       /* [B][3] : R, lo, hi of the final draw */
     int32_t* flags;          /* [sum k + B] */
+    int greedy;              /* 1: T = 0 verification (f1) */
     int b0, b1;              /* sequence range for this worker */
     int status;
 } verify_job;
+
+/* argmax of a row, smallest index among equal maxima (D18) */
+static int row_argmax(const double* x, int V) {
+    int best = 0;
+    for (int v = 1; v < V; ++v)
+        if (x[v] > x[best]) best = v;
+    return best;
+}
 
 /* Verification of one sequence i (S:125-127 / P:260):
  *   for j in [0,k): KL_j (all positions, D3), r_j = p(x_j)/q(x_j),
@@ -232,6 +241,11 @@ static int verify_one(verify_job* J, int i, double* t, double* d, double* w) {
         J->u_acc[slot0 + j] = ua;
         J->u_smp[slot0 + j] = us;
         J->flags[slot0 + j] = 0;
+        if (J->greedy) {
+            /* T = 0: accept iff x_j is the target argmax */
+            if (a == k && x != row_argmax(t, V)) a = j;
+            continue;
+        }
         const double r = exp(lr);
         const double pacc = r < 1.0 ? r : 1.0;
         if (fabs(ua - pacc) < 1e-6) J->flags[slot0 + j] |= OR_FLAG_ACCEPT_TIE;
@@ -249,7 +263,11 @@ static int verify_one(verify_job* J, int i, double* t, double* d, double* w) {
     const double u = J->u_smp[slot0 + a];
     int tok;
     double R = 0.0, lo = 0.0, hi = 0.0;
-    if (a < k) {
+    if (J->greedy) {
+        /* the target argmax of row a (recovery, a < k) or of the bonus row k */
+        load_row(t, J->tl, J->dtype, trow0 + a, J->ld_t, V);
+        tok = row_argmax(t, V);
+    } else if (a < k) {
         load_row(t, J->tl, J->dtype, trow0 + a, J->ld_t, V);
         load_row(d, J->dl, J->dtype, (int64_t)base + a, J->ld_d, V);
         const double lt = row_lse(t, V), ld = row_lse(d, V);
@@ -269,7 +287,7 @@ static int verify_one(verify_job* J, int i, double* t, double* d, double* w) {
         for (int v = 0; v < V; ++v) w[v] = exp(t[v] - lt);  /* p_v */
         tok = inverse_cdf(w, V, u, &R, &lo, &hi);
     }
-    if (fabs(u - lo) < 1e-6 || fabs(u - hi) < 1e-6) J->flags[slot0 + a] |= OR_FLAG_SAMPLE_TIE;
+    if (!J->greedy && (fabs(u - lo) < 1e-6 || fabs(u - hi) < 1e-6)) J->flags[slot0 + a] |= OR_FLAG_SAMPLE_TIE;
     J->samp_diag[3 * i + 0] = R;
     J->samp_diag[3 * i + 1] = lo;
     J->samp_diag[3 * i + 2] = hi;
@@ -300,12 +318,12 @@ static void* verify_worker(void* arg) {
  * cu_sl[i]+i+j for j in [0,k_i]; per-slot outputs (emitted, u_acc, u_smp,
  * flags) use the target-row index. nthreads <= 1 runs serially.
  * Returns 0, or -1 on invalid data (k < 1, token out of range). */
-OR_EXPORT int oracle_verify(int B, int V, int dtype, const int32_t* cu_sl,
-                            const int32_t* draft_tokens, const void* target_logits, int64_t ld_t,
-                            const void* draft_logits, int64_t ld_d, const uint64_t* seeds,
-                            int32_t* accepted_len, int32_t* emitted, double* kld,
-                            double* log_ratio, double* u_acc, double* u_smp, double* samp_diag,
-                            int32_t* flags, int nthreads) {
+OR_EXPORT int oracle_verify_mode(int B, int V, int dtype, const int32_t* cu_sl,
+                                 const int32_t* draft_tokens, const void* target_logits, int64_t ld_t,
+                                 const void* draft_logits, int64_t ld_d, const uint64_t* seeds,
+                                 int32_t* accepted_len, int32_t* emitted, double* kld,
+                                 double* log_ratio, double* u_acc, double* u_smp, double* samp_diag,
+                                 int32_t* flags, int nthreads, int greedy) {
     if (B < 1 || V < 2 || (dtype != 0 && dtype != 1)) return -1;
     if (nthreads < 1) nthreads = 1;
     if (nthreads > B) nthreads = B;
@@ -335,6 +353,7 @@ OR_EXPORT int oracle_verify(int B, int V, int dtype, const int32_t* cu_sl,
         J->u_smp = u_smp;
         J->samp_diag = samp_diag;
         J->flags = flags;
+        J->greedy = greedy;
         J->b0 = (int)((int64_t)B * n / nthreads);
         J->b1 = (int)((int64_t)B * (n + 1) / nthreads);
     }
@@ -350,6 +369,17 @@ OR_EXPORT int oracle_verify(int B, int V, int dtype, const int32_t* cu_sl,
     free(jobs);
     free(th);
     return rc;
+}
+
+/* The rejection-sampling verification (the default, C1). */
+OR_EXPORT int oracle_verify(int B, int V, int dtype, const int32_t* cu_sl, const int32_t* draft_tokens,
+                            const void* target_logits, int64_t ld_t, const void* draft_logits,
+                            int64_t ld_d, const uint64_t* seeds, int32_t* accepted_len,
+                            int32_t* emitted, double* kld, double* log_ratio, double* u_acc,
+                            double* u_smp, double* samp_diag, int32_t* flags, int nthreads) {
+    return oracle_verify_mode(B, V, dtype, cu_sl, draft_tokens, target_logits, ld_t, draft_logits,
+                              ld_d, seeds, accepted_len, emitted, kld, log_ratio, u_acc, u_smp,
+                              samp_diag, flags, nthreads, 0);
 }
 
 /* ------------------------------------------------------------------ */

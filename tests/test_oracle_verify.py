@@ -185,3 +185,56 @@ def test_invalid_inputs_raise():
     d = np.zeros((1, 4), np.float32)
     with pytest.raises(ValueError):
         oracle.verify(cu, np.int32([9]), t, d, np.uint64([0, 1]), oracle.F32)
+
+
+# ---------------------------------------------------------------- f1: T = 0 ---
+def test_greedy_worked_example_and_tie_break():
+    """T = 0 verification: accept iff x_j is the target
+    argmax; the first mismatch (or the bonus row) emits the target argmax; equal
+    maxima resolve to the smallest token id (D18)."""
+    V = 5
+    cu = np.int32([0, 2])
+    t = np.float32([[0, 3, 1, 3, 2], [5, 1, 1, 1, 1], [0, 0, 0, 9, 0]])
+    d = np.float32([[1, 1, 1, 1, 1], [0, 0, 0, 0, 0]])
+    seeds = np.uint64([1, 2, 3])
+    r = oracle.verify(cu, np.int32([1, 0]), t, d, seeds, oracle.F32, greedy=True)
+    assert r.accepted_len.tolist() == [2] and r.emitted.tolist() == [1, 0, 3]
+    r = oracle.verify(cu, np.int32([3, 0]), t, d, seeds, oracle.F32, greedy=True)  # 3 ties with 1: rejected
+    assert r.accepted_len.tolist() == [0] and r.emitted.tolist() == [1, -1, -1]
+
+
+def test_greedy_emits_the_target_argmax_sequence():
+    """The defining property of greedy speculative decoding, by brute force on
+    random batches: emitted[0..a] = argmax of target rows 0..a, every accepted
+    draft token equals its row's argmax and the first rejected one does not;
+    independent of the seeds; KLDs identical to the sampling mode."""
+    r = np.random.default_rng(18)
+    for trial in range(40):
+        B, V = int(r.integers(1, 6)), int(r.integers(2, 40))
+        k = r.integers(1, 6, B)
+        cu = np.concatenate([[0], np.cumsum(k)]).astype(np.int32)
+        nk = int(cu[-1])
+        # small integer logits make ties frequent
+        t = r.integers(-3, 4, (nk + B, V)).astype(np.float32)
+        d = r.integers(-3, 4, (nk, V)).astype(np.float32)
+        am = lambda row: int(np.flatnonzero(row == row.max())[0])
+        toks = np.empty(nk, np.int32)
+        for i in range(B):
+            for j in range(k[i]):
+                row = t[cu[i] + i + j]
+                toks[cu[i] + j] = am(row) if r.random() < 0.7 else int(r.integers(0, V))
+        s1 = r.integers(0, 2**63, nk + B, dtype=np.uint64)
+        s2 = r.integers(0, 2**63, nk + B, dtype=np.uint64)
+        g1 = oracle.verify(cu, toks, t, d, s1, oracle.F32, greedy=True)
+        g2 = oracle.verify(cu, toks, t, d, s2, oracle.F32, greedy=True)
+        smp = oracle.verify(cu, toks, t, d, s1, oracle.F32)
+        assert np.array_equal(g1.accepted_len, g2.accepted_len) and np.array_equal(g1.emitted, g2.emitted)
+        assert np.array_equal(g1.kld, smp.kld)
+        for i in range(B):
+            a, s0 = int(g1.accepted_len[i]), cu[i] + i
+            for j in range(a):
+                assert toks[cu[i] + j] == am(t[s0 + j]) == g1.emitted[s0 + j]
+            if a < k[i]:
+                assert toks[cu[i] + a] != am(t[s0 + a])
+            assert g1.emitted[s0 + a] == am(t[s0 + a])
+            assert (g1.emitted[s0 + a + 1:s0 + k[i] + 1] == -1).all()
