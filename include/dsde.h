@@ -80,7 +80,7 @@ typedef enum { DSDE_F32 = 0, DSDE_BF16 = 1 } dsde_dtype;
  * Validity (S:173-174 plus D11/D17): 0 < delta <= 1; 1 <= n_short < n_long
  * <= DSDE_MAX_WINDOW; sl_min >= 1; sl_min < sl_ceiling <= DSDE_MAX_SL;
  * epsilon > 0; calib_steps >= 0; 1 <= calib_sl <= sl_ceiling;
- * window_unit in {0,1}; cap_mode in {0,1}. */
+ * window_unit in {0,1}; cap_mode in {0,1}; greedy in {0,1}. */
 typedef struct {
     double delta;      /* decay factor of Eq.5, 0.85                         */
     int n_short;       /* short window, 10                                   */
@@ -92,6 +92,10 @@ typedef struct {
     int calib_sl;      /* SL used while calibrating (D12), 4                         */
     int window_unit;   /* 0 = per-token KLD observations (default), 1 = per-step means (D8) */
     int cap_mode;      /* 0 = no cap (cap = max SL^), 1 = Eq.11 mean / MSE cap (default)     */
+    int greedy;        /* 0 = rejection sampling (default); 1 = T = 0 verification: accept iff
+                          x_j = argmax t_j, emit the target argmax (
+                          ties -> smallest token id, D18). Read by dsde_verify / dsde_step
+                          from the state; KLDs, signal and cap are unchanged. */
 } dsde_config;
 
 typedef struct dsde_state_s* dsde_state; /* per-sequence KLD ring, calibration, SL_max, error word */

@@ -90,7 +90,7 @@ struct SubPartial {
 };
 static_assert(sizeof(SubPartial) == 32, "SubPartial layout");
 
-enum { MODE_NONE = 0, MODE_RESIDUAL = 1, MODE_BONUS = 2, MODE_ERROR = 3 };
+enum { MODE_NONE = 0, MODE_RESIDUAL = 1, MODE_BONUS = 2, MODE_ERROR = 3, MODE_ARGMAX = 4 };  // ARGMAX: greedy bonus row
 
 struct SeqRec {  // 64 bytes
   int mode;
@@ -505,29 +505,52 @@ __device__ __forceinline__ SubPartial finish_partial(float2 S2, float2 A2, float
 
 // `after_max` runs (warp-uniformly) once the slice maxima are reduced over the
 // warp, i.e. once every lane's words have been consumed.
+// Slice-local index of the first t equal to the slice max M (token order
+// (v * 32 + lane) * VEC + e), or INT_MAX when none (NaN): greedy verification.
+template <typename T, int NV>
+__device__ __forceinline__ int slice_argmax(const uint4 (&rt)[NV], float M) {
+  constexpr int VEC = Traits<T>::VEC;
+  const int lane = threadIdx.x & 31;
+  int best = 0x7fffffff;
+#pragma unroll
+  for (int v = NV - 1; v >= 0; --v) {
+#pragma unroll
+    for (int h = VEC - 2; h >= 0; h -= 2) {
+      const float2 tt = pair_of<T>(rt, v * VEC + h);
+      const int e0 = (v * 32 + lane) * VEC + h;
+      if (tt.y == M) best = e0 + 1;
+      if (tt.x == M) best = e0;
+    }
+  }
+  return __reduce_min_sync(kFull, (unsigned)best);
+}
+
 template <typename T, int NV, typename Hook = NoHook>
 __device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const uint4 (&rd)[NV],
-                                                  Hook after_max = Hook()) {
+                                                  Hook after_max = Hook(), bool greedy = false) {
   LaneMax<T> mx;
   mx.init();
 #pragma unroll
   for (int v = 0; v < NV; ++v) mx.add(rt[v], rd[v]);
   float M, Dmax;
   mx.reduce(M, Dmax);
+  const int amax = greedy ? slice_argmax<T>(rt, M) : 0;
   after_max();
   if (M <= -1e30f) return empty_partial();  // slice beyond V (padding only; NaN is not empty)
   const SumRef R(M, Dmax);
   float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
 #pragma unroll
   for (int v = 0; v < NV; ++v) vec_accum<T>(rt[v], rd[v], R, S2, A2, D2);
-  return finish_partial(S2, A2, D2, M, Dmax, R.Cw);
+  SubPartial p = finish_partial(S2, A2, D2, M, Dmax, R.Cw);
+  p.pad0 = __int_as_float(amax);  // slice argmax of t (greedy), else 0
+  return p;
 }
 
 // lane 0 writes the whole 32-byte partial (so a release by lane 0 covers it)
 __device__ __forceinline__ void store_partial(SubPartial* dst, const SubPartial& p) {
   if ((threadIdx.x & 31) == 0) {
     reinterpret_cast<float4*>(dst)[0] = make_float4(p.S, p.A, p.D, p.M);
-    reinterpret_cast<float4*>(dst)[1] = make_float4(p.C, p.maxd, 0.f, 0.f);
+    reinterpret_cast<float4*>(dst)[1] = make_float4(p.C, p.maxd, p.pad0, 0.f);
   }
 }
 
@@ -552,6 +575,7 @@ struct StreamArgs {
   const int32_t* cu_sl;
   int B, V, nsub, total;
   SubPartial* part;
+  int greedy;  // also record the slice argmax of t (T = 0 verification)
 };
 
 // ---------------------------------------------------------------------------
@@ -619,7 +643,7 @@ __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(Strea
     p.S = __uint_as_float(acc);
     store_partial(dst, p);
 #else
-    store_partial(dst, slice_stats<T>(rt, rd));
+    store_partial(dst, slice_stats<T>(rt, rd, NoHook(), a.greedy != 0));
 #endif
     u += du;
     r += dr;
@@ -635,11 +659,11 @@ __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(Strea
   while (true) {
     const long long qb = q + W;
     if (qb < n_units) stream_unit_load<T>(a, qb, seq, bt, bd);
-    store_partial(a.part + q, slice_stats<T>(at, ad));
+    store_partial(a.part + q, slice_stats<T>(at, ad, NoHook(), a.greedy != 0));
     if (qb >= n_units) return;
     const long long qa = qb + W;
     if (qa < n_units) stream_unit_load<T>(a, qa, seq, at, ad);
-    store_partial(a.part + qb, slice_stats<T>(bt, bd));
+    store_partial(a.part + qb, slice_stats<T>(bt, bd, NoHook(), a.greedy != 0));
     if (qa >= n_units) return;
     q = qa;
   }
@@ -805,7 +829,7 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtas) k_stream_tma(StreamArgs
       s = 0;
       ++round;
     }
-    store_partial(a.part + r * a.nsub + c * kCWarps + warp, slice_stats<T>(rt, rd));
+    store_partial(a.part + r * a.nsub + c * kCWarps + warp, slice_stats<T>(rt, rd, NoHook(), a.greedy != 0));
   }
 }
 
@@ -871,7 +895,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
                           const void* tl, int64_t ld_t, const void* dl, int64_t ld_d,
                           const uint64_t* seeds, int32_t* acc_len, int32_t* emitted, float* kld,
                           uint8_t* flags, const VerifyWs& ws, int32_t* err, Profiler* prof,
-                          cudaStream_t s, const StepExtra* step = nullptr) {
+                          cudaStream_t s, const StepExtra* step = nullptr, int greedy = 0) {
   const bool pr = prof != nullptr && prof->on;
   auto mark = [&]() {
     if (pr) cudaEventRecord(prof->next(), s);
@@ -894,7 +918,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
     g.sms = sms;
   }
   const int variant = stream_variant();
-  const int tv = tail_variant();
+  const int tv = greedy && tail_variant() == 2 ? 0 : tail_variant();  // the fused kernel has no T = 0 mode
   if (tv == 2) {
     static int fused_grid[64] = {0};
     int& fg = fused_grid[dev & 63];
@@ -955,7 +979,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   }
   mark();
   // a1: statistics of every (draft row, vocab slice)
-  StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, ns, total, ws.part};
+  StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, ns, total, ws.part, greedy};
   if (variant == 1) {
     const long long items = (long long)total * (ns / kCWarps);
     k_stream_tma<T><<<(int)std::min<long long>(items, g.tma), kTmaThreads, tma_smem<T>(), s>>>(sa);
@@ -967,7 +991,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   mark();
   // a2-a3: row merge, KL, accept test, layout, draw record
   FinArgs fa{B, V, total, ns, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, ws.part,
-             acc_len, emitted, kld, flags, ws.rec, err};
+             acc_len, emitted, kld, flags, ws.rec, err, greedy};
   const int nd = n_subs_d(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32);
   DrawArgs da{B, V, nd, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.ref};
   SelArgs sel{B, V, nd, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.ref, emitted, flags, err};
@@ -1046,11 +1070,11 @@ extern "C" dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_dra
   if (dtype == DSDE_BF16)
     e = launch_verify<uint16_t>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                                 draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld,
-                                flags, ws, st->err, st->prof, s);
+                                flags, ws, st->err, st->prof, s, nullptr, st->cfg.greedy);
   else
     e = launch_verify<float>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                              draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld, flags,
-                             ws, st->err, st->prof, s);
+                             ws, st->err, st->prof, s, nullptr, st->cfg.greedy);
   return e == cudaSuccess ? DSDE_OK : DSDE_ERR_CUDA;
 }
 
@@ -1097,11 +1121,11 @@ extern "C" dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, 
   if (dtype == DSDE_BF16)
     e = launch_verify<uint16_t>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                                 draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld,
-                                flags, ws, st->err, st->prof, s, &x);
+                                flags, ws, st->err, st->prof, s, &x, st->cfg.greedy);
   else
     e = launch_verify<float>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                              draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld, flags,
-                             ws, st->err, st->prof, s, &x);
+                             ws, st->err, st->prof, s, &x, st->cfg.greedy);
   if (e != cudaSuccess) return DSDE_ERR_CUDA;
   if (!comm) return DSDE_OK;
   dsde_status rs = DSDE_OK;

@@ -13,7 +13,7 @@
 //               then inside the crossing slice (re-read from L2)
 //               in ascending token order (a4, D7).
 
-enum { IT_RESID = 1, IT_BONUS = 2, IT_NONE = 3 };
+enum { IT_RESID = 1, IT_BONUS = 2, IT_NONE = 3, IT_ARGMAX = 4 };
 
 struct FinArgs {
   int B, V, total, nsub;
@@ -31,6 +31,7 @@ struct FinArgs {
   uint8_t* flags;
   SeqRec* rec;
   int32_t* err;
+  int greedy;  // T = 0: accept iff x = argmax t, emit the argmax
 };
 
 constexpr int kFinThreads = 32 * DSDE_MAX_SL;
@@ -40,6 +41,7 @@ constexpr int kFinThreads = 32 * DSDE_MAX_SL;
 template <typename T>
 __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* out) {
   __shared__ double s_kl[DSDE_MAX_SL], s_lam[DSDE_MAX_SL], s_C[DSDE_MAX_SL], s_S[DSDE_MAX_SL];
+  __shared__ int s_amax[DSDE_MAX_SL];
   __shared__ float s_M[DSDE_MAX_SL];
   __shared__ int s_fin[DSDE_MAX_SL];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -104,6 +106,15 @@ __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* ou
       A += __shfl_xor_sync(kFull, A, o);
       D += __shfl_xor_sync(kFull, D, o);
     }
+    if (a.greedy) {
+      // row argmax of t: slices are in token order, so the smallest global index
+      // among the slices holding the row max (slice argmax in the pad0 bits)
+      unsigned cand = 0x7fffffffu;
+      for (int c = lane; c < nc; c += 32)
+        if (P[c].M == Ml) cand = min(cand, (unsigned)(c * sub_elems<T>() + __float_as_int(P[c].pad0)));
+      cand = __reduce_min_sync(kFull, cand);
+      if (lane == 0) s_amax[j] = (int)cand;
+    }
     if (lane == 0) {
       // y = E_p[exp(-w)] - 1. KL = D/S + (log1p(y) - y) has no cancellation for
       // small KL; when y > 1 (the draft puts far more mass away from the
@@ -140,9 +151,13 @@ __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* ou
       lr = (tx - dx) - s_C[lane] + s_lam[lane];
       nonfin |= !isfinite(lr);
     }
-    const double pacc = lr >= 0.0 ? 1.0 : exp(lr);
-    acc = u.acc < pacc;
-    near = fabs(u.acc - pacc) < 1e-6;
+    if (a.greedy) {
+      acc = x == s_amax[lane];  // T = 0: the draft token must be the target argmax
+    } else {
+      const double pacc = lr >= 0.0 ? 1.0 : exp(lr);
+      acc = u.acc < pacc;
+      near = fabs(u.acc - pacc) < 1e-6;
+    }
   }
   const unsigned bt = __ballot_sync(kFull, bad_tok);
   const unsigned nf = __ballot_sync(kFull, nonfin);
@@ -177,7 +192,23 @@ __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* ou
     if (a.flags) a.flags[slot0 + lane] = (near && lane <= aa && lane < k) ? DSDE_FLAG_ACCEPT_NEAR_TIE : 0;
   }
   if (lane == 0) a.acc_len[i] = aa;
-  if (lane == aa) {
+  if (lane == aa && a.greedy) {
+    // T = 0: the recovery token is the argmax of row aa (known from the stream);
+    // the bonus row's argmax is found by the draw pass
+    r.slot = (int)(slot0 + aa);
+    r.trow = slot0 + aa;
+    r.drow = -1;
+    r.u = 0.0;
+    r.M = 0.f;
+    r.C = r.lam = 0.0;
+    if (aa < k) {
+      a.emitted[slot0 + aa] = s_amax[aa];
+      r.mode = MODE_NONE;
+    } else {
+      r.mode = MODE_ARGMAX;
+    }
+    *out = r;
+  } else if (lane == aa) {
     r.slot = (int)(slot0 + aa);
     r.trow = slot0 + aa;
     r.u = u.smp;
@@ -253,6 +284,18 @@ __device__ __forceinline__ float2 resid_pair_exact(float2 tt, float2 dd, float2 
   const float2 om = make_float2(z.x < 1.f ? sm.x : bg.x, z.y < 1.f ? sm.y : bg.y);
   const float2 r = __fmul2_rn(ev, om);
   return make_float2((z.x > 0.f && ev.x > 0.f) ? r.x : 0.f, (z.y > 0.f && ev.y > 0.f) ? r.y : 0.f);
+}
+
+// lane max of t over one vector (NaN-propagating)
+template <typename T>
+__device__ __forceinline__ float vec_tmax(const uint4& t, float m) {
+  const uint4 x[1] = {t};
+#pragma unroll
+  for (int h = 0; h < Traits<T>::VEC; h += 2) {
+    const float2 tt = pair_of<T>(x, h);
+    m = max_nan(m, max_nan(tt.x, tt.y));
+  }
+  return m;
 }
 
 // Per-slice constants of the draw weights.
@@ -379,7 +422,7 @@ __device__ __forceinline__ DrawUnit draw_unit_load(const DrawArgs& a, long long 
   const int i = (int)(q / a.nsub), u = (int)(q - (long long)i * a.nsub);
   const int mode = r.mode;
   DrawUnit d;
-  d.type = mode == MODE_RESIDUAL ? IT_RESID : mode == MODE_BONUS ? IT_BONUS : IT_NONE;
+  d.type = mode == MODE_RESIDUAL ? IT_RESID : mode == MODE_BONUS ? IT_BONUS : mode == MODE_ARGMAX ? IT_ARGMAX : IT_NONE;
   d.M = 0.f;
   d.Cf = 0.f;
   d.lam = 0.0;
@@ -400,7 +443,7 @@ __device__ __forceinline__ DrawUnit draw_unit_load(const DrawArgs& a, long long 
   const SeqRec* rp = a.rec + (int)(q / a.nsub);
   SeqRec r;
   r.mode = __ldg(&rp->mode);
-  if (r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS) {
+  if (r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS || r.mode == MODE_ARGMAX) {
     r.trow = __ldg(&rp->trow);
     r.drow = __ldg(&rp->drow);
     r.M = __ldg(&rp->M);
@@ -416,6 +459,33 @@ __device__ __forceinline__ void draw_unit_finish(const DrawArgs& a, long long q,
                                                  const uint4 (&rd)[Traits<T>::NVD]) {
   constexpr int VEC = Traits<T>::VEC, NVD = Traits<T>::NVD;
   if (d.type == IT_NONE) return;
+  if (d.type == IT_ARGMAX) {
+    // greedy bonus row: the slice max of t and its first (slice-local) index
+    const int lane = threadIdx.x & 31;
+    float m = -INFINITY;
+#pragma unroll
+    for (int v = 0; v < NVD; ++v) m = vec_tmax<T>(rt[v], m);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(kFull, m, o));
+    int best = 0x7fffffff;
+#pragma unroll
+    for (int v = NVD - 1; v >= 0; --v) {
+      const uint4 x[1] = {rt[v]};
+#pragma unroll
+      for (int h = VEC - 2; h >= 0; h -= 2) {
+        const float2 tt = pair_of<T>(x, h);
+        const int e0 = (v * 32 + lane) * VEC + h;
+        if (tt.y == m) best = e0 + 1;
+        if (tt.x == m) best = e0;
+      }
+    }
+    best = (int)__reduce_min_sync(kFull, (unsigned)best);
+    if (lane == 0) {
+      a.smass[q] = (double)best;
+      a.sref[q] = m;
+    }
+    return;
+  }
   const DrawRef R = draw_ref<T>(rt, d.type == IT_RESID, d.M, d.Cf, d.lam);
   // mass in the select pass's order: per vector an fp32 lane sum, then an fp64 warp sum
   double m = 0.0;
@@ -491,6 +561,28 @@ template <typename T>
 __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec& r) {
   constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NVD, SUB = 32 * VEC * NV;
   const int lane = threadIdx.x & 31;
+  if (r.mode == MODE_ARGMAX) {
+    // greedy bonus token: the smallest index among the slices holding the row max
+    const float* wref = a.sref + (long long)i * a.nsub;
+    const double* wmass = a.smass + (long long)i * a.nsub;
+    float Mg = -INFINITY;
+    for (int s0 = lane; s0 < a.nsub; s0 += 32) Mg = max_nan(Mg, __ldcg(wref + s0));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) Mg = max_nan(Mg, __shfl_xor_sync(kFull, Mg, o));
+    unsigned cand = 0x7fffffffu;
+    for (int s0 = lane; s0 < a.nsub; s0 += 32)
+      if (__ldcg(wref + s0) == Mg) cand = min(cand, (unsigned)(s0 * SUB + (int)__ldcg(wmass + s0)));
+    cand = __reduce_min_sync(kFull, cand);
+    if (lane == 0) {
+      if (Mg != Mg || cand >= (unsigned)a.V) {
+        a.emitted[r.slot] = DSDE_PAD;
+        raise_device_error(a.err, DSDE_DERR_NONFINITE, i);
+      } else {
+        a.emitted[r.slot] = (int)cand;
+      }
+    }
+    return;
+  }
   if (r.mode != MODE_RESIDUAL && r.mode != MODE_BONUS) return;
   const bool resid = r.mode == MODE_RESIDUAL;
   const int nsub = a.nsub;
@@ -672,7 +764,7 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(FinArgs fa, 
   finalize_seq<T>(fa, i, &s_rec);
   __syncthreads();
   const SeqRec r = s_rec;
-  const bool draw = r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS;
+  const bool draw = r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS || r.mode == MODE_ARGMAX;
   if (STEP && warp == NW - 1) {
     signal_seq(sx.sig, i);
     if (sx.fuse_cap) {
