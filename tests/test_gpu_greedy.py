@@ -70,7 +70,8 @@ def test_greedy_parity(m, gstate, V, dtype, kmax, B):
     k = synth.random_k(B, kmax, V + 3 * B)
     host = make_host_batch(V, k, seed=V + B, dtype=dtype, profiles=("code", "low"))
     acc, o = _check(m, gstate, _argmax_drafts(host, 0.85, V), dtype)
-    assert (acc == k).any() and (acc < k).any() or B < 8  # both bonus and recovery paths ran
+    if B >= 32:  # both the bonus-argmax draw and the recovery path ran
+        assert (acc == k).any() and (acc < k).any()
 
 
 def test_greedy_ties_smallest_id(m, gstate):
