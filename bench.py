@@ -143,7 +143,7 @@ def _dist_env():
     return ws, rank, local
 
 
-def oracle_step_sample(host: dict, n_seq: int, nthreads: int, seed: int):
+def oracle_step_sample(host: dict, n_seq: int, nthreads: int, seed: int, greedy: bool = False):
     """Runs the oracle's verify on a sample of n_seq sequences of one step."""
     import oracle
     from tests import parity
@@ -152,7 +152,8 @@ def oracle_step_sample(host: dict, n_seq: int, nthreads: int, seed: int):
     sub = parity.subset_batch(host, np.sort(ids))
     t0 = time.perf_counter()
     r = oracle.verify(sub["cu_sl"], sub["draft_tokens"], sub["target"], sub["draft"], sub["seeds"],
-                      oracle.BF16 if sub["target"].dtype == np.uint16 else oracle.F32, nthreads=nthreads)
+                      oracle.BF16 if sub["target"].dtype == np.uint16 else oracle.F32, nthreads=nthreads,
+                      greedy=greedy)
     dt = time.perf_counter() - t0
     return int(sub["cu_sl"][-1]), dt, sub, r
 
@@ -170,7 +171,8 @@ def run_reference(args):
     cfg = CONFIGS[args.config]
     nthreads = os.cpu_count() or 1
     per_step = args.ref_seqs
-    w = synth.Workload(B=per_step, V=cfg["V"], dtype=torch.bfloat16, profiles=cfg["profiles"], seed=args.seed)
+    w = synth.Workload(B=per_step, V=cfg["V"], dtype=torch.bfloat16, profiles=cfg["profiles"], seed=args.seed,
+                       greedy_draft=args.greedy)
     ost = oracle.OracleState(oracle.Config(sl_ceiling=cfg["ceiling"]), per_step)
     k = np.full(per_step, 4)
     positions, elapsed = 0, 0.0
@@ -178,7 +180,7 @@ def run_reference(args):
         host = synth.generate_step(w, s, k, device="cpu").host_arrays()
         t0 = time.perf_counter()
         r = oracle.verify(host["cu_sl"], host["draft_tokens"], host["target"], host["draft"], host["seeds"],
-                          oracle.BF16, nthreads=nthreads)
+                          oracle.BF16, nthreads=nthreads, greedy=args.greedy)
         sl, cal, _ = ost.update_signal(np.arange(per_step), host["cu_sl"], r.kld, r.accepted_len)
         nx, cap = oracle.next_sl(ost.cfg, sl, cal)
         dt = time.perf_counter() - t0
@@ -204,7 +206,8 @@ def _config_dict(args, cfg, n):
     return {"workload": cfg["name"], "B_per_gpu": cfg["B"], "global_batch": cfg["B"] * n, "V": cfg["V"],
             "logits": "bf16", "sl_ceiling": cfg["ceiling"], "profiles": list(cfg["profiles"]),
             "parallelism": f"dp{n}", "l2": "inputs larger than L2: a distinct ~1 GB input set per step",
-            "replay": "recorded closed-loop DSDE steps replayed in order (cyclic if K+W > R)"}
+            "replay": "recorded closed-loop DSDE steps replayed in order (cyclic if K+W > R)",
+            "verify": "greedy (T=0, draft argmax tokens)" if args.greedy else "rejection sampling (T=1)"}
 
 
 def run(args):
@@ -230,10 +233,11 @@ def run(args):
         uid = [m.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = m.Comm(uid[0], ws, rank)
-    mcfg = m.Config.default(sl_ceiling=cfg["ceiling"], calib_sl=min(4, cfg["ceiling"]))
+    mcfg = m.Config.default(sl_ceiling=cfg["ceiling"], calib_sl=min(4, cfg["ceiling"]), greedy=int(args.greedy))
     state = m.State(mcfg, B)
     step = m.Step(state, B, V, torch.bfloat16, comm=comm)
-    w = synth.Workload(B=B, V=V, dtype=torch.bfloat16, profiles=cfg["profiles"], seed=args.seed + 7919 * rank)
+    w = synth.Workload(B=B, V=V, dtype=torch.bfloat16, profiles=cfg["profiles"], seed=args.seed + 7919 * rank,
+                       greedy_draft=args.greedy)
     stream = torch.cuda.current_stream()
 
     # ---- pre-roll (calibration + settling), inputs not kept
@@ -473,7 +477,7 @@ def _cpu_baseline(args, rec, R):
     j = 0
     while elapsed < budget and j < R:
         host = rec[j]["inp"].host_arrays()
-        p, dt, _, _ = oracle_step_sample(host, args.cpu_seqs, cores, seed=j)
+        p, dt, _, _ = oracle_step_sample(host, args.cpu_seqs, cores, seed=j, greedy=args.greedy)
         positions += p
         elapsed += dt
         n += 1
@@ -498,6 +502,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seqs", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--greedy", action="store_true",
+                    help="T = 0 verification (dsde_config.greedy; draft tokens = draft argmax)")
     ap.add_argument("--split-calls", action="store_true",
                     help="time dsde_verify + dsde_update_signal + dsde_next_sl instead of one dsde_step")
     args = ap.parse_args()

@@ -104,6 +104,7 @@ class Workload:
     seed: int = 1234
     ld_pad: int = 0              # extra columns per row (ld = V + ld_pad)
     phases: bool = True          # stable / unstable phases per sequence
+    greedy_draft: bool = False   # draft tokens = argmax d (T = 0 drafting) instead of x ~ softmax(d)
     profile_of: list = field(default_factory=list)
 
     def __post_init__(self):
@@ -222,7 +223,10 @@ def generate_step(w: Workload, step: int, k, device="cpu") -> StepInputs:
         u = torch.rand((r1 - r0, V), generator=g, device=dev, dtype=torch.float32)
         u = u.clamp_(min=1e-30)
         gumbel = -torch.log(-torch.log(u))
-        tokens[r0:r1] = torch.argmax(dd.float() + gumbel, dim=1).to(torch.int32)
+        if w.greedy_draft:
+            tokens[r0:r1] = torch.argmax(dd.float(), dim=1).to(torch.int32)
+        else:
+            tokens[r0:r1] = torch.argmax(dd.float() + gumbel, dim=1).to(torch.int32)
     seeds = torch.as_tensor(slot_seeds(w.seed, step, cu).view(np.int64), device=dev)
     return StepInputs(torch.as_tensor(cu, device=dev), tokens, target, draft, seeds, V)
 
