@@ -507,22 +507,35 @@ __device__ __forceinline__ SubPartial finish_partial(float2 S2, float2 A2, float
 // warp, i.e. once every lane's words have been consumed.
 // Slice-local index of the first t equal to the slice max M (token order
 // (v * 32 + lane) * VEC + e), or INT_MAX when none (NaN): greedy verification.
+// Vectors are tested whole first (a warp ballot on "this vector holds M"), so
+// only the first vector that holds the maximum is searched element by element.
 template <typename T, int NV>
 __device__ __forceinline__ int slice_argmax(const uint4 (&rt)[NV], float M) {
   constexpr int VEC = Traits<T>::VEC;
   const int lane = threadIdx.x & 31;
-  int best = 0x7fffffff;
 #pragma unroll
-  for (int v = NV - 1; v >= 0; --v) {
+  for (int v = 0; v < NV; ++v) {
+    float vm = -INFINITY;
 #pragma unroll
-    for (int h = VEC - 2; h >= 0; h -= 2) {
+    for (int h = 0; h < VEC; h += 2) {
       const float2 tt = pair_of<T>(rt, v * VEC + h);
-      const int e0 = (v * 32 + lane) * VEC + h;
-      if (tt.y == M) best = e0 + 1;
-      if (tt.x == M) best = e0;
+      vm = fmaxf(vm, fmaxf(tt.x, tt.y));
+    }
+    const unsigned hit = __ballot_sync(kFull, vm == M);
+    if (hit) {
+      int best = 0x7fffffff;
+      if (lane == __ffs(hit) - 1) {
+#pragma unroll
+        for (int h = VEC - 2; h >= 0; h -= 2) {
+          const float2 tt = pair_of<T>(rt, v * VEC + h);
+          if (tt.y == M) best = (v * 32 + lane) * VEC + h + 1;
+          if (tt.x == M) best = (v * 32 + lane) * VEC + h;
+        }
+      }
+      return __shfl_sync(kFull, best, __ffs(hit) - 1);
     }
   }
-  return __reduce_min_sync(kFull, (unsigned)best);
+  return 0x7fffffff;
 }
 
 template <typename T, int NV, typename Hook = NoHook>
@@ -605,7 +618,9 @@ __device__ __forceinline__ void stream_unit_load(const StreamArgs& a, long long 
   load_slice<T>(reinterpret_cast<const T*>(a.dl) + (long long)r * a.ld_d, a.V, u, rd);
 }
 
-template <typename T>
+// GREEDY (T = 0): also record the slice argmax of t; a separate instantiation
+// so the sampling kernel's register allocation is not affected
+template <typename T, bool GREEDY = false>
 __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(StreamArgs a) {
   constexpr int NV = Traits<T>::NV;
   const long long n_units = (long long)a.total * a.nsub;
@@ -643,7 +658,7 @@ __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(Strea
     p.S = __uint_as_float(acc);
     store_partial(dst, p);
 #else
-    store_partial(dst, slice_stats<T>(rt, rd, NoHook(), a.greedy != 0));
+    store_partial(dst, slice_stats<T>(rt, rd, NoHook(), GREEDY));
 #endif
     u += du;
     r += dr;
@@ -659,11 +674,11 @@ __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(Strea
   while (true) {
     const long long qb = q + W;
     if (qb < n_units) stream_unit_load<T>(a, qb, seq, bt, bd);
-    store_partial(a.part + q, slice_stats<T>(at, ad, NoHook(), a.greedy != 0));
+    store_partial(a.part + q, slice_stats<T>(at, ad, NoHook(), GREEDY));
     if (qb >= n_units) return;
     const long long qa = qb + W;
     if (qa < n_units) stream_unit_load<T>(a, qa, seq, at, ad);
-    store_partial(a.part + qb, slice_stats<T>(bt, bd, NoHook(), a.greedy != 0));
+    store_partial(a.part + qb, slice_stats<T>(bt, bd, NoHook(), GREEDY));
     if (qa >= n_units) return;
     q = qa;
   }
@@ -912,7 +927,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_stream_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem<T>());
-    g.ldg = resident_grid(k_stream_ldg<T>, kLdgThreads, 0, sms, 0);
+    g.ldg = resident_grid(k_stream_ldg<T, false>, kLdgThreads, 0, sms, 0);
     g.tma = resident_grid(k_stream_tma<T>, kTmaThreads, tma_smem<T>(), sms, kTmaCtas);
     g.draw = resident_grid(k_draw_ldg<T>, kLdgThreads, 0, sms, 0);
     g.sms = sms;
@@ -986,7 +1001,10 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   } else {
     const long long units = (long long)total * ns;
     const long long blocks = (units + kLdgThreads / 32 - 1) / (kLdgThreads / 32);
-    k_stream_ldg<T><<<(int)std::min<long long>(blocks, g.ldg), kLdgThreads, 0, s>>>(sa);
+    if (greedy)
+      k_stream_ldg<T, true><<<(int)std::min<long long>(blocks, g.ldg), kLdgThreads, 0, s>>>(sa);
+    else
+      k_stream_ldg<T, false><<<(int)std::min<long long>(blocks, g.ldg), kLdgThreads, 0, s>>>(sa);
   }
   mark();
   // a2-a3: row merge, KL, accept test, layout, draw record
