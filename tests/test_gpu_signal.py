@@ -177,3 +177,34 @@ def test_step_matches_three_calls(m):
         assert not bad, (s, bad[:4], [(da[i, j].item(), db[i, j].item()) for i, j in bad[:4]])
         k = oa.next_sl.cpu().numpy().astype(np.int64)
     assert sa.device_error() == (0, -1) and sb.device_error() == (0, -1)
+
+
+def test_step_with_single_rank_nccl_comm(m):
+    """The multi-GPU cap path of dsde_step (k_tail without the fused cap, the
+    exact int64 partial, ncclAllReduce, k_cap_apply) on a one-rank NCCL
+    communicator: bit-identical to the single-GPU path, step after step, for
+    cap_mode 1 (sum) and 0 (sum + max all-reduces)."""
+    B, V, dtype = 48, 32000, torch.bfloat16
+    comm = m.Comm(m.Comm.unique_id(), 1, 0)
+    try:
+        for cap_mode in (1, 0):
+            gc, _ = _cfg_pair(m, sl_ceiling=8, calib_sl=4)
+            gc.cap_mode = cap_mode
+            gc.calib_steps = 2
+            sa, sb = m.State(gc, B), m.State(gc, B)
+            pa = m.Step(sa, B, V, dtype, with_diag=True, comm=comm)
+            pb = m.Step(sb, B, V, dtype, with_diag=True)
+            w = synth.Workload(B=B, V=V, dtype=dtype, profiles=("code", "dialogue"), seed=91 + cap_mode)
+            k = np.full(B, 4)
+            for s in range(8):
+                inp = synth.generate_step(w, s, k, device="cuda")
+                n = int(k.sum())
+                oa = pa(inp.cu_sl, inp.draft_tokens, inp.target, inp.draft, inp.seeds, n)
+                ob = pb(inp.cu_sl, inp.draft_tokens, inp.target, inp.draft, inp.seeds, n)
+                torch.cuda.synchronize()
+                for f in ("accepted_len", "emitted", "kld", "sl_hat", "next_sl", "cap"):
+                    assert torch.equal(getattr(oa, f).cpu(), getattr(ob, f).cpu()), (cap_mode, s, f)
+                k = oa.next_sl.cpu().numpy().astype(np.int64)
+            assert sa.device_error() == (0, -1)
+    finally:
+        comm.close()
