@@ -505,65 +505,29 @@ __device__ __forceinline__ SubPartial finish_partial(float2 S2, float2 A2, float
 
 // `after_max` runs (warp-uniformly) once the slice maxima are reduced over the
 // warp, i.e. once every lane's words have been consumed.
-// Slice-local index of the first t equal to the slice max M (token order
-// (v * 32 + lane) * VEC + e), or INT_MAX when none (NaN): greedy verification.
-// Vectors are tested whole first (a warp ballot on "this vector holds M"), so
-// only the first vector that holds the maximum is searched element by element.
-template <typename T, int NV>
-__device__ __forceinline__ int slice_argmax(const uint4 (&rt)[NV], float M) {
-  constexpr int VEC = Traits<T>::VEC;
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    float vm = -INFINITY;
-#pragma unroll
-    for (int h = 0; h < VEC; h += 2) {
-      const float2 tt = pair_of<T>(rt, v * VEC + h);
-      vm = fmaxf(vm, fmaxf(tt.x, tt.y));
-    }
-    const unsigned hit = __ballot_sync(kFull, vm == M);
-    if (hit) {
-      int best = 0x7fffffff;
-      if (lane == __ffs(hit) - 1) {
-#pragma unroll
-        for (int h = VEC - 2; h >= 0; h -= 2) {
-          const float2 tt = pair_of<T>(rt, v * VEC + h);
-          if (tt.y == M) best = (v * 32 + lane) * VEC + h + 1;
-          if (tt.x == M) best = (v * 32 + lane) * VEC + h;
-        }
-      }
-      return __shfl_sync(kFull, best, __ffs(hit) - 1);
-    }
-  }
-  return 0x7fffffff;
-}
-
 template <typename T, int NV, typename Hook = NoHook>
 __device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const uint4 (&rd)[NV],
-                                                  Hook after_max = Hook(), bool greedy = false) {
+                                                  Hook after_max = Hook()) {
   LaneMax<T> mx;
   mx.init();
 #pragma unroll
   for (int v = 0; v < NV; ++v) mx.add(rt[v], rd[v]);
   float M, Dmax;
   mx.reduce(M, Dmax);
-  const int amax = greedy ? slice_argmax<T>(rt, M) : 0;
   after_max();
   if (M <= -1e30f) return empty_partial();  // slice beyond V (padding only; NaN is not empty)
   const SumRef R(M, Dmax);
   float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
 #pragma unroll
   for (int v = 0; v < NV; ++v) vec_accum<T>(rt[v], rd[v], R, S2, A2, D2);
-  SubPartial p = finish_partial(S2, A2, D2, M, Dmax, R.Cw);
-  p.pad0 = __int_as_float(amax);  // slice argmax of t (greedy), else 0
-  return p;
+  return finish_partial(S2, A2, D2, M, Dmax, R.Cw);
 }
 
 // lane 0 writes the whole 32-byte partial (so a release by lane 0 covers it)
 __device__ __forceinline__ void store_partial(SubPartial* dst, const SubPartial& p) {
   if ((threadIdx.x & 31) == 0) {
     reinterpret_cast<float4*>(dst)[0] = make_float4(p.S, p.A, p.D, p.M);
-    reinterpret_cast<float4*>(dst)[1] = make_float4(p.C, p.maxd, p.pad0, 0.f);
+    reinterpret_cast<float4*>(dst)[1] = make_float4(p.C, p.maxd, 0.f, 0.f);
   }
 }
 
@@ -588,7 +552,6 @@ struct StreamArgs {
   const int32_t* cu_sl;
   int B, V, nsub, total;
   SubPartial* part;
-  int greedy;  // also record the slice argmax of t (T = 0 verification)
 };
 
 // ---------------------------------------------------------------------------
@@ -618,9 +581,7 @@ __device__ __forceinline__ void stream_unit_load(const StreamArgs& a, long long 
   load_slice<T>(reinterpret_cast<const T*>(a.dl) + (long long)r * a.ld_d, a.V, u, rd);
 }
 
-// GREEDY (T = 0): also record the slice argmax of t; a separate instantiation
-// so the sampling kernel's register allocation is not affected
-template <typename T, bool GREEDY = false>
+template <typename T>
 __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(StreamArgs a) {
   constexpr int NV = Traits<T>::NV;
   const long long n_units = (long long)a.total * a.nsub;
@@ -658,7 +619,7 @@ __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(Strea
     p.S = __uint_as_float(acc);
     store_partial(dst, p);
 #else
-    store_partial(dst, slice_stats<T>(rt, rd, NoHook(), GREEDY));
+    store_partial(dst, slice_stats<T>(rt, rd));
 #endif
     u += du;
     r += dr;
@@ -674,11 +635,11 @@ __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(Strea
   while (true) {
     const long long qb = q + W;
     if (qb < n_units) stream_unit_load<T>(a, qb, seq, bt, bd);
-    store_partial(a.part + q, slice_stats<T>(at, ad, NoHook(), GREEDY));
+    store_partial(a.part + q, slice_stats<T>(at, ad));
     if (qb >= n_units) return;
     const long long qa = qb + W;
     if (qa < n_units) stream_unit_load<T>(a, qa, seq, at, ad);
-    store_partial(a.part + qb, slice_stats<T>(bt, bd, NoHook(), GREEDY));
+    store_partial(a.part + qb, slice_stats<T>(bt, bd));
     if (qa >= n_units) return;
     q = qa;
   }
@@ -844,7 +805,7 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtas) k_stream_tma(StreamArgs
       s = 0;
       ++round;
     }
-    store_partial(a.part + r * a.nsub + c * kCWarps + warp, slice_stats<T>(rt, rd, NoHook(), a.greedy != 0));
+    store_partial(a.part + r * a.nsub + c * kCWarps + warp, slice_stats<T>(rt, rd));
   }
 }
 
@@ -927,7 +888,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_stream_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem<T>());
-    g.ldg = resident_grid(k_stream_ldg<T, false>, kLdgThreads, 0, sms, 0);
+    g.ldg = resident_grid(k_stream_ldg<T>, kLdgThreads, 0, sms, 0);
     g.tma = resident_grid(k_stream_tma<T>, kTmaThreads, tma_smem<T>(), sms, kTmaCtas);
     g.draw = resident_grid(k_draw_ldg<T>, kLdgThreads, 0, sms, 0);
     g.sms = sms;
@@ -994,17 +955,14 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   }
   mark();
   // a1: statistics of every (draft row, vocab slice)
-  StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, ns, total, ws.part, greedy};
+  StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, ns, total, ws.part};
   if (variant == 1) {
     const long long items = (long long)total * (ns / kCWarps);
     k_stream_tma<T><<<(int)std::min<long long>(items, g.tma), kTmaThreads, tma_smem<T>(), s>>>(sa);
   } else {
     const long long units = (long long)total * ns;
     const long long blocks = (units + kLdgThreads / 32 - 1) / (kLdgThreads / 32);
-    if (greedy)
-      k_stream_ldg<T, true><<<(int)std::min<long long>(blocks, g.ldg), kLdgThreads, 0, s>>>(sa);
-    else
-      k_stream_ldg<T, false><<<(int)std::min<long long>(blocks, g.ldg), kLdgThreads, 0, s>>>(sa);
+    k_stream_ldg<T><<<(int)std::min<long long>(blocks, g.ldg), kLdgThreads, 0, s>>>(sa);
   }
   mark();
   // a2-a3: row merge, KL, accept test, layout, draw record

@@ -107,13 +107,32 @@ __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* ou
       D += __shfl_xor_sync(kFull, D, o);
     }
     if (a.greedy) {
-      // row argmax of t: slices are in token order, so the smallest global index
-      // among the slices holding the row max (slice argmax in the pad0 bits)
-      unsigned cand = 0x7fffffffu;
+      // row argmax of t: the first slice holding the row max (slices are in
+      // token order), re-read from memory vector by vector (token order is
+      // vector-major) until a lane holds the max; its first such element
+      constexpr int VEC = Traits<T>::VEC, SUB = sub_elems<T>();
+      unsigned cs = 0x7fffffffu;
       for (int c = lane; c < nc; c += 32)
-        if (P[c].M == Ml) cand = min(cand, (unsigned)(c * sub_elems<T>() + __float_as_int(P[c].pad0)));
-      cand = __reduce_min_sync(kFull, cand);
-      if (lane == 0) s_amax[j] = (int)cand;
+        if (P[c].M == Ml) cs = min(cs, (unsigned)c);
+      cs = __reduce_min_sync(kFull, cs);
+      int amax = 0x7fffffff;
+      if (cs < (unsigned)nc) {
+        const T* trow = reinterpret_cast<const T*>(a.tl) + ((long long)c0 + i + j) * a.ld_t + cs * SUB;
+        const int left = a.V - (int)cs * SUB;
+        for (int v = 0; v * 32 * VEC < min(SUB, left); ++v) {
+          const int e0 = (v * 32 + lane) * VEC;
+          int first = 0x7fffffff;
+#pragma unroll
+          for (int e = VEC - 1; e >= 0; --e)
+            if (e0 + e < left && load_logit<T>(trow + e0 + e) == Ml) first = e0 + e;
+          const unsigned hit = __ballot_sync(kFull, first != 0x7fffffff);
+          if (hit) {
+            amax = (int)cs * SUB + __shfl_sync(kFull, first, __ffs(hit) - 1);
+            break;
+          }
+        }
+      }
+      if (lane == 0) s_amax[j] = amax;
     }
     if (lane == 0) {
       // y = E_p[exp(-w)] - 1. KL = D/S + (log1p(y) - y) has no cancellation for
