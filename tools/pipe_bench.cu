@@ -150,7 +150,7 @@ void run(const char* name, F launch, double lane_ops_per_thread, int sms, int cl
   cudaEventSynchronize(e1);
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
-  const double threads = (double)sms * 4 * 1024;  // grid below
+  const double threads = (double)sms * 4 * 256;  // grid below: sms * 4 blocks of 256 threads
   const double ops = threads * lane_ops_per_thread;
   const double per_clk_sm = ops / (ms * 1e-3) / (clk_khz * 1e3) / sms;
   printf("%-12s %8.3f ms  %8.1f lane-ops/clk/SM  (%s)\n", name, ms, per_clk_sm, cudaGetErrorString(cudaGetLastError()));
