@@ -268,11 +268,9 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs a) {
 // ---------------------------------------------------------------------------
 // residual weights of one element pair (see above)
 template <typename T>
-__device__ __forceinline__ float2 resid_pair_exact(float2 tt, float2 dd, float2 nML2, float Cf, float lhi,
-                                                   float llo) {
+__device__ __forceinline__ float2 resid_pair_exact(float2 tt, float2 dd, float2 nML2, float khi, float klo) {
   const float2 L2 = make_float2(kLog2e, kLog2e), nL2 = make_float2(-kLog2e, -kLog2e);
-  const float2 nC = make_float2(-Cf, -Cf);
-  const float2 LH = make_float2(lhi, lhi), LL = make_float2(llo, llo), ONE = make_float2(1.f, 1.f);
+  const float2 ONE = make_float2(1.f, 1.f);
   const float2 K7 = make_float2(-2.812654656736413e-06f, -2.812654656736413e-06f);
   const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
   const float2 K5 = make_float2(-1.9836986029986292e-04f, -1.9836986029986292e-04f);
@@ -283,13 +281,14 @@ __device__ __forceinline__ float2 resid_pair_exact(float2 tt, float2 dd, float2 
   const float2 K0 = make_float2(0.5f, 0.5f);
   const float2 xt = __ffma2_rn(tt, L2, nML2);
   const float2 ev = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));  // 0 for padding
+  // z = (t - d) - (C - lam), the constant carried as khi + klo
   float2 z;
   if constexpr (sizeof(T) == 2) {
-    z = __fadd2_rn(__fadd2_rn(tt, make_float2(-dd.x, -dd.y)), nC);  // t - d exact
+    z = __fadd2_rn(__fadd2_rn(tt, make_float2(-dd.x, -dd.y)), make_float2(-khi, -khi));  // t - d exact
   } else {
-    z = make_float2(diff_ref<T>(tt.x, dd.x, Cf), diff_ref<T>(tt.y, dd.y, Cf));
+    z = make_float2(diff_ref<T>(tt.x, dd.x, khi), diff_ref<T>(tt.y, dd.y, khi));
   }
-  z = __fadd2_rn(__fadd2_rn(z, LH), LL);
+  z = __fadd2_rn(z, make_float2(-klo, -klo));
   float2 pz = __ffma2_rn(K7, z, K6);
   pz = __ffma2_rn(pz, z, K5);
   pz = __ffma2_rn(pz, z, K4);
@@ -300,9 +299,12 @@ __device__ __forceinline__ float2 resid_pair_exact(float2 tt, float2 dd, float2 
   const float2 sm = __fmul2_rn(z, __ffma2_rn(make_float2(-z.x, -z.y), pz, ONE));  // z (1 - z h(-z))
   const float2 xz = __fmul2_rn(z, nL2);
   const float2 bg = __fadd2_rn(ONE, make_float2(-fast_exp2(xz.x), -fast_exp2(xz.y)));  // 1 - e^-z
-  const float2 om = make_float2(z.x < 1.f ? sm.x : bg.x, z.y < 1.f ? sm.y : bg.y);
+  // 1 - e^-z <= 0 for z <= 0 in both forms (the polynomial only on |z| < 1),
+  // so max(0, .) zeroes exactly the tokens with p_v <= q_v (fmaxf drops the NaN
+  // of padding, 0 * -inf)
+  const float2 om = make_float2(fabsf(z.x) < 1.f ? sm.x : bg.x, fabsf(z.y) < 1.f ? sm.y : bg.y);
   const float2 r = __fmul2_rn(ev, om);
-  return make_float2((z.x > 0.f && ev.x > 0.f) ? r.x : 0.f, (z.y > 0.f && ev.y > 0.f) ? r.y : 0.f);
+  return make_float2(fmaxf(r.x, 0.f), fmaxf(r.y, 0.f));
 }
 
 // lane max of t over one vector (NaN-propagating)
@@ -320,8 +322,8 @@ __device__ __forceinline__ float vec_tmax(const uint4& t, float m) {
 // Per-slice constants of the draw weights.
 struct DrawRef {
   bool resid;
-  float M, Cf, lhi, llo;  // residual: row reference, lam = lhi + llo
-  float m;                // bonus: the slice's warp max of t (reference)
+  float M, khi, klo;  // residual: row reference M, C - lam = khi + klo
+  float m;            // bonus: the slice's warp max of t (reference)
 };
 
 // Slice constants; for the bonus row the warp-wide max of t over the slice.
@@ -330,9 +332,9 @@ __device__ __forceinline__ DrawRef draw_ref(const uint4 (&rt)[NV], bool resid, f
   DrawRef R;
   R.resid = resid;
   R.M = M;
-  R.Cf = Cf;
-  R.lhi = (float)lam;
-  R.llo = (float)(lam - (double)R.lhi);
+  const double K = (double)Cf - lam;
+  R.khi = (float)K;
+  R.klo = (float)(K - (double)R.khi);
   R.m = 0.f;
   if (!resid) {
     float m = -INFINITY;
@@ -364,7 +366,7 @@ __device__ __forceinline__ void vec_weights(const uint4& t4, const uint4& d4, co
     const float2 nML2 = make_float2(-ML2, -ML2);
 #pragma unroll
     for (int h = 0; h < VEC; h += 2) {
-      const float2 r = resid_pair_exact<T>(pair_of<T>(rt, h), pair_of<T>(rd, h), nML2, R.Cf, R.lhi, R.llo);
+      const float2 r = resid_pair_exact<T>(pair_of<T>(rt, h), pair_of<T>(rd, h), nML2, R.khi, R.klo);
       w[h] = r.x;
       w[h + 1] = r.y;
     }
