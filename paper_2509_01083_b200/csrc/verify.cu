@@ -400,16 +400,7 @@ __device__ __forceinline__ void vec_accum(const uint4& t, const uint4& d, const 
     w[h] = diff2<T>(tt[h], pair_of<T>(rd, 2 * h), R.Cw);
     am = fmaxf(am, fmaxf(fabsf(w[h].x), fabsf(w[h].y)));
   }
-#ifndef DSDE_WIDE_R
-#define DSDE_WIDE_R 2
-#endif
-#if DSDE_WIDE_R == 2
   constexpr float kWideR = 2.f;
-#elif DSDE_WIDE_R == 25
-  constexpr float kWideR = 2.5f;
-#else
-  constexpr float kWideR = 3.f;
-#endif
   if (__all_sync(kFull, am < kWideR)) {
     const float2 L2 = make_float2(kLog2e, kLog2e);
 #pragma unroll
@@ -417,9 +408,8 @@ __device__ __forceinline__ void vec_accum(const uint4& t, const uint4& d, const 
       const float2 xt = __ffma2_rn(tt[h], L2, R.nML2);
       const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
       const float2 ww = w[h];
-      // h(-w) in powers of w (odd coefficients negated), Chebyshev fits of
-      // tools/fit_g.py: deg 8 on |u|<=2 (3.3e-7), deg 9 on 2.5 (3.3e-7), deg 10 on 3 (4.0e-7)
-#if DSDE_WIDE_R == 2
+      // h(-w) in powers of w (odd coefficients negated): the degree-8 Chebyshev
+      // fit on |u| <= 2 (tools/fit_g.py --deg 8 --range 2, 3.3e-7 relative)
       float2 pp = __ffma2_rn(make_float2(2.972247159505059e-07f, 2.972247159505059e-07f), ww,
                              make_float2(-2.990256007251446e-06f, -2.990256007251446e-06f));
       pp = __ffma2_rn(pp, ww, make_float2(2.47248935920652e-05f, 2.47248935920652e-05f));
@@ -429,30 +419,6 @@ __device__ __forceinline__ void vec_accum(const uint4& t, const uint4& d, const 
       pp = __ffma2_rn(pp, ww, make_float2(4.166661202907562e-02f, 4.166661202907562e-02f));
       pp = __ffma2_rn(pp, ww, make_float2(-1.666664332151413e-01f, -1.666664332151413e-01f));
       pp = __ffma2_rn(pp, ww, make_float2(0.5f, 0.5f));
-#elif DSDE_WIDE_R == 25
-      float2 pp = __ffma2_rn(make_float2(-2.79628800115006e-08f, -2.79628800115006e-08f), ww,
-                             make_float2(3.10109527390523e-07f, 3.10109527390523e-07f));
-      pp = __ffma2_rn(pp, ww, make_float2(-2.73722048405034e-06f, -2.73722048405034e-06f));
-      pp = __ffma2_rn(pp, ww, make_float2(2.4609160391264595e-05f, 2.4609160391264595e-05f));
-      pp = __ffma2_rn(pp, ww, make_float2(-1.9846374925691634e-04f, -1.9846374925691634e-04f));
-      pp = __ffma2_rn(pp, ww, make_float2(1.3893224531784654e-03f, 1.3893224531784654e-03f));
-      pp = __ffma2_rn(pp, ww, make_float2(-8.333276025950909e-03f, -8.333276025950909e-03f));
-      pp = __ffma2_rn(pp, ww, make_float2(4.166632518172264e-02f, 4.166632518172264e-02f));
-      pp = __ffma2_rn(pp, ww, make_float2(-1.666666865348816e-01f, -1.666666865348816e-01f));
-      pp = __ffma2_rn(pp, ww, make_float2(0.5000000596046448f, 0.5000000596046448f));
-#else
-      float2 pp = __ffma2_rn(make_float2(2.4204336313005115e-09f, 2.4204336313005115e-09f), ww,
-                             make_float2(-2.934377540952937e-08f, -2.934377540952937e-08f));
-      pp = __ffma2_rn(pp, ww, make_float2(2.721244527492672e-07f, 2.721244527492672e-07f));
-      pp = __ffma2_rn(pp, ww, make_float2(-2.7161327125213575e-06f, -2.7161327125213575e-06f));
-      pp = __ffma2_rn(pp, ww, make_float2(2.4817869416438043e-05f, 2.4817869416438043e-05f));
-      pp = __ffma2_rn(pp, ww, make_float2(-1.9857056031469256e-04f, -1.9857056031469256e-04f));
-      pp = __ffma2_rn(pp, ww, make_float2(1.3888543471693993e-03f, 1.3888543471693993e-03f));
-      pp = __ffma2_rn(pp, ww, make_float2(-8.333077654242516e-03f, -8.333077654242516e-03f));
-      pp = __ffma2_rn(pp, ww, make_float2(4.166669398546219e-02f, 4.166669398546219e-02f));
-      pp = __ffma2_rn(pp, ww, make_float2(-1.6666677594184875e-01f, -1.6666677594184875e-01f));
-      pp = __ffma2_rn(pp, ww, make_float2(0.5f, 0.5f));
-#endif
       const float2 ew = __fmul2_rn(e, ww);
       S2 = __fadd2_rn(S2, e);
       A2 = __fadd2_rn(A2, ew);
@@ -460,13 +426,8 @@ __device__ __forceinline__ void vec_accum(const uint4& t, const uint4& d, const 
     }
     return;
   }
-#ifdef DSDE_WIDE_RECOMPUTE
-#pragma unroll
-  for (int h = 0; h < Traits<T>::VEC; h += 2) pair_accum<T>(pair_of<T>(rt, h), pair_of<T>(rd, h), R, S2, A2, D2);
-#else
 #pragma unroll
   for (int h = 0; h < P; ++h) pair_accum_w<T>(tt[h], pair_of<T>(rd, 2 * h), w[h], R, S2, A2, D2);
-#endif
 #else
 #pragma unroll
   for (int h = 0; h < Traits<T>::VEC; h += 2) pair_accum<T>(pair_of<T>(rt, h), pair_of<T>(rd, h), R, S2, A2, D2);
@@ -564,22 +525,9 @@ constexpr int kLdgThreads = 256;
 #ifndef DSDE_LDG_MINB
 #define DSDE_LDG_MINB 3
 #endif
-#ifndef DSDE_LDG_PREFETCH
-#define DSDE_LDG_PREFETCH 0
-#endif
 #ifndef DSDE_EXPERIMENT
 #define DSDE_EXPERIMENT 0
 #endif
-
-template <typename T>
-__device__ __forceinline__ void stream_unit_load(const StreamArgs& a, long long q, int& seq,
-                                                 uint4 (&rt)[Traits<T>::NV], uint4 (&rd)[Traits<T>::NV]) {
-  const int r = (int)((unsigned)q / (unsigned)a.nsub);  // units < 2^31 (checked by dsde_verify)
-  const int u = (int)q - r * a.nsub;
-  seq = seq_of_row(a.cu_sl, a.B, seq, r);
-  load_slice<T>(reinterpret_cast<const T*>(a.tl) + (long long)(r + seq) * a.ld_t, a.V, u, rt);
-  load_slice<T>(reinterpret_cast<const T*>(a.dl) + (long long)r * a.ld_d, a.V, u, rd);
-}
 
 template <typename T>
 __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(StreamArgs a) {
@@ -592,7 +540,6 @@ __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(Strea
   asm volatile("griddepcontrol.launch_dependents;");
   if (q >= n_units) return;
   int seq = 0;
-#if !DSDE_LDG_PREFETCH
   // (row r, slice u) of unit q advanced incrementally by W units per step
   int r = (int)((unsigned)q / (unsigned)a.nsub), u = (int)q - r * a.nsub;
   const int dr = (int)((unsigned long long)W / (unsigned)a.nsub), du = (int)(W - (long long)dr * a.nsub);
@@ -627,21 +574,6 @@ __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(Strea
       u -= a.nsub;
       ++r;
     }
-  }
-  return;
-#endif
-  uint4 at[NV], ad[NV], bt[NV], bd[NV];
-  stream_unit_load<T>(a, q, seq, at, ad);
-  while (true) {
-    const long long qb = q + W;
-    if (qb < n_units) stream_unit_load<T>(a, qb, seq, bt, bd);
-    store_partial(a.part + q, slice_stats<T>(at, ad));
-    if (qb >= n_units) return;
-    const long long qa = qb + W;
-    if (qa < n_units) stream_unit_load<T>(a, qa, seq, at, ad);
-    store_partial(a.part + qb, slice_stats<T>(bt, bd));
-    if (qa >= n_units) return;
-    q = qa;
   }
 }
 

@@ -537,26 +537,10 @@ __global__ void __launch_bounds__(kLdgThreads, DSDE_DRAW_MINB) k_draw_ldg(DrawAr
   const long long W = (long long)gridDim.x * (kLdgThreads / 32);
   long long q = (long long)blockIdx.x * (kLdgThreads / 32) + (threadIdx.x >> 5);
   if (q >= n_units) return;
-#if !DSDE_LDG_PREFETCH
   for (; q < n_units; q += W) {
     uint4 rt[NV], rd[NV];
     const DrawUnit d = draw_unit_load<T>(a, q, rt, rd);
     draw_unit_finish<T>(a, q, d, rt, rd);
-  }
-  return;
-#endif
-  uint4 at[NV], ad[NV], bt[NV], bd[NV];
-  DrawUnit da = draw_unit_load<T>(a, q, at, ad), db;
-  while (true) {
-    const long long qb = q + W;
-    if (qb < n_units) db = draw_unit_load<T>(a, qb, bt, bd);
-    draw_unit_finish<T>(a, q, da, at, ad);
-    if (qb >= n_units) return;
-    const long long qa = qb + W;
-    if (qa < n_units) da = draw_unit_load<T>(a, qa, at, ad);
-    draw_unit_finish<T>(a, qb, db, bt, bd);
-    if (qa >= n_units) return;
-    q = qa;
   }
 }
 
