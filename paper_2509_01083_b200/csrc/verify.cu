@@ -1041,3 +1041,13 @@ extern "C" dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, 
   if (rs != DSDE_OK) return rs;
   return e == cudaSuccess ? DSDE_OK : DSDE_ERR_CUDA;
 }
+
+#if DSDE_TAIL_TRACE
+// measurement build only: copy n CTA records (6 u64 each: after the PDL wait,
+// after finalize, after the draw, after the select, -, smid << 8 | mode)
+extern "C" int dsde_debug_tail_trace(unsigned long long* host, int n) {
+  n = n < dsde::kTraceMax ? n : dsde::kTraceMax;
+  return cudaMemcpyFromSymbol(host, dsde::g_tail_trace, sizeof(unsigned long long) * 6 * n) == cudaSuccess ? 0 : -1;
+}
+#endif
+

@@ -326,6 +326,33 @@ struct DrawRef {
   float m;            // bonus: the slice's warp max of t (reference)
 };
 
+// Warp-wide max of t over a lane's NV vectors (NaN-propagating; packed
+// max.NaN.bf16x2 for bf16: max is exact, so any grouping gives the same value).
+template <typename T, int NV>
+__device__ __forceinline__ float slice_tmax(const uint4 (&rt)[NV]) {
+  float m;
+  if constexpr (sizeof(T) == 2) {
+    __nv_bfloat162 b0 = __floats2bfloat162_rn(-INFINITY, -INFINITY), b1 = b0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const uint32_t w4[4] = {rt[v].x, rt[v].y, rt[v].z, rt[v].w};
+      b0 = __hmax2_nan(b0, *reinterpret_cast<const __nv_bfloat162*>(&w4[0]));
+      b1 = __hmax2_nan(b1, *reinterpret_cast<const __nv_bfloat162*>(&w4[1]));
+      b0 = __hmax2_nan(b0, *reinterpret_cast<const __nv_bfloat162*>(&w4[2]));
+      b1 = __hmax2_nan(b1, *reinterpret_cast<const __nv_bfloat162*>(&w4[3]));
+    }
+    const __nv_bfloat162 b = __hmax2_nan(b0, b1);
+    m = max_nan(__low2float(b), __high2float(b));
+  } else {
+    m = -INFINITY;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) m = vec_tmax<T>(rt[v], m);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(kFull, m, o));
+  return m;
+}
+
 // Slice constants; for the bonus row the warp-wide max of t over the slice.
 template <typename T, int NV>
 __device__ __forceinline__ DrawRef draw_ref(const uint4 (&rt)[NV], bool resid, float M, float Cf, double lam) {
@@ -335,22 +362,7 @@ __device__ __forceinline__ DrawRef draw_ref(const uint4 (&rt)[NV], bool resid, f
   const double K = (double)Cf - lam;
   R.khi = (float)K;
   R.klo = (float)(K - (double)R.khi);
-  R.m = 0.f;
-  if (!resid) {
-    float m = -INFINITY;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const uint4 x[1] = {rt[v]};
-#pragma unroll
-      for (int h = 0; h < Traits<T>::VEC; h += 2) {
-        const float2 tt = pair_of<T>(x, h);
-        m = max_nan(m, max_nan(tt.x, tt.y));
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(kFull, m, o));
-    R.m = m;
-  }
+  R.m = resid ? 0.f : slice_tmax<T, NV>(rt);
   return R;
 }
 
@@ -372,13 +384,18 @@ __device__ __forceinline__ void vec_weights(const uint4& t4, const uint4& d4, co
     }
     return;
   }
+  if (R.m <= -1e30f) {  // an all-padding slice (warp-uniform)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) w[e] = 0.f;
+    return;
+  }
   const float mL2 = R.m * kLog2e;
   const float2 nmL2 = make_float2(-mL2, -mL2);
 #pragma unroll
   for (int h = 0; h < VEC; h += 2) {
     const float2 x = __ffma2_rn(pair_of<T>(rt, h), L2, nmL2);
-    w[h] = R.m <= -1e30f ? 0.f : fast_exp2(x.x);
-    w[h + 1] = R.m <= -1e30f ? 0.f : fast_exp2(x.y);
+    w[h] = fast_exp2(x.x);
+    w[h + 1] = fast_exp2(x.y);
   }
 }
 
@@ -416,6 +433,41 @@ __device__ __forceinline__ double wscan_d(double x, int lane) {
   return x;
 }
 
+// sum_v (sum over the 32 lanes of x[v]) in vector order, valid in lane 0: the
+// NV per-vector warp sums by recursive halving (the first log2(NV) butterfly
+// rounds exchange half of the remaining vectors, so each round moves one
+// double per kept vector instead of one per vector), lanes 8 j .. hold vector
+// j's total (NV = 4), then lane 0 gathers them.
+template <int NV>
+__device__ __forceinline__ double warp_sum_vectors(double (&x)[NV]) {
+  static_assert(NV == 1 || NV == 2 || NV == 4 || NV == 8, "NV");
+  const int lane = threadIdx.x & 31;
+  int o = 16;
+#pragma unroll
+  for (int cnt = NV; cnt > 1; cnt >>= 1, o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int j = 0; j < cnt / 2; ++j) {
+      const double send = up ? x[j] : x[j + cnt / 2];
+      const double keep = up ? x[j + cnt / 2] : x[j];
+      x[j] = keep + __shfl_xor_sync(kFull, send, o);
+    }
+  }
+#pragma unroll
+  for (; o > 0; o >>= 1) x[0] += __shfl_xor_sync(kFull, x[0], o);
+  // vector index of lane l's total: bit (log2 NV - 1 - b) of it is bit (4 - b) of l
+  double m = 0.0;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    int src = 0;
+#pragma unroll
+    for (int b = 0, n = NV; n > 1; ++b, n >>= 1)
+      if (v & (n >> 1)) src |= 16 >> b;
+    m += __shfl_sync(kFull, x[0], src);
+  }
+  return m;
+}
+
 // ---------------------------------------------------------------------------
 // a4 first pass: units q = (sequence i, slice u), q = i * nsub + u. Each warp
 // writes the mass of its slice's draw weights and the slice reference.
@@ -438,9 +490,8 @@ struct DrawUnit {
 };
 
 template <typename T>
-__device__ __forceinline__ DrawUnit draw_unit_load(const DrawArgs& a, long long q, const SeqRec& r,
+__device__ __forceinline__ DrawUnit draw_unit_load(const DrawArgs& a, int u, const SeqRec& r,
                                                    uint4 (&rt)[Traits<T>::NVD], uint4 (&rd)[Traits<T>::NVD]) {
-  const int i = (int)(q / a.nsub), u = (int)(q - (long long)i * a.nsub);
   const int mode = r.mode;
   DrawUnit d;
   d.type = mode == MODE_RESIDUAL ? IT_RESID : mode == MODE_BONUS ? IT_BONUS : mode == MODE_ARGMAX ? IT_ARGMAX : IT_NONE;
@@ -471,7 +522,7 @@ __device__ __forceinline__ DrawUnit draw_unit_load(const DrawArgs& a, long long 
     r.C = __ldg(&rp->C);
     r.lam = __ldg(&rp->lam);
   }
-  return draw_unit_load<T>(a, q, r, rt, rd);
+  return draw_unit_load<T>(a, (int)(q - (q / a.nsub) * a.nsub), r, rt, rd);
 }
 
 template <typename T>
@@ -483,11 +534,7 @@ __device__ __forceinline__ void draw_unit_finish(const DrawArgs& a, long long q,
   if (d.type == IT_ARGMAX) {
     // greedy bonus row: the slice max of t and its first (slice-local) index
     const int lane = threadIdx.x & 31;
-    float m = -INFINITY;
-#pragma unroll
-    for (int v = 0; v < NVD; ++v) m = vec_tmax<T>(rt[v], m);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(kFull, m, o));
+    const float m = slice_tmax<T, NVD>(rt);
     int best = 0x7fffffff;
 #pragma unroll
     for (int v = NVD - 1; v >= 0; --v) {
@@ -508,8 +555,9 @@ __device__ __forceinline__ void draw_unit_finish(const DrawArgs& a, long long q,
     return;
   }
   const DrawRef R = draw_ref<T>(rt, d.type == IT_RESID, d.M, d.Cf, d.lam);
-  // mass in the select pass's order: per vector an fp32 lane sum, then an fp64 warp sum
-  double m = 0.0;
+  // mass in the select pass's grouping: per vector an fp32 lane sum, an fp64
+  // sum over the 32 lanes, the vectors added in order
+  double x[NVD];
 #pragma unroll
   for (int v = 0; v < NVD; ++v) {
     float w[VEC];
@@ -517,8 +565,9 @@ __device__ __forceinline__ void draw_unit_finish(const DrawArgs& a, long long q,
     float ls = 0.f;
 #pragma unroll
     for (int e = 0; e < VEC; ++e) ls += w[e];
-    m += wsum_d((double)ls);
+    x[v] = (double)ls;
   }
+  const double m = warp_sum_vectors<NVD>(x);
   if ((threadIdx.x & 31) == 0) {
     a.smass[q] = m;
     a.sref[q] = R.resid ? R.M : (R.m <= -1e30f ? -INFINITY : R.m);
@@ -754,6 +803,27 @@ struct StepExtra {
   unsigned* counter;
 };
 
+#ifndef DSDE_TAIL_TRACE
+#define DSDE_TAIL_TRACE 0
+#endif
+#if DSDE_TAIL_TRACE
+// measurement build only (-DDSDE_TAIL_TRACE=1): per-CTA globaltimer stamps at
+// the phase boundaries of k_tail, read back by dsde_debug_tail_trace
+constexpr int kTraceMax = 4096;
+__device__ unsigned long long g_tail_trace[kTraceMax * 6];
+__device__ __forceinline__ void tail_stamp(int slot, unsigned long long v) {
+  if (threadIdx.x == 0 && blockIdx.x < kTraceMax) g_tail_trace[blockIdx.x * 6 + slot] = v;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TAIL_STAMP(slot) tail_stamp(slot, gtimer())
+#else
+#define TAIL_STAMP(slot)
+#endif
+
 template <typename T, bool STEP, int NW>
 __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(FinArgs fa, DrawArgs da, SelArgs sa,
                                                                    StepExtra sx) {
@@ -766,10 +836,17 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(FinArgs fa, 
   // kernel has finished; wait for its completion (and memory) here
   asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
+  TAIL_STAMP(0);
   finalize_seq<T>(fa, i, &s_rec);
   __syncthreads();
+  TAIL_STAMP(1);
   const SeqRec r = s_rec;
   const bool draw = r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS || r.mode == MODE_ARGMAX;
+#if DSDE_TAIL_TRACE
+  unsigned smid;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+  tail_stamp(5, ((unsigned long long)smid << 8) | (unsigned)r.mode);
+#endif
   if (STEP && warp == NW - 1) {
     signal_seq(sx.sig, i);
     if (sx.fuse_cap) {
@@ -791,10 +868,12 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(FinArgs fa, 
     const long long q0 = (long long)i * da.nsub;
     for (int u = warp; u < da.nsub; u += NW) {
       uint4 rt[NVD], rd[NVD];
-      const DrawUnit d = draw_unit_load<T>(da, q0 + u, r, rt, rd);
+      const DrawUnit d = draw_unit_load<T>(da, u, r, rt, rd);
       draw_unit_finish<T>(da, q0 + u, d, rt, rd);
     }
   }
   __syncthreads();
+  TAIL_STAMP(2);
   if (draw && warp == 0) select_seq<T>(sa, i, r);
+  TAIL_STAMP(3);
 }

@@ -391,7 +391,7 @@ __device__ __noinline__ void draw_unit_fused(const FusedArgs& a, long long c, in
     DrawArgs da{a.B, a.V, a.nd, a.tl, a.ld_t, a.dl, a.ld_d, a.rec, a.smass, a.sref};
     const long long q = (long long)i * a.nd + u;
     uint4 rt[NVD], rd[NVD];
-    const DrawUnit d = draw_unit_load<T>(da, q, r, rt, rd);
+    const DrawUnit d = draw_unit_load<T>(da, (int)u, r, rt, rd);
     draw_unit_finish<T>(da, q, d, rt, rd);
   }
   __syncwarp();
