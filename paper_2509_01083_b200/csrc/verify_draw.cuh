@@ -525,8 +525,10 @@ __device__ __forceinline__ DrawUnit draw_unit_load(const DrawArgs& a, long long 
   return draw_unit_load<T>(a, (int)(q - (q / a.nsub) * a.nsub), r, rt, rd);
 }
 
+// mass_out / ref_out: this unit's record (global a.smass + q, or the k_tail
+// CTA's shared arrays)
 template <typename T>
-__device__ __forceinline__ void draw_unit_finish(const DrawArgs& a, long long q, const DrawUnit& d,
+__device__ __forceinline__ void draw_unit_finish(double* mass_out, float* ref_out, const DrawUnit& d,
                                                  const uint4 (&rt)[Traits<T>::NVD],
                                                  const uint4 (&rd)[Traits<T>::NVD]) {
   constexpr int VEC = Traits<T>::VEC, NVD = Traits<T>::NVD;
@@ -549,8 +551,8 @@ __device__ __forceinline__ void draw_unit_finish(const DrawArgs& a, long long q,
     }
     best = (int)__reduce_min_sync(kFull, (unsigned)best);
     if (lane == 0) {
-      a.smass[q] = (double)best;
-      a.sref[q] = m;
+      *mass_out = (double)best;
+      *ref_out = m;
     }
     return;
   }
@@ -569,8 +571,8 @@ __device__ __forceinline__ void draw_unit_finish(const DrawArgs& a, long long q,
   }
   const double m = warp_sum_vectors<NVD>(x);
   if ((threadIdx.x & 31) == 0) {
-    a.smass[q] = m;
-    a.sref[q] = R.resid ? R.M : (R.m <= -1e30f ? -INFINITY : R.m);
+    *mass_out = m;
+    *ref_out = R.resid ? R.M : (R.m <= -1e30f ? -INFINITY : R.m);
   }
 }
 
@@ -589,7 +591,7 @@ __global__ void __launch_bounds__(kLdgThreads, DSDE_DRAW_MINB) k_draw_ldg(DrawAr
   for (; q < n_units; q += W) {
     uint4 rt[NV], rd[NV];
     const DrawUnit d = draw_unit_load<T>(a, q, rt, rd);
-    draw_unit_finish<T>(a, q, d, rt, rd);
+    draw_unit_finish<T>(a.smass + q, a.sref + q, d, rt, rd);
   }
 }
 
@@ -610,22 +612,63 @@ struct SelArgs {
   int32_t* err;
 };
 
+#ifndef DSDE_TAIL_TRACE
+#define DSDE_TAIL_TRACE 0
+#endif
+#if DSDE_TAIL_TRACE
+// measurement build only (-DDSDE_TAIL_TRACE=1): per-CTA globaltimer stamps at
+// the phase boundaries of k_tail, read back by dsde_debug_tail_trace
+constexpr int kTraceMax = 4096;
+__device__ unsigned long long g_tail_trace[kTraceMax * 6];
+__device__ __forceinline__ void tail_stamp(int slot, unsigned long long v) {
+  if (threadIdx.x == 0 && blockIdx.x < kTraceMax) g_tail_trace[blockIdx.x * 6 + slot] = v;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TAIL_STAMP(slot) tail_stamp(slot, gtimer())
+#else
+#define TAIL_STAMP(slot)
+#endif
+
+// Where select_seq reads the slice records from: global memory written by
+// another kernel / CTA (masses about each slice's own reference, rescaled
+// here), or the k_tail CTA's shared arrays with the bonus masses already
+// rescaled to the row reference by the whole CTA (scale[] = the factors).
+struct SelSrcGlobal {
+  static constexpr bool kPrescaled = false;
+  const double* m;
+  const float* r;
+  __device__ __forceinline__ double mass(int s) const { return __ldcg(m + s); }
+  __device__ __forceinline__ float ref(int s) const { return __ldcg(r + s); }
+  __device__ __forceinline__ double scale(int) const { return 1.0; }
+};
+struct SelSrcSmem {
+  static constexpr bool kPrescaled = true;
+  const double* m;
+  const float* r;
+  const double* sc;
+  __device__ __forceinline__ double mass(int s) const { return m[s]; }
+  __device__ __forceinline__ float ref(int s) const { return r[s]; }
+  __device__ __forceinline__ double scale(int s) const { return sc[s]; }
+};
+
 // One warp: the inverse-CDF select of sequence i from its slice masses.
-template <typename T>
-__device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec& r) {
+template <typename T, typename Src>
+__device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec& r, const Src& src) {
   constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NVD, SUB = 32 * VEC * NV;
   const int lane = threadIdx.x & 31;
   if (r.mode == MODE_ARGMAX) {
     // greedy bonus token: the smallest index among the slices holding the row max
-    const float* wref = a.sref + (long long)i * a.nsub;
-    const double* wmass = a.smass + (long long)i * a.nsub;
     float Mg = -INFINITY;
-    for (int s0 = lane; s0 < a.nsub; s0 += 32) Mg = max_nan(Mg, __ldcg(wref + s0));
+    for (int s0 = lane; s0 < a.nsub; s0 += 32) Mg = max_nan(Mg, src.ref(s0));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) Mg = max_nan(Mg, __shfl_xor_sync(kFull, Mg, o));
     unsigned cand = 0x7fffffffu;
     for (int s0 = lane; s0 < a.nsub; s0 += 32)
-      if (__ldcg(wref + s0) == Mg) cand = min(cand, (unsigned)(s0 * SUB + (int)__ldcg(wmass + s0)));
+      if (src.ref(s0) == Mg) cand = min(cand, (unsigned)(s0 * SUB + (int)src.mass(s0)));
     cand = __reduce_min_sync(kFull, cand);
     if (lane == 0) {
       if (Mg != Mg || cand >= (unsigned)a.V) {
@@ -640,21 +683,27 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   if (r.mode != MODE_RESIDUAL && r.mode != MODE_BONUS) return;
   const bool resid = r.mode == MODE_RESIDUAL;
   const int nsub = a.nsub;
-  const double* wmass = a.smass + (long long)i * nsub;
-  const float* wref = a.sref + (long long)i * nsub;
   float Mg = -INFINITY;
-  if (!resid) {
-    for (int s0 = lane; s0 < nsub; s0 += 32) Mg = max_nan(Mg, __ldcg(wref + s0));
+  if (!resid && !Src::kPrescaled) {
+    for (int s0 = lane; s0 < nsub; s0 += 32) Mg = max_nan(Mg, src.ref(s0));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) Mg = max_nan(Mg, __shfl_xor_sync(kFull, Mg, o));
   }
   auto scale_of = [&](int s0) -> double {  // sub-chunk mass scale to the common reference
     if (resid) return 1.0;
-    const float ms = __ldcg(wref + s0);
-    return ms == -INFINITY ? 0.0 : exp((double)ms - (double)Mg);
+    if constexpr (Src::kPrescaled) {
+      return src.scale(s0);
+    } else {
+      const float ms = src.ref(s0);
+      return ms == -INFINITY ? 0.0 : exp((double)ms - (double)Mg);
+    }
+  };
+  auto mass_of = [&](int s0) -> double {  // scale_of(s0) * the slice's own mass
+    if constexpr (Src::kPrescaled) return src.mass(s0);
+    else return scale_of(s0) * src.mass(s0);
   };
   double R = 0.0;
-  for (int s0 = lane; s0 < nsub; s0 += 32) R += scale_of(s0) * __ldcg(wmass + s0);
+  for (int s0 = lane; s0 < nsub; s0 += 32) R += mass_of(s0);
   R = wsum_d(R);
   uint8_t fl = 0;
   const T* tp = reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t;
@@ -689,7 +738,7 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   double base = 0.0, base_last = 0.0, cum = 0.0;
   for (int g = 0; g < nsub; g += 32) {
     const int s0 = g + lane;
-    const double ms = s0 < nsub ? scale_of(s0) * __ldcg(wmass + s0) : 0.0;
+    const double ms = s0 < nsub ? mass_of(s0) : 0.0;
     const double incl = wscan_d(ms, lane);
     const unsigned pos = __ballot_sync(kFull, ms > 0.0);
     const unsigned cross = __ballot_sync(kFull, ms > 0.0 && cum + incl > target);
@@ -711,6 +760,7 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
     base = base_last;
     fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
   }
+  TAIL_STAMP(4);
   const double f = scale_of(us);
   uint4 rt[NV], rd[NV];
   load_sub_raw<T>(tp, a.V, us, rt);
@@ -783,7 +833,7 @@ __global__ void __launch_bounds__(128) k_select(SelArgs a) {
   const int i = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (i >= a.B) return;
   const SeqRec r = a.rec[i];
-  select_seq<T>(a, i, r);
+  select_seq<T>(a, i, r, SelSrcGlobal{a.smass + (long long)i * a.nsub, a.sref + (long long)i * a.nsub});
 }
 
 // ---------------------------------------------------------------------------
@@ -803,32 +853,18 @@ struct StepExtra {
   unsigned* counter;
 };
 
-#ifndef DSDE_TAIL_TRACE
-#define DSDE_TAIL_TRACE 0
-#endif
-#if DSDE_TAIL_TRACE
-// measurement build only (-DDSDE_TAIL_TRACE=1): per-CTA globaltimer stamps at
-// the phase boundaries of k_tail, read back by dsde_debug_tail_trace
-constexpr int kTraceMax = 4096;
-__device__ unsigned long long g_tail_trace[kTraceMax * 6];
-__device__ __forceinline__ void tail_stamp(int slot, unsigned long long v) {
-  if (threadIdx.x == 0 && blockIdx.x < kTraceMax) g_tail_trace[blockIdx.x * 6 + slot] = v;
-}
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define TAIL_STAMP(slot) tail_stamp(slot, gtimer())
-#else
-#define TAIL_STAMP(slot)
-#endif
+
+// draw slices per row whose records k_tail keeps in shared memory (V <= 262144
+// bf16 / 131072 fp32; larger vocabularies use the workspace)
+constexpr int kTailMaxSub = 256;
 
 template <typename T, bool STEP, int NW>
 __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(FinArgs fa, DrawArgs da, SelArgs sa,
                                                                    StepExtra sx) {
   constexpr int NVD = Traits<T>::NVD;
   __shared__ SeqRec s_rec;
+  __shared__ double s_mass[kTailMaxSub], s_scale[kTailMaxSub];
+  __shared__ float s_ref[kTailMaxSub];
   const int i = blockIdx.x;
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_rec.mode = MODE_NONE;
@@ -864,16 +900,47 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(FinArgs fa, 
       }
     }
   }
+  // slice records in shared memory when they fit (the select then reads no
+  // global memory but the crossing slice), else in the workspace
+  const bool smem = da.nsub <= kTailMaxSub;
+  const long long q0 = (long long)i * da.nsub;
   if (draw) {
-    const long long q0 = (long long)i * da.nsub;
     for (int u = warp; u < da.nsub; u += NW) {
       uint4 rt[NVD], rd[NVD];
       const DrawUnit d = draw_unit_load<T>(da, u, r, rt, rd);
-      draw_unit_finish<T>(da, q0 + u, d, rt, rd);
+      if (smem) draw_unit_finish<T>(s_mass + u, s_ref + u, d, rt, rd);
+      else draw_unit_finish<T>(da.smass + q0 + u, da.sref + q0 + u, d, rt, rd);
     }
   }
   __syncthreads();
   TAIL_STAMP(2);
-  if (draw && warp == 0) select_seq<T>(sa, i, r);
+  if (!draw) return;
+  if (!smem) {
+    if (warp == 0) select_seq<T>(sa, i, r, SelSrcGlobal{da.smass + q0, da.sref + q0});
+    TAIL_STAMP(3);
+    return;
+  }
+  if (r.mode == MODE_BONUS) {
+    // the whole CTA rescales the bonus slice masses to the row max Mg (one fp64
+    // exp per slice, in parallel), as select_seq would slice by slice
+    __shared__ float s_wmax[NW];
+    float mg = -INFINITY;
+    for (int u = threadIdx.x; u < da.nsub; u += NW * 32) mg = max_nan(mg, s_ref[u]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mg = max_nan(mg, __shfl_xor_sync(kFull, mg, o));
+    if ((threadIdx.x & 31) == 0) s_wmax[warp] = mg;
+    __syncthreads();
+    float Mg = s_wmax[0];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) Mg = max_nan(Mg, s_wmax[w]);
+    for (int u = threadIdx.x; u < da.nsub; u += NW * 32) {
+      const float ms = s_ref[u];
+      const double f = ms == -INFINITY ? 0.0 : exp((double)ms - (double)Mg);
+      s_scale[u] = f;
+      s_mass[u] = f * s_mass[u];
+    }
+    __syncthreads();
+  }
+  if (warp == 0) select_seq<T>(sa, i, r, SelSrcSmem{s_mass, s_ref, s_scale});
   TAIL_STAMP(3);
 }

@@ -392,7 +392,7 @@ __device__ __noinline__ void draw_unit_fused(const FusedArgs& a, long long c, in
     const long long q = (long long)i * a.nd + u;
     uint4 rt[NVD], rd[NVD];
     const DrawUnit d = draw_unit_load<T>(da, (int)u, r, rt, rd);
-    draw_unit_finish<T>(da, q, d, rt, rd);
+    draw_unit_finish<T>(da.smass + q, da.sref + q, d, rt, rd);
   }
   __syncwarp();
   int last = 0;
@@ -400,7 +400,7 @@ __device__ __noinline__ void draw_unit_fused(const FusedArgs& a, long long c, in
   if (__shfl_sync(kFull, last, 0) && draw) {
     fence_acquire();
     SelArgs sa{a.B, a.V, a.nd, a.tl, a.ld_t, a.dl, a.ld_d, a.rec, a.smass, a.sref, a.emitted, a.flags, a.err};
-    select_seq<T>(sa, i, r);
+    select_seq<T>(sa, i, r, SelSrcGlobal{sa.smass + (long long)i * sa.nsub, sa.sref + (long long)i * sa.nsub});
   }
 }
 

@@ -64,6 +64,7 @@ def _argmax_drafts(host, frac, seed):
 @pytest.mark.parametrize("V,dtype,kmax,B", [
     (32000, torch.float32, 4, 8), (32000, torch.bfloat16, 8, 64), (128256, torch.bfloat16, 8, 12),
     (50000, torch.bfloat16, 8, 9), (1003, torch.bfloat16, 3, 7), (8193, torch.float32, 16, 5),
+    (300007, torch.bfloat16, 3, 6),
     (2, torch.float32, 2, 16), (3, torch.bfloat16, 1, 16),
 ])
 def test_greedy_parity(m, gstate, V, dtype, kmax, B):

@@ -42,6 +42,8 @@ def _check(m, state, host, dtype, ld_pad=0, expect_ties_max=None):
     (32000, torch.bfloat16, 8, 64),       # config 2 shape
     (128256, torch.bfloat16, 8, 12),      # config 3-5 row shape (sampled batch)
     (50000, torch.bfloat16, 8, 9),        # ragged last chunk
+    (300007, torch.bfloat16, 3, 6),       # > 256 draw slices: k_tail keeps slice records in the workspace
+    (140000, torch.float32, 3, 5),        # the same for fp32 (> 256 slices of 512)
     (8193, torch.float32, 16, 5),         # one element past a chunk
     (1003, torch.bfloat16, 3, 7),         # V not a multiple of 8
     (2, torch.float32, 2, 16), (3, torch.bfloat16, 1, 16), (8, torch.bfloat16, 5, 16),

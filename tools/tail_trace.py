@@ -59,15 +59,16 @@ def main():
             fin = (t[sel, 1] - t[sel, 0]) / 1e3
             drw = (t[sel, 2] - t[sel, 1]) / 1e3
             slc = (t[sel, 3] - t[sel, 2]) / 1e3
+            srch = (t[sel, 4] - t[sel, 2]) / 1e3 if md in (1, 2) else slc * 0
             end = (t[sel, 3] - t0) / 1e3
             print(f"  {MODES.get(md, md):7s} n={sel.sum():4d} finalize {fin.mean():5.1f} (max {fin.max():5.1f})  "
                   f"draw {drw.mean():5.1f} (max {drw.max():5.1f})  select {slc.mean():5.1f} (max {slc.max():5.1f})  "
-                  f"end max {end.max():5.1f}")
+                  f"(search {srch.mean():4.1f})  end max {end.max():5.1f}")
         last = int(np.argmax(t[:, 3]))
         print(f"  last CTA {last} ({MODES.get(int(mode[last]))}, SM {sm[last]}, "
               f"{int(np.sum(sm == sm[last]))} CTAs on it): start {(t[last, 0] - t0) / 1e3:.1f} "
               f"fin {(t[last, 1] - t[last, 0]) / 1e3:.1f} draw {(t[last, 2] - t[last, 1]) / 1e3:.1f} "
-              f"sel {(t[last, 3] - t[last, 2]) / 1e3:.1f}")
+              f"sel {(t[last, 3] - t[last, 2]) / 1e3:.1f} (search {(t[last, 4] - t[last, 2]) / 1e3:.1f})")
 
 
 if __name__ == "__main__":
