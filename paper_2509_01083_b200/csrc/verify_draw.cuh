@@ -702,9 +702,14 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
     if constexpr (Src::kPrescaled) return src.mass(s0);
     else return scale_of(s0) * src.mass(s0);
   };
-  double R = 0.0;
-  for (int s0 = lane; s0 < nsub; s0 += 32) R += mass_of(s0);
-  R = wsum_d(R);
+  // lane l owns the contiguous slices [l c, (l + 1) c): its sum in slice order,
+  // one warp scan gives every lane's prefix and R (the scan's total)
+  const int cw = (nsub + 31) >> 5;
+  const int s_lo = min(lane * cw, nsub), s_hi = min(s_lo + cw, nsub);
+  double lsum = 0.0;
+  for (int s0 = s_lo; s0 < s_hi; ++s0) lsum += mass_of(s0);
+  const double lincl = wscan_d(lsum, lane);
+  const double R = __shfl_sync(kFull, lincl, 31);
   uint8_t fl = 0;
   const T* tp = reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t;
   if (!(R > 0.0) || !isfinite(R)) {
@@ -733,32 +738,42 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
     return;
   }
   const double target = r.u * R;
-  // crossing sub-chunk: first u with prefix(u) > target (fallback: last with mass)
-  int us = -1, ulast = -1;
-  double base = 0.0, base_last = 0.0, cum = 0.0;
-  for (int g = 0; g < nsub; g += 32) {
-    const int s0 = g + lane;
-    const double ms = s0 < nsub ? mass_of(s0) : 0.0;
-    const double incl = wscan_d(ms, lane);
-    const unsigned pos = __ballot_sync(kFull, ms > 0.0);
-    const unsigned cross = __ballot_sync(kFull, ms > 0.0 && cum + incl > target);
-    if (pos) {
-      const int lp = 31 - __clz(pos);
-      ulast = g + lp;
-      base_last = cum + __shfl_sync(kFull, incl - ms, lp);
+  // crossing sub-chunk: first u with prefix(u) > target (fallback: last with
+  // mass): the first lane whose span crosses, then that lane's slices in order
+  int us = -1;
+  double base = 0.0;
+  {
+    double lexcl = __shfl_up_sync(kFull, lincl, 1);
+    if (lane == 0) lexcl = 0.0;
+    const unsigned cross = __ballot_sync(kFull, lsum > 0.0 && lincl > target);
+    const unsigned pos = __ballot_sync(kFull, lsum > 0.0);
+    // the crossing lane, else (rounding corner) the last lane with mass
+    const int ln = cross ? __ffs(cross) - 1 : (pos ? 31 - __clz(pos) : 0);
+    int mine = -1, last = -1;
+    double mbase = 0.0, lbase = 0.0;
+    if (lane == ln) {
+      double cum = lexcl;
+      for (int s0 = s_lo; s0 < s_hi; ++s0) {
+        const double ms = mass_of(s0);
+        if (ms > 0.0) {
+          if (cross && cum + ms > target) {
+            mine = s0;
+            mbase = cum;
+            break;
+          }
+          last = s0;
+          lbase = cum;
+        }
+        cum += ms;
+      }
     }
-    if (cross) {
-      const int lc = __ffs(cross) - 1;
-      us = g + lc;
-      base = cum + __shfl_sync(kFull, incl - ms, lc);
-      break;
+    us = __shfl_sync(kFull, mine, ln);
+    base = __shfl_sync(kFull, mbase, ln);
+    if (us < 0) {
+      us = __shfl_sync(kFull, last, ln);
+      base = __shfl_sync(kFull, lbase, ln);
+      fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
     }
-    cum += __shfl_sync(kFull, incl, 31);
-  }
-  if (us < 0) {
-    us = ulast;
-    base = base_last;
-    fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
   }
   TAIL_STAMP(4);
   const double f = scale_of(us);
