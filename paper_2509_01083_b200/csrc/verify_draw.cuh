@@ -38,8 +38,42 @@ constexpr int kFinThreads = 32 * DSDE_MAX_SL;
 
 // One CTA (kFinThreads) per sequence i; the draw record goes to *out (global
 // or shared; written by one lane of warp 0, visible to the CTA after a barrier).
+// Warp 0's per-position inputs of the accept test (lane j = position j): the
+// Philox uniforms and the gathered t_x, d_x. They depend only on the step's
+// inputs, so k_tail gathers them before griddepcontrol.wait, while the stream
+// kernel still runs (the inputs were complete before the stream kernel began).
+struct FinPre {
+  Uniforms u;
+  float tx, dx;
+  int x;
+};
+
 template <typename T>
-__device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* out) {
+__device__ __forceinline__ FinPre fin_prefetch(const FinArgs& a, int i) {
+  const int lane = threadIdx.x & 31;
+  FinPre p;
+  p.u = Uniforms{0.0, 0.0};
+  p.tx = p.dx = 0.f;
+  p.x = -1;
+  const int c0 = __ldg(a.cu_sl + i), c1 = __ldg(a.cu_sl + i + 1);
+  const int k = c1 - c0;
+  if (!(c0 >= 0 && k >= 1 && k <= DSDE_MAX_SL && c1 <= a.total)) return p;  // finalize_seq reports it
+  const long long slot0 = (long long)c0 + i;
+  if (lane <= k) p.u = philox_uniforms(__ldg(a.seeds + slot0 + lane));
+  if (lane < k) {
+    const long long drow = (long long)c0 + lane;
+    p.x = __ldg(a.tokens + drow);
+    if (p.x >= 0 && p.x < a.V) {
+      p.tx = load_logit<T>(reinterpret_cast<const T*>(a.tl) + (drow + i) * a.ld_t + p.x);
+      p.dx = load_logit<T>(reinterpret_cast<const T*>(a.dl) + drow * a.ld_d + p.x);
+    }
+  }
+  return p;
+}
+
+// pre: warp 0's fin_prefetch results (k_tail), or nullptr to load them here.
+template <typename T>
+__device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* out, const FinPre* pre = nullptr) {
   __shared__ double s_kl[DSDE_MAX_SL], s_lam[DSDE_MAX_SL], s_C[DSDE_MAX_SL], s_S[DSDE_MAX_SL];
   __shared__ int s_amax[DSDE_MAX_SL];
   __shared__ float s_M[DSDE_MAX_SL];
@@ -157,16 +191,18 @@ __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* ou
   double lr = 0.0;
   bool acc = false, near = false, bad_tok = false, nonfin = false;
   Uniforms u = {0.0, 0.0};
-  if (lane <= k) u = philox_uniforms(__ldg(a.seeds + slot0 + lane));
+  if (pre) u = pre->u;
+  else if (lane <= k) u = philox_uniforms(__ldg(a.seeds + slot0 + lane));
   if (lane < k) {
     const long long drow = (long long)c0 + lane;
-    const int x = __ldg(a.tokens + drow);
+    const int x = pre ? pre->x : __ldg(a.tokens + drow);
     bad_tok = x < 0 || x >= a.V;
     nonfin = !s_fin[lane];
     if (!bad_tok) {
       const T* tp = reinterpret_cast<const T*>(a.tl) + (drow + i) * a.ld_t;
       const T* dp = reinterpret_cast<const T*>(a.dl) + drow * a.ld_d;
-      const double tx = (double)load_logit<T>(tp + x), dx = (double)load_logit<T>(dp + x);
+      const double tx = (double)(pre ? pre->tx : load_logit<T>(tp + x));
+      const double dx = (double)(pre ? pre->dx : load_logit<T>(dp + x));
       lr = (tx - dx) - s_C[lane] + s_lam[lane];
       nonfin |= !isfinite(lr);
     }
@@ -883,12 +919,14 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(FinArgs fa, 
   const int i = blockIdx.x;
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_rec.mode = MODE_NONE;
+  FinPre pre;
+  if (warp == 0) pre = fin_prefetch<T>(fa, i);
   // programmatic dependent launch: the CTA may be resident before the stream
   // kernel has finished; wait for its completion (and memory) here
   asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   TAIL_STAMP(0);
-  finalize_seq<T>(fa, i, &s_rec);
+  finalize_seq<T>(fa, i, &s_rec, &pre);
   __syncthreads();
   TAIL_STAMP(1);
   const SeqRec r = s_rec;
