@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define DSDE_ABI_VERSION 1
+#define DSDE_ABI_VERSION 2
 
 typedef enum {
     DSDE_OK = 0,
@@ -96,6 +96,13 @@ typedef struct {
                           x_j = argmax t_j, emit the target argmax (
                           ties -> smallest token id, D18). Read by dsde_verify / dsde_step
                           from the state; KLDs, signal and cap are unchanged. */
+    int device_rows;   /* 0 = total_draft_rows is exactly sum_i k_i (default). 1 = it is a row
+                          capacity >= sum_i k_i: the kernels read sum_i k_i = cu_sl[B] on the device,
+                          grids and workspace are sized for the capacity, and a sequence whose rows
+                          end beyond it is a DSDE_DERR_BAD_SL device error. Output arrays are sized
+                          for the capacity. The launch configuration of dsde_verify / dsde_step then
+                          no longer depends on the SLs, so one captured CUDA graph serves every SL
+                          pattern (the SLs are device data). */
 } dsde_config;
 
 typedef struct dsde_state_s* dsde_state; /* per-sequence KLD ring, calibration, SL_max, error word */

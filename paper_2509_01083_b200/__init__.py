@@ -51,7 +51,7 @@ class Config(C.Structure):
     _fields_ = [("delta", C.c_double), ("n_short", C.c_int), ("n_long", C.c_int),
                 ("sl_min", C.c_int), ("sl_ceiling", C.c_int), ("epsilon", C.c_double),
                 ("calib_steps", C.c_int), ("calib_sl", C.c_int), ("window_unit", C.c_int),
-                ("cap_mode", C.c_int), ("greedy", C.c_int)]
+                ("cap_mode", C.c_int), ("greedy", C.c_int), ("device_rows", C.c_int)]
 
     @classmethod
     def default(cls, **kw) -> "Config":

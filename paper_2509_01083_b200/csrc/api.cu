@@ -25,7 +25,8 @@ bool cfg_valid(const dsde_config& c) {
          c.n_long <= DSDE_MAX_WINDOW && c.sl_min >= 1 && c.sl_ceiling > c.sl_min &&
          c.sl_ceiling <= DSDE_MAX_SL && c.epsilon > 0.0 && c.calib_steps >= 0 &&
          c.calib_sl >= 1 && c.calib_sl <= c.sl_ceiling && (c.window_unit == 0 || c.window_unit == 1) &&
-         (c.cap_mode == 0 || c.cap_mode == 1) && (c.greedy == 0 || c.greedy == 1);
+         (c.cap_mode == 0 || c.cap_mode == 1) && (c.greedy == 0 || c.greedy == 1) &&
+         (c.device_rows == 0 || c.device_rows == 1);
 }
 
 __global__ void k_reset_slots(SeqState* seq, int max_seqs, const int32_t* slots, int n) {
@@ -97,6 +98,7 @@ void dsde_config_default(dsde_config* c) {
   c->window_unit = 0;
   c->cap_mode = 1;
   c->greedy = 0;
+  c->device_rows = 0;
 }
 
 const char* dsde_status_string(dsde_status s) {

@@ -511,9 +511,16 @@ struct StreamArgs {
   const void* dl;
   long long ld_d;
   const int32_t* cu_sl;
-  int B, V, nsub, total;
+  int B, V, nsub, total;  // total: Σk_i, or the row capacity when dev_rows
   SubPartial* part;
+  int dev_rows;           // dsde_config.device_rows: Σk_i = cu_sl[B] (<= total), read here
 };
+
+// rows this launch streams: the host's Σk_i, or (device_rows) cu_sl[B] clamped
+// to the capacity the grid and workspace were sized for
+__device__ __forceinline__ int stream_rows(const StreamArgs& a) {
+  return a.dev_rows ? min(max(__ldg(a.cu_sl + a.B), 0), a.total) : a.total;
+}
 
 // ---------------------------------------------------------------------------
 // a1, "ldg" variant: persistent warps over the units q = (draft row r, slice u),
@@ -529,10 +536,11 @@ constexpr int kLdgThreads = 256;
 #define DSDE_EXPERIMENT 0
 #endif
 
-template <typename T>
+template <typename T, bool DEV_ROWS>
 __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(StreamArgs a) {
   constexpr int NV = Traits<T>::NV;
-  const long long n_units = (long long)a.total * a.nsub;
+  const int total = DEV_ROWS ? stream_rows(a) : a.total;
+  const long long n_units = (long long)total * a.nsub;
   const long long W = (long long)gridDim.x * (kLdgThreads / 32);
   long long q = (long long)blockIdx.x * (kLdgThreads / 32) + (threadIdx.x >> 5);
   // let the tail kernel launch (programmatic dependent launch) and become
@@ -543,7 +551,7 @@ __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(Strea
   // (row r, slice u) of unit q advanced incrementally by W units per step
   int r = (int)((unsigned)q / (unsigned)a.nsub), u = (int)q - r * a.nsub;
   const int dr = (int)((unsigned long long)W / (unsigned)a.nsub), du = (int)(W - (long long)dr * a.nsub);
-  while (r < a.total) {
+  while (r < total) {
     uint4 rt[NV], rd[NV];
 #if DSDE_EXPERIMENT == 2  // measurement only: math without the loads
 #pragma unroll
@@ -672,7 +680,7 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaCtas) k_stream_tma(StreamArgs
   uint64_t* full = reinterpret_cast<uint64_t*>(sdesc + kTmaStages);
   uint64_t* consumed = full + kTmaStages;
   const int nc = a.nsub / kCWarps;
-  const long long n_items = (long long)a.total * nc;
+  const long long n_items = (long long)stream_rows(a) * nc;
   const int G = gridDim.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -803,7 +811,8 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
                           const void* tl, int64_t ld_t, const void* dl, int64_t ld_d,
                           const uint64_t* seeds, int32_t* acc_len, int32_t* emitted, float* kld,
                           uint8_t* flags, const VerifyWs& ws, int32_t* err, Profiler* prof,
-                          cudaStream_t s, const StepExtra* step = nullptr, int greedy = 0) {
+                          cudaStream_t s, const StepExtra* step = nullptr, int greedy = 0,
+                          int dev_rows = 0) {
   const bool pr = prof != nullptr && prof->on;
   auto mark = [&]() {
     if (pr) cudaEventRecord(prof->next(), s);
@@ -820,13 +829,14 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_stream_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem<T>());
-    g.ldg = resident_grid(k_stream_ldg<T>, kLdgThreads, 0, sms, 0);
+    g.ldg = resident_grid(k_stream_ldg<T, false>, kLdgThreads, 0, sms, 0);
     g.tma = resident_grid(k_stream_tma<T>, kTmaThreads, tma_smem<T>(), sms, kTmaCtas);
     g.draw = resident_grid(k_draw_ldg<T>, kLdgThreads, 0, sms, 0);
     g.sms = sms;
   }
   const int variant = stream_variant();
-  const int tv = greedy && tail_variant() == 2 ? 0 : tail_variant();  // the fused kernel has no T = 0 mode
+  // the fused kernel has no T = 0 mode and sizes its counters from the host total
+  const int tv = (greedy || dev_rows) && tail_variant() == 2 ? 0 : tail_variant();
   if (tv == 2) {
     static int fused_grid[64] = {0};
     int& fg = fused_grid[dev & 63];
@@ -887,19 +897,22 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   }
   mark();
   // a1: statistics of every (draft row, vocab slice)
-  StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, ns, total, ws.part};
+  StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, ns, total, ws.part, dev_rows};
   if (variant == 1) {
     const long long items = (long long)total * (ns / kCWarps);
     k_stream_tma<T><<<(int)std::min<long long>(items, g.tma), kTmaThreads, tma_smem<T>(), s>>>(sa);
   } else {
     const long long units = (long long)total * ns;
     const long long blocks = (units + kLdgThreads / 32 - 1) / (kLdgThreads / 32);
-    k_stream_ldg<T><<<(int)std::min<long long>(blocks, g.ldg), kLdgThreads, 0, s>>>(sa);
+    if (dev_rows)
+      k_stream_ldg<T, true><<<(int)std::min<long long>(blocks, g.ldg), kLdgThreads, 0, s>>>(sa);
+    else
+      k_stream_ldg<T, false><<<(int)std::min<long long>(blocks, g.ldg), kLdgThreads, 0, s>>>(sa);
   }
   mark();
   // a2-a3: row merge, KL, accept test, layout, draw record
   FinArgs fa{B, V, total, ns, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, ws.part,
-             acc_len, emitted, kld, flags, ws.rec, err, greedy};
+             acc_len, emitted, kld, flags, ws.rec, err, greedy, dev_rows};
   const int nd = n_subs_d(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32);
   DrawArgs da{B, V, nd, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.ref};
   SelArgs sel{B, V, nd, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.ref, emitted, flags, err};
@@ -978,11 +991,11 @@ extern "C" dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_dra
   if (dtype == DSDE_BF16)
     e = launch_verify<uint16_t>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                                 draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld,
-                                flags, ws, st->err, st->prof, s, nullptr, st->cfg.greedy);
+                                flags, ws, st->err, st->prof, s, nullptr, st->cfg.greedy, st->cfg.device_rows);
   else
     e = launch_verify<float>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                              draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld, flags,
-                             ws, st->err, st->prof, s, nullptr, st->cfg.greedy);
+                             ws, st->err, st->prof, s, nullptr, st->cfg.greedy, st->cfg.device_rows);
   return e == cudaSuccess ? DSDE_OK : DSDE_ERR_CUDA;
 }
 
@@ -1029,11 +1042,11 @@ extern "C" dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, 
   if (dtype == DSDE_BF16)
     e = launch_verify<uint16_t>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                                 draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld,
-                                flags, ws, st->err, st->prof, s, &x, st->cfg.greedy);
+                                flags, ws, st->err, st->prof, s, &x, st->cfg.greedy, st->cfg.device_rows);
   else
     e = launch_verify<float>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                              draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld, flags,
-                             ws, st->err, st->prof, s, &x, st->cfg.greedy);
+                             ws, st->err, st->prof, s, &x, st->cfg.greedy, st->cfg.device_rows);
   if (e != cudaSuccess) return DSDE_ERR_CUDA;
   if (!comm) return DSDE_OK;
   dsde_status rs = DSDE_OK;

@@ -32,6 +32,7 @@ struct FinArgs {
   SeqRec* rec;
   int32_t* err;
   int greedy;  // T = 0: accept iff x = argmax t, emit the argmax
+  int dev_rows;  // dsde_config.device_rows: total is a capacity, Σk_i = cu_sl[B]
 };
 
 constexpr int kFinThreads = 32 * DSDE_MAX_SL;
@@ -82,7 +83,7 @@ __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* ou
   const int c0 = __ldg(a.cu_sl + i), c1 = __ldg(a.cu_sl + i + 1);
   const int k = c1 - c0;
   const bool range_ok = c0 >= 0 && k >= 1 && k <= DSDE_MAX_SL && c1 <= a.total;
-  const bool rows_ok = (i != a.B - 1) || (c1 == a.total);
+  const bool rows_ok = a.dev_rows || (i != a.B - 1) || (c1 == a.total);
   if (!range_ok || !rows_ok) {
     if (threadIdx.x == 0) {
       a.acc_len[i] = -1;
