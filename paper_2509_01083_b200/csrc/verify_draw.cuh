@@ -820,7 +820,11 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   const DrawRef DR = draw_ref<T>(rt, resid, r.M, (float)r.C, r.lam);
   int tok = -1, last_pos = -1;
   double lo = 0.0, hi = 0.0, lp_lo = 0.0, lp_hi = 0.0, vbase = base;
-#pragma unroll
+  // not unrolled: this runs once per sequence, so its instructions are cold;
+  // a rolled loop re-fetches one vector's code from the instruction cache
+  // instead of NV copies from L2 (ncu: the per-CTA code of k_tail stalled on
+  // instruction fetch ~47% of its samples)
+#pragma unroll 1
   for (int v = 0; v < NV; ++v) {
     float wv[VEC];
     vec_weights<T>(rt[v], rd[v], DR, wv);
