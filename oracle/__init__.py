@@ -62,6 +62,10 @@ def lib():
         L.oracle_row_kld.argtypes = [C.c_int, P, P]
         L.oracle_row_kld.restype = C.c_double
         L.oracle_row_log_ratio.argtypes = [C.c_int, P, P, C.c_int]
+        L.oracle_row_entropy.argtypes = [C.c_int, P]
+        L.oracle_row_entropy.restype = C.c_double
+        L.oracle_draft_entropy.argtypes = [C.c_int, C.c_int, C.c_int, P, C.c_int64, P]
+        L.oracle_draft_entropy.restype = None
         L.oracle_row_log_ratio.restype = C.c_double
         L.oracle_verify.argtypes = [C.c_int, C.c_int, C.c_int, P, P, P, C.c_int64, P, C.c_int64,
                                     P, P, P, P, P, P, P, P, P, C.c_int]
@@ -121,6 +125,21 @@ def row_kld(t, d) -> float:
     d = np.ascontiguousarray(d, dtype=np.float64)
     assert t.shape == d.shape and t.ndim == 1
     return lib().oracle_row_kld(t.size, _p(t), _p(d))
+
+
+def row_entropy(d) -> float:
+    """H(softmax(d)) = -sum q log q."""
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    assert d.ndim == 1
+    return lib().oracle_row_entropy(d.size, _p(d))
+
+
+def draft_entropy(draft_logits, dtype: int) -> np.ndarray:
+    """H(q) of every row of a [n, V] draft-logit array (fp32, or bf16 bit patterns as uint16)."""
+    d = np.ascontiguousarray(draft_logits)
+    out = np.empty(d.shape[0], dtype=np.float64)
+    lib().oracle_draft_entropy(d.shape[0], d.shape[1], int(dtype), _p(d), d.shape[1], _p(out))
+    return out
 
 
 def row_log_ratio(t, d, x: int) -> float:

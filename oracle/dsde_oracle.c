@@ -143,6 +143,32 @@ OR_EXPORT double oracle_row_kld(int V, const double* t, const double* d) {
     return kl;
 }
 
+/* Draft entropy H(q) = -sum_v q_v log q_v, q = softmax(d) (SURVEY §8(f) f2:
+ * the paper's optional entropy signal next to the KLD); terms
+ * with q_v == 0 contribute 0. */
+OR_EXPORT double oracle_row_entropy(int V, const double* d) {
+    const double ld = row_lse(d, V);
+    double h = 0.0;
+    for (int v = 0; v < V; ++v) {
+        const double logq = d[v] - ld;
+        const double q = exp(logq);
+        if (q == 0.0) continue;
+        h -= q * logq;
+    }
+    return h;
+}
+
+/* H(q) of every draft row of a batch (rows in the layout of oracle_verify). */
+OR_EXPORT void oracle_draft_entropy(int n_rows, int V, int dtype, const void* draft, int64_t ld_d,
+                                    double* out) {
+    double* d = (double*)malloc(sizeof(double) * (size_t)V);
+    for (int r = 0; r < n_rows; ++r) {
+        load_row(d, draft, dtype, r, ld_d, V);
+        out[r] = oracle_row_entropy(V, d);
+    }
+    free(d);
+}
+
 /* log r = log p(x) - log q(x) (S:125 acceptance ratio p(x)/q(x)). */
 OR_EXPORT double oracle_row_log_ratio(int V, const double* t, const double* d, int x) {
     return (t[x] - row_lse(t, V)) - (d[x] - row_lse(d, V));
