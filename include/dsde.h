@@ -303,6 +303,17 @@ dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, int total_d
                       int32_t* sl_hat, double* diag, int32_t* next_sl, int32_t* cap,
                       void* workspace, size_t ws_bytes, dsde_comm comm, void* stream);
 
+/* Draft entropy (the paper's optional entropy signal next to
+ * the KLD). While entropy != NULL, every dsde_verify / dsde_step
+ * call on this state also writes H(q_j) = -sum_v q_v log q_v, q = softmax of
+ * draft row j, to entropy[j] for j in [0, sum_i k_i) (device memory, float,
+ * sized for the rows of the calls; not owned). It is formed in the same
+ * streaming pass (two extra per-slice sums of the draft's own softmax, merged
+ * in fp64 with the row), at ~1e-6 relative accuracy. NULL (the default) turns
+ * it off and the stream kernel compiled without it runs. Errors: DSDE_ERR_ARG
+ * for a NULL state. Host-side setting, no stream work. */
+dsde_status dsde_set_draft_entropy(dsde_state st, float* entropy);
+
 /* Host-callable form of the cap rule used by dsde_next_sl (same code): the
  * cap from the global exact partial (sum of SL^, N, max SL^). Lets callers
  * that all-reduce the partial themselves (and the CPU tests) apply it. */

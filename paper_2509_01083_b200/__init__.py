@@ -30,7 +30,7 @@ DERR = {0: "none", 1: "bad_sl", 2: "bad_token", 3: "nonfinite", 4: "rows", 5: "b
 
 # Every function the header declares (checked against include/dsde.h by the tests).
 EXPORTS = (
-    "dsde_config_default", "dsde_status_string", "dsde_abi_version", "dsde_state_create",
+    "dsde_config_default", "dsde_status_string", "dsde_abi_version", "dsde_set_draft_entropy", "dsde_state_create",
     "dsde_state_reset", "dsde_state_destroy", "dsde_state_bytes", "dsde_state_export",
     "dsde_state_import", "dsde_get_device_error", "dsde_clear_device_error",
     "dsde_verify_workspace_size", "dsde_verify", "dsde_update_signal", "dsde_next_sl", "dsde_step",
@@ -82,6 +82,7 @@ def lib() -> C.CDLL:
         L.dsde_status_string.argtypes = [I]
         L.dsde_status_string.restype = C.c_char_p
         L.dsde_abi_version.restype = I
+        L.dsde_set_draft_entropy.argtypes = [P, P]
         L.dsde_state_create.argtypes = [P, I, P]
         L.dsde_state_reset.argtypes = [P, P, I, P]
         L.dsde_state_destroy.argtypes = [P]
@@ -181,6 +182,12 @@ class State:
 
     def clear_error(self, stream=None):
         _check(lib().dsde_clear_device_error(self.h, _stream(stream)), "dsde_clear_device_error")
+
+    def set_draft_entropy(self, out=None):
+        """dsde_set_draft_entropy: later verify / step calls also write H(q) of every
+        draft row to ``out`` (float32 device tensor, >= sum k rows); None turns it off."""
+        self._entropy_ref = out  # keep the buffer alive while the library holds its pointer
+        _check(lib().dsde_set_draft_entropy(self.h, None if out is None else _ptr(out)), "dsde_set_draft_entropy")
 
     def profile(self, enable: bool = True):
         """Turns on/off per-kernel CUDA-event timing of dsde_verify calls on this state."""

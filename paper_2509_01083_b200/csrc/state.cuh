@@ -59,6 +59,7 @@ struct dsde_state_s {
   int32_t* err;          // [2]: code, sequence
   long long* scratch;    // [8]: cap partials (sum, n, max) for dsde_next_sl
   dsde::Profiler* prof;  // kernel timing (host side), created by dsde_profile_enable
+  float* entropy_out;    // dsde_set_draft_entropy: H(q) per draft row, NULL = off
 };
 
 struct dsde_comm_s {

@@ -323,9 +323,15 @@ struct SumRef {
 
 // a1 accumulation of one element pair (packed FFMA2 math, two MUFU.EX2 per
 // element): S += e, A += e w, D += e g(w).
-template <typename T>
+// ENT (opt-in): also Sd += f and E += f (d - max d), f = e^{d - max d},
+// the draft's own softmax sums about the slice max of d (H(q) = log Sd - E / Sd).
+struct EntAcc {
+  float2 Sd, E;
+};
+
+template <typename T, bool ENT = false>
 __device__ __forceinline__ void pair_accum_w(float2 tt, float2 dd, float2 w, const SumRef& R, float2& S2,
-                                             float2& A2, float2& D2) {
+                                             float2& A2, float2& D2, EntAcc* ent = nullptr) {
   const float2 L2 = make_float2(kLog2e, kLog2e);
 #ifndef DSDE_POLY_DEG7
   const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
@@ -367,12 +373,16 @@ __device__ __forceinline__ void pair_accum_w(float2 tt, float2 dd, float2 w, con
   const float2 bg = __ffma2_rn(e, w, __fadd2_rn(f, make_float2(-e.x, -e.y)));
   const float2 term = make_float2(fabsf(w.x) < 1.f ? sm.x : bg.x, fabsf(w.y) < 1.f ? sm.y : bg.y);
   D2 = __fadd2_rn(D2, term);
+  if constexpr (ENT) {
+    ent->Sd = __fadd2_rn(ent->Sd, f);
+    ent->E = __ffma2_rn(f, __fmul2_rn(arg, make_float2(kLn2, kLn2)), ent->E);
+  }
 }
 
-template <typename T>
+template <typename T, bool ENT = false>
 __device__ __forceinline__ void pair_accum(float2 tt, float2 dd, const SumRef& R, float2& S2, float2& A2,
-                                           float2& D2) {
-  pair_accum_w<T>(tt, dd, diff2<T>(tt, dd, R.Cw), R, S2, A2, D2);
+                                           float2& D2, EntAcc* ent = nullptr) {
+  pair_accum_w<T, ENT>(tt, dd, diff2<T>(tt, dd, R.Cw), R, S2, A2, D2, ent);
 }
 
 // The sums of one 16-byte vector pair. When every |w| of the vector is below 2
@@ -386,9 +396,9 @@ __device__ __forceinline__ void pair_accum(float2 tt, float2 dd, const SumRef& R
 #ifndef DSDE_WIDE_POLY
 #define DSDE_WIDE_POLY 1
 #endif
-template <typename T>
+template <typename T, bool ENT = false>
 __device__ __forceinline__ void vec_accum(const uint4& t, const uint4& d, const SumRef& R, float2& S2,
-                                          float2& A2, float2& D2) {
+                                          float2& A2, float2& D2, EntAcc* ent = nullptr) {
   constexpr int P = Traits<T>::VEC / 2;
   const uint4 rt[1] = {t}, rd[1] = {d};
 #if DSDE_WIDE_POLY
@@ -422,15 +432,24 @@ __device__ __forceinline__ void vec_accum(const uint4& t, const uint4& d, const 
       const float2 ew = __fmul2_rn(e, ww);
       S2 = __fadd2_rn(S2, e);
       A2 = __fadd2_rn(A2, ew);
-      D2 = __ffma2_rn(ew, __fmul2_rn(ww, pp), D2);  // e w^2 h(-w)
+      const float2 wh = __fmul2_rn(ww, pp);
+      D2 = __ffma2_rn(ew, wh, D2);  // e w^2 h(-w)
+      if constexpr (ENT) {
+        // f = e e^{-w} = e (1 - w + w^2 h(-w)); d - max d = (t - M) - w
+        const float2 f = __ffma2_rn(ew, __fadd2_rn(wh, make_float2(-1.f, -1.f)), e);
+        const float2 dm = __ffma2_rn(xt, make_float2(kLn2, kLn2), make_float2(-ww.x, -ww.y));
+        ent->Sd = __fadd2_rn(ent->Sd, f);
+        ent->E = __ffma2_rn(f, dm, ent->E);
+      }
     }
     return;
   }
 #pragma unroll
-  for (int h = 0; h < P; ++h) pair_accum_w<T>(tt[h], pair_of<T>(rd, 2 * h), w[h], R, S2, A2, D2);
+  for (int h = 0; h < P; ++h) pair_accum_w<T, ENT>(tt[h], pair_of<T>(rd, 2 * h), w[h], R, S2, A2, D2, ent);
 #else
 #pragma unroll
-  for (int h = 0; h < Traits<T>::VEC; h += 2) pair_accum<T>(pair_of<T>(rt, h), pair_of<T>(rd, h), R, S2, A2, D2);
+  for (int h = 0; h < Traits<T>::VEC; h += 2)
+    pair_accum<T, ENT>(pair_of<T>(rt, h), pair_of<T>(rd, h), R, S2, A2, D2, ent);
 #endif
 }
 
@@ -466,7 +485,7 @@ __device__ __forceinline__ SubPartial finish_partial(float2 S2, float2 A2, float
 
 // `after_max` runs (warp-uniformly) once the slice maxima are reduced over the
 // warp, i.e. once every lane's words have been consumed.
-template <typename T, int NV, typename Hook = NoHook>
+template <typename T, int NV, typename Hook = NoHook, bool ENT = false>
 __device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const uint4 (&rd)[NV],
                                                   Hook after_max = Hook()) {
   LaneMax<T> mx;
@@ -479,16 +498,32 @@ __device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const u
   if (M <= -1e30f) return empty_partial();  // slice beyond V (padding only; NaN is not empty)
   const SumRef R(M, Dmax);
   float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
+  if constexpr (ENT) {
+    EntAcc ent{S2, S2};
 #pragma unroll
-  for (int v = 0; v < NV; ++v) vec_accum<T>(rt[v], rd[v], R, S2, A2, D2);
-  return finish_partial(S2, A2, D2, M, Dmax, R.Cw);
+    for (int v = 0; v < NV; ++v) vec_accum<T, true>(rt[v], rd[v], R, S2, A2, D2, &ent);
+    SubPartial p = finish_partial(S2, A2, D2, M, Dmax, R.Cw);
+    float Sd = ent.Sd.x + ent.Sd.y, E = ent.E.x + ent.E.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      Sd += __shfl_xor_sync(kFull, Sd, o);
+      E += __shfl_xor_sync(kFull, E, o);
+    }
+    p.pad0 = Sd;
+    p.pad1 = E;
+    return p;
+  } else {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) vec_accum<T>(rt[v], rd[v], R, S2, A2, D2);
+    return finish_partial(S2, A2, D2, M, Dmax, R.Cw);
+  }
 }
 
 // lane 0 writes the whole 32-byte partial (so a release by lane 0 covers it)
 __device__ __forceinline__ void store_partial(SubPartial* dst, const SubPartial& p) {
   if ((threadIdx.x & 31) == 0) {
     reinterpret_cast<float4*>(dst)[0] = make_float4(p.S, p.A, p.D, p.M);
-    reinterpret_cast<float4*>(dst)[1] = make_float4(p.C, p.maxd, 0.f, 0.f);
+    reinterpret_cast<float4*>(dst)[1] = make_float4(p.C, p.maxd, p.pad0, p.pad1);
   }
 }
 
@@ -536,7 +571,7 @@ constexpr int kLdgThreads = 256;
 #define DSDE_EXPERIMENT 0
 #endif
 
-template <typename T, bool DEV_ROWS>
+template <typename T, bool DEV_ROWS, bool ENT = false>
 __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(StreamArgs a) {
   constexpr int NV = Traits<T>::NV;
   const int total = DEV_ROWS ? stream_rows(a) : a.total;
@@ -574,7 +609,7 @@ __global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(Strea
     p.S = __uint_as_float(acc);
     store_partial(dst, p);
 #else
-    store_partial(dst, slice_stats<T>(rt, rd));
+    store_partial(dst, slice_stats<T, NV, NoHook, ENT>(rt, rd));
 #endif
     u += du;
     r += dr;
@@ -812,7 +847,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
                           const uint64_t* seeds, int32_t* acc_len, int32_t* emitted, float* kld,
                           uint8_t* flags, const VerifyWs& ws, int32_t* err, Profiler* prof,
                           cudaStream_t s, const StepExtra* step = nullptr, int greedy = 0,
-                          int dev_rows = 0) {
+                          int dev_rows = 0, float* ent = nullptr) {
   const bool pr = prof != nullptr && prof->on;
   auto mark = [&]() {
     if (pr) cudaEventRecord(prof->next(), s);
@@ -834,9 +869,9 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
     g.draw = resident_grid(k_draw_ldg<T>, kLdgThreads, 0, sms, 0);
     g.sms = sms;
   }
-  const int variant = stream_variant();
+  const int variant = ent ? 0 : stream_variant();  // the draft entropy is in the ldg kernel only
   // the fused kernel has no T = 0 mode and sizes its counters from the host total
-  const int tv = (greedy || dev_rows) && tail_variant() == 2 ? 0 : tail_variant();
+  const int tv = (greedy || dev_rows || ent) && tail_variant() == 2 ? 0 : tail_variant();
   if (tv == 2) {
     static int fused_grid[64] = {0};
     int& fg = fused_grid[dev & 63];
@@ -904,15 +939,19 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   } else {
     const long long units = (long long)total * ns;
     const long long blocks = (units + kLdgThreads / 32 - 1) / (kLdgThreads / 32);
-    if (dev_rows)
-      k_stream_ldg<T, true><<<(int)std::min<long long>(blocks, g.ldg), kLdgThreads, 0, s>>>(sa);
-    else
-      k_stream_ldg<T, false><<<(int)std::min<long long>(blocks, g.ldg), kLdgThreads, 0, s>>>(sa);
+    const int grid = (int)std::min<long long>(blocks, g.ldg);
+    if (ent) {
+      if (dev_rows) k_stream_ldg<T, true, true><<<grid, kLdgThreads, 0, s>>>(sa);
+      else k_stream_ldg<T, false, true><<<grid, kLdgThreads, 0, s>>>(sa);
+    } else {
+      if (dev_rows) k_stream_ldg<T, true><<<grid, kLdgThreads, 0, s>>>(sa);
+      else k_stream_ldg<T, false><<<grid, kLdgThreads, 0, s>>>(sa);
+    }
   }
   mark();
   // a2-a3: row merge, KL, accept test, layout, draw record
   FinArgs fa{B, V, total, ns, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds, ws.part,
-             acc_len, emitted, kld, flags, ws.rec, err, greedy, dev_rows};
+             acc_len, emitted, kld, flags, ws.rec, err, greedy, dev_rows, ent};
   const int nd = n_subs_d(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32);
   DrawArgs da{B, V, nd, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.ref};
   SelArgs sel{B, V, nd, tl, ld_t, dl, ld_d, ws.rec, ws.mass, ws.ref, emitted, flags, err};
@@ -991,11 +1030,13 @@ extern "C" dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_dra
   if (dtype == DSDE_BF16)
     e = launch_verify<uint16_t>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                                 draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld,
-                                flags, ws, st->err, st->prof, s, nullptr, st->cfg.greedy, st->cfg.device_rows);
+                                flags, ws, st->err, st->prof, s, nullptr, st->cfg.greedy, st->cfg.device_rows,
+                                st->entropy_out);
   else
     e = launch_verify<float>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                              draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld, flags,
-                             ws, st->err, st->prof, s, nullptr, st->cfg.greedy, st->cfg.device_rows);
+                             ws, st->err, st->prof, s, nullptr, st->cfg.greedy, st->cfg.device_rows,
+                                st->entropy_out);
   return e == cudaSuccess ? DSDE_OK : DSDE_ERR_CUDA;
 }
 
@@ -1042,11 +1083,13 @@ extern "C" dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, 
   if (dtype == DSDE_BF16)
     e = launch_verify<uint16_t>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                                 draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld,
-                                flags, ws, st->err, st->prof, s, &x, st->cfg.greedy, st->cfg.device_rows);
+                                flags, ws, st->err, st->prof, s, &x, st->cfg.greedy, st->cfg.device_rows,
+                                st->entropy_out);
   else
     e = launch_verify<float>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                              draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld, flags,
-                             ws, st->err, st->prof, s, &x, st->cfg.greedy, st->cfg.device_rows);
+                             ws, st->err, st->prof, s, &x, st->cfg.greedy, st->cfg.device_rows,
+                                st->entropy_out);
   if (e != cudaSuccess) return DSDE_ERR_CUDA;
   if (!comm) return DSDE_OK;
   dsde_status rs = DSDE_OK;
@@ -1063,4 +1106,10 @@ extern "C" int dsde_debug_tail_trace(unsigned long long* host, int n) {
   return cudaMemcpyFromSymbol(host, dsde::g_tail_trace, sizeof(unsigned long long) * 6 * n) == cudaSuccess ? 0 : -1;
 }
 #endif
+
+extern "C" dsde_status dsde_set_draft_entropy(dsde_state st, float* entropy) {
+  if (!st) return DSDE_ERR_ARG;
+  st->entropy_out = entropy;
+  return DSDE_OK;
+}
 

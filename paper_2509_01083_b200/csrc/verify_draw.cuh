@@ -33,6 +33,7 @@ struct FinArgs {
   int32_t* err;
   int greedy;  // T = 0: accept iff x = argmax t, emit the argmax
   int dev_rows;  // dsde_config.device_rows: total is a capacity, Σk_i = cu_sl[B]
+  float* ent;    // [Σk_i] optional out: draft entropy H(q) per row; partials carry Sd, E
 };
 
 constexpr int kFinThreads = 32 * DSDE_MAX_SL;
@@ -112,11 +113,17 @@ __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* ou
       Dl = fmaxf(Dl, __shfl_xor_sync(kFull, Dl, o));
     }
     const double M = (double)Ml, C = (double)(Ml - Dl);  // C is an fp32 value
-    double S = 0.0, A = 0.0, D = 0.0;
+    double S = 0.0, A = 0.0, D = 0.0, Sd = 0.0, E = 0.0;
     for (int c = lane; c < nc; c += 32) {
       const float4 q0 = __ldg(reinterpret_cast<const float4*>(P + c));
       const float4 q1 = __ldg(reinterpret_cast<const float4*>(P + c) + 1);
       const double qS = q0.x, qA = q0.y, qD = q0.z, qM = q0.w, qC = q1.x;
+      if (a.ent && q1.z > 0.f) {
+        // draft sums about the row max of d: Sd += s Sd_c, E += s (E_c + (maxd_c - maxd) Sd_c)
+        const double dd = (double)q1.y - (double)Dl, sd = exp(dd);
+        Sd += sd * (double)q1.z;
+        E += sd * ((double)q1.w + dd * (double)q1.z);
+      }
       const double ls = qM - M;
       const double s = exp(ls);
       const double dl = qC - C;
@@ -140,6 +147,15 @@ __device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* ou
       S += __shfl_xor_sync(kFull, S, o);
       A += __shfl_xor_sync(kFull, A, o);
       D += __shfl_xor_sync(kFull, D, o);
+    }
+    if (a.ent) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        Sd += __shfl_xor_sync(kFull, Sd, o);
+        E += __shfl_xor_sync(kFull, E, o);
+      }
+      // H(q) = log Sd - E / Sd (E <= 0: both terms non-negative, no cancellation)
+      if (lane == 0) a.ent[c0 + j] = (float)(log(Sd) - E / Sd);
     }
     if (a.greedy) {
       // row argmax of t: the first slice holding the row max (slices are in
