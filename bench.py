@@ -207,7 +207,8 @@ def _config_dict(args, cfg, n):
             "logits": "bf16", "sl_ceiling": cfg["ceiling"], "profiles": list(cfg["profiles"]),
             "parallelism": f"dp{n}", "l2": "inputs larger than L2: a distinct ~1 GB input set per step",
             "replay": "recorded closed-loop DSDE steps replayed in order (cyclic if K+W > R)",
-            "verify": "greedy (T=0, draft argmax tokens)" if args.greedy else "rejection sampling (T=1)"}
+            "verify": "greedy (T=0, draft argmax tokens)" if args.greedy else "rejection sampling (T=1)",
+            "draft_entropy": bool(args.entropy)}
 
 
 def run(args):
@@ -236,6 +237,8 @@ def run(args):
     mcfg = m.Config.default(sl_ceiling=cfg["ceiling"], calib_sl=min(4, cfg["ceiling"]), greedy=int(args.greedy))
     state = m.State(mcfg, B)
     step = m.Step(state, B, V, torch.bfloat16, comm=comm)
+    if args.entropy:  # the fused draft entropy in the same stream pass
+        state.set_draft_entropy(torch.empty(B * 16, dtype=torch.float32, device=dev))
     w = synth.Workload(B=B, V=V, dtype=torch.bfloat16, profiles=cfg["profiles"], seed=args.seed + 7919 * rank,
                        greedy_draft=args.greedy)
     stream = torch.cuda.current_stream()
@@ -504,6 +507,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--greedy", action="store_true",
                     help="T = 0 verification (dsde_config.greedy; draft tokens = draft argmax)")
+    ap.add_argument("--entropy", action="store_true",
+                    help="also compute the draft entropy H(q) per draft row (dsde_set_draft_entropy, SURVEY f2)")
     ap.add_argument("--split-calls", action="store_true",
                     help="time dsde_verify + dsde_update_signal + dsde_next_sl instead of one dsde_step")
     args = ap.parse_args()
