@@ -571,8 +571,13 @@ constexpr int kLdgThreads = 256;
 #define DSDE_EXPERIMENT 0
 #endif
 
+#ifndef DSDE_ENT_MINB
+#define DSDE_ENT_MINB 2
+#endif
+// the entropy variant carries two more accumulators: 2 CTAs per SM (up to 128
+// registers) instead of spilling at the 80-register cap of 3 CTAs per SM
 template <typename T, bool DEV_ROWS, bool ENT = false>
-__global__ void __launch_bounds__(kLdgThreads, DSDE_LDG_MINB) k_stream_ldg(StreamArgs a) {
+__global__ void __launch_bounds__(kLdgThreads, ENT ? DSDE_ENT_MINB : DSDE_LDG_MINB) k_stream_ldg(StreamArgs a) {
   constexpr int NV = Traits<T>::NV;
   const int total = DEV_ROWS ? stream_rows(a) : a.total;
   const long long n_units = (long long)total * a.nsub;
@@ -856,7 +861,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   int dev = 0;
   cudaGetDevice(&dev);
   struct Grids {
-    int sms = 0, ldg = 0, tma = 0, draw = 0;
+    int sms = 0, ldg = 0, ldg_ent = 0, tma = 0, draw = 0;
   };
   static Grids grids[64];
   Grids& g = grids[dev & 63];
@@ -865,6 +870,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_stream_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem<T>());
     g.ldg = resident_grid(k_stream_ldg<T, false>, kLdgThreads, 0, sms, 0);
+    g.ldg_ent = resident_grid(k_stream_ldg<T, false, true>, kLdgThreads, 0, sms, 0);
     g.tma = resident_grid(k_stream_tma<T>, kTmaThreads, tma_smem<T>(), sms, kTmaCtas);
     g.draw = resident_grid(k_draw_ldg<T>, kLdgThreads, 0, sms, 0);
     g.sms = sms;
@@ -939,7 +945,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   } else {
     const long long units = (long long)total * ns;
     const long long blocks = (units + kLdgThreads / 32 - 1) / (kLdgThreads / 32);
-    const int grid = (int)std::min<long long>(blocks, g.ldg);
+    const int grid = (int)std::min<long long>(blocks, ent ? g.ldg_ent : g.ldg);
     if (ent) {
       if (dev_rows) k_stream_ldg<T, true, true><<<grid, kLdgThreads, 0, s>>>(sa);
       else k_stream_ldg<T, false, true><<<grid, kLdgThreads, 0, s>>>(sa);
