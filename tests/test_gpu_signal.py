@@ -156,7 +156,8 @@ def test_closed_loop_parity(m, cfg_id, fused):
 
 def test_step_matches_three_calls(m):
     """dsde_step (stream + fused tail/signal/cap) and the three separate calls
-    give bit-identical results and state, step after step (config-2 shapes)."""
+    give bit-identical results and state, step after step (config-2 shapes),
+    with and without a per-sequence budget."""
     B, V, dtype = 64, 32000, torch.bfloat16
     gc, _ = _cfg_pair(m, sl_ceiling=8, calib_sl=4)
     sa, sb = m.State(gc, B), m.State(gc, B)
@@ -166,8 +167,12 @@ def test_step_matches_three_calls(m):
     for s in range(12):
         inp = synth.generate_step(w, s, k, device="cuda")
         n = int(k.sum())
-        oa = pa(inp.cu_sl, inp.draft_tokens, inp.target, inp.draft, inp.seeds, n, fused=True)
-        ob = pb(inp.cu_sl, inp.draft_tokens, inp.target, inp.draft, inp.seeds, n, fused=False)
+        # every third step a per-sequence token budget clamps the next SL
+        bud = (torch.arange(B, dtype=torch.int32, device="cuda") % 7 + 1) if s % 3 == 1 else None
+        oa = pa(inp.cu_sl, inp.draft_tokens, inp.target, inp.draft, inp.seeds, n, budget=bud, fused=True)
+        ob = pb(inp.cu_sl, inp.draft_tokens, inp.target, inp.draft, inp.seeds, n, budget=bud, fused=False)
+        if bud is not None:
+            assert torch.all(oa.next_sl <= bud), s
         torch.cuda.synchronize()
         for f in ("accepted_len", "emitted", "kld", "sl_hat", "next_sl", "cap"):
             x, y = getattr(oa, f).cpu(), getattr(ob, f).cpu()
