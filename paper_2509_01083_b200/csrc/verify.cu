@@ -803,6 +803,11 @@ static int tail_variant() {
   return v;
 }
 
+// k_tail CTA shape: 16 warps while B <= this many sequences per SM, else 8
+#ifndef DSDE_TAIL16_MAXB_PER_SM
+#define DSDE_TAIL16_MAXB_PER_SM 2
+#endif
+
 // Launch with programmatic stream serialization (PDL): the kernel may start
 // while the previous kernel on the stream drains and must call
 // griddepcontrol.wait before touching that kernel's results. DSDE_PDL=0
@@ -964,7 +969,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   if (step) {
     // 16-warp CTAs while every sequence gets a resident CTA (2 per SM), 8-warp
     // CTAs (4 per SM) for larger batches so the tail stays one wave longer
-    if (B <= 2 * g.sms)
+    if (B <= DSDE_TAIL16_MAXB_PER_SM * g.sms)
       launch_pdl(k_tail<T, true, 16>, B, 512, s, fa, da, sel, *step);
     else
       launch_pdl(k_tail<T, true, 8>, B, 256, s, fa, da, sel, *step);
@@ -975,7 +980,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   }
   if (tv == 0) {
     // a2-a4 fused: one CTA per sequence (the profiler's later phases read 0)
-    if (B <= 2 * g.sms)
+    if (B <= DSDE_TAIL16_MAXB_PER_SM * g.sms)
       launch_pdl(k_tail<T, false, 16>, B, 512, s, fa, da, sel, StepExtra{});
     else
       launch_pdl(k_tail<T, false, 8>, B, 256, s, fa, da, sel, StepExtra{});
