@@ -387,14 +387,18 @@ __device__ __forceinline__ void pair_accum(float2 tt, float2 dd, const SumRef& R
 
 // The sums of one 16-byte vector pair. When every |w| of the vector is below 2
 // in every lane of the warp (the common case once the draft tracks the target),
-// g(w) = w^2 h(-w) is a single degree-8 polynomial (Chebyshev fit of h on
-// |u| <= 2, 3.3e-7 relative in fp32 Horner, `tools/fit_g.py --deg 8 --range 2`)
+// g(w) = w^2 h(-w) is a single degree-7 polynomial (Chebyshev fit of h on
+// |u| <= 2, 2.1e-6 relative in fp32 Horner, `tools/fit_g.py --deg 7 --range 2`;
+// DESIGN D19 — DSDE_WIDE_DEG=8 selects the 3.3e-7 degree-8 fit)
 // and the e^{d - max d} exponential, the big-|w| form and the per-element
 // select are skipped; otherwise every pair takes pair_accum (the test costs one
 // FMNMX3 per pair; a slice-level "stop testing after a failure" flag and a
 // separate untested path both measured slower on cfg3, faster only on cfg4).
 #ifndef DSDE_WIDE_POLY
 #define DSDE_WIDE_POLY 1
+#endif
+#ifndef DSDE_WIDE_DEG
+#define DSDE_WIDE_DEG 7
 #endif
 template <typename T, bool ENT = false>
 __device__ __forceinline__ void vec_accum(const uint4& t, const uint4& d, const SumRef& R, float2& S2,
@@ -418,8 +422,17 @@ __device__ __forceinline__ void vec_accum(const uint4& t, const uint4& d, const 
       const float2 xt = __ffma2_rn(tt[h], L2, R.nML2);
       const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
       const float2 ww = w[h];
-      // h(-w) in powers of w (odd coefficients negated): the degree-8 Chebyshev
-      // fit on |u| <= 2 (tools/fit_g.py --deg 8 --range 2, 3.3e-7 relative)
+      // h(-w) in powers of w (odd coefficients negated)
+#if DSDE_WIDE_DEG == 7  // degree 7 on |u| <= 2 (2.1e-6 relative, the default)
+      float2 pp = __ffma2_rn(make_float2(-2.990256007251446e-06f, -2.990256007251446e-06f), ww,
+                             make_float2(2.7102691092295572e-05f, 2.7102691092295572e-05f));
+      pp = __ffma2_rn(pp, ww, make_float2(-1.9769996288232505e-04f, -1.9769996288232505e-04f));
+      pp = __ffma2_rn(pp, ww, make_float2(1.3830546522513032e-03f, 1.3830546522513032e-03f));
+      pp = __ffma2_rn(pp, ww, make_float2(-8.334130048751831e-03f, -8.334130048751831e-03f));
+      pp = __ffma2_rn(pp, ww, make_float2(4.167136549949646e-02f, 4.167136549949646e-02f));
+      pp = __ffma2_rn(pp, ww, make_float2(-1.666664332151413e-01f, -1.666664332151413e-01f));
+      pp = __ffma2_rn(pp, ww, make_float2(0.49999940395355225f, 0.49999940395355225f));
+#else  // degree 8 on |u| <= 2 (3.3e-7 relative)
       float2 pp = __ffma2_rn(make_float2(2.972247159505059e-07f, 2.972247159505059e-07f), ww,
                              make_float2(-2.990256007251446e-06f, -2.990256007251446e-06f));
       pp = __ffma2_rn(pp, ww, make_float2(2.47248935920652e-05f, 2.47248935920652e-05f));
@@ -429,6 +442,7 @@ __device__ __forceinline__ void vec_accum(const uint4& t, const uint4& d, const 
       pp = __ffma2_rn(pp, ww, make_float2(4.166661202907562e-02f, 4.166661202907562e-02f));
       pp = __ffma2_rn(pp, ww, make_float2(-1.666664332151413e-01f, -1.666664332151413e-01f));
       pp = __ffma2_rn(pp, ww, make_float2(0.5f, 0.5f));
+#endif
       const float2 ew = __fmul2_rn(e, ww);
       S2 = __fadd2_rn(S2, e);
       A2 = __fadd2_rn(A2, ew);
