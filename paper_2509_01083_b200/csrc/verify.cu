@@ -821,6 +821,10 @@ static int tail_variant() {
 #ifndef DSDE_TAIL16_MAXB_PER_SM
 #define DSDE_TAIL16_MAXB_PER_SM 2
 #endif
+// 32-warp CTAs (one per SM) while B <= this many sequences per SM (0 = never)
+#ifndef DSDE_TAIL32_MAXB_PER_SM
+#define DSDE_TAIL32_MAXB_PER_SM 1
+#endif
 
 // Launch with programmatic stream serialization (PDL): the kernel may start
 // while the previous kernel on the stream drains and must call
@@ -983,7 +987,9 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   if (step) {
     // 16-warp CTAs while every sequence gets a resident CTA (2 per SM), 8-warp
     // CTAs (4 per SM) for larger batches so the tail stays one wave longer
-    if (B <= DSDE_TAIL16_MAXB_PER_SM * g.sms)
+    if (B <= DSDE_TAIL32_MAXB_PER_SM * g.sms)
+      launch_pdl(k_tail<T, true, 32>, B, 1024, s, fa, da, sel, *step);
+    else if (B <= DSDE_TAIL16_MAXB_PER_SM * g.sms)
       launch_pdl(k_tail<T, true, 16>, B, 512, s, fa, da, sel, *step);
     else
       launch_pdl(k_tail<T, true, 8>, B, 256, s, fa, da, sel, *step);
@@ -994,7 +1000,9 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   }
   if (tv == 0) {
     // a2-a4 fused: one CTA per sequence (the profiler's later phases read 0)
-    if (B <= DSDE_TAIL16_MAXB_PER_SM * g.sms)
+    if (B <= DSDE_TAIL32_MAXB_PER_SM * g.sms)
+      launch_pdl(k_tail<T, false, 32>, B, 1024, s, fa, da, sel, StepExtra{});
+    else if (B <= DSDE_TAIL16_MAXB_PER_SM * g.sms)
       launch_pdl(k_tail<T, false, 16>, B, 512, s, fa, da, sel, StepExtra{});
     else
       launch_pdl(k_tail<T, false, 8>, B, 256, s, fa, da, sel, StepExtra{});
