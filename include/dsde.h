@@ -68,13 +68,12 @@ typedef enum { DSDE_F32 = 0, DSDE_BF16 = 1 } dsde_dtype;
 #define DSDE_DERR_NONFINITE 3     /* non-finite logits in a row                          */
 #define DSDE_DERR_ROWS 4          /* cu_sl[B] != total_draft_rows                         */
 #define DSDE_DERR_BAD_SLOT 5      /* state slot outside [0, max_seqs)                     */
-#define DSDE_DERR_STALL 6         /* internal: a fused-kernel wait timed out (bug guard)  */
+#define DSDE_DERR_STALL 6         /* internal: a pass-kernel wait timed out (~2 s bug guard; never expected) */
 
 /* Per-slot bits of the optional `flags` output of dsde_verify. */
 #define DSDE_FLAG_ACCEPT_NEAR_TIE 1  /* |u_acc - min(1, p/q)| < 1e-6 at this position      */
 #define DSDE_FLAG_SAMPLE_NEAR_TIE 2  /* |u_smp - C/R| < 1e-6 at a CDF edge of the draw      */
 #define DSDE_FLAG_FALLBACK 4         /* residual mass 0: the token was drawn from p (D7)  */
-#define DSDE_FLAG_OVERFLOW 8         /* a draft logit exceeds the reference by > 64 nats: reference lowered (informational) */
 
 /* Adapter configuration; defaults from the paper / SPEC (dsde_config_default).
  * Validity (S:173-174 plus D11/D17): 0 < delta <= 1; 1 <= n_short < n_long
@@ -200,10 +199,21 @@ size_t dsde_verify_workspace_size(int B, int total_draft_rows, int V, dsde_dtype
  *                     256-byte aligned, not used concurrently by another call.
  *   st                state whose error word receives device-detected errors.
  *   stream            CUDA stream.
- * Device-detected data errors (sticky, first one wins): k_i outside
- * [1, DSDE_MAX_SL] or cu_sl not monotone, a token outside [0,V), non-finite
- * logits, cu_sl[B] != total_draft_rows. The offending sequence gets
- * accepted_len -1, all-pad tokens and NaN KLD; the others are unaffected. */
+ * Device-detected data errors (sticky, first one wins): a token outside
+ * [0,V) or non-finite logits in a row (DSDE_DERR_BAD_TOKEN / _NONFINITE: the
+ * sequence gets accepted_len -1, all-pad tokens and NaN KLD; the others are
+ * unaffected); k_i outside [1, DSDE_MAX_SL] or rows beyond the launch
+ * (DSDE_DERR_BAD_SL, or DSDE_DERR_ROWS when cu_sl[B] != total_draft_rows:
+ * that sequence gets accepted_len -1, the others are unaffected); a cu_sl that
+ * is not a non-decreasing prefix starting at 0 (DSDE_DERR_BAD_SL: no row can be
+ * attributed, every sequence gets accepted_len -1). No device error ever
+ * causes an out-of-bounds access.
+ *
+ * Execution: a memset of the workspace counters and ONE persistent kernel
+ * (k_pass) on `stream`: its warps stream every (draft row, 2048-token slice)
+ * of the target and draft logits once; the warp completing a row merges it,
+ * the warp completing a sequence lays it out, and the draw of each sequence's
+ * token is spread over later warp iterations, interleaved with the stream. */
 dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_draft_rows,
                         const int32_t* cu_sl, const int32_t* draft_tokens,
                         const void* target_logits, int64_t ld_t,
@@ -212,10 +222,13 @@ dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_draft_rows,
                         int32_t* emitted_tokens, float* kld, uint8_t* flags,
                         void* workspace, size_t ws_bytes, dsde_state st, void* stream);
 
-/* Kernel timing of dsde_verify (instrumentation; off by default). While
- * enabled, every dsde_verify call on this state records CUDA events on its
- * stream before its first launch and after each of its DSDE_VERIFY_PHASES
- * launches (a1 stream, a2-a3 finalize, a4 draw mass, a4 select).
+/* Kernel timing of dsde_verify / dsde_step (instrumentation; off by
+ * default). While enabled, every dsde_verify / dsde_step call on this state
+ * records CUDA events on its stream before its first launch and after each of
+ * its DSDE_VERIFY_PHASES phases: 0 = the workspace counter reset (a memset),
+ * 1 = the pass kernel k_pass (a1-a4, and in dsde_step a5-a6 plus the
+ * single-GPU cap a7), 2 and 3 = unused (read 0; dsde_step's multi-GPU cap
+ * kernels and all-reduce are not inside the recorded phases).
  * dsde_profile_read blocks until the last recorded event completes, writes
  * the summed milliseconds of each phase over the calls recorded since the
  * previous read to ms[DSDE_VERIFY_PHASES] (host memory) and the call count to
@@ -286,12 +299,12 @@ dsde_status dsde_next_sl(dsde_state st, int B, const int32_t* slots, const int32
  *   dsde_update_signal(st, B, slots, cu_sl, kld, accepted_len, sl_hat, diag);
  *   dsde_next_sl(st, B, slots, sl_hat, budget, next_sl, cap, comm);
  * with the same arguments, results, state updates and errors as those three
- * calls made in that order on `stream` (bit-identical outputs), but launched as
- * two kernels on one GPU: the row stream (a1) and one tail kernel per batch
- * that finalizes each sequence (a2-a3), draws its token (a4), updates its
- * signal and predicts SL^ (a5-a6) in the same CTA, the CTA finishing last
- * applying the cap (a7). With a communicator the cap's exact partial is
- * all-reduced over NCCL in between (two more launches + the collective).
+ * calls made in that order on `stream` (bit-identical outputs), but in one
+ * pass kernel on one GPU: the warp that lays out a sequence (a3) also updates
+ * its signal and predicts SL^ (a5-a6) and the warp completing the batch's last
+ * signal applies the cap (a7). With a communicator the cap's exact partial is
+ * all-reduced over NCCL after the pass kernel (two more launches + the
+ * collective).
  * The workspace is the one dsde_verify takes. Errors: the union of the three
  * calls' synchronous checks (DSDE_ERR_ARG / DSDE_ERR_STATE) and
  * DSDE_ERR_CUDA / DSDE_ERR_NCCL. Calls on one state must be serialised. */

@@ -25,8 +25,8 @@ DSDE_F32, DSDE_BF16 = 0, 1
 DSDE_PAD = -1
 DSDE_MAX_SL = 16
 DSDE_MAX_WINDOW = 64
-FLAG_ACCEPT_NEAR_TIE, FLAG_SAMPLE_NEAR_TIE, FLAG_FALLBACK, FLAG_OVERFLOW = 1, 2, 4, 8
-DERR = {0: "none", 1: "bad_sl", 2: "bad_token", 3: "nonfinite", 4: "rows", 5: "bad_slot"}
+FLAG_ACCEPT_NEAR_TIE, FLAG_SAMPLE_NEAR_TIE, FLAG_FALLBACK = 1, 2, 4
+DERR = {0: "none", 1: "bad_sl", 2: "bad_token", 3: "nonfinite", 4: "rows", 5: "bad_slot", 6: "stall"}
 
 # Every function the header declares (checked against include/dsde.h by the tests).
 EXPORTS = (
@@ -37,9 +37,9 @@ EXPORTS = (
     "dsde_cap_value", "dsde_comm_unique_id", "dsde_comm_init", "dsde_comm_destroy",
     "dsde_profile_enable", "dsde_profile_read",
 )
-VERIFY_PHASES = ("stream", "finalize", "draw", "select")
-# default launch sequence: the stream kernel, then k_tail (finalize + draw + select)
-VERIFY_PHASES_FUSED = ("stream", "tail", "", "")
+# dsde_profile_read phases (include/dsde.h): the counter reset, then the one
+# persistent pass kernel k_pass (a1-a4, + a5-a7 in dsde_step); two spare slots
+VERIFY_PHASES = ("reset", "pass", "", "")
 
 
 class DsdeError(RuntimeError):
@@ -198,8 +198,7 @@ class State:
         ms = (C.c_float * len(VERIFY_PHASES))()
         calls = C.c_int()
         _check(lib().dsde_profile_read(self.h, ms, C.byref(calls)), "dsde_profile_read")
-        names = VERIFY_PHASES if os.environ.get("DSDE_TAIL") == "split" else VERIFY_PHASES_FUSED
-        out = {n: float(x) for n, x in zip(names, ms) if n}
+        out = {n: float(x) for n, x in zip(VERIFY_PHASES, ms) if n}
         return out, calls.value
 
 
@@ -300,26 +299,36 @@ class Step:
         self.diag = torch.empty((B, 8), dtype=torch.float64, device=device) if with_diag else None
         self.slots = torch.arange(B, **i32)
 
+    def _batch(self, cu_sl) -> int:
+        B = cu_sl.numel() - 1
+        if not 1 <= B <= self.B:
+            raise DsdeError(f"batch of {B} sequences for a Step sized for {self.B}")
+        return B
+
     def verify(self, cu_sl, draft_tokens, target, draft, seeds, total_draft_rows: int, stream=None):
-        n = total_draft_rows
+        n, B = total_draft_rows, self._batch(cu_sl)
         dsde_verify(self.state, self.V, n, cu_sl, draft_tokens, target, draft, seeds,
-                    self.accepted_len, self.emitted[: n + self.B], self.kld[:n], self.flags[: n + self.B],
+                    self.accepted_len[:B], self.emitted[: n + B], self.kld[:n], self.flags[: n + B],
                     self.ws, stream)
 
     def signal_and_cap(self, cu_sl, budget=None, stream=None):
-        dsde_update_signal(self.state, self.slots, cu_sl, self.kld, self.accepted_len, self.sl_hat,
-                           self.diag, stream)
-        dsde_next_sl(self.state, self.slots, self.sl_hat, budget, self.next_sl, self.cap, self.comm, stream)
+        """Batch B = cu_sl.numel() - 1 <= the Step's size: slots [0, B) (the same slots dsde_step uses)."""
+        B = self._batch(cu_sl)
+        dsde_update_signal(self.state, self.slots[:B], cu_sl, self.kld, self.accepted_len[:B], self.sl_hat[:B],
+                           None if self.diag is None else self.diag[:B], stream)
+        dsde_next_sl(self.state, self.slots[:B], self.sl_hat[:B], budget, self.next_sl[:B], self.cap, self.comm,
+                     stream)
 
     def __call__(self, cu_sl, draft_tokens, target, draft, seeds, total_draft_rows: int, budget=None,
                  stream=None, fused: bool = True) -> StepOut:
-        n = total_draft_rows
-        if fused:  # one dsde_step call: stream kernel + tail kernel (+ the NCCL cap at N > 1)
-            dsde_step(self.state, self.V, n, self.slots, cu_sl, draft_tokens, target, draft, seeds, budget,
-                      self.accepted_len, self.emitted[: n + self.B], self.kld[:n], self.flags[: n + self.B],
-                      self.sl_hat, self.diag, self.next_sl, self.cap, self.ws, self.comm, stream)
+        n, B = total_draft_rows, self._batch(cu_sl)
+        diag = None if self.diag is None else self.diag[:B]
+        if fused:  # one dsde_step call (+ the NCCL cap at N > 1)
+            dsde_step(self.state, self.V, n, self.slots[:B], cu_sl, draft_tokens, target, draft, seeds, budget,
+                      self.accepted_len[:B], self.emitted[: n + B], self.kld[:n], self.flags[: n + B],
+                      self.sl_hat[:B], diag, self.next_sl[:B], self.cap, self.ws, self.comm, stream)
         else:
             self.verify(cu_sl, draft_tokens, target, draft, seeds, total_draft_rows, stream)
             self.signal_and_cap(cu_sl, budget, stream)
-        return StepOut(self.accepted_len, self.emitted[: n + self.B], self.kld[:n], self.flags[: n + self.B],
-                       self.sl_hat, self.next_sl, self.cap, self.diag)
+        return StepOut(self.accepted_len[:B], self.emitted[: n + B], self.kld[:n], self.flags[: n + B],
+                       self.sl_hat[:B], self.next_sl[:B], self.cap, diag)

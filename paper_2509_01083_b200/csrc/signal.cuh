@@ -53,7 +53,10 @@ __device__ __forceinline__ double wsum(double v) {
 // One warp per sequence. Lane m holds history observations m and m + 32
 // (most recent first, alpha = delta^m); the weighted mean and variance of
 // Eq.6-7 are two warp-wide fp64 passes over the short and long windows.
-__device__ __forceinline__ void signal_seq(const SignalArgs& a, int i) {
+// signal_seq_vals: the update from values in registers — lane j < k holds
+// the fp32 KLD of position j (as a double), acc = a_i in every lane (-1: the
+// verify flagged the sequence). signal_seq loads them from kld / acc_len.
+__device__ __forceinline__ void signal_seq_vals(const SignalArgs& a, int i, int k, double x, int acc) {
   const int lane = threadIdx.x & 31;
   const dsde_config& c = a.cfg;
   const int slot = a.slots[i];
@@ -66,8 +69,7 @@ __device__ __forceinline__ void signal_seq(const SignalArgs& a, int i) {
     return;
   }
   SeqState& s = a.seq[slot];
-  const int c0 = a.cu_sl[i], k = a.cu_sl[i + 1] - c0;
-  if (a.acc_len[i] < 0 || k < 1 || k > DSDE_MAX_SL || c0 < 0) {
+  if (acc < 0 || k < 1 || k > DSDE_MAX_SL) {
     if (lane == 0) {
       a.sl_hat[i] = c.sl_min;  // verify flagged this sequence; its state is left untouched
       s.last_sl_hat = c.sl_min;
@@ -75,8 +77,8 @@ __device__ __forceinline__ void signal_seq(const SignalArgs& a, int i) {
     if (dg && lane < 8) dg[lane] = NAN;
     return;
   }
+  if (lane >= k) x = 0.0;
   // 1-2: mu_last and the history append (Fig.5; D8)
-  const double x = lane < k ? (double)a.kld[c0 + lane] : 0.0;
   const double mu_last = wsum(x) / (double)k;
   const int cap = c.n_long;
   const int head0 = s.head, count0 = s.count;
@@ -103,7 +105,7 @@ __device__ __forceinline__ void signal_seq(const SignalArgs& a, int i) {
   double kld_sum = s.kld_sum, kld_max = s.kld_max;
   long long kld_cnt = s.kld_cnt;
   if (steps <= c.calib_steps) {
-    sl_a_max = max(sl_a_max, a.acc_len[i]);
+    sl_a_max = max(sl_a_max, acc);
     kld_sum += ksum;
     kld_cnt += k;
     kld_max = fmax(kld_max, kmax);
@@ -189,6 +191,14 @@ __device__ __forceinline__ void signal_seq(const SignalArgs& a, int i) {
     dg[6] = xr;
     dg[7] = (double)sl_max;
   }
+}
+
+__device__ __forceinline__ void signal_seq(const SignalArgs& a, int i) {
+  const int lane = threadIdx.x & 31;
+  const int c0 = a.cu_sl[i], k = a.cu_sl[i + 1] - c0;
+  const int acc = (c0 < 0 || k < 1 || k > DSDE_MAX_SL) ? -1 : a.acc_len[i];
+  const double x = (acc >= 0 && lane < k) ? (double)a.kld[c0 + lane] : 0.0;
+  signal_seq_vals(a, i, k, x, acc);
 }
 
 // Eq.11 integerised exactly (D14): q, r = divmod(sum, n); round half

@@ -1,17 +1,20 @@
-// verify_draw.cuh — a2-a4 of dsde_verify after the stream pass (included by
-// verify.cu inside namespace dsde; uses its helpers).
+// verify_draw.cuh — a2-a4 of the verification pass after the row stream
+// (included by verify.cu inside namespace dsde; uses its helpers). The same
+// device functions serve the persistent pass kernel (pass.cuh, the default
+// path of dsde_verify / dsde_step) and the staged kernels of the
+// vocab-parallel path (vocab.cu), so both give bit-identical results:
 //
-//   k_finalize  one CTA per sequence, one warp per draft position: fp64 merge of
-//               the row's slice partials (lanes over slices), KL, log p/q; then
-//               warp 0 runs the Philox accept test of every position, finds the
-//               first rejection a_i, lays out the emitted tokens and publishes
-//               the draw record (residual row a_i, or the bonus row k_i) (a2-a3).
-//   k_draw_*    every warp forms the draw weights of one 1024-token (bf16) /
-//               512-token (fp32) slice of the drawn row and writes their mass
-//               (a4, first pass); persistent warps as k_stream_ldg.
-//   k_select    one warp per sequence: the inverse CDF over the slice masses,
-//               then inside the crossing slice (re-read from L2)
-//               in ascending token order (a4, D7).
+//   row_finalize  one warp per draft row: fp64 merge of the row's slice
+//                 partials, KL(p||q), log p(x)/q(x) and the Philox accept test
+//                 of its position (a2) -> a RowRes record;
+//   seq_layout    one warp per sequence (lane j = position j): the first
+//                 rejection a_i, the emitted-token layout and the draw record
+//                 of the residual row a_i or the bonus row k_i (a3);
+//   draw_mass     one warp per (sequence, vocab slice): the draw-weight mass of
+//                 the slice of the drawn row (a4, first pass);
+//   select_seq    one warp per sequence: the inverse CDF over the slice masses,
+//                 then inside the crossing slice in ascending token order (a4,
+//                 D7).
 
 enum { IT_RESID = 1, IT_BONUS = 2, IT_NONE = 3, IT_ARGMAX = 4 };
 
@@ -31,319 +34,337 @@ struct FinArgs {
   uint8_t* flags;
   SeqRec* rec;
   int32_t* err;
-  int greedy;  // T = 0: accept iff x = argmax t, emit the argmax
-  int dev_rows;  // dsde_config.device_rows: total is a capacity, Σk_i = cu_sl[B]
-  float* ent;    // [Σk_i] optional out: draft entropy H(q) per row; partials carry Sd, E
+  int greedy;    // T = 0: accept iff x = argmax t, emit the argmax
+  int dev_rows;  // dsde_config.device_rows: total is a capacity, sum k_i = cu_sl[B]
+  float* ent;    // [sum k_i] optional out: draft entropy H(q) per row; partials carry Sd, E
+  int v0;        // vocabulary offset of the rows (vocab-parallel shard; 0 otherwise)
 };
 
-constexpr int kFinThreads = 32 * DSDE_MAX_SL;
-
-// One CTA (kFinThreads) per sequence i; the draw record goes to *out (global
-// or shared; written by one lane of warp 0, visible to the CTA after a barrier).
-// Warp 0's per-position inputs of the accept test (lane j = position j): the
-// Philox uniforms and the gathered t_x, d_x. They depend only on the step's
-// inputs, so k_tail gathers them before griddepcontrol.wait, while the stream
-// kernel still runs (the inputs were complete before the stream kernel began).
-struct FinPre {
-  Uniforms u;
-  float tx, dx;
-  int x;
+// Per-row result of row_finalize (64 bytes).
+struct RowRes {
+  double kl;   // KL(p || q)
+  double lam;  // log1p(y) = log sum_v p_v exp(-w_v)
+  double C;    // reference t - d (an fp32 value)
+  double S;    // sum_v exp(t_v - M)
+  float M;     // reference max of t
+  int amax;    // greedy: argmax of t (smallest index)
+  int bits;    // RR_* bits
+  int pad;
+  double pad2[2];
 };
+static_assert(sizeof(RowRes) == 64, "RowRes layout");
+enum { RR_FINITE = 1, RR_ACCEPT = 2, RR_NEAR = 4, RR_BADTOK = 8 };
 
-template <typename T>
-__device__ __forceinline__ FinPre fin_prefetch(const FinArgs& a, int i) {
-  const int lane = threadIdx.x & 31;
-  FinPre p;
-  p.u = Uniforms{0.0, 0.0};
-  p.tx = p.dx = 0.f;
-  p.x = -1;
-  const int c0 = __ldg(a.cu_sl + i), c1 = __ldg(a.cu_sl + i + 1);
-  const int k = c1 - c0;
-  if (!(c0 >= 0 && k >= 1 && k <= DSDE_MAX_SL && c1 <= a.total)) return p;  // finalize_seq reports it
-  const long long slot0 = (long long)c0 + i;
-  if (lane <= k) p.u = philox_uniforms(__ldg(a.seeds + slot0 + lane));
-  if (lane < k) {
-    const long long drow = (long long)c0 + lane;
-    p.x = __ldg(a.tokens + drow);
-    if (p.x >= 0 && p.x < a.V) {
-      p.tx = load_logit<T>(reinterpret_cast<const T*>(a.tl) + (drow + i) * a.ld_t + p.x);
-      p.dx = load_logit<T>(reinterpret_cast<const T*>(a.dl) + drow * a.ld_d + p.x);
-    }
-  }
-  return p;
-}
-
-// pre: warp 0's fin_prefetch results (k_tail), or nullptr to load them here.
-template <typename T>
-__device__ __forceinline__ void finalize_seq(const FinArgs& a, int i, SeqRec* out, const FinPre* pre = nullptr) {
-  __shared__ double s_kl[DSDE_MAX_SL], s_lam[DSDE_MAX_SL], s_C[DSDE_MAX_SL], s_S[DSDE_MAX_SL];
-  __shared__ int s_amax[DSDE_MAX_SL];
-  __shared__ float s_M[DSDE_MAX_SL];
-  __shared__ int s_fin[DSDE_MAX_SL];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c0 = __ldg(a.cu_sl + i), c1 = __ldg(a.cu_sl + i + 1);
-  const int k = c1 - c0;
+// Sequence i's row range and whether it is well formed: 1 <= k_i <= DSDE_MAX_SL,
+// rows inside the launch (and, unless device_rows, the last sequence ends at
+// total). `ok_rows` distinguishes DSDE_DERR_ROWS from DSDE_DERR_BAD_SL.
+__device__ __forceinline__ bool seq_ok(const FinArgs& a, int i, int& c0, int& k, bool* ok_rows = nullptr) {
+  c0 = __ldg(a.cu_sl + i);
+  const int c1 = __ldg(a.cu_sl + i + 1);
+  k = c1 - c0;
   const bool range_ok = c0 >= 0 && k >= 1 && k <= DSDE_MAX_SL && c1 <= a.total;
   const bool rows_ok = a.dev_rows || (i != a.B - 1) || (c1 == a.total);
-  if (!range_ok || !rows_ok) {
-    if (threadIdx.x == 0) {
-      a.acc_len[i] = -1;
-      out->mode = MODE_ERROR;
-      raise_device_error(a.err, range_ok ? DSDE_DERR_ROWS : DSDE_DERR_BAD_SL, i);
-    }
-    return;
+  if (ok_rows) *ok_rows = rows_ok;
+  return range_ok && rows_ok;
+}
+
+// ---------------------------------------------------------------------------
+// a2: fp64 merge of row r's slice partials (lanes over slices c) about
+// M = max_c M_c, C = fp32(M - max d). Slice c's w is shifted by Delta = C_c - C;
+// with s = e^(M_c - M), E1 = s e^-Delta:
+//   S += s S_c,  A += s (A_c + S_c Delta),
+//   D += E1 D_c - A_c s expm1(-Delta) + S_c s g(Delta),  g(x) = expm1(-x) + x.
+// Partials are read with ld.global.cg: in the pass kernel other SMs wrote them
+// during this launch. Result in every lane.
+// ---------------------------------------------------------------------------
+struct RowSums {
+  double S, A, D, Sd, E;
+  float M, Dmax;
+};
+
+__device__ __forceinline__ RowSums row_merge(const SubPartial* P, int nc, bool ent) {
+  const int lane = threadIdx.x & 31;
+  float Ml = -INFINITY, Dl = -INFINITY;
+  for (int c = lane; c < nc; c += 32) {
+    Ml = max_nan(Ml, __ldcg(&P[c].M));
+    Dl = fmaxf(Dl, __ldcg(&P[c].maxd));
   }
-  const int nc = a.nsub;
-  const int nwarps = blockDim.x >> 5;
-  for (int j = warp; j < k; j += nwarps) {
-    // ---- row j: fp64 merge of the slice partials (lanes over slices c)
-    // about M = max_c M_c, C = fp32(M - max d). Slice c's w is shifted by
-    // Delta = C_c - C; with s = e^(M_c - M), E1 = s e^-Delta:
-    //   S += s S_c,  A += s (A_c + S_c Delta),
-    //   D += E1 D_c - A_c s expm1(-Delta) + S_c s g(Delta),  g(x) = expm1(-x) + x.
-    const SubPartial* P = a.part + ((long long)c0 + j) * nc;
-    float Ml = -INFINITY, Dl = -INFINITY;
-    for (int c = lane; c < nc; c += 32) {
-      Ml = max_nan(Ml, P[c].M);
-      Dl = fmaxf(Dl, P[c].maxd);
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      Ml = max_nan(Ml, __shfl_xor_sync(kFull, Ml, o));
-      Dl = fmaxf(Dl, __shfl_xor_sync(kFull, Dl, o));
-    }
-    const double M = (double)Ml, C = (double)(Ml - Dl);  // C is an fp32 value
-    double S = 0.0, A = 0.0, D = 0.0, Sd = 0.0, E = 0.0;
-    for (int c = lane; c < nc; c += 32) {
-      const float4 q0 = __ldg(reinterpret_cast<const float4*>(P + c));
-      const float4 q1 = __ldg(reinterpret_cast<const float4*>(P + c) + 1);
-      const double qS = q0.x, qA = q0.y, qD = q0.z, qM = q0.w, qC = q1.x;
-      if (a.ent && q1.z > 0.f) {
-        // draft sums about the row max of d: Sd += s Sd_c, E += s (E_c + (maxd_c - maxd) Sd_c)
-        const double dd = (double)q1.y - (double)Dl, sd = exp(dd);
-        Sd += sd * (double)q1.z;
-        E += sd * ((double)q1.w + dd * (double)q1.z);
-      }
-      const double ls = qM - M;
-      const double s = exp(ls);
-      const double dl = qC - C;
-      double sem, sg, E1;
-      if (fabs(dl) < 1.0) {
-        const double em = expm1(-dl);
-        sem = s * em;
-        sg = s * (em + dl);
-        E1 = s + sem;
-      } else {
-        E1 = exp(ls - dl);
-        sem = E1 - s;
-        sg = sem + s * dl;
-      }
-      S += s * qS;
-      A += s * qA + s * qS * dl;
-      D += E1 * qD - qA * sem + qS * sg;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      S += __shfl_xor_sync(kFull, S, o);
-      A += __shfl_xor_sync(kFull, A, o);
-      D += __shfl_xor_sync(kFull, D, o);
-    }
-    if (a.ent) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        Sd += __shfl_xor_sync(kFull, Sd, o);
-        E += __shfl_xor_sync(kFull, E, o);
-      }
-      // H(q) = log Sd - E / Sd (E <= 0: both terms non-negative, no cancellation)
-      if (lane == 0) a.ent[c0 + j] = (float)(log(Sd) - E / Sd);
-    }
-    if (a.greedy) {
-      // row argmax of t: the first slice holding the row max (slices are in
-      // token order), re-read from memory vector by vector (token order is
-      // vector-major) until a lane holds the max; its first such element
-      constexpr int VEC = Traits<T>::VEC, SUB = sub_elems<T>();
-      unsigned cs = 0x7fffffffu;
-      for (int c = lane; c < nc; c += 32)
-        if (P[c].M == Ml) cs = min(cs, (unsigned)c);
-      cs = __reduce_min_sync(kFull, cs);
-      int amax = 0x7fffffff;
-      if (cs < (unsigned)nc) {
-        const T* trow = reinterpret_cast<const T*>(a.tl) + ((long long)c0 + i + j) * a.ld_t + cs * SUB;
-        const int left = a.V - (int)cs * SUB;
-        for (int v = 0; v * 32 * VEC < min(SUB, left); ++v) {
-          const int e0 = (v * 32 + lane) * VEC;
-          int first = 0x7fffffff;
-#pragma unroll
-          for (int e = VEC - 1; e >= 0; --e)
-            if (e0 + e < left && load_logit<T>(trow + e0 + e) == Ml) first = e0 + e;
-          const unsigned hit = __ballot_sync(kFull, first != 0x7fffffff);
-          if (hit) {
-            amax = (int)cs * SUB + __shfl_sync(kFull, first, __ffs(hit) - 1);
-            break;
-          }
-        }
-      }
-      if (lane == 0) s_amax[j] = amax;
-    }
-    if (lane == 0) {
-      // y = E_p[exp(-w)] - 1. KL = D/S + (log1p(y) - y) has no cancellation for
-      // small KL; when y > 1 (the draft puts far more mass away from the
-      // reference, e.g. disjoint supports) the equal form A/S + log1p(y) is used.
-      const double y = (D - A) / S;
-      const double lam = log1p(y);
-      const double kl = fmax(0.0, y <= 1.0 ? D / S + (lam - y) : A / S + lam);
-      s_kl[j] = kl;
-      s_lam[j] = lam;
-      s_C[j] = C;
-      s_M[j] = Ml;
-      s_S[j] = S;
-      s_fin[j] = isfinite(S) && isfinite(A) && isfinite(D) && S > 0.0 && isfinite(M) &&
-                    isfinite(C) && isfinite(kl);
-    }
+  for (int o = 16; o > 0; o >>= 1) {
+    Ml = max_nan(Ml, __shfl_xor_sync(kFull, Ml, o));
+    Dl = fmaxf(Dl, __shfl_xor_sync(kFull, Dl, o));
   }
-  __syncthreads();
-  if (warp != 0) return;
-  // ---- warp 0, lane j = position j: accept test, first rejection, layout ----
-  const long long slot0 = (long long)c0 + i;
-  double lr = 0.0;
-  bool acc = false, near = false, bad_tok = false, nonfin = false;
-  Uniforms u = {0.0, 0.0};
-  if (pre) u = pre->u;
-  else if (lane <= k) u = philox_uniforms(__ldg(a.seeds + slot0 + lane));
-  if (lane < k) {
-    const long long drow = (long long)c0 + lane;
-    const int x = pre ? pre->x : __ldg(a.tokens + drow);
-    bad_tok = x < 0 || x >= a.V;
-    nonfin = !s_fin[lane];
-    if (!bad_tok) {
-      const T* tp = reinterpret_cast<const T*>(a.tl) + (drow + i) * a.ld_t;
-      const T* dp = reinterpret_cast<const T*>(a.dl) + drow * a.ld_d;
-      const double tx = (double)(pre ? pre->tx : load_logit<T>(tp + x));
-      const double dx = (double)(pre ? pre->dx : load_logit<T>(dp + x));
-      lr = (tx - dx) - s_C[lane] + s_lam[lane];
-      nonfin |= !isfinite(lr);
+  const double M = (double)Ml, C = (double)(Ml - Dl);  // C is an fp32 value
+  double S = 0.0, A = 0.0, D = 0.0, Sd = 0.0, E = 0.0;
+  for (int c = lane; c < nc; c += 32) {
+    const float4 q0 = __ldcg(reinterpret_cast<const float4*>(P + c));
+    const float4 q1 = __ldcg(reinterpret_cast<const float4*>(P + c) + 1);
+    const double qS = q0.x, qA = q0.y, qD = q0.z, qM = q0.w, qC = q1.x;
+    if (ent && q1.z > 0.f) {
+      // draft sums about the row max of d: Sd += s Sd_c, E += s (E_c + (maxd_c - maxd) Sd_c)
+      const double dd = (double)q1.y - (double)Dl, sd = exp(dd);
+      Sd += sd * (double)q1.z;
+      E += sd * ((double)q1.w + dd * (double)q1.z);
     }
-    if (a.greedy) {
-      acc = x == s_amax[lane];  // T = 0: the draft token must be the target argmax
+    const double ls = qM - M;
+    const double s = exp(ls);
+    const double dl = qC - C;
+    double sem, sg, E1;
+    if (fabs(dl) < 1.0) {
+      const double em = expm1(-dl);
+      sem = s * em;
+      sg = s * (em + dl);
+      E1 = s + sem;
     } else {
-      const double pacc = lr >= 0.0 ? 1.0 : exp(lr);
-      acc = u.acc < pacc;
-      near = fabs(u.acc - pacc) < 1e-6;
+      E1 = exp(ls - dl);
+      sem = E1 - s;
+      sg = sem + s * dl;
+    }
+    S += s * qS;
+    A += s * qA + s * qS * dl;
+    D += E1 * qD - qA * sem + qS * sg;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    S += __shfl_xor_sync(kFull, S, o);
+    A += __shfl_xor_sync(kFull, A, o);
+    D += __shfl_xor_sync(kFull, D, o);
+  }
+  if (ent) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      Sd += __shfl_xor_sync(kFull, Sd, o);
+      E += __shfl_xor_sync(kFull, E, o);
     }
   }
-  const unsigned bt = __ballot_sync(kFull, bad_tok);
-  const unsigned nf = __ballot_sync(kFull, nonfin);
-  const unsigned am = __ballot_sync(kFull, acc);
+  return RowSums{S, A, D, Sd, E, Ml, Dl};
+}
+
+// Greedy (T = 0): row argmax of t, smallest index among equal maxima (D18): the
+// first slice holding the row max (slices are in token order), re-read vector
+// by vector (token order is vector-major) until a lane holds the max.
+template <typename T>
+__device__ __forceinline__ int row_argmax(const FinArgs& a, const SubPartial* P, int nc, float Ml,
+                                          const T* trow) {
+  constexpr int VEC = Traits<T>::VEC, SUB = sub_elems<T>();
+  const int lane = threadIdx.x & 31;
+  unsigned cs = 0x7fffffffu;
+  for (int c = lane; c < nc; c += 32)
+    if (__ldcg(&P[c].M) == Ml) cs = min(cs, (unsigned)c);
+  cs = __reduce_min_sync(kFull, cs);
+  int amax = 0x7fffffff;
+  if (cs < (unsigned)nc) {
+    const T* row = trow + cs * SUB;
+    const int left = a.V - (int)cs * SUB;
+    for (int v = 0; v * 32 * VEC < min(SUB, left); ++v) {
+      const int e0 = (v * 32 + lane) * VEC;
+      int first = 0x7fffffff;
+#pragma unroll
+      for (int e = VEC - 1; e >= 0; --e)
+        if (e0 + e < left && load_logit<T>(row + e0 + e) == Ml) first = e0 + e;
+      const unsigned hit = __ballot_sync(kFull, first != 0x7fffffff);
+      if (hit) {
+        amax = a.v0 + (int)cs * SUB + __shfl_sync(kFull, first, __ffs(hit) - 1);
+        break;
+      }
+    }
+  }
+  return amax;
+}
+
+// a2 for draft row r = cu_sl[i] + j (one warp). The accept-test inputs (Philox
+// uniform of slot cu_sl[i] + i + j, token x, t_x, d_x) are gathered first so
+// their latency overlaps the merge. Returns the record in every lane.
+template <typename T>
+__device__ __forceinline__ RowRes row_finalize(const FinArgs& a, int r, int i) {
+  const int lane = threadIdx.x & 31;
+  const long long slot = (long long)r + i;
+  const T* trow = reinterpret_cast<const T*>(a.tl) + slot * a.ld_t;
+  const T* drow = reinterpret_cast<const T*>(a.dl) + (long long)r * a.ld_d;
+  int x = 0;
+  float tx = 0.f, dx = 0.f;
+  double uacc = 0.0;
+  if (lane == 0) {
+    x = __ldg(a.tokens + r);
+    if (x >= 0 && x < a.V) {
+      tx = load_logit<T>(trow + x);
+      dx = load_logit<T>(drow + x);
+    }
+    if (!a.greedy) uacc = philox_uniforms(__ldg(a.seeds + slot)).acc;
+  }
+  const SubPartial* P = a.part + (long long)r * a.nsub;
+  const RowSums R = row_merge(P, a.nsub, a.ent != nullptr);
+  int amax = 0;
+  if (a.greedy) amax = row_argmax<T>(a, P, a.nsub, R.M, trow);
+  RowRes rr;
+  rr.pad = 0;
+  rr.pad2[0] = rr.pad2[1] = 0.0;
+  rr.amax = amax;
+  rr.M = R.M;
+  rr.C = (double)(R.M - R.Dmax);
+  rr.S = R.S;
+  // y = E_p[exp(-w)] - 1. KL = D/S + (log1p(y) - y) has no cancellation for
+  // small KL; when y > 1 (the draft puts far more mass away from the
+  // reference, e.g. disjoint supports) the equal form A/S + log1p(y) is used.
+  const double y = (R.D - R.A) / R.S;
+  rr.lam = log1p(y);
+  rr.kl = fmax(0.0, y <= 1.0 ? R.D / R.S + (rr.lam - y) : R.A / R.S + rr.lam);
+  bool fin = isfinite(R.S) && isfinite(R.A) && isfinite(R.D) && R.S > 0.0 && isfinite((double)R.M) &&
+             isfinite(rr.C) && isfinite(rr.kl);
+  int bits = 0;
+  if (lane == 0) {
+    if (a.ent) a.ent[r] = (float)(log(R.Sd) - R.E / R.Sd);  // H(q) = log Sd - E / Sd (E <= 0)
+    if (x < 0 || x >= a.V) {
+      bits |= RR_BADTOK;
+    } else {
+      const double lr = ((double)tx - (double)dx) - rr.C + rr.lam;  // log p(x) - log q(x)
+      fin = fin && isfinite(lr);
+      if (a.greedy) {
+        if (x == amax) bits |= RR_ACCEPT;  // T = 0: the draft token must be the target argmax
+      } else {
+        const double pacc = lr >= 0.0 ? 1.0 : exp(lr);
+        if (uacc < pacc) bits |= RR_ACCEPT;
+        if (fabs(uacc - pacc) < 1e-6) bits |= RR_NEAR;
+      }
+    }
+    if (fin) bits |= RR_FINITE;
+  }
+  rr.bits = __shfl_sync(kFull, bits, 0);
+  return rr;
+}
+
+__device__ __forceinline__ void store_rowres(RowRes* dst, const RowRes& r) {
+  if ((threadIdx.x & 31) == 0) *dst = r;
+}
+
+__device__ __forceinline__ RowRes load_rowres(const RowRes* p) {
+  RowRes r;
+  const double2 a0 = __ldcg(reinterpret_cast<const double2*>(p));
+  const double2 a1 = __ldcg(reinterpret_cast<const double2*>(p) + 1);
+  const int4 b = __ldcg(reinterpret_cast<const int4*>(p) + 2);
+  r.kl = a0.x;
+  r.lam = a0.y;
+  r.C = a1.x;
+  r.S = a1.y;
+  r.M = __int_as_float(b.x);
+  r.amax = b.y;
+  r.bits = b.z;
+  r.pad = 0;
+  r.pad2[0] = r.pad2[1] = 0.0;
+  return r;
+}
+
+// Outputs of a sequence with a data error: accepted_len -1, all-pad tokens, NaN KLD.
+__device__ __forceinline__ void seq_error_outputs(const FinArgs& a, int i, int c0, int k, int code) {
+  const int lane = threadIdx.x & 31;
+  const long long slot0 = (long long)c0 + i;
+  for (int j = lane; j < k; j += 32) a.kld[c0 + j] = NAN;
+  for (int j = lane; j <= k; j += 32) {
+    a.emitted[slot0 + j] = DSDE_PAD;
+    if (a.flags) a.flags[slot0 + j] = 0;
+  }
+  if (lane == 0) {
+    a.acc_len[i] = -1;
+    raise_device_error(a.err, code, i);
+  }
+}
+
+__device__ __forceinline__ SeqRec error_rec(long long slot0) {
   SeqRec r;
+  r.mode = MODE_ERROR;
+  r.slot = (int)slot0;
+  r.trow = slot0;
+  r.drow = -1;
+  r.M = 0.f;
   r.pad0 = 0;
-  r.S = 0.0;
+  r.C = r.lam = r.u = r.S = 0.0;
+  return r;
+}
+
+// a3 (one warp; lane j < k holds position j's RowRes): the first rejection a_i,
+// KLDs, the emitted-token layout (x_0 .. x_{a-1}, the drawn token at a, pads
+// after), flags and the draw record (written by lane a to *out).
+// Returns a_i (-1 on a data error) in every lane.
+__device__ __forceinline__ int seq_layout(const FinArgs& a, int i, int c0, int k, const RowRes& rr,
+                                          SeqRec* out) {
+  const int lane = threadIdx.x & 31;
+  const long long slot0 = (long long)c0 + i;
+  const unsigned bt = __ballot_sync(kFull, lane < k && (rr.bits & RR_BADTOK));
+  const unsigned nf = __ballot_sync(kFull, lane < k && !(rr.bits & RR_FINITE));
+  const unsigned am = __ballot_sync(kFull, lane < k && (rr.bits & RR_ACCEPT));
   if (bt | nf) {
-    if (lane < k) a.kld[c0 + lane] = NAN;
-    if (lane <= k) {
-      a.emitted[slot0 + lane] = DSDE_PAD;
-      if (a.flags) a.flags[slot0 + lane] = 0;
-    }
-    if (lane == 0) {
-      a.acc_len[i] = -1;
-      raise_device_error(a.err, bt ? DSDE_DERR_BAD_TOKEN : DSDE_DERR_NONFINITE, i);
-      r.mode = MODE_ERROR;
-      r.slot = (int)slot0;
-      r.trow = slot0;
-      r.drow = -1;
-      r.M = 0.f;
-      r.C = r.lam = r.u = 0.0;
-      *out = r;
-    }
-    return;
+    seq_error_outputs(a, i, c0, k, bt ? DSDE_DERR_BAD_TOKEN : DSDE_DERR_NONFINITE);
+    if (lane == 0) *out = error_rec(slot0);
+    return -1;
   }
   const int acc_run = __ffs(~am) - 1;  // first rejected lane (lanes >= k never accept)
   const int aa = acc_run < k ? acc_run : k;
-  if (lane < k) a.kld[c0 + lane] = (float)s_kl[lane];
+  if (lane < k) a.kld[c0 + lane] = (float)rr.kl;
   if (lane <= k) {
     a.emitted[slot0 + lane] = lane < aa ? __ldg(a.tokens + c0 + lane) : DSDE_PAD;
-    if (a.flags) a.flags[slot0 + lane] = (near && lane <= aa && lane < k) ? DSDE_FLAG_ACCEPT_NEAR_TIE : 0;
+    if (a.flags)
+      a.flags[slot0 + lane] = ((rr.bits & RR_NEAR) && lane <= aa && lane < k) ? DSDE_FLAG_ACCEPT_NEAR_TIE : 0;
   }
   if (lane == 0) a.acc_len[i] = aa;
-  if (lane == aa && a.greedy) {
-    // T = 0: the recovery token is the argmax of row aa (known from the stream);
-    // the bonus row's argmax is found by the draw pass
+  if (lane == aa) {
+    SeqRec r;
+    r.pad0 = 0;
+    r.S = 0.0;
     r.slot = (int)(slot0 + aa);
     r.trow = slot0 + aa;
     r.drow = -1;
-    r.u = 0.0;
     r.M = 0.f;
-    r.C = r.lam = 0.0;
-    if (aa < k) {
-      a.emitted[slot0 + aa] = s_amax[aa];
-      r.mode = MODE_NONE;
+    r.C = r.lam = r.u = 0.0;
+    if (a.greedy) {
+      // T = 0: the recovery token is the argmax of row aa (known from its
+      // finalize); the bonus row's argmax is found by the draw pass
+      if (aa < k) {
+        a.emitted[slot0 + aa] = rr.amax;
+        r.mode = MODE_NONE;
+      } else {
+        r.mode = MODE_ARGMAX;
+      }
     } else {
-      r.mode = MODE_ARGMAX;
-    }
-    *out = r;
-  } else if (lane == aa) {
-    r.slot = (int)(slot0 + aa);
-    r.trow = slot0 + aa;
-    r.u = u.smp;
-    if (aa < k) {
-      r.mode = MODE_RESIDUAL;
-      r.drow = (long long)c0 + aa;
-      r.M = s_M[aa];
-      r.C = s_C[aa];
-      r.lam = s_lam[aa];
-      r.S = s_S[aa];
-    } else {
-      r.mode = MODE_BONUS;
-      r.drow = -1;
-      r.M = 0.f;
-      r.C = 0.0;
-      r.lam = 0.0;
+      r.u = philox_uniforms(__ldg(a.seeds + slot0 + aa)).smp;
+      if (aa < k) {
+        r.mode = MODE_RESIDUAL;
+        r.drow = (long long)c0 + aa;
+        r.M = rr.M;
+        r.C = rr.C;
+        r.lam = rr.lam;
+        r.S = rr.S;
+      } else {
+        r.mode = MODE_BONUS;
+      }
     }
     *out = r;
   }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kFinThreads) k_finalize(FinArgs a) {
-  finalize_seq<T>(a, blockIdx.x, a.rec + blockIdx.x);
+  return aa;
 }
 
 // ---------------------------------------------------------------------------
-// draw weights of one lane over a 1024-token (bf16) / 512-token (fp32)
-// sub-chunk u, token u*SUB + (v*32 + lane)*VEC + e, from raw words; returns the
-// reference (residual: M of the row; bonus: warp max of t).
+// Draw weights of one lane over the slice u of a row (NV 16-byte vectors per
+// lane, token u*SUB + (v*32 + lane)*VEC + e), from raw words; the reference
+// (residual: M of the row; bonus: warp max of t over the slice):
 //   residual: rho_v = e_v (1 - exp(-z_v)) for z_v > 0, else 0, with
 //             e_v = exp(t_v - M), z_v = w_v + lam, w_v = (t_v - d_v) - C exact,
 //             lam added as hi + lo floats; 1 - exp(-z) = z (1 - z h(-z)) for
-//             z < 1 (no cancellation), 1 - 2^(-z log2 e) otherwise;
-//   bonus:    p_v up to a scale: exp(t_v - m_u) about the warp max m_u,
-//             rescaled by exp(m_u - max_u m_u) in fp64 by k_select.
+//             |z| < 1 (no cancellation), 1 - 2^(-z log2 e) otherwise;
+//   bonus:    p_v up to a scale: exp(t_v - m_u) about the slice max m_u,
+//             rescaled by exp(m_u - max_u m_u) in fp64 by the select.
 // The select recomputes every weight bit-identically from the same words.
 // ---------------------------------------------------------------------------
-// degree of the h(-z) fit on |z| < 1 in the residual weights
-#ifndef DSDE_RESID_DEG
-#define DSDE_RESID_DEG 6
-#endif
-// residual weights of one element pair (see above)
 template <typename T>
 __device__ __forceinline__ float2 resid_pair_exact(float2 tt, float2 dd, float2 nML2, float khi, float klo) {
   const float2 L2 = make_float2(kLog2e, kLog2e), nL2 = make_float2(-kLog2e, -kLog2e);
   const float2 ONE = make_float2(1.f, 1.f);
-#if DSDE_RESID_DEG == 7  // degree 7 on |z| <= 1 (1.1e-7 relative)
-  const float2 K7 = make_float2(-2.812654656736413e-06f, -2.812654656736413e-06f);
-  const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
-  const float2 K5 = make_float2(-1.9836986029986292e-04f, -1.9836986029986292e-04f);
-  const float2 K4 = make_float2(1.3885394437238574e-03f, 1.3885394437238574e-03f);
-  const float2 K3 = make_float2(-8.33334494382143e-03f, -8.33334494382143e-03f);
-  const float2 K2 = make_float2(4.166673496365547e-02f, 4.166673496365547e-02f);
-  const float2 K1 = make_float2(-1.666666716337204e-01f, -1.666666716337204e-01f);
-#else  // degree 6 on |z| <= 1 (2.0e-7 relative; the stream's exact-path fit)
+  // degree 6 on |z| <= 1 (2.0e-7 relative; tools/fit_g.py --deg 6)
   const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
   const float2 K5 = make_float2(-2.0329201652202755e-04f, -2.0329201652202755e-04f);
   const float2 K4 = make_float2(1.3885394437238574e-03f, 1.3885394437238574e-03f);
   const float2 K3 = make_float2(-8.330884389579296e-03f, -8.330884389579296e-03f);
   const float2 K2 = make_float2(4.166673496365547e-02f, 4.166673496365547e-02f);
   const float2 K1 = make_float2(-1.6666696965694427e-01f, -1.6666696965694427e-01f);
-#endif
   const float2 K0 = make_float2(0.5f, 0.5f);
   const float2 xt = __ffma2_rn(tt, L2, nML2);
   const float2 ev = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));  // 0 for padding
@@ -355,12 +376,7 @@ __device__ __forceinline__ float2 resid_pair_exact(float2 tt, float2 dd, float2 
     z = make_float2(diff_ref<T>(tt.x, dd.x, khi), diff_ref<T>(tt.y, dd.y, khi));
   }
   z = __fadd2_rn(z, make_float2(-klo, -klo));
-#if DSDE_RESID_DEG == 7
-  float2 pz = __ffma2_rn(K7, z, K6);
-  pz = __ffma2_rn(pz, z, K5);
-#else
   float2 pz = __ffma2_rn(K6, z, K5);
-#endif
   pz = __ffma2_rn(pz, z, K4);
   pz = __ffma2_rn(pz, z, K3);
   pz = __ffma2_rn(pz, z, K2);
@@ -396,15 +412,14 @@ struct DrawRef {
   float m;            // bonus: the slice's warp max of t (reference)
 };
 
-// Warp-wide max of t over a lane's NV vectors (NaN-propagating; packed
+// Warp-wide max of t over a lane's N vectors (NaN-propagating; packed
 // max.NaN.bf16x2 for bf16: max is exact, so any grouping gives the same value).
-template <typename T, int NV>
-__device__ __forceinline__ float slice_tmax(const uint4 (&rt)[NV]) {
-  float m;
+template <typename T, int N>
+__device__ __forceinline__ float lane_tmax(const uint4 (&rt)[N], float m) {
   if constexpr (sizeof(T) == 2) {
     __nv_bfloat162 b0 = __floats2bfloat162_rn(-INFINITY, -INFINITY), b1 = b0;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
+    for (int v = 0; v < N; ++v) {
       const uint32_t w4[4] = {rt[v].x, rt[v].y, rt[v].z, rt[v].w};
       b0 = __hmax2_nan(b0, *reinterpret_cast<const __nv_bfloat162*>(&w4[0]));
       b1 = __hmax2_nan(b1, *reinterpret_cast<const __nv_bfloat162*>(&w4[1]));
@@ -412,27 +427,28 @@ __device__ __forceinline__ float slice_tmax(const uint4 (&rt)[NV]) {
       b1 = __hmax2_nan(b1, *reinterpret_cast<const __nv_bfloat162*>(&w4[3]));
     }
     const __nv_bfloat162 b = __hmax2_nan(b0, b1);
-    m = max_nan(__low2float(b), __high2float(b));
+    return max_nan(m, max_nan(__low2float(b), __high2float(b)));
   } else {
-    m = -INFINITY;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) m = vec_tmax<T>(rt[v], m);
+    for (int v = 0; v < N; ++v) m = vec_tmax<T>(rt[v], m);
+    return m;
   }
+}
+
+__device__ __forceinline__ float warp_max_nan(float m) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(kFull, m, o));
   return m;
 }
 
-// Slice constants; for the bonus row the warp-wide max of t over the slice.
-template <typename T, int NV>
-__device__ __forceinline__ DrawRef draw_ref(const uint4 (&rt)[NV], bool resid, float M, float Cf, double lam) {
+__device__ __forceinline__ DrawRef draw_ref(bool resid, float M, float Cf, double lam, float m) {
   DrawRef R;
   R.resid = resid;
   R.M = M;
   const double K = (double)Cf - lam;
   R.khi = (float)K;
   R.klo = (float)(K - (double)R.khi);
-  R.m = resid ? 0.f : slice_tmax<T, NV>(rt);
+  R.m = m;
   return R;
 }
 
@@ -469,14 +485,15 @@ __device__ __forceinline__ void vec_weights(const uint4& t4, const uint4& d4, co
   }
 }
 
-// raw words of sub-chunk u of a row, from global memory (select pass)
-template <typename T, int NV>
-__device__ __forceinline__ void load_sub_raw(const T* row, int V, int u, uint4 (&r)[NV]) {
-  constexpr int VEC = Traits<T>::VEC, SUB = 32 * VEC * NV;
+// raw words of vectors [v0, v0 + N) of slice u of a row (draw / select passes;
+// L2-resident data: ld.global.cg)
+template <typename T, int N>
+__device__ __forceinline__ void load_vecs(const T* row, int V, int u, int v0, uint4 (&r)[N]) {
+  constexpr int VEC = Traits<T>::VEC, SUB = sub_elems<T>();
   const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    const int e0 = u * SUB + (v * 32 + lane) * VEC;
+  for (int v = 0; v < N; ++v) {
+    const int e0 = u * SUB + ((v0 + v) * 32 + lane) * VEC;
     if (e0 + VEC <= V) {
       r[v] = __ldcg(reinterpret_cast<const uint4*>(row + e0));
     } else {
@@ -486,12 +503,6 @@ __device__ __forceinline__ void load_sub_raw(const T* row, int V, int u, uint4 (
       r[v] = *reinterpret_cast<const uint4*>(b);
     }
   }
-}
-
-__device__ __forceinline__ double wsum_d(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  return v;
 }
 
 __device__ __forceinline__ double wscan_d(double x, int lane) {
@@ -506,8 +517,7 @@ __device__ __forceinline__ double wscan_d(double x, int lane) {
 // sum_v (sum over the 32 lanes of x[v]) in vector order, valid in lane 0: the
 // NV per-vector warp sums by recursive halving (the first log2(NV) butterfly
 // rounds exchange half of the remaining vectors, so each round moves one
-// double per kept vector instead of one per vector), lanes 8 j .. hold vector
-// j's total (NV = 4), then lane 0 gathers them.
+// double per kept vector instead of one per vector), then lane 0 gathers them.
 template <int NV>
 __device__ __forceinline__ double warp_sum_vectors(double (&x)[NV]) {
   static_assert(NV == 1 || NV == 2 || NV == 4 || NV == 8, "NV");
@@ -539,134 +549,115 @@ __device__ __forceinline__ double warp_sum_vectors(double (&x)[NV]) {
 }
 
 // ---------------------------------------------------------------------------
-// a4 first pass: units q = (sequence i, slice u), q = i * nsub + u. Each warp
-// writes the mass of its slice's draw weights and the slice reference.
+// a4 first pass, one warp: the draw-weight mass of slice u of sequence i's
+// drawn row (record r), written to mass_out / ref_out (lane 0). The slice is
+// processed in chunks of DCH vectors per lane (registers); the mass is the
+// chunks' fp64 warp sums added in order, each the per-vector fp32 lane sums
+// summed over lanes in fp64 (warp_sum_vectors). Greedy bonus rows (ARGMAX)
+// record the slice max of t and its first index instead.
 // ---------------------------------------------------------------------------
-struct DrawArgs {
-  int B, V, nsub;
-  const void* tl;
-  long long ld_t;
-  const void* dl;
-  long long ld_d;
-  const SeqRec* rec;
-  double* smass;  // [B * nsub]
-  float* sref;    // [B * nsub]
-};
-
-struct DrawUnit {
-  int type;  // IT_RESID / IT_BONUS / IT_NONE
-  float M, Cf;
-  double lam;
+template <typename T>
+struct DrawChunk {
+  static constexpr int N = Traits<T>::NV < 4 ? Traits<T>::NV : 4;
 };
 
 template <typename T>
-__device__ __forceinline__ DrawUnit draw_unit_load(const DrawArgs& a, int u, const SeqRec& r,
-                                                   uint4 (&rt)[Traits<T>::NVD], uint4 (&rd)[Traits<T>::NVD]) {
+__device__ __forceinline__ void draw_mass(const SeqRec& r, int u, int V, const void* tl, long long ld_t,
+                                          const void* dl, long long ld_d, double* mass_out, float* ref_out) {
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, CH = DrawChunk<T>::N;
+  const int lane = threadIdx.x & 31;
   const int mode = r.mode;
-  DrawUnit d;
-  d.type = mode == MODE_RESIDUAL ? IT_RESID : mode == MODE_BONUS ? IT_BONUS : mode == MODE_ARGMAX ? IT_ARGMAX : IT_NONE;
-  d.M = 0.f;
-  d.Cf = 0.f;
-  d.lam = 0.0;
-  if (d.type == IT_NONE) return d;
-  load_slice<T>(reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t, a.V, u, rt);
-  if (d.type == IT_RESID) {
-    load_slice<T>(reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d, a.V, u, rd);
-    d.M = r.M;
-    d.Cf = (float)r.C;
-    d.lam = r.lam;
-  }
-  return d;
-}
-
-template <typename T>
-__device__ __forceinline__ DrawUnit draw_unit_load(const DrawArgs& a, long long q, uint4 (&rt)[Traits<T>::NVD],
-                                                   uint4 (&rd)[Traits<T>::NVD]) {
-  const SeqRec* rp = a.rec + (int)(q / a.nsub);
-  SeqRec r;
-  r.mode = __ldg(&rp->mode);
-  if (r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS || r.mode == MODE_ARGMAX) {
-    r.trow = __ldg(&rp->trow);
-    r.drow = __ldg(&rp->drow);
-    r.M = __ldg(&rp->M);
-    r.C = __ldg(&rp->C);
-    r.lam = __ldg(&rp->lam);
-  }
-  return draw_unit_load<T>(a, (int)(q - (q / a.nsub) * a.nsub), r, rt, rd);
-}
-
-// mass_out / ref_out: this unit's record (global a.smass + q, or the k_tail
-// CTA's shared arrays)
-template <typename T>
-__device__ __forceinline__ void draw_unit_finish(double* mass_out, float* ref_out, const DrawUnit& d,
-                                                 const uint4 (&rt)[Traits<T>::NVD],
-                                                 const uint4 (&rd)[Traits<T>::NVD]) {
-  constexpr int VEC = Traits<T>::VEC, NVD = Traits<T>::NVD;
-  if (d.type == IT_NONE) return;
-  if (d.type == IT_ARGMAX) {
-    // greedy bonus row: the slice max of t and its first (slice-local) index
-    const int lane = threadIdx.x & 31;
-    const float m = slice_tmax<T, NVD>(rt);
-    int best = 0x7fffffff;
-#pragma unroll
-    for (int v = NVD - 1; v >= 0; --v) {
-      const uint4 x[1] = {rt[v]};
-#pragma unroll
-      for (int h = VEC - 2; h >= 0; h -= 2) {
-        const float2 tt = pair_of<T>(x, h);
-        const int e0 = (v * 32 + lane) * VEC + h;
-        if (tt.y == m) best = e0 + 1;
-        if (tt.x == m) best = e0;
-      }
+  if (mode != MODE_RESIDUAL && mode != MODE_BONUS && mode != MODE_ARGMAX) return;
+  const T* tp = reinterpret_cast<const T*>(tl) + r.trow * ld_t;
+  const T* dp = mode == MODE_RESIDUAL ? reinterpret_cast<const T*>(dl) + r.drow * ld_d : nullptr;
+  if (mode != MODE_RESIDUAL) {
+    // bonus / argmax: the slice max of t first (the reference of the weights)
+    float m = -INFINITY;
+#pragma unroll 1
+    for (int c = 0; c < NV; c += CH) {
+      uint4 rt[CH];
+      load_vecs<T, CH>(tp, V, u, c, rt);
+      m = lane_tmax<T, CH>(rt, m);
     }
-    best = (int)__reduce_min_sync(kFull, (unsigned)best);
+    m = warp_max_nan(m);
+    if (mode == MODE_ARGMAX) {
+      int best = 0x7fffffff;
+#pragma unroll 1
+      for (int c = NV - CH; c >= 0; c -= CH) {
+        uint4 rt[CH];
+        load_vecs<T, CH>(tp, V, u, c, rt);
+#pragma unroll
+        for (int v = CH - 1; v >= 0; --v) {
+          const uint4 x[1] = {rt[v]};
+#pragma unroll
+          for (int h = VEC - 2; h >= 0; h -= 2) {
+            const float2 tt = pair_of<T>(x, h);
+            const int e0 = ((c + v) * 32 + lane) * VEC + h;
+            if (tt.y == m) best = e0 + 1;
+            if (tt.x == m) best = e0;
+          }
+        }
+      }
+      best = (int)__reduce_min_sync(kFull, (unsigned)best);
+      if (lane == 0) {
+        *mass_out = (double)best;
+        *ref_out = m;
+      }
+      return;
+    }
+    const DrawRef R = draw_ref(false, 0.f, 0.f, 0.0, m);
+    double tot = 0.0;
+#pragma unroll 1
+    for (int c = 0; c < NV; c += CH) {
+      uint4 rt[CH];
+      load_vecs<T, CH>(tp, V, u, c, rt);
+      double x[CH];
+#pragma unroll
+      for (int v = 0; v < CH; ++v) {
+        float w[VEC];
+        vec_weights<T>(rt[v], rt[v], R, w);
+        float ls = 0.f;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) ls += w[e];
+        x[v] = (double)ls;
+      }
+      tot += warp_sum_vectors<CH>(x);
+    }
     if (lane == 0) {
-      *mass_out = (double)best;
-      *ref_out = m;
+      *mass_out = tot;
+      *ref_out = m <= -1e30f ? -INFINITY : m;
     }
     return;
   }
-  const DrawRef R = draw_ref<T>(rt, d.type == IT_RESID, d.M, d.Cf, d.lam);
-  // mass in the select pass's grouping: per vector an fp32 lane sum, an fp64
-  // sum over the 32 lanes, the vectors added in order
-  double x[NVD];
+  const DrawRef R = draw_ref(true, r.M, (float)r.C, r.lam, 0.f);
+  double tot = 0.0;
+#pragma unroll 1
+  for (int c = 0; c < NV; c += CH) {
+    uint4 rt[CH], rd[CH];
+    load_vecs<T, CH>(tp, V, u, c, rt);
+    load_vecs<T, CH>(dp, V, u, c, rd);
+    double x[CH];
 #pragma unroll
-  for (int v = 0; v < NVD; ++v) {
-    float w[VEC];
-    vec_weights<T>(rt[v], rd[v], R, w);
-    float ls = 0.f;
+    for (int v = 0; v < CH; ++v) {
+      float w[VEC];
+      vec_weights<T>(rt[v], rd[v], R, w);
+      float ls = 0.f;
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) ls += w[e];
-    x[v] = (double)ls;
+      for (int e = 0; e < VEC; ++e) ls += w[e];
+      x[v] = (double)ls;
+    }
+    tot += warp_sum_vectors<CH>(x);
   }
-  const double m = warp_sum_vectors<NVD>(x);
-  if ((threadIdx.x & 31) == 0) {
-    *mass_out = m;
-    *ref_out = R.resid ? R.M : (R.m <= -1e30f ? -INFINITY : R.m);
-  }
-}
-
-// "ldg" variant: persistent warps, the next unit's vectors in flight while the
-// current one is computed (as k_stream_ldg).
-#ifndef DSDE_DRAW_MINB
-#define DSDE_DRAW_MINB 3
-#endif
-template <typename T>
-__global__ void __launch_bounds__(kLdgThreads, DSDE_DRAW_MINB) k_draw_ldg(DrawArgs a) {
-  constexpr int NV = Traits<T>::NVD;
-  const long long n_units = (long long)a.B * a.nsub;
-  const long long W = (long long)gridDim.x * (kLdgThreads / 32);
-  long long q = (long long)blockIdx.x * (kLdgThreads / 32) + (threadIdx.x >> 5);
-  if (q >= n_units) return;
-  for (; q < n_units; q += W) {
-    uint4 rt[NV], rd[NV];
-    const DrawUnit d = draw_unit_load<T>(a, q, rt, rd);
-    draw_unit_finish<T>(a.smass + q, a.sref + q, d, rt, rd);
+  if (lane == 0) {
+    *mass_out = tot;
+    *ref_out = R.M;
   }
 }
 
 // ---------------------------------------------------------------------------
-// k_select: one warp per sequence (4 per CTA).
+// a4 second pass, one warp: the inverse-CDF select of sequence i from its
+// slice masses (mass[s], ref[s], s < nsub, read with ld.global.cg) — D7: the
+// smallest token v with C_v > u R in ascending token order.
 // ---------------------------------------------------------------------------
 struct SelArgs {
   int B, V, nsub;
@@ -674,78 +665,36 @@ struct SelArgs {
   long long ld_t;
   const void* dl;
   long long ld_d;
-  const SeqRec* rec;
-  const double* smass;
-  const float* sref;
   int32_t* emitted;
   uint8_t* flags;
   int32_t* err;
+  int v0;  // vocabulary offset of the rows (vocab-parallel shard)
 };
 
 #ifndef DSDE_TAIL_TRACE
 #define DSDE_TAIL_TRACE 0
 #endif
-#if DSDE_TAIL_TRACE
-// measurement build only (-DDSDE_TAIL_TRACE=1): per-CTA globaltimer stamps at
-// the phase boundaries of k_tail, read back by dsde_debug_tail_trace
-constexpr int kTraceMax = 4096;
-__device__ unsigned long long g_tail_trace[kTraceMax * 6];
-__device__ __forceinline__ void tail_stamp(int slot, unsigned long long v) {
-  if (threadIdx.x == 0 && blockIdx.x < kTraceMax) g_tail_trace[blockIdx.x * 6 + slot] = v;
-}
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define TAIL_STAMP(slot) tail_stamp(slot, gtimer())
-#else
-#define TAIL_STAMP(slot)
-#endif
 
-// Where select_seq reads the slice records from: global memory written by
-// another kernel / CTA (masses about each slice's own reference, rescaled
-// here), or the k_tail CTA's shared arrays with the bonus masses already
-// rescaled to the row reference by the whole CTA (scale[] = the factors).
-struct SelSrcGlobal {
-  static constexpr bool kPrescaled = false;
-  const double* m;
-  const float* r;
-  __device__ __forceinline__ double mass(int s) const { return __ldcg(m + s); }
-  __device__ __forceinline__ float ref(int s) const { return __ldcg(r + s); }
-  __device__ __forceinline__ double scale(int) const { return 1.0; }
-};
-struct SelSrcSmem {
-  static constexpr bool kPrescaled = true;
-  const double* m;
-  const float* r;
-  const double* sc;
-  __device__ __forceinline__ double mass(int s) const { return m[s]; }
-  __device__ __forceinline__ float ref(int s) const { return r[s]; }
-  __device__ __forceinline__ double scale(int s) const { return sc[s]; }
-};
-
-// One warp: the inverse-CDF select of sequence i from its slice masses.
-template <typename T, typename Src>
-__device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec& r, const Src& src) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NVD, SUB = 32 * VEC * NV;
+template <typename T>
+__device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec& r, const double* smass,
+                                           const float* sref) {
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, SUB = sub_elems<T>();
   const int lane = threadIdx.x & 31;
   if (r.mode == MODE_ARGMAX) {
     // greedy bonus token: the smallest index among the slices holding the row max
     float Mg = -INFINITY;
-    for (int s0 = lane; s0 < a.nsub; s0 += 32) Mg = max_nan(Mg, src.ref(s0));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) Mg = max_nan(Mg, __shfl_xor_sync(kFull, Mg, o));
+    for (int s0 = lane; s0 < a.nsub; s0 += 32) Mg = max_nan(Mg, __ldcg(sref + s0));
+    Mg = warp_max_nan(Mg);
     unsigned cand = 0x7fffffffu;
     for (int s0 = lane; s0 < a.nsub; s0 += 32)
-      if (src.ref(s0) == Mg) cand = min(cand, (unsigned)(s0 * SUB + (int)src.mass(s0)));
+      if (__ldcg(sref + s0) == Mg) cand = min(cand, (unsigned)(s0 * SUB + (int)__ldcg(smass + s0)));
     cand = __reduce_min_sync(kFull, cand);
     if (lane == 0) {
       if (Mg != Mg || cand >= (unsigned)a.V) {
         a.emitted[r.slot] = DSDE_PAD;
         raise_device_error(a.err, DSDE_DERR_NONFINITE, i);
       } else {
-        a.emitted[r.slot] = (int)cand;
+        a.emitted[r.slot] = a.v0 + (int)cand;
       }
     }
     return;
@@ -754,24 +703,16 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   const bool resid = r.mode == MODE_RESIDUAL;
   const int nsub = a.nsub;
   float Mg = -INFINITY;
-  if (!resid && !Src::kPrescaled) {
-    for (int s0 = lane; s0 < nsub; s0 += 32) Mg = max_nan(Mg, src.ref(s0));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) Mg = max_nan(Mg, __shfl_xor_sync(kFull, Mg, o));
+  if (!resid) {
+    for (int s0 = lane; s0 < nsub; s0 += 32) Mg = max_nan(Mg, __ldcg(sref + s0));
+    Mg = warp_max_nan(Mg);
   }
-  auto scale_of = [&](int s0) -> double {  // sub-chunk mass scale to the common reference
+  auto scale_of = [&](int s0) -> double {  // slice mass scale to the common reference
     if (resid) return 1.0;
-    if constexpr (Src::kPrescaled) {
-      return src.scale(s0);
-    } else {
-      const float ms = src.ref(s0);
-      return ms == -INFINITY ? 0.0 : exp((double)ms - (double)Mg);
-    }
+    const float ms = __ldcg(sref + s0);
+    return ms == -INFINITY ? 0.0 : exp((double)ms - (double)Mg);
   };
-  auto mass_of = [&](int s0) -> double {  // scale_of(s0) * the slice's own mass
-    if constexpr (Src::kPrescaled) return src.mass(s0);
-    else return scale_of(s0) * src.mass(s0);
-  };
+  auto mass_of = [&](int s0) -> double { return scale_of(s0) * __ldcg(smass + s0); };
   // lane l owns the contiguous slices [l c, (l + 1) c): its sum in slice order,
   // one warp scan gives every lane's prefix and R (the scan's total)
   const int cw = (nsub + 31) >> 5;
@@ -798,7 +739,7 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
           if (wv > 0.0) tok = v;
           if (wv > 0.0 && cum > target) break;
         }
-        a.emitted[r.slot] = tok;
+        a.emitted[r.slot] = a.v0 + tok;
         if (a.flags) a.flags[r.slot] |= DSDE_FLAG_FALLBACK;
       } else {
         a.emitted[r.slot] = DSDE_PAD;
@@ -808,7 +749,7 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
     return;
   }
   const double target = r.u * R;
-  // crossing sub-chunk: first u with prefix(u) > target (fallback: last with
+  // crossing slice: first s with prefix(s) > target (fallback: last with
   // mass): the first lane whose span crosses, then that lane's slices in order
   int us = -1;
   double base = 0.0;
@@ -845,22 +786,21 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
       fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
     }
   }
-  TAIL_STAMP(4);
   const double f = scale_of(us);
-  uint4 rt[NV], rd[NV];
-  load_sub_raw<T>(tp, a.V, us, rt);
-  if (resid) load_sub_raw<T>(reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d, a.V, us, rd);
-  const DrawRef DR = draw_ref<T>(rt, resid, r.M, (float)r.C, r.lam);
+  const T* dp = resid ? reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d : tp;
+  const DrawRef DR = draw_ref(resid, r.M, (float)r.C, r.lam, resid ? 0.f : __ldcg(sref + us));
   int tok = -1, last_pos = -1;
   double lo = 0.0, hi = 0.0, lp_lo = 0.0, lp_hi = 0.0, vbase = base;
-  // not unrolled: this runs once per sequence, so its instructions are cold;
-  // a rolled loop re-fetches one vector's code from the instruction cache
-  // instead of NV copies from L2 (ncu: the per-CTA code of k_tail stalled on
-  // instruction fetch ~47% of its samples)
+  // one vector at a time, not unrolled: this runs once per sequence, so its
+  // instructions are cold (a rolled loop fetches one vector's code)
 #pragma unroll 1
   for (int v = 0; v < NV; ++v) {
+    uint4 rt[1], rd[1];
+    load_vecs<T, 1>(tp, a.V, us, v, rt);
+    if (resid) load_vecs<T, 1>(dp, a.V, us, v, rd);
+    else rd[0] = rt[0];
     float wv[VEC];
-    vec_weights<T>(rt[v], rd[v], DR, wv);
+    vec_weights<T>(rt[0], rd[0], DR, wv);
     float ls = 0.f;
 #pragma unroll
     for (int e = 0; e < VEC; ++e) ls += wv[e];
@@ -904,7 +844,7 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
     }
     vbase += f * __shfl_sync(kFull, incl, 31);
   }
-  if (tok < 0) {  // rounding corner: u R within rounding of the sub-chunk total
+  if (tok < 0) {  // rounding corner: u R within rounding of the slice total
     tok = last_pos;
     lo = lp_lo;
     hi = lp_hi;
@@ -912,126 +852,22 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   }
   if (lane == 0) {
     if (fabs(r.u - lo / R) < 1e-6 || fabs(r.u - hi / R) < 1e-6) fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
-    a.emitted[r.slot] = tok < 0 ? 0 : tok;
+    a.emitted[r.slot] = a.v0 + (tok < 0 ? 0 : tok);
     if (a.flags) a.flags[r.slot] |= fl;
   }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(128) k_select(SelArgs a) {
-  const int i = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (i >= a.B) return;
-  const SeqRec r = a.rec[i];
-  select_seq<T>(a, i, r, SelSrcGlobal{a.smass + (long long)i * a.nsub, a.sref + (long long)i * a.nsub});
-}
-
-// ---------------------------------------------------------------------------
-// k_tail: a2-a4 fused, one CTA (kFinThreads) per sequence: finalize (warp per
-// position), then every warp forms the draw-weight masses of its slices of the
-// drawn row (a4 first pass), then warp 0 selects the token. The drawn row is
-// read by the CTA that decided it, so no launch boundary separates the steps.
-// ---------------------------------------------------------------------------
-// Extra arguments of the fused whole-step launch (dsde_step): the signal of
-// every sequence (a5-a6) runs on the CTA's last warp as soon as its KLDs and
-// a_i exist, and the CTA that finishes last computes the batch cap and next SLs
-// (a7, single GPU; `counter` is zero before the launch and reset by that CTA).
-struct StepExtra {
-  SignalArgs sig;
-  CapArgs cap;
-  int fuse_cap;
-  unsigned* counter;
-};
-
-
-// draw slices per row whose records k_tail keeps in shared memory (V <= 262144
-// bf16 / 131072 fp32; larger vocabularies use the workspace)
-constexpr int kTailMaxSub = 256;
-
-template <typename T, bool STEP, int NW>
-__global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(FinArgs fa, DrawArgs da, SelArgs sa,
-                                                                   StepExtra sx) {
-  constexpr int NVD = Traits<T>::NVD;
-  __shared__ SeqRec s_rec;
-  __shared__ double s_mass[kTailMaxSub], s_scale[kTailMaxSub];
-  __shared__ float s_ref[kTailMaxSub];
-  const int i = blockIdx.x;
-  const int warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_rec.mode = MODE_NONE;
-  FinPre pre;
-  if (warp == 0) pre = fin_prefetch<T>(fa, i);
-  // programmatic dependent launch: the CTA may be resident before the stream
-  // kernel has finished; wait for its completion (and memory) here
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  __syncthreads();
-  TAIL_STAMP(0);
-  finalize_seq<T>(fa, i, &s_rec, &pre);
-  __syncthreads();
-  TAIL_STAMP(1);
-  const SeqRec r = s_rec;
-  const bool draw = r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS || r.mode == MODE_ARGMAX;
-#if DSDE_TAIL_TRACE
-  unsigned smid;
-  asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-  tail_stamp(5, ((unsigned long long)smid << 8) | (unsigned)r.mode);
-#endif
-  if (STEP && warp == NW - 1) {
-    signal_seq(sx.sig, i);
-    if (sx.fuse_cap) {
-      // release ticket: this warp's sl_hat / state writes before the count; the
-      // warp drawing the last ticket acquires and applies the cap (a7), without
-      // waiting for any CTA's draw or select
-      __syncwarp();
-      unsigned old = 0;
-      if ((threadIdx.x & 31) == 0)
-        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(sx.counter) : "memory");
-      if (__shfl_sync(kFull, old, 0) == gridDim.x - 1) {
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        cap_warp(sx.cap);
-        if ((threadIdx.x & 31) == 0) *sx.counter = 0u;
-      }
-    }
-  }
-  // slice records in shared memory when they fit (the select then reads no
-  // global memory but the crossing slice), else in the workspace
-  const bool smem = da.nsub <= kTailMaxSub;
-  const long long q0 = (long long)i * da.nsub;
-  if (draw) {
-    for (int u = warp; u < da.nsub; u += NW) {
-      uint4 rt[NVD], rd[NVD];
-      const DrawUnit d = draw_unit_load<T>(da, u, r, rt, rd);
-      if (smem) draw_unit_finish<T>(s_mass + u, s_ref + u, d, rt, rd);
-      else draw_unit_finish<T>(da.smass + q0 + u, da.sref + q0 + u, d, rt, rd);
-    }
-  }
-  __syncthreads();
-  TAIL_STAMP(2);
-  if (!draw) return;
-  if (!smem) {
-    if (warp == 0) select_seq<T>(sa, i, r, SelSrcGlobal{da.smass + q0, da.sref + q0});
-    TAIL_STAMP(3);
-    return;
-  }
-  if (r.mode == MODE_BONUS) {
-    // the whole CTA rescales the bonus slice masses to the row max Mg (one fp64
-    // exp per slice, in parallel), as select_seq would slice by slice
-    __shared__ float s_wmax[NW];
-    float mg = -INFINITY;
-    for (int u = threadIdx.x; u < da.nsub; u += NW * 32) mg = max_nan(mg, s_ref[u]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mg = max_nan(mg, __shfl_xor_sync(kFull, mg, o));
-    if ((threadIdx.x & 31) == 0) s_wmax[warp] = mg;
-    __syncthreads();
-    float Mg = s_wmax[0];
-#pragma unroll
-    for (int w = 1; w < NW; ++w) Mg = max_nan(Mg, s_wmax[w]);
-    for (int u = threadIdx.x; u < da.nsub; u += NW * 32) {
-      const float ms = s_ref[u];
-      const double f = ms == -INFINITY ? 0.0 : exp((double)ms - (double)Mg);
-      s_scale[u] = f;
-      s_mass[u] = f * s_mass[u];
-    }
-    __syncthreads();
-  }
-  if (warp == 0) select_seq<T>(sa, i, r, SelSrcSmem{s_mass, s_ref, s_scale});
-  TAIL_STAMP(3);
+__device__ __forceinline__ SeqRec load_seqrec(const SeqRec* p) {
+  SeqRec r;
+  r.mode = __ldcg(&p->mode);
+  r.slot = __ldcg(&p->slot);
+  r.trow = __ldcg(&p->trow);
+  r.drow = __ldcg(&p->drow);
+  r.M = __ldcg(&p->M);
+  r.pad0 = 0;
+  r.C = __ldcg(&p->C);
+  r.lam = __ldcg(&p->lam);
+  r.u = __ldcg(&p->u);
+  r.S = __ldcg(&p->S);
+  return r;
 }

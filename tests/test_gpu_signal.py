@@ -154,11 +154,13 @@ def test_closed_loop_parity(m, cfg_id, fused):
     print(f"cfg{cfg_id}: {total} sl_ties={sl_ties}")
 
 
-def test_step_matches_three_calls(m):
-    """dsde_step (stream + fused tail/signal/cap) and the three separate calls
-    give bit-identical results and state, step after step (config-2 shapes),
-    with and without a per-sequence budget."""
-    B, V, dtype = 64, 32000, torch.bfloat16
+@pytest.mark.parametrize("B,V", [(64, 32000), (256, 4096), (512, 4096), (2048, 4096)])
+def test_step_matches_three_calls(m, B, V):
+    """dsde_step (one fused launch: verify + signal + cap) and the three separate
+    calls give bit-identical results and state, step after step, with and
+    without a per-sequence budget; B spans the batch sizes of configs 2-5
+    (the launch shapes bench.py times; a small V keeps it cheap)."""
+    dtype = torch.bfloat16
     gc, _ = _cfg_pair(m, sl_ceiling=8, calib_sl=4)
     sa, sb = m.State(gc, B), m.State(gc, B)
     pa, pb = m.Step(sa, B, V, dtype, with_diag=True), m.Step(sb, B, V, dtype, with_diag=True)
@@ -185,7 +187,7 @@ def test_step_matches_three_calls(m):
 
 
 def test_step_with_single_rank_nccl_comm(m):
-    """The multi-GPU cap path of dsde_step (k_tail without the fused cap, the
+    """The multi-GPU cap path of dsde_step (the pass kernel without the fused cap, the
     exact int64 partial, ncclAllReduce, k_cap_apply) on a one-rank NCCL
     communicator: bit-identical to the single-GPU path, step after step, for
     cap_mode 1 (sum) and 0 (sum + max all-reduces)."""

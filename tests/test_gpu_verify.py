@@ -42,8 +42,8 @@ def _check(m, state, host, dtype, ld_pad=0, expect_ties_max=None):
     (32000, torch.bfloat16, 8, 64),       # config 2 shape
     (128256, torch.bfloat16, 8, 12),      # config 3-5 row shape (sampled batch)
     (50000, torch.bfloat16, 8, 9),        # ragged last chunk
-    (300007, torch.bfloat16, 3, 6),       # > 256 draw slices: k_tail keeps slice records in the workspace
-    (140000, torch.float32, 3, 5),        # the same for fp32 (> 256 slices of 512)
+    (300007, torch.bfloat16, 3, 6),       # 147 slices per row, V = 300007 (Gemma-class and beyond)
+    (140000, torch.float32, 3, 5),        # 274 fp32 slices of 512 per row
     (8193, torch.float32, 16, 5),         # one element past a chunk
     (1003, torch.bfloat16, 3, 7),         # V not a multiple of 8
     (2, torch.float32, 2, 16), (3, torch.bfloat16, 1, 16), (8, torch.bfloat16, 5, 16),
@@ -56,8 +56,8 @@ def test_verify_parity(m, state, V, dtype, kmax, B):
 
 
 def test_verify_large_batch_tail_variant(m, state):
-    """B beyond two resident 16-warp tail CTAs per SM (k_tail switches to 8-warp
-    CTAs): parity on every sequence of a 400-sequence batch, both profiles."""
+    """A 400-sequence batch (more sequences than the pass kernel has warps per
+    iteration's rows): parity on every sequence, both profiles."""
     B = 400
     k = synth.random_k(B, 8, 17)
     host = make_host_batch(4096, k, seed=41, profiles=("code", "low"))

@@ -63,7 +63,7 @@ def _cases():
         if t == 0:
             cal[:] = 1  # every sequence calibrating: cap = ceiling
         cut = int(r.integers(0, B + 1)) if t % 3 else B // 2  # ragged shards, empty shards too
-        cases.append((t % 4 == 3 and 0 or 1, sl, cal, [0, cut, B]))
+        cases.append((0 if t % 4 == 3 else 1, sl, cal, [0, cut, B]))
     return cases
 
 

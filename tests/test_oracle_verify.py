@@ -238,3 +238,41 @@ def test_greedy_emits_the_target_argmax_sequence():
                 assert toks[cu[i] + a] != am(t[s0 + a])
             assert g1.emitted[s0 + a] == am(t[s0 + a])
             assert (g1.emitted[s0 + a + 1:s0 + k[i] + 1] == -1).all()
+
+
+@pytest.mark.parametrize("seed", [31, 32, 33])
+def test_sample_diag_edges_pinned(seed):
+    """The oracle's samp_diag (R, lo, hi) — the CDF edges the sample tie band of
+    D16 is measured against — pinned by an independent inverse CDF: weights from
+    scipy softmax (max(0, p - q) for a recovery draw, p for a bonus draw),
+    numpy's sequential cumsum, and np.searchsorted for the smallest v with
+    C_v > u R (D7)."""
+    k = np.array([1, 2, 3, 4, 2, 1, 3, 4] * 4)
+    cu, tok, t, d, seeds = _batch(37, k, seed)
+    d = (t[np.concatenate([np.arange(cu[i], cu[i + 1]) + i for i in range(len(k))])] +
+         np.random.default_rng(seed).normal(0, 0.7, (int(cu[-1]), 37))).astype(np.float32)
+    # draft tokens ~ q so that both recovery and bonus draws occur
+    r = np.random.default_rng(seed + 1)
+    q_all = sps.softmax(d.astype(np.float64), axis=1)
+    tok = np.array([r.choice(37, p=qq) for qq in q_all], dtype=np.int32)
+    res = oracle.verify(cu, tok, t, d, seeds, oracle.F32)
+    n_res = n_bonus = 0
+    for i in range(len(k)):
+        a, ki, s0 = int(res.accepted_len[i]), int(k[i]), int(cu[i]) + i
+        p = sps.softmax(t[s0 + a].astype(np.float64))
+        if a < ki:
+            w = np.maximum(0.0, p - sps.softmax(d[cu[i] + a].astype(np.float64)))
+            n_res += 1
+        else:
+            w = p
+            n_bonus += 1
+        c = np.cumsum(w)
+        R, lo, hi = res.samp_diag[i]
+        u = res.u_smp[s0 + a]
+        v = int(np.searchsorted(c, u * c[-1], side="right"))
+        assert res.emitted[s0 + a] == v
+        assert abs(R - c[-1]) <= 1e-12 * c[-1]
+        assert abs(lo - (c[v - 1] / c[-1] if v else 0.0)) <= 1e-12
+        assert abs(hi - c[v] / c[-1]) <= 1e-12
+        assert lo <= u < hi
+    assert n_res > 0 and n_bonus > 0
