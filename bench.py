@@ -3,8 +3,8 @@
 
 One "step" = one pass of the whole hot path over one
 batch: one dsde_step call = verify (a1-a4) + signal / SL^ (a5-a6) + cap (a7),
-i.e. the counter reset and the persistent pass kernel k_pass (with the NCCL
-cap all-reduce between two small kernels when N > 1).
+i.e. the row stream k_stream_ldg and the tail k_tail (with the NCCL cap
+all-reduce between two small kernels when N > 1).
 
 Workloads (BASELINE.json configs, --config): 1 = B 4, V 32000 fp32, SL <= 4;
 2 = B 64, V 32000 bf16, code + dialogue; 3 (default) = B 256 per GPU,
@@ -23,9 +23,11 @@ Measurement:
     if K + W > R), bracketed by barrier + synchronize, CUDA events on the
     launching stream, max over ranks (pass 1: nothing else in the region);
   * roofline (pass 2, the same replay with the library's per-launch events):
-    the algorithmic bytes of the step (target + draft row of every
-    draft position, plus the bonus row of every fully accepted sequence) over
-    the pass kernel's own CUDA-event time, against MEASURED_PEAKS.json hbm_gbs;
+    the dominant kernel k_stream_ldg's algorithmic bytes (the
+    target + draft row of every draft position) over its own CUDA-event time,
+    against MEASURED_PEAKS.json hbm_gbs; `whole_step` = the step's algorithmic
+    bytes (plus the bonus row of every fully accepted sequence) over pass 1's
+    ms_per_step;
   * parity: the fp64 oracle (oracle/, test infrastructure) recomputes a fixed
     sample of sequences of every recorded step it has time for and compares
     them with the GPU's outputs (tests/parity.py bands; ties counted);
@@ -51,7 +53,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "verify positions/s and HBM GB/s vs peak at V=128256, 1/2/4/8 B200"
 UNIT = "positions/s"
-PASS_KERNEL = "k_pass"
+STREAM_KERNEL = "k_stream_ldg"
 
 CONFIGS = {
     # BASELINE.json configs[0]: the small case (closed loop, correctness config)
@@ -290,7 +292,7 @@ def run(args):
     free, _ = torch.cuda.mem_get_info(dev)
     R = max(1, min(args.record, args.warmup + args.steps, int(0.5 * free // max(1, per_step_bytes))))
     snap = state.export()
-    rec, stats = [], dict(pos=0, acc=0, resid=0, bonus=0, seqs=0, rows=0, vbytes=0)
+    rec, stats = [], dict(pos=0, acc=0, resid=0, bonus=0, seqs=0, rows=0, vbytes=0, sbytes=0)
     for r in range(R):
         inp = synth.generate_step(w, s, k, device=dev)
         n = int(k.sum())
@@ -302,7 +304,8 @@ def run(args):
         # SURVEY §8(d) algorithmic bytes: logits of every draft position's row pair and of
         # every bonus row, tokens, seeds, outputs (kld, emitted, flags, accepted_len)
         vbytes = rows * V * esz + n * 4 + (n + B) * 8 + n * 4 + (n + B) * 5 + B * 4
-        rec.append(dict(inp=inp, n=n, k=k.copy(), rows=rows, vbytes=vbytes, next=nx, acc=acc.copy(),
+        sbytes = 2 * n * V * esz  # the stream kernel's rows: target + draft row of every draft position
+        rec.append(dict(inp=inp, n=n, k=k.copy(), rows=rows, vbytes=vbytes, sbytes=sbytes, next=nx, acc=acc.copy(),
                         emitted=out.emitted.cpu().numpy().copy(), kld=out.kld.cpu().numpy().copy()))
         stats["pos"] += n
         stats["acc"] += int(acc.sum())
@@ -369,9 +372,10 @@ def run(args):
     if ws > 1:
         dist.barrier()
     step_ms2 = sum(a.elapsed_time(b) for a, b in ev)
-    pass_ms = phase_ms["pass"]
+    pass_ms = phase_ms["stream"]
     positions = sum(rec[(args.warmup + j) % R]["n"] for j in range(args.steps))
     vbytes = sum(rec[(args.warmup + j) % R]["vbytes"] for j in range(args.steps))
+    sbytes = sum(rec[(args.warmup + j) % R]["sbytes"] for j in range(args.steps))
     code, _ = state.device_error()
     if code != 0 and not os.environ.get("DSDE_BENCH_IGNORE_ERRORS"):  # (set only for kernel experiments)
         raise SystemExit(f"device error {code} during the bench")
@@ -381,7 +385,7 @@ def run(args):
     multi = None
     if ws > 1:
         multi = _allreduce_cost(m, state, step, comm, B, dist, stream)
-    t = torch.tensor([elapsed_ms, step_ms2, pass_ms, float(positions), float(vbytes)],
+    t = torch.tensor([elapsed_ms, step_ms2, pass_ms, float(positions), float(vbytes), float(sbytes)],
                      dtype=torch.float64, device=dev)
     if ws > 1:
         mx = t[:3].clone()
@@ -395,7 +399,7 @@ def run(args):
         multi["positions_per_rank_max_over_mean"] = max(allrows) / (sum(allrows) / ws)
         multi["positions_per_rank"] = allrows
         elapsed_ms, step_ms2, pass_ms = float(mx[0]), float(mx[1]), float(mx[2])
-        positions, vbytes = float(tot[0]), float(tot[1])
+        positions, vbytes, sbytes = float(tot[0]), float(tot[1]), float(tot[2])
     value = positions / (elapsed_ms / 1e3)
 
     # ---- e2e through the public API from pinned host buffers (rank-local, max over ranks)
@@ -408,22 +412,21 @@ def run(args):
 
     if rank == 0:
         peak, peak_kind = _peaks()
-        ach = (vbytes / ws) / (pass_ms / 1e3) / 1e9 if pass_ms > 0 else None
+        ach = (sbytes / ws) / (pass_ms / 1e3) / 1e9 if pass_ms > 0 else None
         trec = _traffic_record(f"cfg{args.config}")
-        traffic = (trec["ratio"] * vbytes / ws / args.steps) if trec else None
+        traffic = (trec["ratio"] * sbytes / ws / args.steps) if trec else None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if cfg.get("strong") else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": _config_dict(args, cfg, ws),
             "roofline": {"bound": "hbm",
-                         "kernel": f"{PASS_KERNEL} (the whole step: a1 stream + a2-a4 finalize/draw/select"
-                                   f"{' + a5-a7 signal/cap' if not args.split_calls else ''})",
+                         "kernel": f"{STREAM_KERNEL} (a1, the row stream: the dominant kernel)",
                          "achieved": ach, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": (ach / peak) if ach else None,
                          "traffic": traffic,
                          "traffic_source": trec["source"] if trec else None,
-                         "algorithmic_bytes_per_launch": vbytes / ws / args.steps,
+                         "algorithmic_bytes_per_launch": sbytes / ws / args.steps,
                          "avg_launch_ms": pass_ms / args.steps},
             "timing": "value / ms_per_step: pass 1, only the two bracketing events in the region; roofline: "
                       "pass 2, the same replay with per-launch CUDA events on the launching stream",
@@ -436,9 +439,9 @@ def run(args):
             "parity": par,
             "replay_identical": replay_identical,
             "e2e": e2e,
-            # our kernels per step: k_pass (the counter reset is a driver memset);
-            # split calls: k_pass + k_update_signal + k_cap_local; N > 1: + k_cap_partial/apply
-            "gpu_launches": args.steps * ((1 if ws == 1 else 3) if not args.split_calls else (3 if ws == 1 else 4)),
+            # our kernels per step: k_stream_ldg + k_tail; split calls: + k_update_signal +
+            # k_cap_local; N > 1: + k_cap_partial / k_cap_apply
+            "gpu_launches": args.steps * ((2 if ws == 1 else 4) if not args.split_calls else (4 if ws == 1 else 5)),
             "clocks": sampler.summary(),
             "multi_gpu": multi,
             "rows_per_s": None,

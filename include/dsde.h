@@ -68,7 +68,6 @@ typedef enum { DSDE_F32 = 0, DSDE_BF16 = 1 } dsde_dtype;
 #define DSDE_DERR_NONFINITE 3     /* non-finite logits in a row                          */
 #define DSDE_DERR_ROWS 4          /* cu_sl[B] != total_draft_rows                         */
 #define DSDE_DERR_BAD_SLOT 5      /* state slot outside [0, max_seqs)                     */
-#define DSDE_DERR_STALL 6         /* internal: a pass-kernel wait timed out (~2 s bug guard; never expected) */
 
 /* Per-slot bits of the optional `flags` output of dsde_verify. */
 #define DSDE_FLAG_ACCEPT_NEAR_TIE 1  /* |u_acc - min(1, p/q)| < 1e-6 at this position      */
@@ -209,11 +208,11 @@ size_t dsde_verify_workspace_size(int B, int total_draft_rows, int V, dsde_dtype
  * attributed, every sequence gets accepted_len -1). No device error ever
  * causes an out-of-bounds access.
  *
- * Execution: a memset of the workspace counters and ONE persistent kernel
- * (k_pass) on `stream`: its warps stream every (draft row, 2048-token slice)
- * of the target and draft logits once; the warp completing a row merges it,
- * the warp completing a sequence lays it out, and the draw of each sequence's
- * token is spread over later warp iterations, interleaved with the stream. */
+ * Execution: two kernels on `stream`: the row stream k_stream_ldg (persistent
+ * warps read every (draft row, 2048-token slice) of the target and draft
+ * logits once and write slice partials to the workspace), then k_tail
+ * (programmatic dependent launch; one CTA per sequence: fp64 row merge,
+ * accept test, layout, draw, select). */
 dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_draft_rows,
                         const int32_t* cu_sl, const int32_t* draft_tokens,
                         const void* target_logits, int64_t ld_t,
@@ -225,10 +224,12 @@ dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_draft_rows,
 /* Kernel timing of dsde_verify / dsde_step (instrumentation; off by
  * default). While enabled, every dsde_verify / dsde_step call on this state
  * records CUDA events on its stream before its first launch and after each of
- * its DSDE_VERIFY_PHASES phases: 0 = the workspace counter reset (a memset),
- * 1 = the pass kernel k_pass (a1-a4, and in dsde_step a5-a6 plus the
- * single-GPU cap a7), 2 and 3 = unused (read 0; dsde_step's multi-GPU cap
- * kernels and all-reduce are not inside the recorded phases).
+ * its DSDE_VERIFY_PHASES phases: 0 = the row stream k_stream_ldg (a1),
+ * 1 = the tail k_tail (a2-a4, and in dsde_step a5-a6 plus the single-GPU cap
+ * a7), 2 and 3 = unused (read 0; dsde_step's multi-GPU cap kernels and
+ * all-reduce are not inside the recorded phases). The tail is launched with
+ * programmatic dependent launch, so the event between the two kernels also
+ * covers the tail's start-up that overlaps the stream's drain.
  * dsde_profile_read blocks until the last recorded event completes, writes
  * the summed milliseconds of each phase over the calls recorded since the
  * previous read to ms[DSDE_VERIFY_PHASES] (host memory) and the call count to
@@ -299,12 +300,12 @@ dsde_status dsde_next_sl(dsde_state st, int B, const int32_t* slots, const int32
  *   dsde_update_signal(st, B, slots, cu_sl, kld, accepted_len, sl_hat, diag);
  *   dsde_next_sl(st, B, slots, sl_hat, budget, next_sl, cap, comm);
  * with the same arguments, results, state updates and errors as those three
- * calls made in that order on `stream` (bit-identical outputs), but in one
- * pass kernel on one GPU: the warp that lays out a sequence (a3) also updates
- * its signal and predicts SL^ (a5-a6) and the warp completing the batch's last
- * signal applies the cap (a7). With a communicator the cap's exact partial is
- * all-reduced over NCCL after the pass kernel (two more launches + the
- * collective).
+ * calls made in that order on `stream` (bit-identical outputs), but in two
+ * kernels on one GPU: the row stream and the tail, whose CTA for sequence i
+ * also updates its signal and predicts SL^ (a5-a6); the warp completing the
+ * batch's last signal applies the cap (a7). With a communicator the cap's
+ * exact partial is all-reduced over NCCL after the tail (two more launches +
+ * the collective).
  * The workspace is the one dsde_verify takes. Errors: the union of the three
  * calls' synchronous checks (DSDE_ERR_ARG / DSDE_ERR_STATE) and
  * DSDE_ERR_CUDA / DSDE_ERR_NCCL. Calls on one state must be serialised. */

@@ -26,7 +26,7 @@ DSDE_PAD = -1
 DSDE_MAX_SL = 16
 DSDE_MAX_WINDOW = 64
 FLAG_ACCEPT_NEAR_TIE, FLAG_SAMPLE_NEAR_TIE, FLAG_FALLBACK = 1, 2, 4
-DERR = {0: "none", 1: "bad_sl", 2: "bad_token", 3: "nonfinite", 4: "rows", 5: "bad_slot", 6: "stall"}
+DERR = {0: "none", 1: "bad_sl", 2: "bad_token", 3: "nonfinite", 4: "rows", 5: "bad_slot"}
 
 # Every function the header declares (checked against include/dsde.h by the tests).
 EXPORTS = (
@@ -37,9 +37,9 @@ EXPORTS = (
     "dsde_cap_value", "dsde_comm_unique_id", "dsde_comm_init", "dsde_comm_destroy",
     "dsde_profile_enable", "dsde_profile_read",
 )
-# dsde_profile_read phases (include/dsde.h): the counter reset, then the one
-# persistent pass kernel k_pass (a1-a4, + a5-a7 in dsde_step); two spare slots
-VERIFY_PHASES = ("reset", "pass", "", "")
+# dsde_profile_read phases (include/dsde.h): the row stream k_stream_ldg (a1),
+# then the tail k_tail (a2-a4, + a5-a7 in dsde_step); two spare slots
+VERIFY_PHASES = ("stream", "tail", "", "")
 
 
 class DsdeError(RuntimeError):

@@ -1,0 +1,119 @@
+// tail.cuh — k_tail: a2-a4 (and, in dsde_step, a5-a7) of the verification
+// step after the row stream (included by verify.cu inside namespace dsde,
+// after verify_draw.cuh).
+//
+// One CTA of NW warps per sequence i (grid-stride over the batch):
+//   1. warp j < k_i merges draft row c0 + j's slice partials in fp64 and runs
+//      its accept test (row_finalize, a2) -> RowRes in shared memory;
+//   2. warp 0 finds the first rejection a_i, writes the KLDs, the emitted-token
+//      layout and the draw record of row a_i (residual) or k_i (bonus)
+//      (seq_layout, a3);
+//   3. the warps sweep the vocabulary slices of the drawn row and record each
+//      slice's draw-weight mass (draw_mass, a4 first pass); meanwhile, in
+//      dsde_step, warp NW-1 first updates the sequence's signal and SL^
+//      (signal_seq_vals, a5-a6) and the warp completing the batch's last
+//      signal applies the cap (cap_warp, a7, single GPU);
+//   4. warp 0 selects the token by the inverse CDF over the slice masses and
+//      inside the crossing slice (select_seq, a4).
+// The kernel is launched with programmatic dependent launch after the stream
+// kernel: it becomes resident while the stream drains, checks the batch layout
+// and waits (griddepcontrol.wait) before touching the stream's partials.
+
+struct TailArgs {
+  FinArgs fa;
+  SelArgs sa;
+  double* mass;  // [B * nsub] draw-weight mass per slice of the drawn row
+  float* mref;   // [B * nsub] its reference
+  int* ctl;      // [1] signals done (dsde_step, single GPU), zeroed by the stream kernel
+  int step, fuse_cap;
+  SignalArgs sig;
+  CapArgs cap;
+};
+
+__device__ __forceinline__ int atomic_add_acq_rel(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// a5-a7 of sequence i by one warp (dsde_step): the signal from the layout's
+// values, then the batch cap by the warp whose signal completes the batch.
+__device__ __forceinline__ void tail_signal(const TailArgs& p, int i, int k, double x, int acc) {
+  if (!p.step) return;
+  signal_seq_vals(p.sig, i, k, x, acc);
+  __syncwarp();
+  int last = 0;
+  if ((threadIdx.x & 31) == 0) last = atomic_add_acq_rel(p.ctl, 1) == p.fa.B - 1;
+  last = __shfl_sync(kFull, last, 0);
+  if (last && p.fuse_cap) cap_warp(p.cap);
+}
+
+template <typename T, int NW>
+__global__ void __launch_bounds__(NW * 32) k_tail(TailArgs p) {
+  const FinArgs& a = p.fa;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ RowRes s_rr[DSDE_MAX_SL];
+  __shared__ SeqRec s_rec;
+  __shared__ int s_acc, s_bad;
+  // batch check while the stream kernel drains: cu_sl must be a
+  // non-decreasing prefix from 0, else no row can be attributed to a sequence
+  // and every sequence is a DSDE_DERR_BAD_SL error
+  if (warp == 0) {
+    int bad = __ldg(a.cu_sl) != 0;
+    for (int i = lane; i < a.B; i += 32) bad |= __ldg(a.cu_sl + i + 1) < __ldg(a.cu_sl + i);
+    bad = __any_sync(kFull, bad);
+    if (lane == 0) s_bad = bad;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __syncthreads();
+  const bool all_bad = s_bad != 0;
+  for (int i = blockIdx.x; i < a.B; i += gridDim.x) {
+    int c0 = 0, k = 0;
+    bool rows_ok = true;
+    const bool ok = !all_bad && seq_ok(a, i, c0, k, &rows_ok);
+    if (!ok) {
+      // malformed sequence: accepted_len -1 and the device error; with
+      // dsde_step it counts towards the cap (SL^ = sl_min, state untouched),
+      // exactly as dsde_update_signal treats it
+      if (warp == 0) {
+        if (lane == 0) {
+          a.acc_len[i] = -1;
+          raise_device_error(a.err, rows_ok ? DSDE_DERR_BAD_SL : DSDE_DERR_ROWS, i);
+        }
+        tail_signal(p, i, 0, 0.0, -1);
+      }
+      continue;  // CTA-uniform
+    }
+    // 1. a2: row finalize, warp j -> draft row c0 + j
+    for (int j = warp; j < k; j += NW) {
+      const RowRes rr = row_finalize<T>(a, c0 + j, i);
+      if (lane == 0) s_rr[j] = rr;
+    }
+    __syncthreads();
+    // 2. a3: layout and draw record (warp 0)
+    if (warp == 0) {
+      RowRes rr;
+      rr.bits = 0;
+      rr.kl = 0.0;
+      if (lane < k) rr = s_rr[lane];
+      const int acc = seq_layout(a, i, c0, k, rr, &s_rec);
+      if (lane == 0) s_acc = acc;
+    }
+    __syncthreads();
+    const SeqRec r = s_rec;
+    // 3. a5-a7 (dsde_step) by the last warp, then a4's slice masses by all
+    if (warp == NW - 1 && p.step) {
+      const double x = lane < k ? (double)(float)s_rr[lane].kl : 0.0;  // the fp32 KLDs, as the 3-call path
+      tail_signal(p, i, k, x, s_acc);
+    }
+    if (r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS || r.mode == MODE_ARGMAX) {
+      const long long q0 = (long long)i * a.nsub;
+      for (int u = warp; u < a.nsub; u += NW)
+        draw_mass<T>(r, u, a.V, a.tl, a.ld_t, a.dl, a.ld_d, p.mass + q0 + u, p.mref + q0 + u);
+      __syncthreads();
+      // 4. a4 select (warp 0)
+      if (warp == 0) select_seq<T>(p.sa, i, r, p.mass + q0, p.mref + q0);
+    }
+    __syncthreads();  // s_rr / s_rec are reused by the next sequence
+  }
+}

@@ -2,16 +2,15 @@
 // (§8(a) a1-a4; with dsde_step also a5-a7).
 //
 // Launch sequence (on the caller's stream, no host synchronisation):
-//   1. cudaMemsetAsync of the pass's counters (workspace);
-//   2. k_pass (pass.cuh): ONE persistent kernel. Its warps stream every
-//      (draft position row, vocab slice) of the target and draft logits once
-//      (a1: per 2048-token bf16 / 512-token fp32 slice S = sum e_v,
-//      A = sum e_v w_v, D = sum e_v g(w_v) about the slice reference); the warp
-//      completing a row merges it in fp64 (KL, log p/q, Philox accept test,
-//      a2), the warp completing a sequence lays it out (a3) and, in dsde_step,
-//      updates its signal and SL^ (a5-a6); the draw of each sequence's token
-//      (a4) is spread over the warps' later iterations, interleaved with the
-//      stream; the last signal applies the batch cap (a7, single GPU).
+//   1. k_stream_ldg: persistent warps stream every (draft position row, vocab
+//      slice) of the target and draft logits once (a1: per 2048-token bf16 /
+//      512-token fp32 slice S = sum e_v, A = sum e_v w_v, D = sum e_v g(w_v)
+//      about the slice reference) and write 32-byte slice partials;
+//   2. k_tail (tail.cuh), launched with programmatic dependent launch: one CTA
+//      per sequence merges its rows in fp64 (KL, log p/q, Philox accept test,
+//      a2), lays it out (a3), draws its token (a4) and, in dsde_step, updates
+//      its signal and SL^ (a5-a6); the last signal applies the batch cap (a7,
+//      single GPU);
 //   3. (dsde_step with a communicator) k_cap_partial, ncclAllReduce, k_cap_apply.
 //
 // Numerics: with e_v = exp(t_v - M), w_v = (t_v - d_v) - C, C = M - max d
@@ -97,34 +96,29 @@ inline int n_subs(int V, dsde_dtype dt) {
 
 // Workspace of dsde_verify / dsde_step (caller-owned, 256-byte aligned): the
 // slice partials (32 B per draft row x slice: 1.6% of the logit bytes),
-// per-row results (64 B), per-sequence draw records (64 B) and per-slice draw
-// masses (12 B per slice of each sequence's drawn row), then the pass's
-// counters, zeroed by every call.
+// per-sequence draw records (64 B), per-slice draw masses (12 B per slice of
+// each sequence's drawn row) and the tail's signal counter.
 struct VerifyWs {
   void* part;   // SubPartial [total * nsub]
-  void* rowres;  // RowRes [total]
   void* rec;    // SeqRec [B]
   double* mass;  // [B * nsub]
   float* mref;   // [B * nsub]
-  int* counters;  // row_cnt[total], seq_cnt[B], draw_cnt[B], pub[B], ctl[8]
+  int* counters;  // [8]: [0] signals done (zeroed by the stream kernel)
   size_t counter_bytes;
 };
 
 inline size_t ws_layout(int B, int total, int V, dsde_dtype dt, VerifyWs* ws, char* base) {
   const int ns = n_subs(V, dt);
   const size_t p_bytes = align256((size_t)32 * total * ns);
-  const size_t rr_bytes = align256((size_t)64 * total);
   const size_t r_bytes = align256((size_t)64 * B);
   const size_t m_bytes = align256(sizeof(double) * (size_t)B * ns);
   const size_t x_bytes = align256(sizeof(float) * (size_t)B * ns);
-  const size_t cnt = (size_t)total + 3 * (size_t)B + 8;
+  const size_t cnt = 8;
   const size_t c_bytes = align256(sizeof(int) * cnt);
   if (ws) {
     size_t o = 0;
     ws->part = base + o;
     o += p_bytes;
-    ws->rowres = base + o;
-    o += rr_bytes;
     ws->rec = base + o;
     o += r_bytes;
     ws->mass = reinterpret_cast<double*>(base + o);
@@ -134,7 +128,7 @@ inline size_t ws_layout(int B, int total, int V, dsde_dtype dt, VerifyWs* ws, ch
     ws->counters = reinterpret_cast<int*>(base + o);
     ws->counter_bytes = sizeof(int) * cnt;
   }
-  return p_bytes + rr_bytes + r_bytes + m_bytes + x_bytes + c_bytes;
+  return p_bytes + r_bytes + m_bytes + x_bytes + c_bytes;
 }
 
 // max that propagates NaN (a NaN logit must reach the non-finite check)
@@ -546,6 +540,7 @@ struct StreamArgs {
   int B, V, nsub, total;  // total: Σk_i, or the row capacity when dev_rows
   SubPartial* part;
   int dev_rows;           // dsde_config.device_rows: Σk_i = cu_sl[B] (<= total), read here
+  int* ctl;               // the tail's signal counter, zeroed here (the tail reads it after griddepcontrol.wait)
 };
 
 // rows this launch streams: the host's Σk_i, or (device_rows) cu_sl[B] clamped
@@ -580,6 +575,7 @@ __global__ void __launch_bounds__(kLdgThreads, ENT ? DSDE_ENT_MINB : DSDE_LDG_MI
   const long long n_units = (long long)total * a.nsub;
   const long long W = (long long)gridDim.x * (kLdgThreads / 32);
   long long q = (long long)blockIdx.x * (kLdgThreads / 32) + (threadIdx.x >> 5);
+  if (q == 0 && a.ctl) *a.ctl = 0;
   // let the tail kernel launch (programmatic dependent launch) and become
   // resident on SMs as this grid drains; it waits for our completion
   asm volatile("griddepcontrol.launch_dependents;");
@@ -628,39 +624,52 @@ struct StepExtra {  // the whole-step launch (dsde_step): signal (a5-a6) and cap
   CapArgs cap;
   int fuse_cap;  // single GPU: the warp completing the last signal applies the cap
 };
-#include "pass.cuh"  // k_pass: the whole pass in one persistent kernel
+#include "tail.cuh"  // k_tail: a2-a4 (+ a5-a7 in dsde_step)
 
 template <typename KernelT>
-static int resident_grid(KernelT k, int threads, int smem, int sms) {
+static int resident_per_sm(KernelT k, int threads) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
-  return std::max(1, per_sm) * sms;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, 0);
+  return std::max(1, per_sm);
 }
 
-// Resident grid of k_pass per (device, dtype, ENT): every CTA must be resident
-// at once (pass.cuh's progress argument).
-template <typename T>
-static int pass_grid(bool ent) {
-  int dev = 0;
+static int sm_count() {
+  int dev = 0, sms = 148;
   cudaGetDevice(&dev);
-  static int grids[64][2] = {};
-  int& g = grids[dev & 63][ent ? 1 : 0];
-  if (g == 0) {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    g = ent ? resident_grid(k_pass<T, true>, kPassThreads, 0, sms)
-            : resident_grid(k_pass<T, false>, kPassThreads, 0, sms);
-  }
-  return g;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
 }
 
-// the row-finalize lag, in stream iterations (>= 1, pass.cuh)
-#ifndef DSDE_PASS_LAG_ITERS
-#define DSDE_PASS_LAG_ITERS 1
-#endif
+// Launch with programmatic dependent launch: the kernel may start while the
+// previous kernel on the stream drains; it calls griddepcontrol.wait before
+// touching that kernel's results.
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+// k_tail CTA shape: 32 warps while B <= SMs (one sequence per SM), 16 while
+// B <= 2 SMs, else 8 (4 per SM, one wave up to B = 4 SMs).
+template <typename T>
+static void launch_tail(const TailArgs& p, int B, cudaStream_t s) {
+  const int sms = sm_count();
+  if (B <= sms) launch_pdl(k_tail<T, 32>, B, 1024, s, p);
+  else if (B <= 2 * sms) launch_pdl(k_tail<T, 16>, B, 512, s, p);
+  else launch_pdl(k_tail<T, 8>, std::min(B, 4 * sms), 256, s, p);
+}
 
 // step != nullptr: the whole-step launch (dsde_step) with the signal (and, if
-// step->fuse_cap, the cap) in the pass kernel.
+// step->fuse_cap, the cap) in the tail kernel.
 template <typename T>
 cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const int32_t* tokens,
                           const void* tl, int64_t ld_t, const void* dl, int64_t ld_d,
@@ -674,41 +683,38 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   };
   const int ns = n_subs(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32);
   mark();
-  cudaError_t e = cudaMemsetAsync(ws.counters, 0, ws.counter_bytes, s);
-  if (e != cudaSuccess) return e;
+  // a1: the row stream (persistent warps; grid = resident CTAs)
+  StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, ns, total, reinterpret_cast<SubPartial*>(ws.part), dev_rows,
+                ws.counters};
+  const int sms = sm_count();
+  if (ent) {
+    static int g = 0;
+    if (!g) g = sms * resident_per_sm(dev_rows ? k_stream_ldg<T, true, true> : k_stream_ldg<T, false, true>, kLdgThreads);
+    if (dev_rows) k_stream_ldg<T, true, true><<<g, kLdgThreads, 0, s>>>(sa);
+    else k_stream_ldg<T, false, true><<<g, kLdgThreads, 0, s>>>(sa);
+  } else {
+    static int g = 0;
+    if (!g) g = sms * resident_per_sm(k_stream_ldg<T, false, false>, kLdgThreads);
+    if (dev_rows) k_stream_ldg<T, true, false><<<g, kLdgThreads, 0, s>>>(sa);
+    else k_stream_ldg<T, false, false><<<g, kLdgThreads, 0, s>>>(sa);
+  }
   mark();
-  PassArgs p{};
+  // a2-a4 (+ a5-a7): the tail
+  TailArgs p{};
   p.fa = FinArgs{B, V, total, ns, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds,
                  reinterpret_cast<const SubPartial*>(ws.part), acc_len, emitted, kld, flags,
                  reinterpret_cast<SeqRec*>(ws.rec), err, greedy, dev_rows, ent, 0};
   p.sa = SelArgs{B, V, ns, tl, ld_t, dl, ld_d, emitted, flags, err, 0};
-  p.rowres = reinterpret_cast<RowRes*>(ws.rowres);
   p.mass = ws.mass;
   p.mref = ws.mref;
-  p.row_cnt = ws.counters;
-  p.seq_cnt = p.row_cnt + total;
-  p.draw_cnt = p.seq_cnt + B;
-  p.pub = p.draw_cnt + B;
-  p.ctl = p.pub + B;
+  p.ctl = ws.counters;
   if (step) {
     p.step = 1;
     p.fuse_cap = step->fuse_cap;
     p.sig = step->sig;
     p.cap = step->cap;
   }
-  const int grid = pass_grid<T>(ent != nullptr);
-  const long long W = (long long)grid * (kPassThreads / 32);
-  p.Lr = (int)(DSDE_PASS_LAG_ITERS * ((W + ns - 1) / ns) + 1);
-  p.Ld = 2 * p.Lr + 1;
-#if DSDE_PASS_EXP == 9  // measurement only: the round-1 stream kernel alone
-  {
-    StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, ns, total, const_cast<SubPartial*>(p.fa.part), dev_rows};
-    k_stream_ldg<T, false><<<pass_grid<T>(false), kLdgThreads, 0, s>>>(sa);
-  }
-#else
-  if (ent) k_pass<T, true><<<grid, kPassThreads, 0, s>>>(p);
-  else k_pass<T, false><<<grid, kPassThreads, 0, s>>>(p);
-#endif
+  launch_tail<T>(p, B, s);
   mark();
   mark();
   mark();
@@ -820,15 +826,6 @@ extern "C" dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, 
   return e == cudaSuccess ? DSDE_OK : DSDE_ERR_CUDA;
 }
 
-#if DSDE_PASS_TRACE
-// measurement build only: copy the k_pass trace (8 u64 per warp, 4 per sequence)
-extern "C" int dsde_debug_pass_trace(unsigned long long* warps, int nw, unsigned long long* seqs, int ns) {
-  nw = nw < dsde::kTraceWarps ? nw : dsde::kTraceWarps;
-  ns = ns < dsde::kTraceSeqs ? ns : dsde::kTraceSeqs;
-  if (cudaMemcpyFromSymbol(warps, dsde::g_warp_trace, sizeof(unsigned long long) * 8 * nw) != cudaSuccess) return -1;
-  return cudaMemcpyFromSymbol(seqs, dsde::g_seq_trace, sizeof(unsigned long long) * 4 * ns) == cudaSuccess ? 0 : -1;
-}
-#endif
 
 extern "C" dsde_status dsde_set_draft_entropy(dsde_state st, float* entropy) {
   if (!st) return DSDE_ERR_ARG;

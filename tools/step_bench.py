@@ -4,7 +4,7 @@ outputs are not meaningful). Prints the median µs per call over --iters calls
 and the achieved algorithmic GB/s of the logit rows (2 rows per draft position
 + the bonus rows reported by the call).
 
-usage: python tools/pass_bench.py [--config 3] [--iters 30] [--sets 3]
+usage: python tools/step_bench.py [--config 3] [--iters 30] [--sets 3]
 """
 import argparse
 import os
