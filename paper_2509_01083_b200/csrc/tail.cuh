@@ -48,21 +48,39 @@ __device__ __forceinline__ void tail_signal(const TailArgs& p, int i, int k, dou
   if (last && p.fuse_cap) cap_warp(p.cap);
 }
 
+// draw slices per row whose records k_tail keeps in shared memory (V <= 262144
+// bf16 / 131072 fp32; larger vocabularies use the workspace)
+constexpr int kTailMaxSub = 256;
+
 template <typename T, int NW>
-__global__ void __launch_bounds__(NW * 32) k_tail(TailArgs p) {
+__global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) {
   const FinArgs& a = p.fa;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nd = p.sa.nsub;  // draw slices per row
   __shared__ RowRes s_rr[DSDE_MAX_SL];
   __shared__ SeqRec s_rec;
   __shared__ int s_acc, s_bad;
-  // batch check while the stream kernel drains: cu_sl must be a
+  __shared__ double s_mass[kTailMaxSub], s_scale[kTailMaxSub];
+  __shared__ float s_ref[kTailMaxSub], s_wmax[NW];
+  const bool smem = nd <= kTailMaxSub;
+  // while the stream kernel drains: the batch check (cu_sl must be a
   // non-decreasing prefix from 0, else no row can be attributed to a sequence
-  // and every sequence is a DSDE_DERR_BAD_SL error
+  // and every sequence is a DSDE_DERR_BAD_SL error) and the accept-test
+  // inputs of this CTA's first sequence (warp j: row j)
   if (warp == 0) {
     int bad = __ldg(a.cu_sl) != 0;
     for (int i = lane; i < a.B; i += 32) bad |= __ldg(a.cu_sl + i + 1) < __ldg(a.cu_sl + i);
     bad = __any_sync(kFull, bad);
     if (lane == 0) s_bad = bad;
+  }
+  RowPre pre{0, 0.f, 0.f, 0.0};
+  int pre_i = -1;
+  {
+    const int i = blockIdx.x, c0 = __ldg(a.cu_sl + i), k = __ldg(a.cu_sl + i + 1) - c0;
+    if (warp < k && k <= DSDE_MAX_SL && c0 >= 0 && c0 + k <= a.total) {
+      pre = row_prefetch<T>(a, c0 + warp, i);
+      pre_i = i;
+    }
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
@@ -86,7 +104,7 @@ __global__ void __launch_bounds__(NW * 32) k_tail(TailArgs p) {
     }
     // 1. a2: row finalize, warp j -> draft row c0 + j
     for (int j = warp; j < k; j += NW) {
-      const RowRes rr = row_finalize<T>(a, c0 + j, i);
+      const RowRes rr = row_finalize<T>(a, c0 + j, i, (i == pre_i && j == warp) ? &pre : nullptr);
       if (lane == 0) s_rr[j] = rr;
     }
     __syncthreads();
@@ -107,13 +125,38 @@ __global__ void __launch_bounds__(NW * 32) k_tail(TailArgs p) {
       tail_signal(p, i, k, x, s_acc);
     }
     if (r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS || r.mode == MODE_ARGMAX) {
-      const long long q0 = (long long)i * a.nsub;
-      for (int u = warp; u < a.nsub; u += NW)
-        draw_mass<T>(r, u, a.V, a.tl, a.ld_t, a.dl, a.ld_d, p.mass + q0 + u, p.mref + q0 + u);
+      const long long q0 = (long long)i * nd;
+      double* gm = p.mass + q0;
+      float* gr = p.mref + q0;
+      for (int u = warp; u < nd; u += NW)
+        draw_mass<T>(r, u, a.V, a.tl, a.ld_t, a.dl, a.ld_d, smem ? s_mass + u : gm + u, smem ? s_ref + u : gr + u);
       __syncthreads();
       // 4. a4 select (warp 0)
-      if (warp == 0) select_seq<T>(p.sa, i, r, p.mass + q0, p.mref + q0);
+      if (!smem) {
+        if (warp == 0) select_seq<T, false>(p.sa, i, r, SliceSrc<false>{gm, gr, nullptr});
+      } else {
+        if (r.mode == MODE_BONUS) {
+          // the whole CTA rescales the bonus slice masses to the row max Mg (one
+          // fp64 exp per slice, in parallel), as select_seq would slice by slice
+          float mg = -INFINITY;
+          for (int u = threadIdx.x; u < nd; u += NW * 32) mg = max_nan(mg, s_ref[u]);
+          mg = warp_max_nan(mg);
+          if (lane == 0) s_wmax[warp] = mg;
+          __syncthreads();
+          float Mg = s_wmax[0];
+#pragma unroll
+          for (int w = 1; w < NW; ++w) Mg = max_nan(Mg, s_wmax[w]);
+          for (int u = threadIdx.x; u < nd; u += NW * 32) {
+            const float ms = s_ref[u];
+            const double f = ms == -INFINITY ? 0.0 : exp((double)ms - (double)Mg);
+            s_scale[u] = f;
+            s_mass[u] = f * s_mass[u];
+          }
+          __syncthreads();
+        }
+        if (warp == 0) select_seq<T, true>(p.sa, i, r, SliceSrc<true>{s_mass, s_ref, s_scale});
+      }
     }
-    __syncthreads();  // s_rr / s_rec are reused by the next sequence
+    __syncthreads();  // shared records are reused by the next sequence
   }
 }

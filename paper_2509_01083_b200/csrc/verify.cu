@@ -47,12 +47,14 @@ struct Traits;
 template <>
 struct Traits<uint16_t> {                  // bf16 bit patterns
   static constexpr int VEC = 8;            // elements per 16-byte vector
-  static constexpr int NV = DSDE_NV_BF16;  // vectors per lane per row slice (stream and draw)
+  static constexpr int NV = DSDE_NV_BF16;  // vectors per lane per stream slice (2048 tokens)
+  static constexpr int NVD = 4;            // vectors per lane per draw slice (1024 tokens)
 };
 template <>
 struct Traits<float> {
   static constexpr int VEC = 4;
-  static constexpr int NV = 4;
+  static constexpr int NV = 4;   // 512 tokens
+  static constexpr int NVD = 4;  // 512 tokens
 };
 // one warp's slice of a row: 32 lanes x NV vectors x VEC elements
 template <typename T>
@@ -88,9 +90,20 @@ static_assert(sizeof(SeqRec) == 64, "SeqRec layout");
 
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// slices per row (2048 tokens bf16, 512 fp32)
+// one warp's slice of a row in the draw and select passes
+template <typename T>
+__host__ __device__ constexpr int draw_elems() {
+  return 32 * Traits<T>::VEC * Traits<T>::NVD;
+}
+
+// stream slices per row (2048 tokens bf16, 512 fp32)
 inline int n_subs(int V, dsde_dtype dt) {
   const int se = dt == DSDE_BF16 ? sub_elems<uint16_t>() : sub_elems<float>();
+  return (V + se - 1) / se;
+}
+// draw slices per row (1024 tokens bf16, 512 fp32)
+inline int n_draws(int V, dsde_dtype dt) {
+  const int se = dt == DSDE_BF16 ? draw_elems<uint16_t>() : draw_elems<float>();
   return (V + se - 1) / se;
 }
 
@@ -108,11 +121,11 @@ struct VerifyWs {
 };
 
 inline size_t ws_layout(int B, int total, int V, dsde_dtype dt, VerifyWs* ws, char* base) {
-  const int ns = n_subs(V, dt);
+  const int ns = n_subs(V, dt), nd = n_draws(V, dt);
   const size_t p_bytes = align256((size_t)32 * total * ns);
   const size_t r_bytes = align256((size_t)64 * B);
-  const size_t m_bytes = align256(sizeof(double) * (size_t)B * ns);
-  const size_t x_bytes = align256(sizeof(float) * (size_t)B * ns);
+  const size_t m_bytes = align256(sizeof(double) * (size_t)B * nd);
+  const size_t x_bytes = align256(sizeof(float) * (size_t)B * nd);
   const size_t cnt = 8;
   const size_t c_bytes = align256(sizeof(int) * cnt);
   if (ws) {
@@ -704,7 +717,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   p.fa = FinArgs{B, V, total, ns, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds,
                  reinterpret_cast<const SubPartial*>(ws.part), acc_len, emitted, kld, flags,
                  reinterpret_cast<SeqRec*>(ws.rec), err, greedy, dev_rows, ent, 0};
-  p.sa = SelArgs{B, V, ns, tl, ld_t, dl, ld_d, emitted, flags, err, 0};
+  p.sa = SelArgs{B, V, n_draws(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32), tl, ld_t, dl, ld_d, emitted, flags, err, 0};
   p.mass = ws.mass;
   p.mref = ws.mref;
   p.ctl = ws.counters;

@@ -172,26 +172,43 @@ __device__ __forceinline__ int row_argmax(const FinArgs& a, const SubPartial* P,
   return amax;
 }
 
-// a2 for draft row r = cu_sl[i] + j (one warp). The accept-test inputs (Philox
-// uniform of slot cu_sl[i] + i + j, token x, t_x, d_x) are gathered first so
-// their latency overlaps the merge. Returns the record in every lane.
+// The accept-test inputs of draft row r = cu_sl[i] + j (lane 0): the token x,
+// t_x, d_x and the Philox uniform of slot cu_sl[i] + i + j. They depend only
+// on the step's inputs, so k_tail gathers them before griddepcontrol.wait,
+// while the stream kernel still runs.
+struct RowPre {
+  int x;
+  float tx, dx;
+  double uacc;
+};
+
 template <typename T>
-__device__ __forceinline__ RowRes row_finalize(const FinArgs& a, int r, int i) {
+__device__ __forceinline__ RowPre row_prefetch(const FinArgs& a, int r, int i) {
+  RowPre p{0, 0.f, 0.f, 0.0};
+  if ((threadIdx.x & 31) == 0) {
+    const long long slot = (long long)r + i;
+    p.x = __ldg(a.tokens + r);
+    if (p.x >= 0 && p.x < a.V) {
+      p.tx = load_logit<T>(reinterpret_cast<const T*>(a.tl) + slot * a.ld_t + p.x);
+      p.dx = load_logit<T>(reinterpret_cast<const T*>(a.dl) + (long long)r * a.ld_d + p.x);
+    }
+    if (!a.greedy) p.uacc = philox_uniforms(__ldg(a.seeds + slot)).acc;
+  }
+  return p;
+}
+
+// a2 for draft row r = cu_sl[i] + j (one warp); pre: the row's row_prefetch,
+// or nullptr to gather it here (its latency then overlaps the merge). Returns
+// the record in every lane.
+template <typename T>
+__device__ __forceinline__ RowRes row_finalize(const FinArgs& a, int r, int i, const RowPre* pre = nullptr) {
   const int lane = threadIdx.x & 31;
   const long long slot = (long long)r + i;
   const T* trow = reinterpret_cast<const T*>(a.tl) + slot * a.ld_t;
-  const T* drow = reinterpret_cast<const T*>(a.dl) + (long long)r * a.ld_d;
-  int x = 0;
-  float tx = 0.f, dx = 0.f;
-  double uacc = 0.0;
-  if (lane == 0) {
-    x = __ldg(a.tokens + r);
-    if (x >= 0 && x < a.V) {
-      tx = load_logit<T>(trow + x);
-      dx = load_logit<T>(drow + x);
-    }
-    if (!a.greedy) uacc = philox_uniforms(__ldg(a.seeds + slot)).acc;
-  }
+  const RowPre in = pre ? *pre : row_prefetch<T>(a, r, i);
+  const int x = in.x;
+  const float tx = in.tx, dx = in.dx;
+  const double uacc = in.uacc;
   const SubPartial* P = a.part + (long long)r * a.nsub;
   const RowSums R = row_merge(P, a.nsub, a.ent != nullptr);
   int amax = 0;
@@ -485,11 +502,11 @@ __device__ __forceinline__ void vec_weights(const uint4& t4, const uint4& d4, co
   }
 }
 
-// raw words of vectors [v0, v0 + N) of slice u of a row (draw / select passes;
-// L2-resident data: ld.global.cg)
+// raw words of vectors [v0, v0 + N) of draw slice u of a row (draw / select
+// passes; ld.global.cg)
 template <typename T, int N>
 __device__ __forceinline__ void load_vecs(const T* row, int V, int u, int v0, uint4 (&r)[N]) {
-  constexpr int VEC = Traits<T>::VEC, SUB = sub_elems<T>();
+  constexpr int VEC = Traits<T>::VEC, SUB = draw_elems<T>();
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int v = 0; v < N; ++v) {
@@ -549,53 +566,39 @@ __device__ __forceinline__ double warp_sum_vectors(double (&x)[NV]) {
 }
 
 // ---------------------------------------------------------------------------
-// a4 first pass, one warp: the draw-weight mass of slice u of sequence i's
-// drawn row (record r), written to mass_out / ref_out (lane 0). The slice is
-// processed in chunks of DCH vectors per lane (registers); the mass is the
-// chunks' fp64 warp sums added in order, each the per-vector fp32 lane sums
-// summed over lanes in fp64 (warp_sum_vectors). Greedy bonus rows (ARGMAX)
-// record the slice max of t and its first index instead.
+// a4 first pass, one warp: the draw-weight mass of draw slice u (1024 bf16 /
+// 512 fp32 tokens: NVD vectors per lane, all loaded at once) of sequence i's
+// drawn row (record r), written to mass_out / ref_out (lane 0). The mass is the
+// per-vector fp32 lane sums summed over lanes in fp64 (warp_sum_vectors), in
+// the select pass's grouping. Greedy bonus rows (ARGMAX) record the slice max
+// of t and its first index instead.
 // ---------------------------------------------------------------------------
-template <typename T>
-struct DrawChunk {
-  static constexpr int N = Traits<T>::NV < 4 ? Traits<T>::NV : 4;
-};
-
 template <typename T>
 __device__ __forceinline__ void draw_mass(const SeqRec& r, int u, int V, const void* tl, long long ld_t,
                                           const void* dl, long long ld_d, double* mass_out, float* ref_out) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, CH = DrawChunk<T>::N;
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NVD;
   const int lane = threadIdx.x & 31;
   const int mode = r.mode;
   if (mode != MODE_RESIDUAL && mode != MODE_BONUS && mode != MODE_ARGMAX) return;
   const T* tp = reinterpret_cast<const T*>(tl) + r.trow * ld_t;
-  const T* dp = mode == MODE_RESIDUAL ? reinterpret_cast<const T*>(dl) + r.drow * ld_d : nullptr;
+  uint4 rt[NV], rd[NV];
+  load_vecs<T, NV>(tp, V, u, 0, rt);
+  if (mode == MODE_RESIDUAL) load_vecs<T, NV>(reinterpret_cast<const T*>(dl) + r.drow * ld_d, V, u, 0, rd);
+  DrawRef R;
   if (mode != MODE_RESIDUAL) {
     // bonus / argmax: the slice max of t first (the reference of the weights)
-    float m = -INFINITY;
-#pragma unroll 1
-    for (int c = 0; c < NV; c += CH) {
-      uint4 rt[CH];
-      load_vecs<T, CH>(tp, V, u, c, rt);
-      m = lane_tmax<T, CH>(rt, m);
-    }
-    m = warp_max_nan(m);
+    const float m = warp_max_nan(lane_tmax<T, NV>(rt, -INFINITY));
     if (mode == MODE_ARGMAX) {
       int best = 0x7fffffff;
-#pragma unroll 1
-      for (int c = NV - CH; c >= 0; c -= CH) {
-        uint4 rt[CH];
-        load_vecs<T, CH>(tp, V, u, c, rt);
 #pragma unroll
-        for (int v = CH - 1; v >= 0; --v) {
-          const uint4 x[1] = {rt[v]};
+      for (int v = NV - 1; v >= 0; --v) {
+        const uint4 x[1] = {rt[v]};
 #pragma unroll
-          for (int h = VEC - 2; h >= 0; h -= 2) {
-            const float2 tt = pair_of<T>(x, h);
-            const int e0 = ((c + v) * 32 + lane) * VEC + h;
-            if (tt.y == m) best = e0 + 1;
-            if (tt.x == m) best = e0;
-          }
+        for (int h = VEC - 2; h >= 0; h -= 2) {
+          const float2 tt = pair_of<T>(x, h);
+          const int e0 = (v * 32 + lane) * VEC + h;
+          if (tt.y == m) best = e0 + 1;
+          if (tt.x == m) best = e0;
         }
       }
       best = (int)__reduce_min_sync(kFull, (unsigned)best);
@@ -605,52 +608,24 @@ __device__ __forceinline__ void draw_mass(const SeqRec& r, int u, int V, const v
       }
       return;
     }
-    const DrawRef R = draw_ref(false, 0.f, 0.f, 0.0, m);
-    double tot = 0.0;
-#pragma unroll 1
-    for (int c = 0; c < NV; c += CH) {
-      uint4 rt[CH];
-      load_vecs<T, CH>(tp, V, u, c, rt);
-      double x[CH];
-#pragma unroll
-      for (int v = 0; v < CH; ++v) {
-        float w[VEC];
-        vec_weights<T>(rt[v], rt[v], R, w);
-        float ls = 0.f;
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) ls += w[e];
-        x[v] = (double)ls;
-      }
-      tot += warp_sum_vectors<CH>(x);
-    }
-    if (lane == 0) {
-      *mass_out = tot;
-      *ref_out = m <= -1e30f ? -INFINITY : m;
-    }
-    return;
+    R = draw_ref(false, 0.f, 0.f, 0.0, m);
+  } else {
+    R = draw_ref(true, r.M, (float)r.C, r.lam, 0.f);
   }
-  const DrawRef R = draw_ref(true, r.M, (float)r.C, r.lam, 0.f);
-  double tot = 0.0;
-#pragma unroll 1
-  for (int c = 0; c < NV; c += CH) {
-    uint4 rt[CH], rd[CH];
-    load_vecs<T, CH>(tp, V, u, c, rt);
-    load_vecs<T, CH>(dp, V, u, c, rd);
-    double x[CH];
+  double x[NV];
 #pragma unroll
-    for (int v = 0; v < CH; ++v) {
-      float w[VEC];
-      vec_weights<T>(rt[v], rd[v], R, w);
-      float ls = 0.f;
+  for (int v = 0; v < NV; ++v) {
+    float w[VEC];
+    vec_weights<T>(rt[v], R.resid ? rd[v] : rt[v], R, w);
+    float ls = 0.f;
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) ls += w[e];
-      x[v] = (double)ls;
-    }
-    tot += warp_sum_vectors<CH>(x);
+    for (int e = 0; e < VEC; ++e) ls += w[e];
+    x[v] = (double)ls;
   }
+  const double tot = warp_sum_vectors<NV>(x);
   if (lane == 0) {
     *mass_out = tot;
-    *ref_out = R.M;
+    *ref_out = R.resid ? R.M : (R.m <= -1e30f ? -INFINITY : R.m);
   }
 }
 
@@ -675,19 +650,30 @@ struct SelArgs {
 #define DSDE_TAIL_TRACE 0
 #endif
 
-template <typename T>
-__device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec& r, const double* smass,
-                                           const float* sref) {
-  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, SUB = sub_elems<T>();
+// Slice records: in global memory (ld.global.cg: written by other warps of the
+// launch) or in the CTA's shared memory (SMEM; the bonus masses then already
+// rescaled to the row max by the CTA, `sscale` holding the factors).
+template <bool SMEM>
+struct SliceSrc {
+  const double* mass;
+  const float* ref;
+  const double* scale;  // SMEM only
+  __device__ __forceinline__ double m(int s) const { return SMEM ? mass[s] : __ldcg(mass + s); }
+  __device__ __forceinline__ float r(int s) const { return SMEM ? ref[s] : __ldcg(ref + s); }
+};
+
+template <typename T, bool SMEM = false>
+__device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec& r, const SliceSrc<SMEM> src) {
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NVD, SUB = draw_elems<T>();
   const int lane = threadIdx.x & 31;
   if (r.mode == MODE_ARGMAX) {
     // greedy bonus token: the smallest index among the slices holding the row max
     float Mg = -INFINITY;
-    for (int s0 = lane; s0 < a.nsub; s0 += 32) Mg = max_nan(Mg, __ldcg(sref + s0));
+    for (int s0 = lane; s0 < a.nsub; s0 += 32) Mg = max_nan(Mg, src.r(s0));
     Mg = warp_max_nan(Mg);
     unsigned cand = 0x7fffffffu;
     for (int s0 = lane; s0 < a.nsub; s0 += 32)
-      if (__ldcg(sref + s0) == Mg) cand = min(cand, (unsigned)(s0 * SUB + (int)__ldcg(smass + s0)));
+      if (src.r(s0) == Mg) cand = min(cand, (unsigned)(s0 * SUB + (int)src.m(s0)));
     cand = __reduce_min_sync(kFull, cand);
     if (lane == 0) {
       if (Mg != Mg || cand >= (unsigned)a.V) {
@@ -703,16 +689,18 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   const bool resid = r.mode == MODE_RESIDUAL;
   const int nsub = a.nsub;
   float Mg = -INFINITY;
-  if (!resid) {
-    for (int s0 = lane; s0 < nsub; s0 += 32) Mg = max_nan(Mg, __ldcg(sref + s0));
+  if (!resid && !SMEM) {
+    for (int s0 = lane; s0 < nsub; s0 += 32) Mg = max_nan(Mg, src.r(s0));
     Mg = warp_max_nan(Mg);
   }
   auto scale_of = [&](int s0) -> double {  // slice mass scale to the common reference
     if (resid) return 1.0;
-    const float ms = __ldcg(sref + s0);
+    if (SMEM) return src.scale[s0];
+    const float ms = src.r(s0);
     return ms == -INFINITY ? 0.0 : exp((double)ms - (double)Mg);
   };
-  auto mass_of = [&](int s0) -> double { return scale_of(s0) * __ldcg(smass + s0); };
+  // shared-memory bonus masses are already rescaled
+  auto mass_of = [&](int s0) -> double { return (SMEM || resid) ? src.m(s0) : scale_of(s0) * src.m(s0); };
   // lane l owns the contiguous slices [l c, (l + 1) c): its sum in slice order,
   // one warp scan gives every lane's prefix and R (the scan's total)
   const int cw = (nsub + 31) >> 5;
@@ -788,7 +776,7 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   }
   const double f = scale_of(us);
   const T* dp = resid ? reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d : tp;
-  const DrawRef DR = draw_ref(resid, r.M, (float)r.C, r.lam, resid ? 0.f : __ldcg(sref + us));
+  const DrawRef DR = draw_ref(resid, r.M, (float)r.C, r.lam, resid ? 0.f : src.r(us));
   int tok = -1, last_pos = -1;
   double lo = 0.0, hi = 0.0, lp_lo = 0.0, lp_hi = 0.0, vbase = base;
   // one vector at a time, not unrolled: this runs once per sequence, so its

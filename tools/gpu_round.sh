@@ -2,7 +2,7 @@
 #   gpurun --timeout 1500 -- 'bash tools/gpu_round.sh TAG'
 TAG=${1:-x}
 mkdir -p gpurun_out/$TAG
-timeout 900 python -m pytest tests -m gpu -x -q --durations=8 > gpurun_out/$TAG/gt.log 2>&1; tail -15 gpurun_out/$TAG/gt.log
+timeout 900 python -m pytest tests -m gpu -x -q --durations=5 > gpurun_out/$TAG/gt.log 2>&1; tail -15 gpurun_out/$TAG/gt.log
 for c in 3 4 2; do
   timeout 300 python bench.py --config $c --steps 40 --warmup 5 --no-cpu-baseline --e2e-steps 1 > gpurun_out/$TAG/b$c.json 2>gpurun_out/$TAG/b$c.err
   python - <<PY
