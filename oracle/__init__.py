@@ -72,6 +72,8 @@ def lib():
         L.oracle_verify.restype = C.c_int
         L.oracle_verify_mode.argtypes = list(L.oracle_verify.argtypes) + [C.c_int]
         L.oracle_verify_mode.restype = C.c_int
+        L.oracle_verify_temp.argtypes = list(L.oracle_verify.argtypes) + [C.c_int, C.c_void_p]
+        L.oracle_verify_temp.restype = C.c_int
         L.oracle_weighted_variance.argtypes = [P, C.c_int, C.c_double]
         L.oracle_weighted_variance.restype = C.c_double
         L.oracle_scale_factor.argtypes = [C.c_double]
@@ -87,6 +89,10 @@ def lib():
         L.oracle_state_reset.argtypes = [P, P, C.c_int]
         L.oracle_update_signal.argtypes = [P, C.c_int, P, P, P, P, P, P, P]
         L.oracle_update_signal.restype = C.c_int
+        L.oracle_update_signal_ent.argtypes = [P, C.c_int, P, P, P, P, P, P, P, P]
+        L.oracle_update_signal_ent.restype = C.c_int
+        L.oracle_entropy_sl.argtypes = [C.c_double, C.c_double, C.c_int, C.c_int, P]
+        L.oracle_entropy_sl.restype = C.c_int
         L.oracle_next_sl.argtypes = [P, C.c_int, P, P, P, P, P]
         L.oracle_next_sl.restype = C.c_int
         L.oracle_cap_partial.argtypes = [C.c_int, P, P, P, P]
@@ -161,11 +167,14 @@ class VerifyResult:
 
 
 def verify(cu_sl, draft_tokens, target_logits, draft_logits, seeds, dtype: int,
-           nthreads: int = 1, greedy: bool = False) -> VerifyResult:
+           nthreads: int = 1, greedy: bool = False, temperature=None) -> VerifyResult:
     """Batched verification. ``target_logits`` / ``draft_logits`` are 2-D numpy
-    arrays of float32 (dtype=F32) or uint16 bf16 bit patterns (dtype=BF16).
+    arrays of float32 (dtype=F32) or uint16 bf16 bit patterns (dtype=BF16);
+    -inf entries are masked tokens (D21).
     greedy=True: T = 0 verification (accept iff x_j = argmax t_j, emit the
-    target argmax)."""
+    target argmax).
+    temperature: optional per-sequence temperatures [B] (D20): p = softmax(t/T),
+    q = softmax(d/T); T = 0 makes that sequence greedy."""
     cu_sl = np.ascontiguousarray(cu_sl, dtype=np.int32)
     toks = np.ascontiguousarray(draft_tokens, dtype=np.int32)
     tl = np.ascontiguousarray(target_logits)
@@ -182,10 +191,13 @@ def verify(cu_sl, draft_tokens, target_logits, draft_logits, seeds, dtype: int,
         kld=np.zeros(nk, np.float64), log_ratio=np.zeros(nk, np.float64),
         u_acc=np.zeros(nk + B, np.float64), u_smp=np.zeros(nk + B, np.float64),
         samp_diag=np.zeros((B, 3), np.float64), flags=np.zeros(nk + B, np.int32))
-    rc = lib().oracle_verify_mode(B, V, dtype, _p(cu_sl), _p(toks), _p(tl), tl.shape[1], _p(dl),
+    temps = None if temperature is None else np.ascontiguousarray(temperature, dtype=np.float64)
+    assert temps is None or temps.size == B
+    rc = lib().oracle_verify_temp(B, V, dtype, _p(cu_sl), _p(toks), _p(tl), tl.shape[1], _p(dl),
                                   dl.shape[1], _p(seeds), _p(r.accepted_len), _p(r.emitted), _p(r.kld),
                                   _p(r.log_ratio), _p(r.u_acc), _p(r.u_smp), _p(r.samp_diag),
-                                  _p(r.flags), int(nthreads), int(bool(greedy)))
+                                  _p(r.flags), int(nthreads), int(bool(greedy)),
+                                  None if temps is None else _p(temps))
     if rc != 0:
         raise ValueError(f"oracle_verify failed: {rc}")
     return r
@@ -197,7 +209,7 @@ class _Cfg(C.Structure):
     _fields_ = [("delta", C.c_double), ("n_short", C.c_int), ("n_long", C.c_int),
                 ("sl_min", C.c_int), ("sl_ceiling", C.c_int), ("epsilon", C.c_double),
                 ("calib_steps", C.c_int), ("calib_sl", C.c_int), ("window_unit", C.c_int),
-                ("cap_mode", C.c_int)]
+                ("cap_mode", C.c_int), ("entropy_mode", C.c_int), ("entropy_gamma", C.c_double)]
 
 
 @dataclass
@@ -212,11 +224,13 @@ class Config:
     calib_sl: int = 4
     window_unit: int = 0
     cap_mode: int = 1
+    entropy_mode: int = 0      # 1: min(SL^, SL_H) with the draft-entropy predictor (D22)
+    entropy_gamma: float = 0.5
 
     def c(self) -> _Cfg:
         return _Cfg(self.delta, self.n_short, self.n_long, self.sl_min, self.sl_ceiling,
                     self.epsilon, self.calib_steps, self.calib_sl, self.window_unit,
-                    self.cap_mode)
+                    self.cap_mode, self.entropy_mode, self.entropy_gamma)
 
 
 def weighted_variance(values_recent_first, delta: float) -> float:
@@ -234,6 +248,13 @@ def calibrate(sl_a_max: int, mu_pre: float, kld_pre_max: float, sl_min: int = 2,
     r = lib().oracle_calibrate(int(sl_a_max), float(mu_pre), float(kld_pre_max), int(sl_min),
                                int(sl_ceiling), float(epsilon), C.byref(raw))
     return r, raw.value
+
+
+def entropy_sl(h_mean: float, gamma: float, sl_max: int, sl_min: int = 2) -> tuple[int, float]:
+    """D22: SL_H = clamp(rint(max(0, 1 - sqrt(gamma H)) (SL_max - SL_min) + SL_min))."""
+    x = C.c_double()
+    r = lib().oracle_entropy_sl(float(h_mean), float(gamma), int(sl_max), int(sl_min), C.byref(x))
+    return r, x.value
 
 
 def predict_sl(penalty: float, sl_max: int, sl_min: int = 2) -> tuple[int, float]:
@@ -262,7 +283,8 @@ class OracleState:
         s = np.ascontiguousarray(slots, dtype=np.int32)
         lib().oracle_state_reset(self._h, _p(s), s.size)
 
-    def update_signal(self, slots, cu_sl, kld, accepted_len):
+    def update_signal(self, slots, cu_sl, kld, accepted_len, entropy=None):
+        """entropy: optional draft entropy per draft position (cfg.entropy_mode, D22)."""
         slots = np.ascontiguousarray(slots, dtype=np.int32)
         cu_sl = np.ascontiguousarray(cu_sl, dtype=np.int32)
         kld = np.ascontiguousarray(kld, dtype=np.float64)
@@ -271,8 +293,9 @@ class OracleState:
         sl_hat = np.zeros(B, np.int32)
         calib = np.zeros(B, np.int32)
         diag = np.zeros((B, 8), np.float64)
-        rc = lib().oracle_update_signal(self._h, B, _p(slots), _p(cu_sl), _p(kld), _p(acc),
-                                        _p(sl_hat), _p(calib), _p(diag))
+        ent = None if entropy is None else np.ascontiguousarray(entropy, dtype=np.float64)
+        rc = lib().oracle_update_signal_ent(self._h, B, _p(slots), _p(cu_sl), _p(kld), _p(acc),
+                                            None if ent is None else _p(ent), _p(sl_hat), _p(calib), _p(diag))
         if rc != 0:
             raise ValueError("oracle_update_signal failed")
         return sl_hat, calib, diag

@@ -226,6 +226,7 @@ typedef struct {
     double* samp_diag;       /* [B][3] : R, lo, hi of the final draw */
     int32_t* flags;          /* [sum k + B] */
     int greedy;              /* 1: T = 0 verification (f1) */
+    const double* temps;     /* [B] per-sequence temperature (f1) or NULL = 1; T_i == 0: greedy */
     int b0, b1;              /* sequence range for this worker */
     int status;
 } verify_job;
@@ -245,19 +246,44 @@ static int row_argmax(const double* x, int V) {
  *   a <  k: recovery token ~ normalize(max(0, p - q)) on row a;
  *   a == k: bonus token ~ p on target row k;
  *   emitted = x_0..x_{a-1}, token, then DSDE pad (-1) up to slot k. */
+/* Logit row (sequence i) as the method sees it: the stored value divided by
+ * the sequence's temperature T_i > 0 (p = softmax(t / T), q = softmax(d / T):
+ * sampling at temperature T; D20). T_i == 0 (greedy) and no
+ * temperatures use the stored values (T = 1 semantics for the KLD, D18).
+ * Masked tokens (-inf logits, top-k / top-p, D21) stay -inf. */
+static void load_row_t(double* dst, const verify_job* J, const void* base, int64_t row, int64_t ld, int i) {
+    load_row(dst, base, J->dtype, row, ld, J->V);
+    if (J->temps && J->temps[i] > 0.0)
+        for (int v = 0; v < J->V; ++v) dst[v] = dst[v] / J->temps[i];
+}
+
+/* a row with no finite logit (everything masked) or a +inf / NaN logit is not
+ * a distribution */
+static int row_ok(const double* x, int V) {
+    int fin = 0;
+    for (int v = 0; v < V; ++v) {
+        if (isnan(x[v]) || x[v] == INFINITY) return 0;
+        if (x[v] > -INFINITY) fin = 1;
+    }
+    return fin;
+}
+
 static int verify_one(verify_job* J, int i, double* t, double* d, double* w) {
     const int V = J->V;
     const int32_t base = J->cu_sl[i];
     const int k = J->cu_sl[i + 1] - base;
     if (k < 1) return -1;
+    const int greedy = J->greedy || (J->temps && J->temps[i] == 0.0);
     const int64_t trow0 = (int64_t)base + i; /* target row of (i, j) = cu_sl[i] + i + j */
     const int64_t slot0 = (int64_t)base + i; /* output slot of (i, j), j in [0, k]     */
     int a = k;
     for (int j = 0; j < k; ++j) {
         const int x = J->draft_tokens[base + j];
         if (x < 0 || x >= V) return -1;
-        load_row(t, J->tl, J->dtype, trow0 + j, J->ld_t, V);
-        load_row(d, J->dl, J->dtype, (int64_t)base + j, J->ld_d, V);
+        load_row_t(t, J, J->tl, trow0 + j, J->ld_t, i);
+        load_row_t(d, J, J->dl, (int64_t)base + j, J->ld_d, i);
+        if (!row_ok(t, V) || !row_ok(d, V)) return -1;
+        if (d[x] == -INFINITY) return -1; /* x ~ q: a token the draft masked cannot be drafted (D21) */
         const double kl = oracle_row_kld(V, t, d);
         const double lr = oracle_row_log_ratio(V, t, d, x);
         double ua, us;
@@ -267,7 +293,7 @@ static int verify_one(verify_job* J, int i, double* t, double* d, double* w) {
         J->u_acc[slot0 + j] = ua;
         J->u_smp[slot0 + j] = us;
         J->flags[slot0 + j] = 0;
-        if (J->greedy) {
+        if (greedy) {
             /* T = 0: accept iff x_j is the target argmax */
             if (a == k && x != row_argmax(t, V)) a = j;
             continue;
@@ -289,13 +315,14 @@ static int verify_one(verify_job* J, int i, double* t, double* d, double* w) {
     const double u = J->u_smp[slot0 + a];
     int tok;
     double R = 0.0, lo = 0.0, hi = 0.0;
-    if (J->greedy) {
+    if (greedy) {
         /* the target argmax of row a (recovery, a < k) or of the bonus row k */
-        load_row(t, J->tl, J->dtype, trow0 + a, J->ld_t, V);
+        load_row_t(t, J, J->tl, trow0 + a, J->ld_t, i);
+        if (!row_ok(t, V)) return -1;
         tok = row_argmax(t, V);
     } else if (a < k) {
-        load_row(t, J->tl, J->dtype, trow0 + a, J->ld_t, V);
-        load_row(d, J->dl, J->dtype, (int64_t)base + a, J->ld_d, V);
+        load_row_t(t, J, J->tl, trow0 + a, J->ld_t, i);
+        load_row_t(d, J, J->dl, (int64_t)base + a, J->ld_d, i);
         const double lt = row_lse(t, V), ld = row_lse(d, V);
         for (int v = 0; v < V; ++v) {
             const double pv = exp(t[v] - lt), qv = exp(d[v] - ld);
@@ -308,12 +335,13 @@ static int verify_one(verify_job* J, int i, double* t, double* d, double* w) {
             J->flags[slot0 + a] |= OR_FLAG_FALLBACK;
         }
     } else {
-        load_row(t, J->tl, J->dtype, trow0 + k, J->ld_t, V);
+        load_row_t(t, J, J->tl, trow0 + k, J->ld_t, i);
+        if (!row_ok(t, V)) return -1;
         const double lt = row_lse(t, V);
         for (int v = 0; v < V; ++v) w[v] = exp(t[v] - lt);  /* p_v */
         tok = inverse_cdf(w, V, u, &R, &lo, &hi);
     }
-    if (!J->greedy && (fabs(u - lo) < 1e-6 || fabs(u - hi) < 1e-6)) J->flags[slot0 + a] |= OR_FLAG_SAMPLE_TIE;
+    if (!greedy && (fabs(u - lo) < 1e-6 || fabs(u - hi) < 1e-6)) J->flags[slot0 + a] |= OR_FLAG_SAMPLE_TIE;
     J->samp_diag[3 * i + 0] = R;
     J->samp_diag[3 * i + 1] = lo;
     J->samp_diag[3 * i + 2] = hi;
@@ -344,12 +372,12 @@ static void* verify_worker(void* arg) {
  * cu_sl[i]+i+j for j in [0,k_i]; per-slot outputs (emitted, u_acc, u_smp,
  * flags) use the target-row index. nthreads <= 1 runs serially.
  * Returns 0, or -1 on invalid data (k < 1, token out of range). */
-OR_EXPORT int oracle_verify_mode(int B, int V, int dtype, const int32_t* cu_sl,
+OR_EXPORT int oracle_verify_temp(int B, int V, int dtype, const int32_t* cu_sl,
                                  const int32_t* draft_tokens, const void* target_logits, int64_t ld_t,
                                  const void* draft_logits, int64_t ld_d, const uint64_t* seeds,
                                  int32_t* accepted_len, int32_t* emitted, double* kld,
                                  double* log_ratio, double* u_acc, double* u_smp, double* samp_diag,
-                                 int32_t* flags, int nthreads, int greedy) {
+                                 int32_t* flags, int nthreads, int greedy, const double* temps) {
     if (B < 1 || V < 2 || (dtype != 0 && dtype != 1)) return -1;
     if (nthreads < 1) nthreads = 1;
     if (nthreads > B) nthreads = B;
@@ -380,6 +408,7 @@ OR_EXPORT int oracle_verify_mode(int B, int V, int dtype, const int32_t* cu_sl,
         J->samp_diag = samp_diag;
         J->flags = flags;
         J->greedy = greedy;
+        J->temps = temps;
         J->b0 = (int)((int64_t)B * n / nthreads);
         J->b1 = (int)((int64_t)B * (n + 1) / nthreads);
     }
@@ -395,6 +424,18 @@ OR_EXPORT int oracle_verify_mode(int B, int V, int dtype, const int32_t* cu_sl,
     free(jobs);
     free(th);
     return rc;
+}
+
+/* Global T = 0 (greedy = 1) or T = 1 (greedy = 0) verification. */
+OR_EXPORT int oracle_verify_mode(int B, int V, int dtype, const int32_t* cu_sl,
+                                 const int32_t* draft_tokens, const void* target_logits, int64_t ld_t,
+                                 const void* draft_logits, int64_t ld_d, const uint64_t* seeds,
+                                 int32_t* accepted_len, int32_t* emitted, double* kld,
+                                 double* log_ratio, double* u_acc, double* u_smp, double* samp_diag,
+                                 int32_t* flags, int nthreads, int greedy) {
+    return oracle_verify_temp(B, V, dtype, cu_sl, draft_tokens, target_logits, ld_t, draft_logits, ld_d,
+                              seeds, accepted_len, emitted, kld, log_ratio, u_acc, u_smp, samp_diag, flags,
+                              nthreads, greedy, NULL);
 }
 
 /* The rejection-sampling verification (the default, C1). */
@@ -425,6 +466,8 @@ typedef struct {
     int calib_sl;       /* SL used while calibrating (D12 default 4)      */
     int window_unit;    /* 0 = per-token observations, 1 = per-step means (D8) */
     int cap_mode;       /* 0 = none (cap = max), 1 = mean / MSE (Eq.11)   */
+    int entropy_mode;   /* 0 = KLD signal only; 1 = also the draft-entropy predictor (D22) */
+    double entropy_gamma; /* gamma of the entropy bound alpha_H = 1 - sqrt(gamma H) (D22) */
 } oracle_cfg;
 
 typedef struct {
@@ -534,10 +577,30 @@ static void hist_append(oracle_seq* q, int n_long, double x) {
  * x (pre-round SL^), sl_max. Calibrating sequences (D12) return calib_sl
  * and report their flag in calibrating[i] (1) — they are not capped and
  * do not enter the cap mean. */
-OR_EXPORT int oracle_update_signal(oracle_state* s, int B, const int32_t* slots,
-                                   const int32_t* cu_sl, const double* kld,
-                                   const int32_t* accepted_len, int32_t* sl_hat,
-                                   int32_t* calibrating, double* diag) {
+/* The draft-entropy predictor ("KLD variance (optionally
+ * combined with entropy)"; the entropy early-stopping bound of AdaEDL,
+ * P:135), reading D22: with H the mean draft entropy of the step's positions,
+ * alpha_H = max(0, 1 - sqrt(gamma H)) bounds the per-token acceptance from
+ * below, and SL_H maps it to [SL_min, SL_max] as Eq.8 maps 1 - penalty:
+ * SL_H = clamp(rint(alpha_H (SL_max - SL_min) + SL_min)). x_out: pre-round value. */
+OR_EXPORT int oracle_entropy_sl(double h_mean, double gamma, int sl_max, int sl_min, double* x_out) {
+    double a = 1.0 - sqrt(gamma * h_mean);
+    if (a < 0.0) a = 0.0;
+    const double x = a * (double)(sl_max - sl_min) + (double)sl_min;
+    if (x_out) *x_out = x;
+    double r = rint(x);
+    if (r < sl_min) r = sl_min;
+    if (r > sl_max) r = sl_max;
+    return (int)r;
+}
+
+/* entropy (optional, [sum k]): the draft entropy of every draft position;
+ * with cfg.entropy_mode = 1 the post-calibration prediction is
+ * min(SL^ of Eq.8, SL_H) (D22). */
+OR_EXPORT int oracle_update_signal_ent(oracle_state* s, int B, const int32_t* slots,
+                                       const int32_t* cu_sl, const double* kld,
+                                       const int32_t* accepted_len, const double* entropy,
+                                       int32_t* sl_hat, int32_t* calibrating, double* diag) {
     const oracle_cfg* c = &s->cfg;
     for (int i = 0; i < B; ++i) {
         oracle_seq* q = &s->seq[slots[i]];
@@ -591,6 +654,12 @@ OR_EXPORT int oracle_update_signal(oracle_state* s, int B, const int32_t* slots,
             out = c->calib_sl;
         } else {
             out = oracle_predict_sl(penalty, q->sl_max, c->sl_min, &x);
+            if (c->entropy_mode == 1 && entropy) {
+                double hs = 0.0;
+                for (int j = 0; j < k; ++j) hs += entropy[cu_sl[i] + j];
+                const int sl_h = oracle_entropy_sl(hs / (double)k, c->entropy_gamma, q->sl_max, c->sl_min, NULL);
+                if (sl_h < out) out = sl_h;
+            }
         }
         sl_hat[i] = out;
         if (calibrating) calibrating[i] = calib;
@@ -607,6 +676,13 @@ OR_EXPORT int oracle_update_signal(oracle_state* s, int B, const int32_t* slots,
         }
     }
     return 0;
+}
+
+OR_EXPORT int oracle_update_signal(oracle_state* s, int B, const int32_t* slots,
+                                   const int32_t* cu_sl, const double* kld,
+                                   const int32_t* accepted_len, int32_t* sl_hat,
+                                   int32_t* calibrating, double* diag) {
+    return oracle_update_signal_ent(s, B, slots, cu_sl, kld, accepted_len, NULL, sl_hat, calibrating, diag);
 }
 
 /* ------------------------------------------------------------------ */

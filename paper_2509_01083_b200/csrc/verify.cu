@@ -467,20 +467,33 @@ __device__ __forceinline__ SubPartial empty_partial() {
   return p;
 }
 
+// The warp's three sums by recursive halving (6 shuffles instead of 15):
+// after the xor-16 and xor-8 rounds lanes 0-7 hold partial S, 8-15 A, 16-23 D;
+// three more rounds complete them; lane 0 gathers A and D.
 __device__ __forceinline__ SubPartial finish_partial(float2 S2, float2 A2, float2 D2, float M, float Dmax,
                                                      float Cw) {
-  float S = S2.x + S2.y, A = A2.x + A2.y, D = D2.x + D2.y;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    S += __shfl_xor_sync(kFull, S, o);
-    A += __shfl_xor_sync(kFull, A, o);
-    D += __shfl_xor_sync(kFull, D, o);
+  const int lane = threadIdx.x & 31;
+  float s = S2.x + S2.y, aa = A2.x + A2.y;
+  const float dd = D2.x + D2.y;
+  {  // xor 16: lanes < 16 keep (S, A), lanes >= 16 keep (D, 0)
+    const bool up = lane & 16;
+    const float k0 = up ? dd : s, k1 = up ? 0.f : aa;
+    const float s0 = up ? s : dd, s1 = up ? aa : 0.f;
+    s = k0 + __shfl_xor_sync(kFull, s0, 16);
+    aa = k1 + __shfl_xor_sync(kFull, s1, 16);
   }
+  {  // xor 8: lanes with bit 3 clear keep the first, set keep the second
+    const bool up = lane & 8;
+    const float k0 = up ? aa : s, s0 = up ? s : aa;
+    s = k0 + __shfl_xor_sync(kFull, s0, 8);
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
   SubPartial p;
   p.pad0 = p.pad1 = 0.f;
-  p.S = S;
-  p.A = A;
-  p.D = D;
+  p.S = s;
+  p.A = __shfl_sync(kFull, s, 8);
+  p.D = __shfl_sync(kFull, s, 16);
   p.M = M;
   p.C = Cw;
   p.maxd = Dmax;
@@ -563,10 +576,11 @@ __device__ __forceinline__ int stream_rows(const StreamArgs& a) {
 }
 
 // ---------------------------------------------------------------------------
-// a1, "ldg" variant: persistent warps over the units q = (draft row r, slice u),
-// q = global warp + j * (total warps). Each lane keeps the NEXT unit's 2 x 4
-// 16-byte vectors in flight while it computes the current one (ping-pong
-// register buffers, no shared memory, no block barriers).
+// a1: persistent warps over the units q = (draft row r, slice u), q = global
+// warp + j * (total warps), row-major so rows complete in order. Per unit each
+// lane issues its NV + NV 16-byte non-allocating loads at once (the whole
+// 2048-token slice pair of the warp), reduces the slice maxima (the reference)
+// and accumulates S, A, D; no shared memory, no block barriers.
 // ---------------------------------------------------------------------------
 constexpr int kLdgThreads = 256;
 #ifndef DSDE_LDG_MINB

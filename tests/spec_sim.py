@@ -21,8 +21,15 @@ import synth
 
 
 class Tables:
-    def __init__(self, V: int, L: int, seed: int, sigma_t=1.5, sigma_n=0.9, dtype=np.float32):
+    """temp: sampling temperature of both models (p = softmax(T / temp));
+    mask_t / mask_d: probability that an entry of the target / draft table is
+    masked (-inf, as a top-k / top-p filter leaves it); every row keeps at
+    least one token of the target's support unmasked in both tables."""
+
+    def __init__(self, V: int, L: int, seed: int, sigma_t=1.5, sigma_n=0.9, dtype=np.float32,
+                 temp: float = 1.0, mask_t: float = 0.0, mask_d: float = 0.0):
         self.V, self.L = V, L
+        self.temp = temp
         self.off = [0]
         for m in range(L + 1):
             self.off.append(self.off[-1] + V ** m)
@@ -31,8 +38,16 @@ class Tables:
         self.T = (r.normal(0, sigma_t, (n, V))).astype(dtype)
         self.D = (self.T.astype(np.float64) + r.normal(0, sigma_n, (n, V))
                   + r.uniform(-3, 3, (n, 1))).astype(dtype)
-        self.P = sps.softmax(self.T.astype(np.float64), axis=1)
-        self.Q = sps.softmax(self.D.astype(np.float64), axis=1)
+        if mask_t > 0 or mask_d > 0:
+            keep = r.integers(0, V, n)  # one token per row that neither table masks
+            mt = r.random((n, V)) < mask_t
+            md = r.random((n, V)) < mask_d
+            mt[np.arange(n), keep] = False
+            md[np.arange(n), keep] = False
+            self.T[mt] = -np.inf
+            self.D[md] = -np.inf
+        self.P = sps.softmax(self.T.astype(np.float64) / temp, axis=1)
+        self.Q = sps.softmax(self.D.astype(np.float64) / temp, axis=1)
 
     def index(self, ctx_code: np.ndarray, length: np.ndarray) -> np.ndarray:
         """Row index of contexts given as base-V codes of the given lengths."""
