@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define DSDE_ABI_VERSION 2
+#define DSDE_ABI_VERSION 3
 
 typedef enum {
     DSDE_OK = 0,
@@ -78,7 +78,8 @@ typedef enum { DSDE_F32 = 0, DSDE_BF16 = 1 } dsde_dtype;
  * Validity (S:173-174 plus D11/D17): 0 < delta <= 1; 1 <= n_short < n_long
  * <= DSDE_MAX_WINDOW; sl_min >= 1; sl_min < sl_ceiling <= DSDE_MAX_SL;
  * epsilon > 0; calib_steps >= 0; 1 <= calib_sl <= sl_ceiling;
- * window_unit in {0,1}; cap_mode in {0,1}; greedy in {0,1}. */
+ * window_unit in {0,1}; cap_mode in {0,1}; greedy in {0,1}; masked in {0,1};
+ * entropy_mode in {0,1}; entropy_gamma > 0. */
 typedef struct {
     double delta;      /* decay factor of Eq.5, 0.85                         */
     int n_short;       /* short window, 10                                   */
@@ -101,6 +102,17 @@ typedef struct {
                           for the capacity. The launch configuration of dsde_verify / dsde_step then
                           no longer depends on the SLs, so one captured CUDA graph serves every SL
                           pattern (the SLs are device data). */
+    int masked;        /* 0 = every logit is finite (default). 1 = logits may be -inf (top-k / top-p
+                          masks, D21): a -inf target logit has p = 0, a -inf draft
+                          logit q = 0; KL(p||q) = +inf when the draft masks a token the target keeps;
+                          a draft token with q(x) = 0 is DSDE_DERR_BAD_TOKEN. The stream then takes
+                          the exact per-element path everywhere. Not combinable with the draft
+                          entropy (dsde_set_draft_entropy): DSDE_ERR_ARG. */
+    int entropy_mode;  /* 0 = KLD signal only (default). 1 = SL^ = min(Eq.8, SL_H) with the draft-entropy
+                          predictor SL_H = clamp(rint(max(0, 1 - sqrt(gamma H)) (SL_max - SL_min)
+                          + SL_min)), H = the mean draft entropy of the step (D22; "optionally combined
+                          with entropy"). Needs dsde_set_draft_entropy (else DSDE_ERR_ARG). */
+    double entropy_gamma; /* gamma of D22, 0.5 */
 } dsde_config;
 
 typedef struct dsde_state_s* dsde_state; /* per-sequence KLD ring, calibration, SL_max, error word */
@@ -220,6 +232,16 @@ dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_draft_rows,
                         const uint64_t* seeds, int32_t* accepted_len,
                         int32_t* emitted_tokens, float* kld, uint8_t* flags,
                         void* workspace, size_t ws_bytes, dsde_state st, void* stream);
+
+/* Per-sequence sampling temperature (D20; P:312 evaluates T = 0 and 1, P:490
+ * per-sequence temperature) of the following dsde_verify /
+ * dsde_step calls on this state: `temperature` is device float[B] indexed by
+ * batch position (read by every call; the caller owns it), NULL = T = 1 for
+ * every sequence (the default). T > 0: p = softmax(t / T), q = softmax(d / T)
+ * (KLDs, accept test and draws at T); T = 0: that sequence verifies greedily
+ * (as dsde_config.greedy, D18, KLDs at T = 1). A negative or non-finite T is
+ * a DSDE_DERR_NONFINITE device error for its sequence. */
+dsde_status dsde_set_temperature(dsde_state st, const float* temperature);
 
 /* Kernel timing of dsde_verify / dsde_step (instrumentation; off by
  * default). While enabled, every dsde_verify / dsde_step call on this state

@@ -30,7 +30,8 @@ DERR = {0: "none", 1: "bad_sl", 2: "bad_token", 3: "nonfinite", 4: "rows", 5: "b
 
 # Every function the header declares (checked against include/dsde.h by the tests).
 EXPORTS = (
-    "dsde_config_default", "dsde_status_string", "dsde_abi_version", "dsde_set_draft_entropy", "dsde_state_create",
+    "dsde_config_default", "dsde_status_string", "dsde_abi_version", "dsde_set_draft_entropy", "dsde_set_temperature",
+    "dsde_state_create",
     "dsde_state_reset", "dsde_state_destroy", "dsde_state_bytes", "dsde_state_export",
     "dsde_state_import", "dsde_get_device_error", "dsde_clear_device_error",
     "dsde_verify_workspace_size", "dsde_verify", "dsde_update_signal", "dsde_next_sl", "dsde_step",
@@ -51,7 +52,8 @@ class Config(C.Structure):
     _fields_ = [("delta", C.c_double), ("n_short", C.c_int), ("n_long", C.c_int),
                 ("sl_min", C.c_int), ("sl_ceiling", C.c_int), ("epsilon", C.c_double),
                 ("calib_steps", C.c_int), ("calib_sl", C.c_int), ("window_unit", C.c_int),
-                ("cap_mode", C.c_int), ("greedy", C.c_int), ("device_rows", C.c_int)]
+                ("cap_mode", C.c_int), ("greedy", C.c_int), ("device_rows", C.c_int),
+                ("masked", C.c_int), ("entropy_mode", C.c_int), ("entropy_gamma", C.c_double)]
 
     @classmethod
     def default(cls, **kw) -> "Config":
@@ -83,6 +85,7 @@ def lib() -> C.CDLL:
         L.dsde_status_string.restype = C.c_char_p
         L.dsde_abi_version.restype = I
         L.dsde_set_draft_entropy.argtypes = [P, P]
+        L.dsde_set_temperature.argtypes = [P, P]
         L.dsde_state_create.argtypes = [P, I, P]
         L.dsde_state_reset.argtypes = [P, P, I, P]
         L.dsde_state_destroy.argtypes = [P]
@@ -188,6 +191,14 @@ class State:
         draft row to ``out`` (float32 device tensor, >= sum k rows); None turns it off."""
         self._entropy_ref = out  # keep the buffer alive while the library holds its pointer
         _check(lib().dsde_set_draft_entropy(self.h, None if out is None else _ptr(out)), "dsde_set_draft_entropy")
+
+    def set_temperature(self, temperature=None):
+        """dsde_set_temperature (D20): per-sequence temperatures (float32 device
+        tensor [B], batch order) for later verify / step calls; T = 0 makes that
+        sequence greedy; None = T = 1 for every sequence."""
+        self._temp_ref = temperature  # keep the buffer alive while the library holds its pointer
+        _check(lib().dsde_set_temperature(self.h, None if temperature is None else _ptr(temperature)),
+               "dsde_set_temperature")
 
     def profile(self, enable: bool = True):
         """Turns on/off per-kernel CUDA-event timing of dsde_verify calls on this state."""

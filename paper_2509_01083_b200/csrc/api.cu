@@ -26,7 +26,8 @@ bool cfg_valid(const dsde_config& c) {
          c.sl_ceiling <= DSDE_MAX_SL && c.epsilon > 0.0 && c.calib_steps >= 0 &&
          c.calib_sl >= 1 && c.calib_sl <= c.sl_ceiling && (c.window_unit == 0 || c.window_unit == 1) &&
          (c.cap_mode == 0 || c.cap_mode == 1) && (c.greedy == 0 || c.greedy == 1) &&
-         (c.device_rows == 0 || c.device_rows == 1);
+         (c.device_rows == 0 || c.device_rows == 1) && (c.masked == 0 || c.masked == 1) &&
+         (c.entropy_mode == 0 || c.entropy_mode == 1) && c.entropy_gamma > 0.0;
 }
 
 __global__ void k_reset_slots(SeqState* seq, int max_seqs, const int32_t* slots, int n) {
@@ -99,6 +100,9 @@ void dsde_config_default(dsde_config* c) {
   c->cap_mode = 1;
   c->greedy = 0;
   c->device_rows = 0;
+  c->masked = 0;
+  c->entropy_mode = 0;
+  c->entropy_gamma = 0.5;
 }
 
 const char* dsde_status_string(dsde_status s) {

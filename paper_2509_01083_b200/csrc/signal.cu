@@ -72,8 +72,9 @@ extern "C" dsde_status dsde_update_signal(dsde_state st, int B, const int32_t* s
                                           double* diag, void* stream) {
   if (!st || !slots || !cu_sl || !kld || !accepted_len || !sl_hat || B < 1) return DSDE_ERR_ARG;
   if (B > st->max_seqs) return DSDE_ERR_STATE;
+  if (st->cfg.entropy_mode && !st->entropy_out) return DSDE_ERR_ARG;  // D22 reads the draft entropy
   SignalArgs a{st->cfg, B, st->max_seqs, slots, cu_sl, kld, accepted_len, sl_hat, diag, st->seq,
-               st->err};
+               st->err, st->cfg.entropy_mode ? st->entropy_out : nullptr};
   k_update_signal<<<(B + 3) / 4, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
   return cudaGetLastError() == cudaSuccess ? DSDE_OK : DSDE_ERR_CUDA;
 }

@@ -31,6 +31,7 @@ struct SignalArgs {
   double* diag;
   SeqState* seq;
   int32_t* err;
+  const float* ent;  // [sum k] draft entropy per position (cfg.entropy_mode, D22), else NULL
 };
 
 // Eq.1 + D11: SL_max = clamp(rint(raw), sl_min + 1, sl_ceiling).
@@ -56,7 +57,9 @@ __device__ __forceinline__ double wsum(double v) {
 // signal_seq_vals: the update from values in registers — lane j < k holds
 // the fp32 KLD of position j (as a double), acc = a_i in every lane (-1: the
 // verify flagged the sequence). signal_seq loads them from kld / acc_len.
-__device__ __forceinline__ void signal_seq_vals(const SignalArgs& a, int i, int k, double x, int acc) {
+// h: lane j < k holds the draft entropy of position j (entropy_mode, D22).
+__device__ __forceinline__ void signal_seq_vals(const SignalArgs& a, int i, int k, double x, int acc,
+                                                double h = 0.0) {
   const int lane = threadIdx.x & 31;
   const dsde_config& c = a.cfg;
   const int slot = a.slots[i];
@@ -167,6 +170,15 @@ __device__ __forceinline__ void signal_seq_vals(const SignalArgs& a, int i, int 
     if (rr < c.sl_min) rr = c.sl_min;
     if (rr > sl_max) rr = sl_max;
     out = (int)rr;
+    if (c.entropy_mode == 1 && a.ent) {
+      // D22: SL_H from the mean draft entropy of the step, SL^ = min(SL^, SL_H)
+      const double hm = wsum(lane < k ? h : 0.0) / (double)k;
+      const double al = fmax(0.0, 1.0 - sqrt(c.entropy_gamma * hm));
+      double rh = rint(al * (double)(sl_max - c.sl_min) + (double)c.sl_min);
+      if (rh < c.sl_min) rh = c.sl_min;
+      if (rh > sl_max) rh = sl_max;
+      if ((int)rh < out) out = (int)rh;
+    }
   }
   if (lane == 0) {
     s.head = head;
@@ -198,7 +210,8 @@ __device__ __forceinline__ void signal_seq(const SignalArgs& a, int i) {
   const int c0 = a.cu_sl[i], k = a.cu_sl[i + 1] - c0;
   const int acc = (c0 < 0 || k < 1 || k > DSDE_MAX_SL) ? -1 : a.acc_len[i];
   const double x = (acc >= 0 && lane < k) ? (double)a.kld[c0 + lane] : 0.0;
-  signal_seq_vals(a, i, k, x, acc);
+  const double h = (a.ent && acc >= 0 && lane < k) ? (double)a.ent[c0 + lane] : 0.0;
+  signal_seq_vals(a, i, k, x, acc, h);
 }
 
 // Eq.11 integerised exactly (D14): q, r = divmod(sum, n); round half

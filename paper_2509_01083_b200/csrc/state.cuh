@@ -60,6 +60,7 @@ struct dsde_state_s {
   long long* scratch;    // [8]: cap partials (sum, n, max) for dsde_next_sl
   dsde::Profiler* prof;  // kernel timing (host side), created by dsde_profile_enable
   float* entropy_out;    // dsde_set_draft_entropy: H(q) per draft row, NULL = off
+  const float* temps;    // dsde_set_temperature: T per sequence, NULL = 1 (D20)
 };
 
 struct dsde_comm_s {

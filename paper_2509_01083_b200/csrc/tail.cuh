@@ -38,9 +38,9 @@ __device__ __forceinline__ int atomic_add_acq_rel(int* p, int v) {
 
 // a5-a7 of sequence i by one warp (dsde_step): the signal from the layout's
 // values, then the batch cap by the warp whose signal completes the batch.
-__device__ __forceinline__ void tail_signal(const TailArgs& p, int i, int k, double x, int acc) {
+__device__ __forceinline__ void tail_signal(const TailArgs& p, int i, int k, double x, int acc, double h = 0.0) {
   if (!p.step) return;
-  signal_seq_vals(p.sig, i, k, x, acc);
+  signal_seq_vals(p.sig, i, k, x, acc, h);
   __syncwarp();
   int last = 0;
   if ((threadIdx.x & 31) == 0) last = atomic_add_acq_rel(p.ctl, 1) == p.fa.B - 1;
@@ -122,7 +122,9 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
     // 3. a5-a7 (dsde_step) by the last warp, then a4's slice masses by all
     if (warp == NW - 1 && p.step) {
       const double x = lane < k ? (double)(float)s_rr[lane].kl : 0.0;  // the fp32 KLDs, as the 3-call path
-      tail_signal(p, i, k, x, s_acc);
+      // the draft entropies the finalize warps wrote (D22), as the 3-call path reads them
+      const double h = (p.sig.ent && lane < k && s_acc >= 0) ? (double)__ldcg(p.sig.ent + c0 + lane) : 0.0;
+      tail_signal(p, i, k, x, s_acc, h);
     }
     if (r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS || r.mode == MODE_ARGMAX) {
       const long long q0 = (long long)i * nd;

@@ -79,8 +79,8 @@ struct SeqRec {  // 64 bytes
   int slot;          // output slot of the drawn token, cu_sl[i] + i + a_i
   long long trow;    // target row to draw from
   long long drow;    // draft row (residual only)
-  float M;           // reference max of t (residual)
-  int pad0;
+  float M;           // reference max of t / T (residual)
+  float invT;        // 1 / T of the sequence (D20; 1 for greedy)
   double C;          // reference t - d (residual)
   double lam;        // log1p(y) = log(sum_v p_v exp(-w_v)) (residual)
   double u;          // u_smp of the slot
@@ -192,15 +192,32 @@ __device__ __forceinline__ float2 pair_of(const uint4 (&r)[N], int h) {
   }
 }
 
+// w = (t - d) / T - C with the difference t - d exact (bf16) or carried as
+// hi + lo (fp32, TwoDiff) and one rounding for the scale and the reference;
+// invT = 1 gives exactly the FADD of (t - d) and -C.
 template <typename T>
-__device__ __forceinline__ float2 diff2(float2 t, float2 d, float C);
+__device__ __forceinline__ float2 diff2(float2 t, float2 d, float C, float invT);
 template <>
-__device__ __forceinline__ float2 diff2<uint16_t>(float2 t, float2 d, float C) {
-  return __fadd2_rn(__fadd2_rn(t, make_float2(-d.x, -d.y)), make_float2(-C, -C));
+__device__ __forceinline__ float2 diff2<uint16_t>(float2 t, float2 d, float C, float invT) {
+  return __ffma2_rn(__fadd2_rn(t, make_float2(-d.x, -d.y)), make_float2(invT, invT), make_float2(-C, -C));
 }
 template <>
-__device__ __forceinline__ float2 diff2<float>(float2 t, float2 d, float C) {
-  return make_float2(diff_ref<float>(t.x, d.x, C), diff_ref<float>(t.y, d.y, C));
+__device__ __forceinline__ float2 diff2<float>(float2 t, float2 d, float C, float invT) {
+  // (an infinite difference — a masked logit, D21 — keeps its sign: lo = 0)
+  float2 r;
+  {
+    const float hi = __fsub_rn(t.x, d.x), bb = __fsub_rn(hi, t.x);
+    float lo = __fadd_rn(__fsub_rn(t.x, __fsub_rn(hi, bb)), __fsub_rn(-d.x, bb));
+    if (!(fabsf(hi) < INFINITY)) lo = 0.f;
+    r.x = __fadd_rn(__fmaf_rn(hi, invT, -C), __fmul_rn(lo, invT));
+  }
+  {
+    const float hi = __fsub_rn(t.y, d.y), bb = __fsub_rn(hi, t.y);
+    float lo = __fadd_rn(__fsub_rn(t.y, __fsub_rn(hi, bb)), __fsub_rn(-d.y, bb));
+    if (!(fabsf(hi) < INFINITY)) lo = 0.f;
+    r.y = __fadd_rn(__fmaf_rn(hi, invT, -C), __fmul_rn(lo, invT));
+  }
+  return r;
 }
 
 // ---------------------------------------------------------------------------
@@ -299,16 +316,32 @@ struct LaneMax {
   }
 };
 
-// Per-slice constants of the a1 sums about the reference (M, C = M - max d).
+// Per-slice constants of the a1 sums about the reference (M, C = M - max d),
+// at temperature T (D20): logits enter as t / T, so the reference is the raw
+// maxima times invT = 1/T and the exponent scale is invT log2 e (both exact
+// copies of the untempered constants when invT = 1).
 struct SumRef {
-  float2 nML2, nDL2;
-  float Cw;
-  __device__ __forceinline__ SumRef(float M, float Dmax) {
-    Cw = M - Dmax;
-    const float ML2 = M * kLog2e, DL2 = Dmax * kLog2e;
+  float2 nML2, nDL2, L2s;
+  float Cw, invT;
+  __device__ __forceinline__ SumRef(float M, float Dmax, float inv_t = 1.f) {
+    invT = inv_t;
+    const float Ms = M * inv_t, Ds = Dmax * inv_t;
+    Cw = Ms - Ds;
+    const float ML2 = Ms * kLog2e, DL2 = Ds * kLog2e, l2 = kLog2e * inv_t;
     nML2 = make_float2(-ML2, -ML2);
     nDL2 = make_float2(-DL2, -DL2);
+    L2s = make_float2(l2, l2);
   }
+};
+
+// Masked-logit sums (D21; dsde_config.masked): Fp = sum of e e^{-w} (the
+// draft mass on supp p, in e's frame: p's reference minus C), Fm = sum of
+// e^{d/T - max d/T} over the tokens the target masks (draft mass outside
+// supp p, about the slice's max d); cc = some token the draft masks has p > 0
+// (then KL(p||q) = +inf).
+struct MaskAcc {
+  float2 Fp, Fm;
+  int cc;
 };
 
 // a1 accumulation of one element pair (packed FFMA2 math, two MUFU.EX2 per
@@ -319,10 +352,11 @@ struct EntAcc {
   float2 Sd, E;
 };
 
-template <typename T, bool ENT = false>
+template <typename T, bool ENT = false, bool MASK = false>
 __device__ __forceinline__ void pair_accum_w(float2 tt, float2 dd, float2 w, const SumRef& R, float2& S2,
-                                             float2& A2, float2& D2, EntAcc* ent = nullptr) {
-  const float2 L2 = make_float2(kLog2e, kLog2e);
+                                             float2& A2, float2& D2, EntAcc* ent = nullptr,
+                                             MaskAcc* mk = nullptr) {
+  const float2 L2 = R.L2s;
 #ifndef DSDE_POLY_DEG7
   const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
   const float2 K5 = make_float2(-2.0329201652202755e-04f, -2.0329201652202755e-04f);
@@ -342,9 +376,30 @@ __device__ __forceinline__ void pair_accum_w(float2 tt, float2 dd, float2 w, con
   const float2 K0 = make_float2(0.5f, 0.5f);
 #endif
   const float2 xt = __ffma2_rn(tt, L2, R.nML2);
-  const float2 arg = __ffma2_rn(dd, L2, R.nDL2);  // (d - max d) log2 e <= 0
   const float2 e = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));
-  const float2 f = make_float2(fast_exp2(arg.x), fast_exp2(arg.y));
+  if constexpr (MASK) {
+    // t = -inf (p_v = 0): e = 0, the draft mass e^{d/T - max d/T} goes to Fm;
+    // d = -inf while t is finite (q_v = 0 < p_v): KL = +inf (cc); either way w
+    // is replaced by 0 so that A and D get exact zeros instead of 0 * inf
+    const bool mtx = tt.x == -INFINITY, mty = tt.y == -INFINITY;
+    const bool mdx = dd.x == -INFINITY, mdy = dd.y == -INFINITY;
+    const float2 arg = __ffma2_rn(dd, L2, R.nDL2);
+    mk->Fm = __fadd2_rn(mk->Fm, make_float2(mtx ? fast_exp2(arg.x) : 0.f, mty ? fast_exp2(arg.y) : 0.f));
+    mk->cc |= (mdx && !mtx) || (mdy && !mty);
+    w = make_float2((mtx || mdx) ? 0.f : w.x, (mty || mdy) ? 0.f : w.y);
+  }
+  // f = e e^{-w} = e^{d/T - (M/T - C)}, formed from e's own exponent so that
+  // e, f and w share one reference (a separately rounded reference for f would
+  // shift f against e by the rounding of (max d / T) log2 e, which the
+  // cancellation in f - e + e w amplifies); the exponent is <= 0 up to the
+  // slice reference, so f never overflows for finite inputs
+  const float2 xf = __ffma2_rn(w, make_float2(-kLog2e, -kLog2e), xt);
+  float2 f = make_float2(fast_exp2(xf.x), fast_exp2(xf.y));
+  if constexpr (MASK) {
+    if (dd.x == -INFINITY) f.x = 0.f;  // q_v = 0
+    if (dd.y == -INFINITY) f.y = 0.f;
+    mk->Fp = __fadd2_rn(mk->Fp, f);
+  }
   const float2 w2 = __fmul2_rn(w, w);
 #ifndef DSDE_POLY_DEG7
   float2 pp = __ffma2_rn(K6, w, K5);
@@ -361,18 +416,20 @@ __device__ __forceinline__ void pair_accum_w(float2 tt, float2 dd, float2 w, con
   A2 = __ffma2_rn(e, w, A2);
   const float2 sm = __fmul2_rn(__fmul2_rn(e, w2), pp);
   const float2 bg = __ffma2_rn(e, w, __fadd2_rn(f, make_float2(-e.x, -e.y)));
+  // (masked elements have w = 0: the polynomial branch, exactly 0)
   const float2 term = make_float2(fabsf(w.x) < 1.f ? sm.x : bg.x, fabsf(w.y) < 1.f ? sm.y : bg.y);
   D2 = __fadd2_rn(D2, term);
   if constexpr (ENT) {
+    // the draft's own sums in the same frame: Sd = sum f, E = sum f ln f
     ent->Sd = __fadd2_rn(ent->Sd, f);
-    ent->E = __ffma2_rn(f, __fmul2_rn(arg, make_float2(kLn2, kLn2)), ent->E);
+    ent->E = __ffma2_rn(f, __fmul2_rn(xf, make_float2(kLn2, kLn2)), ent->E);
   }
 }
 
-template <typename T, bool ENT = false>
+template <typename T, bool ENT = false, bool MASK = false>
 __device__ __forceinline__ void pair_accum(float2 tt, float2 dd, const SumRef& R, float2& S2, float2& A2,
-                                           float2& D2, EntAcc* ent = nullptr) {
-  pair_accum_w<T, ENT>(tt, dd, diff2<T>(tt, dd, R.Cw), R, S2, A2, D2, ent);
+                                           float2& D2, EntAcc* ent = nullptr, MaskAcc* mk = nullptr) {
+  pair_accum_w<T, ENT, MASK>(tt, dd, diff2<T>(tt, dd, R.Cw, R.invT), R, S2, A2, D2, ent, mk);
 }
 
 // The sums of one 16-byte vector pair. When every |w| of the vector is below 2
@@ -390,23 +447,31 @@ __device__ __forceinline__ void pair_accum(float2 tt, float2 dd, const SumRef& R
 #ifndef DSDE_WIDE_DEG
 #define DSDE_WIDE_DEG 7
 #endif
-template <typename T, bool ENT = false>
+template <typename T, bool ENT = false, bool MASK = false>
 __device__ __forceinline__ void vec_accum(const uint4& t, const uint4& d, const SumRef& R, float2& S2,
-                                          float2& A2, float2& D2, EntAcc* ent = nullptr) {
+                                          float2& A2, float2& D2, EntAcc* ent = nullptr, MaskAcc* mk = nullptr) {
   constexpr int P = Traits<T>::VEC / 2;
   const uint4 rt[1] = {t}, rd[1] = {d};
+  if constexpr (MASK) {
+    // masked logits (D21): every element takes the exact per-element path,
+    // which handles the -inf cases
+#pragma unroll
+    for (int h = 0; h < Traits<T>::VEC; h += 2)
+      pair_accum<T, false, true>(pair_of<T>(rt, h), pair_of<T>(rd, h), R, S2, A2, D2, nullptr, mk);
+    return;
+  }
 #if DSDE_WIDE_POLY
   float2 tt[P], w[P];
   float am = 0.f;
 #pragma unroll
   for (int h = 0; h < P; ++h) {
     tt[h] = pair_of<T>(rt, 2 * h);
-    w[h] = diff2<T>(tt[h], pair_of<T>(rd, 2 * h), R.Cw);
+    w[h] = diff2<T>(tt[h], pair_of<T>(rd, 2 * h), R.Cw, R.invT);
     am = fmaxf(am, fmaxf(fabsf(w[h].x), fabsf(w[h].y)));
   }
   constexpr float kWideR = 2.f;
   if (__all_sync(kFull, am < kWideR)) {
-    const float2 L2 = make_float2(kLog2e, kLog2e);
+    const float2 L2 = R.L2s;
 #pragma unroll
     for (int h = 0; h < P; ++h) {
       const float2 xt = __ffma2_rn(tt[h], L2, R.nML2);
@@ -439,7 +504,8 @@ __device__ __forceinline__ void vec_accum(const uint4& t, const uint4& d, const 
       const float2 wh = __fmul2_rn(ww, pp);
       D2 = __ffma2_rn(ew, wh, D2);  // e w^2 h(-w)
       if constexpr (ENT) {
-        // f = e e^{-w} = e (1 - w + w^2 h(-w)); d - max d = (t - M) - w
+        // f = e e^{-w} = e (1 - w + w^2 h(-w)); ln f = xt ln 2 - w (the frame of
+        // the exact path)
         const float2 f = __ffma2_rn(ew, __fadd2_rn(wh, make_float2(-1.f, -1.f)), e);
         const float2 dm = __ffma2_rn(xt, make_float2(kLn2, kLn2), make_float2(-ww.x, -ww.y));
         ent->Sd = __fadd2_rn(ent->Sd, f);
@@ -501,9 +567,13 @@ __device__ __forceinline__ SubPartial finish_partial(float2 S2, float2 A2, float
 }
 
 // `after_max` runs (warp-uniformly) once the slice maxima are reduced over the
-// warp, i.e. once every lane's words have been consumed.
-template <typename T, int NV, typename Hook = NoHook, bool ENT = false>
-__device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const uint4 (&rd)[NV],
+// warp, i.e. once every lane's words have been consumed. invT = 1/T of the
+// row's sequence (D20). MASK (D21): the partial's spare words carry Fm (its sign bit:
+// cc) and Fp
+// (MaskAcc); a slice whose target logits are all masked keeps its draft mass
+// (reference max d, M = -inf in the partial).
+template <typename T, int NV, typename Hook = NoHook, bool ENT = false, bool MASK = false>
+__device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const uint4 (&rd)[NV], float invT = 1.f,
                                                   Hook after_max = Hook()) {
   LaneMax<T> mx;
   mx.init();
@@ -512,14 +582,23 @@ __device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const u
   float M, Dmax;
   mx.reduce(M, Dmax);
   after_max();
+  bool t_masked = false;
+  if constexpr (MASK) {
+    // every t masked (or row padding), some d kept: keep the draft mass with a
+    // finite reference (all e = 0); every d masked, some t kept: a finite
+    // draft reference (C = 0; every kept t is then a KL = +inf token)
+    t_masked = M <= -1e30f && Dmax > -1e30f;
+    if (t_masked) M = Dmax;
+    if (Dmax <= -1e30f && M > -1e30f) Dmax = M;
+  }
   if (M <= -1e30f) return empty_partial();  // slice beyond V (padding only; NaN is not empty)
-  const SumRef R(M, Dmax);
+  const SumRef R(M, Dmax, invT);
   float2 S2 = make_float2(0.f, 0.f), A2 = S2, D2 = S2;
   if constexpr (ENT) {
     EntAcc ent{S2, S2};
 #pragma unroll
     for (int v = 0; v < NV; ++v) vec_accum<T, true>(rt[v], rd[v], R, S2, A2, D2, &ent);
-    SubPartial p = finish_partial(S2, A2, D2, M, Dmax, R.Cw);
+    SubPartial p = finish_partial(S2, A2, D2, M * invT, Dmax * invT, R.Cw);
     float Sd = ent.Sd.x + ent.Sd.y, E = ent.E.x + ent.E.y;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -529,10 +608,29 @@ __device__ __forceinline__ SubPartial slice_stats(const uint4 (&rt)[NV], const u
     p.pad0 = Sd;
     p.pad1 = E;
     return p;
+  } else if constexpr (MASK) {
+    MaskAcc mk{S2, S2, 0};
+#pragma unroll
+    for (int v = 0; v < NV; ++v) vec_accum<T, false, true>(rt[v], rd[v], R, S2, A2, D2, nullptr, &mk);
+    SubPartial p = finish_partial(S2, A2, D2, M * invT, Dmax * invT, R.Cw);
+    float Fp = mk.Fp.x + mk.Fp.y, Fm = mk.Fm.x + mk.Fm.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      Fp += __shfl_xor_sync(kFull, Fp, o);
+      Fm += __shfl_xor_sync(kFull, Fm, o);
+    }
+    const int cc = __any_sync(kFull, mk.cc);
+    p.pad0 = __int_as_float(__float_as_int(Fm) | (cc ? (int)0x80000000u : 0));  // sign bit: cc
+    p.pad1 = Fp;
+    if (t_masked) {
+      p.M = -INFINITY;
+      p.C = 0.f;
+    }
+    return p;
   } else {
 #pragma unroll
     for (int v = 0; v < NV; ++v) vec_accum<T>(rt[v], rd[v], R, S2, A2, D2);
-    return finish_partial(S2, A2, D2, M, Dmax, R.Cw);
+    return finish_partial(S2, A2, D2, M * invT, Dmax * invT, R.Cw);
   }
 }
 
@@ -567,7 +665,17 @@ struct StreamArgs {
   SubPartial* part;
   int dev_rows;           // dsde_config.device_rows: Σk_i = cu_sl[B] (<= total), read here
   int* ctl;               // the tail's signal counter, zeroed here (the tail reads it after griddepcontrol.wait)
+  const float* temps;     // [B] per-sequence temperature (dsde_set_temperature, D20) or NULL
 };
+
+// 1/T of sequence i (D20): T > 0 samples at T; T = 0 (greedy) and a missing or
+// invalid temperature use the stored logits (T = 1; the finalize reports an
+// invalid one)
+__device__ __forceinline__ float inv_temp(const float* temps, int i) {
+  if (!temps) return 1.f;
+  const float T = __ldg(temps + i);
+  return (T > 0.f && T < INFINITY) ? 1.f / T : 1.f;
+}
 
 // rows this launch streams: the host's Σk_i, or (device_rows) cu_sl[B] clamped
 // to the capacity the grid and workspace were sized for
@@ -595,8 +703,8 @@ constexpr int kLdgThreads = 256;
 #endif
 // the entropy variant carries two more accumulators: 2 CTAs per SM (up to 128
 // registers) instead of spilling at the 80-register cap of 3 CTAs per SM
-template <typename T, bool DEV_ROWS, bool ENT = false>
-__global__ void __launch_bounds__(kLdgThreads, ENT ? DSDE_ENT_MINB : DSDE_LDG_MINB) k_stream_ldg(StreamArgs a) {
+template <typename T, bool DEV_ROWS, bool ENT = false, bool MASK = false>
+__global__ void __launch_bounds__(kLdgThreads, (ENT || MASK) ? DSDE_ENT_MINB : DSDE_LDG_MINB) k_stream_ldg(StreamArgs a) {
   constexpr int NV = Traits<T>::NV;
   const int total = DEV_ROWS ? stream_rows(a) : a.total;
   const long long n_units = (long long)total * a.nsub;
@@ -634,7 +742,7 @@ __global__ void __launch_bounds__(kLdgThreads, ENT ? DSDE_ENT_MINB : DSDE_LDG_MI
     p.S = __uint_as_float(acc);
     store_partial(dst, p);
 #else
-    store_partial(dst, slice_stats<T, NV, NoHook, ENT>(rt, rd));
+    store_partial(dst, slice_stats<T, NV, NoHook, ENT, MASK>(rt, rd, inv_temp(a.temps, seq)));
 #endif
     u += du;
     r += dr;
@@ -703,7 +811,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
                           const uint64_t* seeds, int32_t* acc_len, int32_t* emitted, float* kld,
                           uint8_t* flags, const VerifyWs& ws, int32_t* err, Profiler* prof,
                           cudaStream_t s, const StepExtra* step = nullptr, int greedy = 0,
-                          int dev_rows = 0, float* ent = nullptr) {
+                          int dev_rows = 0, float* ent = nullptr, const float* temps = nullptr, int masked = 0) {
   const bool pr = prof != nullptr && prof->on;
   auto mark = [&]() {
     if (pr) cudaEventRecord(prof->next(), s);
@@ -712,25 +820,29 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   mark();
   // a1: the row stream (persistent warps; grid = resident CTAs)
   StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, ns, total, reinterpret_cast<SubPartial*>(ws.part), dev_rows,
-                ws.counters};
+                ws.counters, temps};
   const int sms = sm_count();
-  if (ent) {
-    static int g = 0;
-    if (!g) g = sms * resident_per_sm(dev_rows ? k_stream_ldg<T, true, true> : k_stream_ldg<T, false, true>, kLdgThreads);
-    if (dev_rows) k_stream_ldg<T, true, true><<<g, kLdgThreads, 0, s>>>(sa);
-    else k_stream_ldg<T, false, true><<<g, kLdgThreads, 0, s>>>(sa);
+  auto go = [&](auto kern) {
+    static int g = 0;  // one per instantiation
+    if (!g) g = sms * resident_per_sm(kern, kLdgThreads);
+    kern<<<g, kLdgThreads, 0, s>>>(sa);
+  };
+  if (masked) {
+    if (dev_rows) go(k_stream_ldg<T, true, false, true>);
+    else go(k_stream_ldg<T, false, false, true>);
+  } else if (ent) {
+    if (dev_rows) go(k_stream_ldg<T, true, true>);
+    else go(k_stream_ldg<T, false, true>);
   } else {
-    static int g = 0;
-    if (!g) g = sms * resident_per_sm(k_stream_ldg<T, false, false>, kLdgThreads);
-    if (dev_rows) k_stream_ldg<T, true, false><<<g, kLdgThreads, 0, s>>>(sa);
-    else k_stream_ldg<T, false, false><<<g, kLdgThreads, 0, s>>>(sa);
+    if (dev_rows) go(k_stream_ldg<T, true, false>);
+    else go(k_stream_ldg<T, false, false>);
   }
   mark();
   // a2-a4 (+ a5-a7): the tail
   TailArgs p{};
   p.fa = FinArgs{B, V, total, ns, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds,
                  reinterpret_cast<const SubPartial*>(ws.part), acc_len, emitted, kld, flags,
-                 reinterpret_cast<SeqRec*>(ws.rec), err, greedy, dev_rows, ent, 0};
+                 reinterpret_cast<SeqRec*>(ws.rec), err, greedy, dev_rows, ent, 0, temps, masked};
   p.sa = SelArgs{B, V, n_draws(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32), tl, ld_t, dl, ld_d, emitted, flags, err, 0};
   p.mass = ws.mass;
   p.mref = ws.mref;
@@ -779,6 +891,7 @@ extern "C" dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_dra
   const size_t need = ws_layout(B, total_draft_rows, V, dtype, nullptr, nullptr);
   if (ws_bytes < need) return DSDE_ERR_ARG;
   if ((long long)(total_draft_rows + B) * n_subs(V, dtype) > 0x3fffffffLL) return DSDE_ERR_ARG;
+  if (st->cfg.masked && st->entropy_out) return DSDE_ERR_ARG;  // masks + draft entropy: not supported
   VerifyWs ws;
   ws_layout(B, total_draft_rows, V, dtype, &ws, reinterpret_cast<char*>(workspace));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -787,12 +900,12 @@ extern "C" dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_dra
     e = launch_verify<uint16_t>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                                 draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld,
                                 flags, ws, st->err, st->prof, s, nullptr, st->cfg.greedy, st->cfg.device_rows,
-                                st->entropy_out);
+                                st->entropy_out, st->temps, st->cfg.masked);
   else
     e = launch_verify<float>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                              draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld, flags,
                              ws, st->err, st->prof, s, nullptr, st->cfg.greedy, st->cfg.device_rows,
-                                st->entropy_out);
+                                st->entropy_out, st->temps, st->cfg.masked);
   return e == cudaSuccess ? DSDE_OK : DSDE_ERR_CUDA;
 }
 
@@ -826,12 +939,14 @@ extern "C" dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, 
   if (((uintptr_t)workspace) & 255) return DSDE_ERR_ARG;
   if (ws_bytes < ws_layout(B, total_draft_rows, V, dtype, nullptr, nullptr)) return DSDE_ERR_ARG;
   if ((long long)(total_draft_rows + B) * n_subs(V, dtype) > 0x3fffffffLL) return DSDE_ERR_ARG;
+  if (st->cfg.masked && st->entropy_out) return DSDE_ERR_ARG;        // masks + draft entropy: not supported
+  if (st->cfg.entropy_mode && !st->entropy_out) return DSDE_ERR_ARG;  // D22 needs the draft entropy
   VerifyWs ws;
   ws_layout(B, total_draft_rows, V, dtype, &ws, reinterpret_cast<char*>(workspace));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   StepExtra x;
   x.sig = SignalArgs{st->cfg, B, st->max_seqs, slots, cu_sl, kld, accepted_len, sl_hat, diag,
-                     st->seq, st->err};
+                     st->seq, st->err, st->cfg.entropy_mode ? st->entropy_out : nullptr};
   x.cap = CapArgs{st->cfg, B, st->max_seqs, slots, sl_hat, budget, next_sl, cap, st->seq, st->scratch};
   x.fuse_cap = comm == nullptr;
   cudaError_t e;
@@ -839,12 +954,12 @@ extern "C" dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, 
     e = launch_verify<uint16_t>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                                 draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld,
                                 flags, ws, st->err, st->prof, s, &x, st->cfg.greedy, st->cfg.device_rows,
-                                st->entropy_out);
+                                st->entropy_out, st->temps, st->cfg.masked);
   else
     e = launch_verify<float>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                              draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld, flags,
                              ws, st->err, st->prof, s, &x, st->cfg.greedy, st->cfg.device_rows,
-                                st->entropy_out);
+                                st->entropy_out, st->temps, st->cfg.masked);
   if (e != cudaSuccess) return DSDE_ERR_CUDA;
   if (!comm) return DSDE_OK;
   dsde_status rs = DSDE_OK;
@@ -857,6 +972,12 @@ extern "C" dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, 
 extern "C" dsde_status dsde_set_draft_entropy(dsde_state st, float* entropy) {
   if (!st) return DSDE_ERR_ARG;
   st->entropy_out = entropy;
+  return DSDE_OK;
+}
+
+extern "C" dsde_status dsde_set_temperature(dsde_state st, const float* temperature) {
+  if (!st) return DSDE_ERR_ARG;
+  st->temps = temperature;
   return DSDE_OK;
 }
 

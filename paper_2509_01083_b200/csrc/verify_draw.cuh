@@ -38,7 +38,14 @@ struct FinArgs {
   int dev_rows;  // dsde_config.device_rows: total is a capacity, sum k_i = cu_sl[B]
   float* ent;    // [sum k_i] optional out: draft entropy H(q) per row; partials carry Sd, E
   int v0;        // vocabulary offset of the rows (vocab-parallel shard; 0 otherwise)
+  const float* temps;  // [B] per-sequence temperature (D20) or NULL; T = 0: greedy for that sequence
+  int masked;          // dsde_config.masked: -inf logits allowed (D21); partials carry Fm (sign: cc), Fa
 };
+
+// Sequence i verifies greedily (T = 0): the global mode or its temperature 0.
+__device__ __forceinline__ bool seq_greedy(const FinArgs& a, int i) {
+  return a.greedy || (a.temps && __ldg(a.temps + i) == 0.f);
+}
 
 // Per-row result of row_finalize (64 bytes).
 struct RowRes {
@@ -69,20 +76,31 @@ __device__ __forceinline__ bool seq_ok(const FinArgs& a, int i, int& c0, int& k,
 }
 
 // ---------------------------------------------------------------------------
-// a2: fp64 merge of row r's slice partials (lanes over slices c) about
-// M = max_c M_c, C = fp32(M - max d). Slice c's w is shifted by Delta = C_c - C;
-// with s = e^(M_c - M), E1 = s e^-Delta:
+// a2: fp64 merge of row r's slice partials (lanes over slices c) about the
+// row's references. A slice's e_v = 2^(t_v L2s - ML2_c) with ML2_c =
+// fl32(M_c log2 e), the product the stream kernel rounded (SumRef), so its
+// sums are exactly about M'_c = ML2_c ln 2 (not M_c): the merge uses M'_c
+// (s = e^(M'_c - M'), M' = the largest). With Delta = C_c - C (C = fp32(M -
+// max d)) and E1 = s e^-Delta:
 //   S += s S_c,  A += s (A_c + S_c Delta),
 //   D += E1 D_c - A_c s expm1(-Delta) + S_c s g(Delta),  g(x) = expm1(-x) + x.
-// Partials are read with ld.global.cg: in the pass kernel other SMs wrote them
-// during this launch. Result in every lane.
+// f = e e^-w of a slice lives in the frame M'_c - C_c, so its sums (ENT: Sd,
+// E; MASK: Fp) are carried over with E1 (E shifted by ln E1); MASK's Fm is
+// about fl32(maxd_c log2 e) ln 2 and is carried into the row's f frame.
+// Partials are read with ld.global.cg: other SMs wrote them. Result in every
+// lane.
 // ---------------------------------------------------------------------------
 struct RowSums {
-  double S, A, D, Sd, E;
+  double S, A, D, Sd, E;  // ENT: Sd, E (draft entropy sums); MASK: Sd = Fm, E = Fp (row f frame)
   float M, Dmax;
+  int cc;                 // MASK: some token the draft masks has p > 0
 };
 
-__device__ __forceinline__ RowSums row_merge(const SubPartial* P, int nc, bool ent) {
+__device__ __forceinline__ double ref_nats(float m) {  // the stream's reference of a max m: fl32(m log2 e) ln 2
+  return (double)__fmul_rn(m, kLog2e) * kLn2d;
+}
+
+__device__ __forceinline__ RowSums row_merge(const SubPartial* P, int nc, bool ent, bool mask = false) {
   const int lane = threadIdx.x & 31;
   float Ml = -INFINITY, Dl = -INFINITY;
   for (int c = lane; c < nc; c += 32) {
@@ -94,19 +112,20 @@ __device__ __forceinline__ RowSums row_merge(const SubPartial* P, int nc, bool e
     Ml = max_nan(Ml, __shfl_xor_sync(kFull, Ml, o));
     Dl = fmaxf(Dl, __shfl_xor_sync(kFull, Dl, o));
   }
-  const double M = (double)Ml, C = (double)(Ml - Dl);  // C is an fp32 value
+  const double Mr = ref_nats(Ml), C = (double)(Ml - Dl);  // C is an fp32 value
   double S = 0.0, A = 0.0, D = 0.0, Sd = 0.0, E = 0.0;
+  int cc = 0;
   for (int c = lane; c < nc; c += 32) {
     const float4 q0 = __ldcg(reinterpret_cast<const float4*>(P + c));
     const float4 q1 = __ldcg(reinterpret_cast<const float4*>(P + c) + 1);
-    const double qS = q0.x, qA = q0.y, qD = q0.z, qM = q0.w, qC = q1.x;
-    if (ent && q1.z > 0.f) {
-      // draft sums about the row max of d: Sd += s Sd_c, E += s (E_c + (maxd_c - maxd) Sd_c)
-      const double dd = (double)q1.y - (double)Dl, sd = exp(dd);
-      Sd += sd * (double)q1.z;
-      E += sd * ((double)q1.w + dd * (double)q1.z);
+    const double qS = q0.x, qA = q0.y, qD = q0.z, qC = q1.x;
+    if (mask) {
+      // Fm about the slice's fl32(maxd log2 e) ln 2, into the row's f frame Mr - C
+      Sd += exp(ref_nats(q1.y) - (Mr - C)) * fabs((double)q1.z);
+      cc |= signbit(q1.z) ? 1 : 0;
+      if (q0.w == -INFINITY) continue;  // a slice whose target logits are all masked: only Fm
     }
-    const double ls = qM - M;
+    const double ls = ref_nats(q0.w) - Mr;
     const double s = exp(ls);
     const double dl = qC - C;
     double sem, sg, E1;
@@ -123,6 +142,12 @@ __device__ __forceinline__ RowSums row_merge(const SubPartial* P, int nc, bool e
     S += s * qS;
     A += s * qA + s * qS * dl;
     D += E1 * qD - qA * sem + qS * sg;
+    if (ent && q1.z > 0.f) {
+      // the draft's sums in the row's f frame: Sd += E1 Sd_c, E += E1 (E_c + ln(E1) Sd_c)
+      Sd += E1 * (double)q1.z;
+      E += E1 * ((double)q1.w + (ls - dl) * (double)q1.z);
+    }
+    if (mask) E += E1 * (double)q1.w;  // Fp
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -130,14 +155,15 @@ __device__ __forceinline__ RowSums row_merge(const SubPartial* P, int nc, bool e
     A += __shfl_xor_sync(kFull, A, o);
     D += __shfl_xor_sync(kFull, D, o);
   }
-  if (ent) {
+  if (ent || mask) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       Sd += __shfl_xor_sync(kFull, Sd, o);
       E += __shfl_xor_sync(kFull, E, o);
     }
   }
-  return RowSums{S, A, D, Sd, E, Ml, Dl};
+  if (mask) cc = __any_sync(kFull, cc);
+  return RowSums{S, A, D, Sd, E, Ml, Dl, cc};
 }
 
 // Greedy (T = 0): row argmax of t, smallest index among equal maxima (D18): the
@@ -192,7 +218,7 @@ __device__ __forceinline__ RowPre row_prefetch(const FinArgs& a, int r, int i) {
       p.tx = load_logit<T>(reinterpret_cast<const T*>(a.tl) + slot * a.ld_t + p.x);
       p.dx = load_logit<T>(reinterpret_cast<const T*>(a.dl) + (long long)r * a.ld_d + p.x);
     }
-    if (!a.greedy) p.uacc = philox_uniforms(__ldg(a.seeds + slot)).acc;
+    if (!seq_greedy(a, i)) p.uacc = philox_uniforms(__ldg(a.seeds + slot)).acc;
   }
   return p;
 }
@@ -210,9 +236,10 @@ __device__ __forceinline__ RowRes row_finalize(const FinArgs& a, int r, int i, c
   const float tx = in.tx, dx = in.dx;
   const double uacc = in.uacc;
   const SubPartial* P = a.part + (long long)r * a.nsub;
-  const RowSums R = row_merge(P, a.nsub, a.ent != nullptr);
+  const bool greedy = seq_greedy(a, i);
+  const RowSums R = row_merge(P, a.nsub, a.ent != nullptr, a.masked != 0);
   int amax = 0;
-  if (a.greedy) amax = row_argmax<T>(a, P, a.nsub, R.M, trow);
+  if (greedy) amax = row_argmax<T>(a, P, a.nsub, R.M, trow);
   RowRes rr;
   rr.pad = 0;
   rr.pad2[0] = rr.pad2[1] = 0.0;
@@ -223,26 +250,43 @@ __device__ __forceinline__ RowRes row_finalize(const FinArgs& a, int r, int i, c
   // y = E_p[exp(-w)] - 1. KL = D/S + (log1p(y) - y) has no cancellation for
   // small KL; when y > 1 (the draft puts far more mass away from the
   // reference, e.g. disjoint supports) the equal form A/S + log1p(y) is used.
+  // Masked logits (D21): in the row's f frame, Fp = sum_{supp p} e e^-w (the
+  // draft mass on supp p; = (1 + y) S without masks) and Fm = the draft mass on
+  // the tokens the target masks. q's normaliser is Fp + Fm, so log p/q at x and
+  // the residual use lam' = log((Fp + Fm) / S) = log1p(y) - log Q with
+  // Q = Fp / (Fp + Fm), and KL = (the formula) - log Q. When the draft masks a
+  // token of supp p (cc), KL = +inf and y (which then omits that mass) is not
+  // used: lam' = log(Fp / S) - log Q.
   const double y = (R.D - R.A) / R.S;
-  rr.lam = log1p(y);
-  rr.kl = fmax(0.0, y <= 1.0 ? R.D / R.S + (rr.lam - y) : R.A / R.S + rr.lam);
+  const double lam = log1p(y);
+  const bool kl_inf = a.masked && R.cc;
+  const double lq = a.masked ? log1p(R.Sd / R.E) : 0.0;  // -log Q >= 0
+  rr.lam = kl_inf ? log(R.E / R.S) + lq : lam + lq;
+  rr.kl = kl_inf ? (double)INFINITY : fmax(0.0, (y <= 1.0 ? R.D / R.S + (lam - y) : R.A / R.S + lam) + lq);
   bool fin = isfinite(R.S) && isfinite(R.A) && isfinite(R.D) && R.S > 0.0 && isfinite((double)R.M) &&
-             isfinite(rr.C) && isfinite(rr.kl);
+             isfinite(rr.C) && (kl_inf || isfinite(rr.kl)) && isfinite(rr.lam);
   int bits = 0;
   if (lane == 0) {
     if (a.ent) a.ent[r] = (float)(log(R.Sd) - R.E / R.Sd);  // H(q) = log Sd - E / Sd (E <= 0)
     if (x < 0 || x >= a.V) {
       bits |= RR_BADTOK;
     } else {
-      const double lr = ((double)tx - (double)dx) - rr.C + rr.lam;  // log p(x) - log q(x)
-      fin = fin && isfinite(lr);
-      if (a.greedy) {
+      const float invT = inv_temp(a.temps, i);
+      // log p(x) - log q(x) at the sequence's temperature
+      const double lr = ((double)tx - (double)dx) * (double)invT - rr.C + rr.lam;
+      if (a.masked && dx == -INFINITY) bits |= RR_BADTOK;  // q(x) = 0: x cannot have been drafted
+      fin = fin && (isfinite(lr) || (a.masked && lr == -INFINITY));  // p(x) = 0: a certain rejection
+      if (greedy) {
         if (x == amax) bits |= RR_ACCEPT;  // T = 0: the draft token must be the target argmax
       } else {
         const double pacc = lr >= 0.0 ? 1.0 : exp(lr);
         if (uacc < pacc) bits |= RR_ACCEPT;
         if (fabs(uacc - pacc) < 1e-6) bits |= RR_NEAR;
       }
+    }
+    if (a.temps) {
+      const float Ti = __ldg(a.temps + i);
+      if (!(Ti >= 0.f && Ti < INFINITY)) fin = false;  // a negative / non-finite temperature
     }
     if (fin) bits |= RR_FINITE;
   }
@@ -293,7 +337,7 @@ __device__ __forceinline__ SeqRec error_rec(long long slot0) {
   r.trow = slot0;
   r.drow = -1;
   r.M = 0.f;
-  r.pad0 = 0;
+  r.invT = 1.f;
   r.C = r.lam = r.u = r.S = 0.0;
   return r;
 }
@@ -324,15 +368,16 @@ __device__ __forceinline__ int seq_layout(const FinArgs& a, int i, int c0, int k
   }
   if (lane == 0) a.acc_len[i] = aa;
   if (lane == aa) {
+    const bool greedy = seq_greedy(a, i);
     SeqRec r;
-    r.pad0 = 0;
+    r.invT = greedy ? 1.f : inv_temp(a.temps, i);
     r.S = 0.0;
     r.slot = (int)(slot0 + aa);
     r.trow = slot0 + aa;
     r.drow = -1;
     r.M = 0.f;
     r.C = r.lam = r.u = 0.0;
-    if (a.greedy) {
+    if (greedy) {
       // T = 0: the recovery token is the argmax of row aa (known from its
       // finalize); the bonus row's argmax is found by the draw pass
       if (aa < k) {
@@ -372,8 +417,10 @@ __device__ __forceinline__ int seq_layout(const FinArgs& a, int i, int c0, int k
 // The select recomputes every weight bit-identically from the same words.
 // ---------------------------------------------------------------------------
 template <typename T>
-__device__ __forceinline__ float2 resid_pair_exact(float2 tt, float2 dd, float2 nML2, float khi, float klo) {
-  const float2 L2 = make_float2(kLog2e, kLog2e), nL2 = make_float2(-kLog2e, -kLog2e);
+__device__ __forceinline__ float2 resid_pair_exact(float2 tt, float2 dd, float2 nML2, float khi, float klo,
+                                                   float invT) {
+  const float l2 = kLog2e * invT;
+  const float2 L2 = make_float2(l2, l2), nL2 = make_float2(-kLog2e, -kLog2e);
   const float2 ONE = make_float2(1.f, 1.f);
   // degree 6 on |z| <= 1 (2.0e-7 relative; tools/fit_g.py --deg 6)
   const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
@@ -385,13 +432,8 @@ __device__ __forceinline__ float2 resid_pair_exact(float2 tt, float2 dd, float2 
   const float2 K0 = make_float2(0.5f, 0.5f);
   const float2 xt = __ffma2_rn(tt, L2, nML2);
   const float2 ev = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));  // 0 for padding
-  // z = (t - d) - (C - lam), the constant carried as khi + klo
-  float2 z;
-  if constexpr (sizeof(T) == 2) {
-    z = __fadd2_rn(__fadd2_rn(tt, make_float2(-dd.x, -dd.y)), make_float2(-khi, -khi));  // t - d exact
-  } else {
-    z = make_float2(diff_ref<T>(tt.x, dd.x, khi), diff_ref<T>(tt.y, dd.y, khi));
-  }
+  // z = (t - d) / T - (C - lam), the constant carried as khi + klo
+  float2 z = diff2<T>(tt, dd, khi, invT);  // t - d exact (bf16) or TwoDiff (fp32)
   z = __fadd2_rn(z, make_float2(-klo, -klo));
   float2 pz = __ffma2_rn(K6, z, K5);
   pz = __ffma2_rn(pz, z, K4);
@@ -425,8 +467,9 @@ __device__ __forceinline__ float vec_tmax(const uint4& t, float m) {
 // Per-slice constants of the draw weights.
 struct DrawRef {
   bool resid;
-  float M, khi, klo;  // residual: row reference M, C - lam = khi + klo
-  float m;            // bonus: the slice's warp max of t (reference)
+  float M, khi, klo;  // residual: row reference M (of t / T), C - lam = khi + klo
+  float m;            // bonus: the slice's warp max of t (raw; the reference is m / T)
+  float invT;         // 1 / T (D20)
 };
 
 // Warp-wide max of t over a lane's N vectors (NaN-propagating; packed
@@ -458,9 +501,10 @@ __device__ __forceinline__ float warp_max_nan(float m) {
   return m;
 }
 
-__device__ __forceinline__ DrawRef draw_ref(bool resid, float M, float Cf, double lam, float m) {
+__device__ __forceinline__ DrawRef draw_ref(bool resid, float M, float Cf, double lam, float m, float invT) {
   DrawRef R;
   R.resid = resid;
+  R.invT = invT;
   R.M = M;
   const double K = (double)Cf - lam;
   R.khi = (float)K;
@@ -475,13 +519,14 @@ __device__ __forceinline__ void vec_weights(const uint4& t4, const uint4& d4, co
                                             float (&w)[Traits<T>::VEC]) {
   constexpr int VEC = Traits<T>::VEC;
   const uint4 rt[1] = {t4}, rd[1] = {d4};
-  const float2 L2 = make_float2(kLog2e, kLog2e);
+  const float l2 = kLog2e * R.invT;
+  const float2 L2 = make_float2(l2, l2);
   if (R.resid) {
     const float ML2 = R.M * kLog2e;
     const float2 nML2 = make_float2(-ML2, -ML2);
 #pragma unroll
     for (int h = 0; h < VEC; h += 2) {
-      const float2 r = resid_pair_exact<T>(pair_of<T>(rt, h), pair_of<T>(rd, h), nML2, R.khi, R.klo);
+      const float2 r = resid_pair_exact<T>(pair_of<T>(rt, h), pair_of<T>(rd, h), nML2, R.khi, R.klo, R.invT);
       w[h] = r.x;
       w[h + 1] = r.y;
     }
@@ -492,7 +537,7 @@ __device__ __forceinline__ void vec_weights(const uint4& t4, const uint4& d4, co
     for (int e = 0; e < VEC; ++e) w[e] = 0.f;
     return;
   }
-  const float mL2 = R.m * kLog2e;
+  const float mL2 = R.m * l2;  // (t - m) / T in base 2
   const float2 nmL2 = make_float2(-mL2, -mL2);
 #pragma unroll
   for (int h = 0; h < VEC; h += 2) {
@@ -608,9 +653,9 @@ __device__ __forceinline__ void draw_mass(const SeqRec& r, int u, int V, const v
       }
       return;
     }
-    R = draw_ref(false, 0.f, 0.f, 0.0, m);
+    R = draw_ref(false, 0.f, 0.f, 0.0, m, r.invT);
   } else {
-    R = draw_ref(true, r.M, (float)r.C, r.lam, 0.f);
+    R = draw_ref(true, r.M, (float)r.C, r.lam, 0.f, r.invT);
   }
   double x[NV];
 #pragma unroll
@@ -625,7 +670,7 @@ __device__ __forceinline__ void draw_mass(const SeqRec& r, int u, int V, const v
   const double tot = warp_sum_vectors<NV>(x);
   if (lane == 0) {
     *mass_out = tot;
-    *ref_out = R.resid ? R.M : (R.m <= -1e30f ? -INFINITY : R.m);
+    *ref_out = R.resid ? R.M : (R.m <= -1e30f ? -INFINITY : R.m * R.invT);  // bonus: the reference m / T
   }
 }
 
@@ -717,12 +762,12 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
       // of the same target row, one lane) or a non-finite bonus row
       if (resid && isfinite(R)) {
         double tot = 0.0;
-        for (int v = 0; v < a.V; ++v) tot += exp((double)load_logit<T>(tp + v) - (double)r.M);
+        for (int v = 0; v < a.V; ++v) tot += exp((double)load_logit<T>(tp + v) * (double)r.invT - (double)r.M);
         const double target = r.u * tot;
         double cum = 0.0;
         int tok = 0;
         for (int v = 0; v < a.V; ++v) {
-          const double wv = exp((double)load_logit<T>(tp + v) - (double)r.M);
+          const double wv = exp((double)load_logit<T>(tp + v) * (double)r.invT - (double)r.M);
           cum += wv;
           if (wv > 0.0) tok = v;
           if (wv > 0.0 && cum > target) break;
@@ -776,7 +821,15 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   }
   const double f = scale_of(us);
   const T* dp = resid ? reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d : tp;
-  const DrawRef DR = draw_ref(resid, r.M, (float)r.C, r.lam, resid ? 0.f : src.r(us));
+  // the crossing slice's bonus reference: its raw max of t, recomputed exactly
+  // as draw_mass did (the record holds m / T)
+  float m_raw = 0.f;
+  if (!resid) {
+    uint4 rt0[NV];
+    load_vecs<T, NV>(tp, a.V, us, 0, rt0);
+    m_raw = warp_max_nan(lane_tmax<T, NV>(rt0, -INFINITY));
+  }
+  const DrawRef DR = draw_ref(resid, r.M, (float)r.C, r.lam, m_raw, r.invT);
   int tok = -1, last_pos = -1;
   double lo = 0.0, hi = 0.0, lp_lo = 0.0, lp_hi = 0.0, vbase = base;
   // one vector at a time, not unrolled: this runs once per sequence, so its
@@ -852,7 +905,7 @@ __device__ __forceinline__ SeqRec load_seqrec(const SeqRec* p) {
   r.trow = __ldcg(&p->trow);
   r.drow = __ldcg(&p->drow);
   r.M = __ldcg(&p->M);
-  r.pad0 = 0;
+  r.invT = __ldcg(&p->invT);
   r.C = __ldcg(&p->C);
   r.lam = __ldcg(&p->lam);
   r.u = __ldcg(&p->u);

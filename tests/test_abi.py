@@ -46,7 +46,8 @@ def test_config_defaults_match_paper(dsde):
     c = dsde.Config.default()
     assert (c.delta, c.n_short, c.n_long, c.sl_min, c.epsilon) == (0.85, 10, 30, 2, 1e-6)
     assert (c.sl_ceiling, c.calib_steps, c.calib_sl, c.window_unit, c.cap_mode) == (8, 5, 4, 0, 1)
-    assert dsde.lib().dsde_abi_version() == 2
+    assert (c.masked, c.entropy_mode, c.entropy_gamma, c.greedy, c.device_rows) == (0, 0, 0.5, 0, 0)
+    assert dsde.lib().dsde_abi_version() == 3
     assert dsde.lib().dsde_status_string(-1) == b"DSDE_ERR_ARG"
 
 
