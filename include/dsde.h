@@ -68,6 +68,8 @@ typedef enum { DSDE_F32 = 0, DSDE_BF16 = 1 } dsde_dtype;
 #define DSDE_DERR_NONFINITE 3     /* non-finite logits in a row                          */
 #define DSDE_DERR_ROWS 4          /* cu_sl[B] != total_draft_rows                         */
 #define DSDE_DERR_BAD_SLOT 5      /* state slot outside [0, max_seqs)                     */
+#define DSDE_DERR_VP_FALLBACK 6   /* vocab-parallel: residual mass 0 (the D7 fallback to p needs the
+                                     whole row on one GPU; not supported by dsde_vp_*)    */
 
 /* Per-slot bits of the optional `flags` output of dsde_verify. */
 #define DSDE_FLAG_ACCEPT_NEAR_TIE 1  /* |u_acc - min(1, p/q)| < 1e-6 at this position      */
@@ -232,6 +234,62 @@ dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_draft_rows,
                         const uint64_t* seeds, int32_t* accepted_len,
                         int32_t* emitted_tokens, float* kld, uint8_t* flags,
                         void* workspace, size_t ws_bytes, dsde_state st, void* stream);
+
+/* ---------------------------------------------------------------------- */
+/* Vocabulary-parallel verification (the    */
+/* 70B target on 8 GPUs implies a vocab-parallel LM head)                   */
+/* ---------------------------------------------------------------------- */
+/* Shard s of n holds columns [v0_s, v0_s + Vs_s) of every target and draft
+ * row (the row layout of dsde_verify, only narrower): v0_s = s W with the
+ * shard width W from dsde_vp_sizes (a multiple of the 2048-token bf16 /
+ * 512-token fp32 stream slice) and the last shard the remainder; ld >= Vs_s.
+ * The stages below, with the caller's exchanges between them, give outputs
+ * bit-identical to dsde_verify on the unsharded rows (every partial and every
+ * draw mass is the unsharded one, read in the unsharded order):
+ *   dsde_vp_stream   (per shard)  -> its partial block, its (t_x, d_x) (zeros
+ *                                   where another shard owns x);
+ *     exchange: all-gather the blocks into part_all [n][total][ns_sh] (32 B
+ *               entries), all-reduce (sum) xlog [total][2] floats;
+ *   dsde_vp_finalize (every shard) -> accepted_len, emitted (all but the
+ *                                   drawn token), kld, flags, rec [B] (64 B);
+ *   dsde_vp_draw     (per shard)  -> its mass block [B][nd_sh] (16 B entries);
+ *     exchange: all-gather into mass_all [n][B][nd_sh];
+ *   dsde_vp_select   (every shard) -> tok [B]: the drawn token (global id, the
+ *                                   sample flags << 24) on the shard owning
+ *                                   the crossing slice, -1 elsewhere;
+ *     exchange: all-reduce (max) tok;
+ *   dsde_vp_place    (every shard) -> the drawn tokens into emitted / flags.
+ * dsde_vp_verify runs the whole sequence over a dsde_comm (NCCL all-gather /
+ * all-reduce; comm NULL = one shard). The signal and cap then run unchanged
+ * (every shard holds every KLD: dsde_update_signal / dsde_next_sl).
+ * Supported: the default sampling mode only (no greedy, temperature, masks,
+ * draft entropy or device_rows on the state: DSDE_ERR_ARG); a residual of
+ * mass 0 (the D7 fallback) is DSDE_DERR_VP_FALLBACK. Buffers are device
+ * memory, 16-byte aligned; asynchronous on stream. */
+dsde_status dsde_vp_sizes(int V, int nshards, dsde_dtype dtype, int* shard_width, int* ns_sh, int* nd_sh);
+dsde_status dsde_vp_stream(dsde_state st, int B, int V, int nshards, int shard, dsde_dtype dtype,
+                           int total_draft_rows, const int32_t* cu_sl, const int32_t* draft_tokens,
+                           const void* target_shard, int64_t ld_t, const void* draft_shard, int64_t ld_d,
+                           void* part_block, float* xlog, void* stream);
+dsde_status dsde_vp_finalize(dsde_state st, int B, int V, int nshards, dsde_dtype dtype, int total_draft_rows,
+                             const int32_t* cu_sl, const int32_t* draft_tokens, const void* part_all,
+                             const float* xlog, const uint64_t* seeds, int32_t* accepted_len,
+                             int32_t* emitted_tokens, float* kld, uint8_t* flags, void* rec, void* stream);
+dsde_status dsde_vp_draw(dsde_state st, int B, int V, int nshards, int shard, dsde_dtype dtype, const void* rec,
+                         const void* target_shard, int64_t ld_t, const void* draft_shard, int64_t ld_d,
+                         void* mass_block, void* stream);
+dsde_status dsde_vp_select(dsde_state st, int B, int V, int nshards, int shard, dsde_dtype dtype,
+                           const void* rec, const void* mass_all, const void* target_shard, int64_t ld_t,
+                           const void* draft_shard, int64_t ld_d, int32_t* tok, void* stream);
+dsde_status dsde_vp_place(dsde_state st, int B, const void* rec, const int32_t* tok_all,
+                          int32_t* emitted_tokens, uint8_t* flags, void* stream);
+/* Workspace of dsde_vp_verify (256-byte aligned): the exchange buffers. */
+size_t dsde_vp_workspace_size(int B, int total_draft_rows, int V, int nshards, dsde_dtype dtype);
+dsde_status dsde_vp_verify(dsde_state st, int B, int V, dsde_dtype dtype, int total_draft_rows,
+                           const int32_t* cu_sl, const int32_t* draft_tokens, const void* target_shard,
+                           int64_t ld_t, const void* draft_shard, int64_t ld_d, const uint64_t* seeds,
+                           int32_t* accepted_len, int32_t* emitted_tokens, float* kld, uint8_t* flags,
+                           void* workspace, size_t ws_bytes, dsde_comm comm, void* stream);
 
 /* Per-sequence sampling temperature (D20; P:312 evaluates T = 0 and 1, P:490
  * per-sequence temperature) of the following dsde_verify /

@@ -26,7 +26,7 @@ DSDE_PAD = -1
 DSDE_MAX_SL = 16
 DSDE_MAX_WINDOW = 64
 FLAG_ACCEPT_NEAR_TIE, FLAG_SAMPLE_NEAR_TIE, FLAG_FALLBACK = 1, 2, 4
-DERR = {0: "none", 1: "bad_sl", 2: "bad_token", 3: "nonfinite", 4: "rows", 5: "bad_slot"}
+DERR = {0: "none", 1: "bad_sl", 2: "bad_token", 3: "nonfinite", 4: "rows", 5: "bad_slot", 6: "vp_fallback"}
 
 # Every function the header declares (checked against include/dsde.h by the tests).
 EXPORTS = (
@@ -37,6 +37,8 @@ EXPORTS = (
     "dsde_verify_workspace_size", "dsde_verify", "dsde_update_signal", "dsde_next_sl", "dsde_step",
     "dsde_cap_value", "dsde_comm_unique_id", "dsde_comm_init", "dsde_comm_destroy",
     "dsde_profile_enable", "dsde_profile_read",
+    "dsde_vp_sizes", "dsde_vp_stream", "dsde_vp_finalize", "dsde_vp_draw", "dsde_vp_select", "dsde_vp_place",
+    "dsde_vp_workspace_size", "dsde_vp_verify",
 )
 # dsde_profile_read phases (include/dsde.h): the row stream k_stream_ldg (a1),
 # then the tail k_tail (a2-a4, + a5-a7 in dsde_step); two spare slots
@@ -98,6 +100,15 @@ def lib() -> C.CDLL:
         L.dsde_verify_workspace_size.argtypes = [I, I, I, I]
         L.dsde_verify_workspace_size.restype = S
         L.dsde_verify.argtypes = [I, I, I, I, P, P, P, I64, P, I64, P, P, P, P, P, P, S, P, P]
+        L.dsde_vp_sizes.argtypes = [I, I, I, P, P, P]
+        L.dsde_vp_stream.argtypes = [P, I, I, I, I, I, I, P, P, P, I64, P, I64, P, P, P]
+        L.dsde_vp_finalize.argtypes = [P, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P]
+        L.dsde_vp_draw.argtypes = [P, I, I, I, I, I, P, P, I64, P, I64, P, P]
+        L.dsde_vp_select.argtypes = [P, I, I, I, I, I, P, P, P, I64, P, I64, P, P]
+        L.dsde_vp_place.argtypes = [P, I, P, P, P, P, P]
+        L.dsde_vp_workspace_size.argtypes = [I, I, I, I, I]
+        L.dsde_vp_workspace_size.restype = S
+        L.dsde_vp_verify.argtypes = [P, I, I, I, I, P, P, P, I64, P, I64, P, P, P, P, P, P, S, P, P]
         L.dsde_update_signal.argtypes = [P, I, P, P, P, P, P, P, P]
         L.dsde_step.argtypes = [P, I, I, I, I, P, P, P, P, I64, P, I64, P, P, P, P, P, P, P, P, P, P,
                                 P, S, P, P]
@@ -247,6 +258,79 @@ def dsde_verify(state: State, V: int, total_draft_rows: int, cu_sl, draft_tokens
         _ptr(draft_tokens), _ptr(target_logits), target_logits.stride(0), _ptr(draft_logits),
         draft_logits.stride(0), _ptr(seeds), _ptr(accepted_len), _ptr(emitted_tokens), _ptr(kld),
         _ptr(flags), _ptr(workspace), workspace.numel(), state.h, _stream(stream)), "dsde_verify")
+
+
+class VocabParallel:
+    """Vocabulary-parallel verification (include/dsde.h
+    dsde_vp_*): the target / draft logits of a batch split by columns over
+    ``nshards`` shards. ``shard_slices(V)`` gives the column ranges. ``run_local``
+    runs every stage of every shard in this process (the exchanges are plain
+    device copies / reductions) — the single-GPU check that the sharded path
+    reproduces dsde_verify; ``verify`` runs this rank's shard over a Comm (NCCL,
+    dsde_vp_verify). Argument marshalling and buffer bookkeeping only."""
+
+    def __init__(self, state: State, V: int, nshards: int, dtype: torch.dtype):
+        self.state, self.V, self.n, self.dtype = state, int(V), int(nshards), dtype
+        w, ns, nd = C.c_int(), C.c_int(), C.c_int()
+        _check(lib().dsde_vp_sizes(self.V, self.n, dtype_code(dtype), C.byref(w), C.byref(ns), C.byref(nd)),
+               "dsde_vp_sizes")
+        self.W, self.ns_sh, self.nd_sh = w.value, ns.value, nd.value
+
+    def shard_slices(self):
+        return [(s * self.W, min(self.V, (s + 1) * self.W)) for s in range(self.n)]
+
+    def run_local(self, cu_sl, draft_tokens, target_shards, draft_shards, seeds, accepted_len, emitted, kld,
+                  flags=None, stream=None):
+        """target_shards / draft_shards: per-shard [rows, >= Vs] tensors."""
+        B, n = cu_sl.numel() - 1, self.n
+        total = draft_tokens.numel()
+        dev = cu_sl.device
+        dt = dtype_code(self.dtype)
+        L, st = lib(), self.state.h
+        part = torch.empty((n, total * self.ns_sh * 32), dtype=torch.uint8, device=dev)
+        xl = torch.zeros((n, total, 2), dtype=torch.float32, device=dev)
+        for s in range(n):
+            t, d = target_shards[s], draft_shards[s]
+            _check(L.dsde_vp_stream(st, B, self.V, n, s, dt, total, _ptr(cu_sl), _ptr(draft_tokens), _ptr(t),
+                                    t.stride(0), _ptr(d), d.stride(0), _ptr(part[s]), _ptr(xl[s]), _stream(stream)),
+                   "dsde_vp_stream")
+        xlog = xl.sum(0).contiguous()  # the all-reduce (sum): exactly one shard owns each x
+        rec = torch.empty(B * 64, dtype=torch.uint8, device=dev)
+        _check(L.dsde_vp_finalize(st, B, self.V, n, dt, total, _ptr(cu_sl), _ptr(draft_tokens), _ptr(part),
+                                  _ptr(xlog), _ptr(seeds), _ptr(accepted_len), _ptr(emitted), _ptr(kld),
+                                  _ptr(flags), _ptr(rec), _stream(stream)), "dsde_vp_finalize")
+        mass = torch.empty((n, B * self.nd_sh * 16), dtype=torch.uint8, device=dev)
+        for s in range(n):
+            t, d = target_shards[s], draft_shards[s]
+            _check(L.dsde_vp_draw(st, B, self.V, n, s, dt, _ptr(rec), _ptr(t), t.stride(0), _ptr(d), d.stride(0),
+                                  _ptr(mass[s]), _stream(stream)), "dsde_vp_draw")
+        toks = torch.empty((n, B), dtype=torch.int32, device=dev)
+        for s in range(n):
+            t, d = target_shards[s], draft_shards[s]
+            _check(L.dsde_vp_select(st, B, self.V, n, s, dt, _ptr(rec), _ptr(mass), _ptr(t), t.stride(0), _ptr(d),
+                                    d.stride(0), _ptr(toks[s]), _stream(stream)), "dsde_vp_select")
+        tok = toks.max(0).values.contiguous()  # the all-reduce (max)
+        _check(L.dsde_vp_place(st, B, _ptr(rec), _ptr(tok), _ptr(emitted), _ptr(flags), _stream(stream)),
+               "dsde_vp_place")
+        return tok
+
+    def workspace(self, B: int, total: int, device="cuda"):
+        n = lib().dsde_vp_workspace_size(B, total, self.V, self.n, dtype_code(self.dtype))
+        if n == 0:
+            raise DsdeError("dsde_vp_workspace_size: invalid shape")
+        ws = torch.empty(n + 256, dtype=torch.uint8, device=device)
+        return ws[(-ws.data_ptr()) % 256:]
+
+    def verify(self, cu_sl, draft_tokens, target_shard, draft_shard, seeds, accepted_len, emitted, kld,
+               flags, workspace, comm: "Comm | None" = None, stream=None):
+        """dsde_vp_verify: this rank's shard (rank = the communicator's; comm
+        None = one shard)."""
+        B = cu_sl.numel() - 1
+        _check(lib().dsde_vp_verify(
+            self.state.h, B, self.V, dtype_code(self.dtype), draft_tokens.numel(), _ptr(cu_sl), _ptr(draft_tokens),
+            _ptr(target_shard), target_shard.stride(0), _ptr(draft_shard), draft_shard.stride(0), _ptr(seeds),
+            _ptr(accepted_len), _ptr(emitted), _ptr(kld), _ptr(flags), _ptr(workspace), workspace.numel(),
+            comm.h if comm is not None else None, _stream(stream)), "dsde_vp_verify")
 
 
 def dsde_update_signal(state: State, slots, cu_sl, kld, accepted_len, sl_hat, diag=None, stream=None):

@@ -47,6 +47,7 @@ struct NcclApi {
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   bool ok = false;
 };
 
@@ -62,7 +63,8 @@ NcclApi& nccl() {
     api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
     api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
     api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(h, "ncclAllReduce"));
-    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce;
+    api.allGather = reinterpret_cast<decltype(api.allGather)>(dlsym(h, "ncclAllGather"));
+    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce && api.allGather;
   });
   return api;
 }
@@ -83,6 +85,31 @@ dsde_status dsde_comm_allreduce_i64(dsde_comm comm, long long* buf, int n_sum, i
     return DSDE_ERR_NCCL;
   return DSDE_OK;
 }
+
+// The vocab-parallel exchanges (vocab.cuh): an in-place byte
+// all-gather (each rank's block at recv + rank * bytes), a float sum and an
+// int32 max all-reduce, enqueued on stream s.
+dsde_status dsde_comm_allgather_bytes(dsde_comm comm, void* recv, size_t bytes, cudaStream_t s) {
+  NcclApi& api = nccl();
+  if (!api.ok || !comm) return DSDE_ERR_NCCL;
+  ncclComm_t c = reinterpret_cast<ncclComm_t>(comm->nccl);
+  const char* send = reinterpret_cast<const char*>(recv) + (size_t)comm->rank * bytes;
+  return api.allGather(send, recv, bytes, ncclUint8, c, s) == ncclSuccess ? DSDE_OK : DSDE_ERR_NCCL;
+}
+dsde_status dsde_comm_allreduce_f32_sum(dsde_comm comm, float* buf, size_t n, cudaStream_t s) {
+  NcclApi& api = nccl();
+  if (!api.ok || !comm) return DSDE_ERR_NCCL;
+  return api.allReduce(buf, buf, n, ncclFloat32, ncclSum, reinterpret_cast<ncclComm_t>(comm->nccl), s) ==
+                 ncclSuccess ? DSDE_OK : DSDE_ERR_NCCL;
+}
+dsde_status dsde_comm_allreduce_i32_max(dsde_comm comm, int32_t* buf, size_t n, cudaStream_t s) {
+  NcclApi& api = nccl();
+  if (!api.ok || !comm) return DSDE_ERR_NCCL;
+  return api.allReduce(buf, buf, n, ncclInt32, ncclMax, reinterpret_cast<ncclComm_t>(comm->nccl), s) ==
+                 ncclSuccess ? DSDE_OK : DSDE_ERR_NCCL;
+}
+int dsde_comm_rank(dsde_comm comm) { return comm ? comm->rank : 0; }
+int dsde_comm_size(dsde_comm comm) { return comm ? comm->nranks : 1; }
 
 extern "C" {
 

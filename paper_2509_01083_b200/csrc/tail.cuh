@@ -26,6 +26,7 @@ struct TailArgs {
   float* mref;   // [B * nsub] its reference
   int* ctl;      // [1] signals done (dsde_step, single GPU), zeroed by the stream kernel
   int step, fuse_cap;
+  int no_draw;   // vocab-parallel finalize: stop after the layout, the draw record to fa.rec[i]
   SignalArgs sig;
   CapArgs cap;
 };
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
         if (lane == 0) {
           a.acc_len[i] = -1;
           raise_device_error(a.err, rows_ok ? DSDE_DERR_BAD_SL : DSDE_DERR_ROWS, i);
+          if (p.no_draw) a.rec[i] = error_rec(0);
         }
         tail_signal(p, i, 0, 0.0, -1);
       }
@@ -119,6 +121,11 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
     }
     __syncthreads();
     const SeqRec r = s_rec;
+    if (p.no_draw) {  // vocab-parallel: the shards draw from the published record
+      if (threadIdx.x == 0) a.rec[i] = r;
+      __syncthreads();
+      continue;
+    }
     // 3. a5-a7 (dsde_step) by the last warp, then a4's slice masses by all
     if (warp == NW - 1 && p.step) {
       const double x = lane < k ? (double)(float)s_rr[lane].kl : 0.0;  // the fp32 KLDs, as the 3-call path

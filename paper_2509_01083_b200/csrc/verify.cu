@@ -842,8 +842,9 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   TailArgs p{};
   p.fa = FinArgs{B, V, total, ns, cu_sl, tokens, tl, ld_t, dl, ld_d, seeds,
                  reinterpret_cast<const SubPartial*>(ws.part), acc_len, emitted, kld, flags,
-                 reinterpret_cast<SeqRec*>(ws.rec), err, greedy, dev_rows, ent, 0, temps, masked};
-  p.sa = SelArgs{B, V, n_draws(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32), tl, ld_t, dl, ld_d, emitted, flags, err, 0};
+                 reinterpret_cast<SeqRec*>(ws.rec), err, greedy, dev_rows, ent, 0, temps, masked, ns, 0, nullptr};
+  const int nd = n_draws(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32);
+  p.sa = SelArgs{B, V, nd, tl, ld_t, dl, ld_d, emitted, flags, err, 0, 0, nd, V, nullptr};
   p.mass = ws.mass;
   p.mref = ws.mref;
   p.ctl = ws.counters;
@@ -968,6 +969,8 @@ extern "C" dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, 
   return e == cudaSuccess ? DSDE_OK : DSDE_ERR_CUDA;
 }
 
+
+#include "vocab.cuh"  // vocab-parallel verification stages
 
 extern "C" dsde_status dsde_set_draft_entropy(dsde_state st, float* entropy) {
   if (!st) return DSDE_ERR_ARG;

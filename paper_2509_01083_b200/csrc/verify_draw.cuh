@@ -40,6 +40,24 @@ struct FinArgs {
   int v0;        // vocabulary offset of the rows (vocab-parallel shard; 0 otherwise)
   const float* temps;  // [B] per-sequence temperature (D20) or NULL; T = 0: greedy for that sequence
   int masked;          // dsde_config.masked: -inf logits allowed (D21); partials carry Fm (sign: cc), Fa
+  // vocab-parallel: the gathered partials are shard blocks
+  // [nshards][total][ns_sh]; slice c of row r is block c / ns_sh, entry
+  // r ns_sh + c % ns_sh (ns_sh = nsub, single block, when not sharded); the
+  // accept-test logits t_x, d_x come from xlog[r] (gathered from the owner shard)
+  int ns_sh;
+  long long blk;
+  const float2* xlog;
+};
+
+// Slice c of row r's partials (the sharded view of FinArgs).
+struct PartView {
+  const SubPartial* base;  // part + r ns_sh
+  int ns_sh;
+  long long blk;
+  __device__ __forceinline__ const SubPartial* at(int c) const {
+    const int s = c / ns_sh;
+    return base + (long long)s * blk + (c - s * ns_sh);
+  }
 };
 
 // Sequence i verifies greedily (T = 0): the global mode or its temperature 0.
@@ -100,12 +118,12 @@ __device__ __forceinline__ double ref_nats(float m) {  // the stream's reference
   return (double)__fmul_rn(m, kLog2e) * kLn2d;
 }
 
-__device__ __forceinline__ RowSums row_merge(const SubPartial* P, int nc, bool ent, bool mask = false) {
+__device__ __forceinline__ RowSums row_merge(const PartView P, int nc, bool ent, bool mask = false) {
   const int lane = threadIdx.x & 31;
   float Ml = -INFINITY, Dl = -INFINITY;
   for (int c = lane; c < nc; c += 32) {
-    Ml = max_nan(Ml, __ldcg(&P[c].M));
-    Dl = fmaxf(Dl, __ldcg(&P[c].maxd));
+    Ml = max_nan(Ml, __ldcg(&P.at(c)->M));
+    Dl = fmaxf(Dl, __ldcg(&P.at(c)->maxd));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -116,8 +134,8 @@ __device__ __forceinline__ RowSums row_merge(const SubPartial* P, int nc, bool e
   double S = 0.0, A = 0.0, D = 0.0, Sd = 0.0, E = 0.0;
   int cc = 0;
   for (int c = lane; c < nc; c += 32) {
-    const float4 q0 = __ldcg(reinterpret_cast<const float4*>(P + c));
-    const float4 q1 = __ldcg(reinterpret_cast<const float4*>(P + c) + 1);
+    const float4 q0 = __ldcg(reinterpret_cast<const float4*>(P.at(c)));
+    const float4 q1 = __ldcg(reinterpret_cast<const float4*>(P.at(c)) + 1);
     const double qS = q0.x, qA = q0.y, qD = q0.z, qC = q1.x;
     if (mask) {
       // Fm about the slice's fl32(maxd log2 e) ln 2, into the row's f frame Mr - C
@@ -170,13 +188,13 @@ __device__ __forceinline__ RowSums row_merge(const SubPartial* P, int nc, bool e
 // first slice holding the row max (slices are in token order), re-read vector
 // by vector (token order is vector-major) until a lane holds the max.
 template <typename T>
-__device__ __forceinline__ int row_argmax(const FinArgs& a, const SubPartial* P, int nc, float Ml,
+__device__ __forceinline__ int row_argmax(const FinArgs& a, const PartView P, int nc, float Ml,
                                           const T* trow) {
   constexpr int VEC = Traits<T>::VEC, SUB = sub_elems<T>();
   const int lane = threadIdx.x & 31;
   unsigned cs = 0x7fffffffu;
   for (int c = lane; c < nc; c += 32)
-    if (__ldcg(&P[c].M) == Ml) cs = min(cs, (unsigned)c);
+    if (__ldcg(&P.at(c)->M) == Ml) cs = min(cs, (unsigned)c);
   cs = __reduce_min_sync(kFull, cs);
   int amax = 0x7fffffff;
   if (cs < (unsigned)nc) {
@@ -214,7 +232,11 @@ __device__ __forceinline__ RowPre row_prefetch(const FinArgs& a, int r, int i) {
   if ((threadIdx.x & 31) == 0) {
     const long long slot = (long long)r + i;
     p.x = __ldg(a.tokens + r);
-    if (p.x >= 0 && p.x < a.V) {
+    if (a.xlog) {  // vocab-parallel: the owner shard's t_x, d_x
+      const float2 g = __ldcg(a.xlog + r);
+      p.tx = g.x;
+      p.dx = g.y;
+    } else if (p.x >= 0 && p.x < a.V) {
       p.tx = load_logit<T>(reinterpret_cast<const T*>(a.tl) + slot * a.ld_t + p.x);
       p.dx = load_logit<T>(reinterpret_cast<const T*>(a.dl) + (long long)r * a.ld_d + p.x);
     }
@@ -235,7 +257,7 @@ __device__ __forceinline__ RowRes row_finalize(const FinArgs& a, int r, int i, c
   const int x = in.x;
   const float tx = in.tx, dx = in.dx;
   const double uacc = in.uacc;
-  const SubPartial* P = a.part + (long long)r * a.nsub;
+  const PartView P{a.part + (long long)r * a.ns_sh, a.ns_sh, a.blk};
   const bool greedy = seq_greedy(a, i);
   const RowSums R = row_merge(P, a.nsub, a.ent != nullptr, a.masked != 0);
   int amax = 0;
@@ -689,6 +711,12 @@ struct SelArgs {
   uint8_t* flags;
   int32_t* err;
   int v0;  // vocabulary offset of the rows (vocab-parallel shard)
+  // vocab-parallel: this shard's draw slices [s_lo, s_lo + nd_sh)
+  // of the row's nsub, its columns' V; tok_out != NULL: the selected token
+  // (global id, sample flags << 24) or -1 when another shard owns the
+  // crossing slice, instead of writing emitted / flags
+  int s_lo, nd_sh, Vs;
+  int32_t* tok_out;
 };
 
 #ifndef DSDE_TAIL_TRACE
@@ -707,8 +735,8 @@ struct SliceSrc {
   __device__ __forceinline__ float r(int s) const { return SMEM ? ref[s] : __ldcg(ref + s); }
 };
 
-template <typename T, bool SMEM = false>
-__device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec& r, const SliceSrc<SMEM> src) {
+template <typename T, bool SMEM = false, typename Src = SliceSrc<SMEM>>
+__device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec& r, const Src src) {
   constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NVD, SUB = draw_elems<T>();
   const int lane = threadIdx.x & 31;
   if (r.mode == MODE_ARGMAX) {
@@ -757,6 +785,13 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   uint8_t fl = 0;
   const T* tp = reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t;
   if (!(R > 0.0) || !isfinite(R)) {
+    if (a.tok_out) {  // vocab-parallel: the D7 fallback scans a whole row; not supported
+      if (lane == 0) {
+        a.tok_out[i] = -2;
+        raise_device_error(a.err, isfinite(R) ? DSDE_DERR_VP_FALLBACK : DSDE_DERR_NONFINITE, i);
+      }
+      return;
+    }
     if (lane == 0) {
       // residual mass 0 (p <= q everywhere in fp32; D7 fallback: draw from p
       // of the same target row, one lane) or a non-finite bonus row
@@ -820,13 +855,23 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
     }
   }
   const double f = scale_of(us);
+  // vocab-parallel: only the shard owning the crossing slice scans it (with
+  // its own columns); the others report -1
+  const int Vl = a.tok_out ? a.Vs : a.V;
+  if (a.tok_out) {
+    if (us < a.s_lo || us >= a.s_lo + a.nd_sh) {
+      if (lane == 0) a.tok_out[i] = -1;
+      return;
+    }
+    us -= a.s_lo;
+  }
   const T* dp = resid ? reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d : tp;
   // the crossing slice's bonus reference: its raw max of t, recomputed exactly
   // as draw_mass did (the record holds m / T)
   float m_raw = 0.f;
   if (!resid) {
     uint4 rt0[NV];
-    load_vecs<T, NV>(tp, a.V, us, 0, rt0);
+    load_vecs<T, NV>(tp, Vl, us, 0, rt0);
     m_raw = warp_max_nan(lane_tmax<T, NV>(rt0, -INFINITY));
   }
   const DrawRef DR = draw_ref(resid, r.M, (float)r.C, r.lam, m_raw, r.invT);
@@ -837,8 +882,8 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
 #pragma unroll 1
   for (int v = 0; v < NV; ++v) {
     uint4 rt[1], rd[1];
-    load_vecs<T, 1>(tp, a.V, us, v, rt);
-    if (resid) load_vecs<T, 1>(dp, a.V, us, v, rd);
+    load_vecs<T, 1>(tp, Vl, us, v, rt);
+    if (resid) load_vecs<T, 1>(dp, Vl, us, v, rd);
     else rd[0] = rt[0];
     float wv[VEC];
     vec_weights<T>(rt[0], rd[0], DR, wv);
@@ -893,8 +938,12 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   }
   if (lane == 0) {
     if (fabs(r.u - lo / R) < 1e-6 || fabs(r.u - hi / R) < 1e-6) fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
-    a.emitted[r.slot] = a.v0 + (tok < 0 ? 0 : tok);
-    if (a.flags) a.flags[r.slot] |= fl;
+    if (a.tok_out) {
+      a.tok_out[i] = (a.v0 + (tok < 0 ? 0 : tok)) | ((int)fl << 24);  // tokens < 2^24
+    } else {
+      a.emitted[r.slot] = a.v0 + (tok < 0 ? 0 : tok);
+      if (a.flags) a.flags[r.slot] |= fl;
+    }
   }
 }
 
