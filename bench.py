@@ -72,6 +72,9 @@ CONFIGS = {
     5: dict(B=2048, V=128256, profiles=("code", "dialogue", "low"), ceiling=8, strong=True,
             name="cfg5: B=2048 total sharded over the GPUs, SL<=8 (DSDE closed loop), V=128256 bf16, "
                  "mixed code/dialogue/low profiles, cap via NCCL"),
+    # the Gemma-27B/2B pair of the paper's low-acceptance study (eager-mode V)
+    6: dict(B=256, V=256000, profiles=("low",), ceiling=8, name="cfg6 (SURVEY f4): B=256/GPU, SL<=8 (DSDE "
+            "closed loop), V=256000 bf16 (Gemma-like), low-acceptance profile"),
 }
 
 

@@ -68,12 +68,13 @@ def compare_all(s, out, chunk=256):
     return rep
 
 
-@pytest.mark.parametrize("B,profiles,steps", [
-    (256, ("code",), 3),                           # config 3 (and config 5's per-GPU shard at 8 GPUs)
-    (512, ("low",), 3),                            # config 4: low acceptance, residual-heavy
-    (2048, ("code", "dialogue", "low"), 2),        # config 5's whole batch on one GPU
-], ids=["cfg3_B256", "cfg4_B512", "cfg5_B2048"])
-def test_dsde_step_full_size_every_sequence(m, B, profiles, steps):
+@pytest.mark.parametrize("B,profiles,steps,V", [
+    (256, ("code",), 3, V),                        # config 3 (and config 5's per-GPU shard at 8 GPUs)
+    (512, ("low",), 3, V),                         # config 4: low acceptance, residual-heavy
+    (2048, ("code", "dialogue", "low"), 2, V),     # config 5's whole batch on one GPU
+    (64, ("low",), 2, 256000),                     # Gemma-like vocabulary
+], ids=["cfg3_B256", "cfg4_B512", "cfg5_B2048", "gemma_V256000_B64"])
+def test_dsde_step_full_size_every_sequence(m, B, profiles, steps, V):
     cfg_g = m.Config.default(calib_steps=1, calib_sl=4)
     cfg_o = oracle.Config(calib_steps=1, calib_sl=4)
     st = m.State(cfg_g, B)

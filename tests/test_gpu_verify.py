@@ -41,6 +41,7 @@ def _check(m, state, host, dtype, ld_pad=0, expect_ties_max=None):
     (32000, torch.float32, 4, 4),         # config 1 shape
     (32000, torch.bfloat16, 8, 64),       # config 2 shape
     (128256, torch.bfloat16, 8, 12),      # config 3-5 row shape (sampled batch)
+    (256000, torch.bfloat16, 8, 10),      # Gemma-like vocabulary
     (50000, torch.bfloat16, 8, 9),        # ragged last chunk
     (300007, torch.bfloat16, 3, 6),       # 147 slices per row, V = 300007 (Gemma-class and beyond)
     (140000, torch.float32, 3, 5),        # 274 fp32 slices of 512 per row
