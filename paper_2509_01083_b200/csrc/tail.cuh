@@ -49,6 +49,26 @@ __device__ __forceinline__ void tail_signal(const TailArgs& p, int i, int k, dou
   if (last && p.fuse_cap) cap_warp(p.cap);
 }
 
+#ifndef DSDE_TAIL_TRACE
+#define DSDE_TAIL_TRACE 0
+#endif
+#if DSDE_TAIL_TRACE
+// measurement build only (-DDSDE_TAIL_TRACE=1): globaltimer stamps per CTA's
+// first sequence: start, after the wait, finalize, layout, draw, select, smid
+constexpr int kTraceMax = 8192;
+__device__ unsigned long long g_tail_trace[kTraceMax * 8];
+__device__ __forceinline__ void tail_stamp(int k) {
+  if (threadIdx.x == 0 && blockIdx.x < kTraceMax) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_tail_trace[blockIdx.x * 8 + k] = t;
+  }
+}
+#define TAIL_STAMP(k) tail_stamp(k)
+#else
+#define TAIL_STAMP(k) do {} while (0)
+#endif
+
 // draw slices per row whose records k_tail keeps in shared memory (V <= 262144
 // bf16 / 131072 fp32; larger vocabularies use the workspace)
 constexpr int kTailMaxSub = 256;
@@ -74,6 +94,7 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
     bad = __any_sync(kFull, bad);
     if (lane == 0) s_bad = bad;
   }
+  TAIL_STAMP(0);
   RowPre pre{0, 0.f, 0.f, 0.0};
   int pre_i = -1;
   {
@@ -85,6 +106,7 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
+  TAIL_STAMP(1);
   const bool all_bad = s_bad != 0;
   for (int i = blockIdx.x; i < a.B; i += gridDim.x) {
     int c0 = 0, k = 0;
@@ -110,6 +132,7 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
       if (lane == 0) s_rr[j] = rr;
     }
     __syncthreads();
+    if (i == (int)blockIdx.x) TAIL_STAMP(2);
     // 2. a3: layout and draw record (warp 0)
     if (warp == 0) {
       RowRes rr;
@@ -120,6 +143,7 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
       if (lane == 0) s_acc = acc;
     }
     __syncthreads();
+    if (i == (int)blockIdx.x) TAIL_STAMP(3);
     const SeqRec r = s_rec;
     if (p.no_draw) {  // vocab-parallel: the shards draw from the published record
       if (threadIdx.x == 0) a.rec[i] = r;
@@ -140,6 +164,7 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
       for (int u = warp; u < nd; u += NW)
         draw_mass<T>(r, u, a.V, a.tl, a.ld_t, a.dl, a.ld_d, smem ? s_mass + u : gm + u, smem ? s_ref + u : gr + u);
       __syncthreads();
+      if (i == (int)blockIdx.x) TAIL_STAMP(4);
       // 4. a4 select (warp 0)
       if (!smem) {
         if (warp == 0) select_seq<T, false>(p.sa, i, r, SliceSrc<false>{gm, gr, nullptr});
@@ -167,5 +192,15 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
       }
     }
     __syncthreads();  // shared records are reused by the next sequence
+    if (i == (int)blockIdx.x) {
+      TAIL_STAMP(5);
+#if DSDE_TAIL_TRACE
+      if (threadIdx.x == 0 && blockIdx.x < kTraceMax) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        g_tail_trace[blockIdx.x * 8 + 6] = ((unsigned long long)smid << 8) | (unsigned)r.mode;
+      }
+#endif
+    }
   }
 }

@@ -972,6 +972,14 @@ extern "C" dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, 
 
 #include "vocab.cuh"  // vocab-parallel verification stages
 
+#if DSDE_TAIL_TRACE
+// measurement build only: copy the k_tail trace (8 u64 per CTA)
+extern "C" int dsde_debug_tail_trace(unsigned long long* out, int n) {
+  n = n < dsde::kTraceMax ? n : dsde::kTraceMax;
+  return cudaMemcpyFromSymbol(out, dsde::g_tail_trace, sizeof(unsigned long long) * 8 * n) == cudaSuccess ? 0 : -1;
+}
+#endif
+
 extern "C" dsde_status dsde_set_draft_entropy(dsde_state st, float* entropy) {
   if (!st) return DSDE_ERR_ARG;
   st->entropy_out = entropy;

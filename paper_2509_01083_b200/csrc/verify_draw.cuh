@@ -223,12 +223,12 @@ __device__ __forceinline__ int row_argmax(const FinArgs& a, const PartView P, in
 struct RowPre {
   int x;
   float tx, dx;
-  double uacc;
+  double uacc, usmp;
 };
 
 template <typename T>
 __device__ __forceinline__ RowPre row_prefetch(const FinArgs& a, int r, int i) {
-  RowPre p{0, 0.f, 0.f, 0.0};
+  RowPre p{0, 0.f, 0.f, 0.0, 0.0};
   if ((threadIdx.x & 31) == 0) {
     const long long slot = (long long)r + i;
     p.x = __ldg(a.tokens + r);
@@ -240,7 +240,11 @@ __device__ __forceinline__ RowPre row_prefetch(const FinArgs& a, int r, int i) {
       p.tx = load_logit<T>(reinterpret_cast<const T*>(a.tl) + slot * a.ld_t + p.x);
       p.dx = load_logit<T>(reinterpret_cast<const T*>(a.dl) + (long long)r * a.ld_d + p.x);
     }
-    if (!seq_greedy(a, i)) p.uacc = philox_uniforms(__ldg(a.seeds + slot)).acc;
+    if (!seq_greedy(a, i)) {
+      const Uniforms U = philox_uniforms(__ldg(a.seeds + slot));
+      p.uacc = U.acc;
+      p.usmp = U.smp;  // the recovery draw's uniform if this position is the first rejection
+    }
   }
   return p;
 }
@@ -257,6 +261,7 @@ __device__ __forceinline__ RowRes row_finalize(const FinArgs& a, int r, int i, c
   const int x = in.x;
   const float tx = in.tx, dx = in.dx;
   const double uacc = in.uacc;
+  const double usmp = __shfl_sync(kFull, in.usmp, 0);
   const PartView P{a.part + (long long)r * a.ns_sh, a.ns_sh, a.blk};
   const bool greedy = seq_greedy(a, i);
   const RowSums R = row_merge(P, a.nsub, a.ent != nullptr, a.masked != 0);
@@ -264,7 +269,8 @@ __device__ __forceinline__ RowRes row_finalize(const FinArgs& a, int r, int i, c
   if (greedy) amax = row_argmax<T>(a, P, a.nsub, R.M, trow);
   RowRes rr;
   rr.pad = 0;
-  rr.pad2[0] = rr.pad2[1] = 0.0;
+  rr.pad2[0] = usmp;  // u_smp of the row's slot (D6)
+  rr.pad2[1] = 0.0;
   rr.amax = amax;
   rr.M = R.M;
   rr.C = (double)(R.M - R.Dmax);
@@ -333,7 +339,9 @@ __device__ __forceinline__ RowRes load_rowres(const RowRes* p) {
   r.amax = b.y;
   r.bits = b.z;
   r.pad = 0;
-  r.pad2[0] = r.pad2[1] = 0.0;
+  const double2 c = __ldcg(reinterpret_cast<const double2*>(p) + 3);
+  r.pad2[0] = c.x;
+  r.pad2[1] = c.y;
   return r;
 }
 
@@ -409,7 +417,9 @@ __device__ __forceinline__ int seq_layout(const FinArgs& a, int i, int c0, int k
         r.mode = MODE_ARGMAX;
       }
     } else {
-      r.u = philox_uniforms(__ldg(a.seeds + slot0 + aa)).smp;
+      // the recovery draw's u_smp was gathered with the row (RowRes.pad2[0]);
+      // the bonus slot has no row
+      r.u = aa < k ? rr.pad2[0] : philox_uniforms(__ldg(a.seeds + slot0 + aa)).smp;
       if (aa < k) {
         r.mode = MODE_RESIDUAL;
         r.drow = (long long)c0 + aa;
