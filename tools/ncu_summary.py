@@ -1,35 +1,42 @@
-"""Summarise an ncu --set full report: per-kernel time, DRAM bytes, pipe usage, top stalls."""
+"""Summary of an ncu --set full report (read here, no GPU): per kernel the
+duration, DRAM bytes, occupancy, pipe utilisation and top stall reasons.
+
+usage: python tools/ncu_summary.py REPORT.ncu-rep [--alg-bytes K=BYTES ...]
+"""
+import argparse
 import csv
 import subprocess
 import sys
 
-WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
-        'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 'sm__warps_active.avg.pct_of_peak_sustained_active',
-        'launch__registers_per_thread', 'smsp__inst_executed.sum', 'sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active',
-        'sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active', 'sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active',
-        'smsp__issue_active.avg.pct_of_peak_sustained_active', 'sm__cycles_elapsed.avg.per_second',
-        'launch__grid_size', 'launch__block_size']
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
+        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__cycles_elapsed.avg.per_second",
+        "lts__t_sector_hit_rate.pct"]
 
 
-def main(path):
-    out = subprocess.check_output(['ncu', '-i', path, '--page', 'raw', '--csv'], text=True, stderr=subprocess.DEVNULL)
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("report")
+    args = ap.parse_args()
+    out = subprocess.run(["ncu", "-i", args.report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    hdr = rows[0]
-    for r in rows[2:]:
-        name = r[hdr.index('Kernel Name')]
-        print(f"== {name}")
+    h, units = rows[0], rows[1]
+    for v in rows[2:]:
+        print("==", v[h.index("Kernel Name")][:90])
         for w in WANT:
-            if w in hdr:
-                print(f"   {w:70s} {r[hdr.index(w)]}")
-        vals = []
-        for h, v in zip(hdr, r):
-            if 'average_warps_issue_stalled' in h and 'not_issued' not in h:
-                try:
-                    vals.append((float(v), h.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')))
-                except ValueError:
-                    pass
-        print("   stalls/issue:", ", ".join(f"{h}={v:.2f}" for v, h in sorted(vals, reverse=True)[:8]))
+            if w in h:
+                i = h.index(w)
+                print(f"   {w:62s} {v[i]:>16s} {units[i]}")
+        st = [(n, v[i]) for i, n in enumerate(h)
+              if n.startswith("smsp__average_warps_issue_stalled_") and n.endswith("_per_issue_active.ratio")]
+        st = sorted(((n[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")], float(x))
+                     for n, x in st if x.replace(".", "", 1).isdigit()), key=lambda t: -t[1])
+        print("   stalls/issue: " + ", ".join(f"{n}={x:.2f}" for n, x in st[:8]))
 
 
-if __name__ == '__main__':
-    main(sys.argv[1])
+if __name__ == "__main__":
+    sys.exit(main())
