@@ -3,8 +3,11 @@ dsde_set_draft_entropy the stream kernel's opt-in variant also sums the draft's
 own softmax per slice (Sd, E about the slice max of d), the finalize merges
 them in fp64 and writes H(q) = log Sd - E / Sd per draft row. Compared element
 by element with the oracle's definition -sum q log q (oracle.draft_entropy);
-band |dH| <= 1e-5 H + 2e-6 (fp32 slice sums: ~1e-7 absolute in log Sd near a
-one-hot draft). The verify outputs must be bit-identical with and without it."""
+band |dH| <= 1e-5 H + 3e-7: relative to H, with an absolute floor (as the
+KLD's 1e-9): the fp32 slice sums leave ~1e-7..3e-7 absolute in log Sd, and
+near a one-hot draft the row max's slice rounds Sd = 1 + delta to 1, losing
+log1p(delta) <= H / (1 + mean -ln q of the other tokens). The verify outputs must be bit-identical with and
+without it."""
 import numpy as np
 import pytest
 import torch
@@ -37,7 +40,7 @@ def _check_entropy(m, host, dtype, sharpen=None):
     h_o = oracle.draft_entropy(host["draft"], oracle.BF16 if dtype == torch.bfloat16 else oracle.F32)
     err = np.abs(h_g - h_o)
     assert np.all(np.isfinite(h_g))
-    assert np.all(err <= 1e-5 * h_o + 2e-6), (np.max(err / (h_o + 1e-300)), h_o[np.argmax(err)], np.max(err))
+    assert np.all(err <= 1e-5 * h_o + 3e-7), (np.max(err / (h_o + 1e-300)), h_o[np.argmax(err)], np.max(err))
     rep = parity.compare_verify(host["cu_sl"], got[0], got[1], got[2], oracle_verify(host))
     assert rep.ok(), str(rep)
     return h_o
@@ -88,7 +91,7 @@ def test_draft_entropy_in_dsde_step(m):
     step(dev["cu_sl"], dev["draft_tokens"], dev["target"], dev["draft"], dev["seeds"], n)
     torch.cuda.synchronize()
     h_o = oracle.draft_entropy(host["draft"], oracle.BF16)
-    assert np.all(np.abs(ent.cpu().numpy() - h_o) <= 1e-5 * h_o + 2e-6)
+    assert np.all(np.abs(ent.cpu().numpy() - h_o) <= 1e-5 * h_o + 3e-7)
     st.set_draft_entropy(None)
     ent.zero_()
     step(dev["cu_sl"], dev["draft_tokens"], dev["target"], dev["draft"], dev["seeds"], n)
