@@ -8,8 +8,19 @@
 #include <stdint.h>
 
 #include "dsde.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace dsde {
+
+// NVTX range over a host API call (a no-op unless a profiler is attached):
+// the call's kernel launches appear under the entry point's name in
+// Nsight Systems / ncu --nvtx.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;

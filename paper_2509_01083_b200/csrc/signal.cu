@@ -70,6 +70,7 @@ extern "C" dsde_status dsde_update_signal(dsde_state st, int B, const int32_t* s
                                           const int32_t* cu_sl, const float* kld,
                                           const int32_t* accepted_len, int32_t* sl_hat,
                                           double* diag, void* stream) {
+  NvtxRange nv("dsde_update_signal");
   if (!st || !slots || !cu_sl || !kld || !accepted_len || !sl_hat || B < 1) return DSDE_ERR_ARG;
   if (B > st->max_seqs) return DSDE_ERR_STATE;
   if (st->cfg.entropy_mode && !st->entropy_out) return DSDE_ERR_ARG;  // D22 reads the draft entropy
@@ -83,6 +84,7 @@ extern "C" dsde_status dsde_next_sl(dsde_state st, int B, const int32_t* slots,
                                     const int32_t* sl_hat, const int32_t* budget,
                                     int32_t* next_sl, int32_t* cap, dsde_comm comm,
                                     void* stream) {
+  NvtxRange nv("dsde_next_sl");
   if (!st || !slots || !sl_hat || !next_sl || !cap || B < 1) return DSDE_ERR_ARG;
   if (B > st->max_seqs) return DSDE_ERR_STATE;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

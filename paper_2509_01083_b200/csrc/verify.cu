@@ -878,6 +878,7 @@ extern "C" dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_dra
                                    const uint64_t* seeds, int32_t* accepted_len,
                                    int32_t* emitted_tokens, float* kld, uint8_t* flags,
                                    void* workspace, size_t ws_bytes, dsde_state st, void* stream) {
+  NvtxRange nv("dsde_verify");
   if (!st || !cu_sl || !draft_tokens || !target_logits || !draft_logits || !seeds ||
       !accepted_len || !emitted_tokens || !kld || !workspace)
     return DSDE_ERR_ARG;
@@ -926,6 +927,7 @@ extern "C" dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, 
                                  uint8_t* flags, int32_t* sl_hat, double* diag, int32_t* next_sl,
                                  int32_t* cap, void* workspace, size_t ws_bytes, dsde_comm comm,
                                  void* stream) {
+  NvtxRange nv("dsde_step");
   if (!st || !slots || !sl_hat || !next_sl || !cap || !cu_sl || !draft_tokens || !target_logits ||
       !draft_logits || !seeds || !accepted_len || !emitted_tokens || !kld || !workspace)
     return DSDE_ERR_ARG;

@@ -320,6 +320,7 @@ extern "C" dsde_status dsde_vp_verify(dsde_state st, int B, int V, dsde_dtype dt
                                       int64_t ld_t, const void* draft_shard, int64_t ld_d, const uint64_t* seeds,
                                       int32_t* accepted_len, int32_t* emitted_tokens, float* kld, uint8_t* flags,
                                       void* workspace, size_t ws_bytes, dsde_comm comm, void* stream) {
+  NvtxRange nv("dsde_vp_verify");
   const int n = dsde_comm_size(comm), rank = dsde_comm_rank(comm);
   VpShape sh;
   if (!workspace || ((uintptr_t)workspace & 255) || vp_shape(V, n, rank, dtype, &sh) != DSDE_OK)
