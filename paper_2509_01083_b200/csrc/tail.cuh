@@ -97,11 +97,14 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
   TAIL_STAMP(0);
   RowPre pre{0, 0.f, 0.f, 0.0};
   int pre_i = -1;
+  __shared__ double s_ubonus;  // u_smp of the first sequence's bonus slot
   {
     const int i = blockIdx.x, c0 = __ldg(a.cu_sl + i), k = __ldg(a.cu_sl + i + 1) - c0;
-    if (warp < k && k <= DSDE_MAX_SL && c0 >= 0 && c0 + k <= a.total) {
-      pre = row_prefetch<T>(a, c0 + warp, i);
+    if (k >= 1 && k <= DSDE_MAX_SL && c0 >= 0 && c0 + k <= a.total) {
       pre_i = i;
+      if (warp < k) pre = row_prefetch<T>(a, c0 + warp, i);
+      if (warp == min(k, NW - 1) && lane == 0 && !seq_greedy(a, i))
+        s_ubonus = philox_uniforms(__ldg(a.seeds + (long long)c0 + i + k)).smp;
     }
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -137,9 +140,10 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
     if (warp == 0) {
       RowRes rr;
       rr.bits = 0;
+      rr.x = 0;
       rr.kl = 0.0;
       if (lane < k) rr = s_rr[lane];
-      const int acc = seq_layout(a, i, c0, k, rr, &s_rec);
+      const int acc = seq_layout(a, i, c0, k, rr, &s_rec, i == pre_i ? &s_ubonus : nullptr);
       if (lane == 0) s_acc = acc;
     }
     __syncthreads();
@@ -172,6 +176,7 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
         if (r.mode == MODE_BONUS) {
           // the whole CTA rescales the bonus slice masses to the row max Mg (one
           // fp64 exp per slice, in parallel), as select_seq would slice by slice
+          // (s_ref holds the raw slice maxima m; the references are fl32(m / T))
           float mg = -INFINITY;
           for (int u = threadIdx.x; u < nd; u += NW * 32) mg = max_nan(mg, s_ref[u]);
           mg = warp_max_nan(mg);
@@ -180,9 +185,10 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
           float Mg = s_wmax[0];
 #pragma unroll
           for (int w = 1; w < NW; ++w) Mg = max_nan(Mg, s_wmax[w]);
+          Mg = __fmul_rn(Mg, r.invT);
           for (int u = threadIdx.x; u < nd; u += NW * 32) {
             const float ms = s_ref[u];
-            const double f = ms == -INFINITY ? 0.0 : exp((double)ms - (double)Mg);
+            const double f = ms == -INFINITY ? 0.0 : exp((double)__fmul_rn(ms, r.invT) - (double)Mg);
             s_scale[u] = f;
             s_mass[u] = f * s_mass[u];
           }

@@ -1,8 +1,8 @@
 // verify_draw.cuh — a2-a4 of the verification pass after the row stream
 // (included by verify.cu inside namespace dsde; uses its helpers). The same
-// device functions serve the persistent pass kernel (pass.cuh, the default
-// path of dsde_verify / dsde_step) and the staged kernels of the
-// vocab-parallel path (vocab.cu), so both give bit-identical results:
+// device functions serve k_tail (tail.cuh, the path of dsde_verify /
+// dsde_step) and the staged kernels of the vocab-parallel path (vocab.cuh),
+// so both give bit-identical results:
 //
 //   row_finalize  one warp per draft row: fp64 merge of the row's slice
 //                 partials, KL(p||q), log p(x)/q(x) and the Philox accept test
@@ -55,6 +55,7 @@ struct PartView {
   int ns_sh;
   long long blk;
   __device__ __forceinline__ const SubPartial* at(int c) const {
+    if (c < ns_sh) return base + c;  // the first (unsharded: the only) block
     const int s = c / ns_sh;
     return base + (long long)s * blk + (c - s * ns_sh);
   }
@@ -74,7 +75,7 @@ struct RowRes {
   float M;     // reference max of t
   int amax;    // greedy: argmax of t (smallest index)
   int bits;    // RR_* bits
-  int pad;
+  int x;       // the draft token of the row
   double pad2[2];
 };
 static_assert(sizeof(RowRes) == 64, "RowRes layout");
@@ -268,7 +269,7 @@ __device__ __forceinline__ RowRes row_finalize(const FinArgs& a, int r, int i, c
   int amax = 0;
   if (greedy) amax = row_argmax<T>(a, P, a.nsub, R.M, trow);
   RowRes rr;
-  rr.pad = 0;
+  rr.x = __shfl_sync(kFull, x, 0);
   rr.pad2[0] = usmp;  // u_smp of the row's slot (D6)
   rr.pad2[1] = 0.0;
   rr.amax = amax;
@@ -338,7 +339,7 @@ __device__ __forceinline__ RowRes load_rowres(const RowRes* p) {
   r.M = __int_as_float(b.x);
   r.amax = b.y;
   r.bits = b.z;
-  r.pad = 0;
+  r.x = b.w;
   const double2 c = __ldcg(reinterpret_cast<const double2*>(p) + 3);
   r.pad2[0] = c.x;
   r.pad2[1] = c.y;
@@ -375,9 +376,11 @@ __device__ __forceinline__ SeqRec error_rec(long long slot0) {
 // a3 (one warp; lane j < k holds position j's RowRes): the first rejection a_i,
 // KLDs, the emitted-token layout (x_0 .. x_{a-1}, the drawn token at a, pads
 // after), flags and the draw record (written by lane a to *out).
-// Returns a_i (-1 on a data error) in every lane.
+// Returns a_i (-1 on a data error) in every lane. u_bonus: the bonus slot's
+// u_smp when the caller gathered it (k_tail, before griddepcontrol.wait), else
+// NULL.
 __device__ __forceinline__ int seq_layout(const FinArgs& a, int i, int c0, int k, const RowRes& rr,
-                                          SeqRec* out) {
+                                          SeqRec* out, const double* u_bonus = nullptr) {
   const int lane = threadIdx.x & 31;
   const long long slot0 = (long long)c0 + i;
   const unsigned bt = __ballot_sync(kFull, lane < k && (rr.bits & RR_BADTOK));
@@ -392,7 +395,7 @@ __device__ __forceinline__ int seq_layout(const FinArgs& a, int i, int c0, int k
   const int aa = acc_run < k ? acc_run : k;
   if (lane < k) a.kld[c0 + lane] = (float)rr.kl;
   if (lane <= k) {
-    a.emitted[slot0 + lane] = lane < aa ? __ldg(a.tokens + c0 + lane) : DSDE_PAD;
+    a.emitted[slot0 + lane] = lane < aa ? rr.x : DSDE_PAD;
     if (a.flags)
       a.flags[slot0 + lane] = ((rr.bits & RR_NEAR) && lane <= aa && lane < k) ? DSDE_FLAG_ACCEPT_NEAR_TIE : 0;
   }
@@ -419,7 +422,7 @@ __device__ __forceinline__ int seq_layout(const FinArgs& a, int i, int c0, int k
     } else {
       // the recovery draw's u_smp was gathered with the row (RowRes.pad2[0]);
       // the bonus slot has no row
-      r.u = aa < k ? rr.pad2[0] : philox_uniforms(__ldg(a.seeds + slot0 + aa)).smp;
+      r.u = aa < k ? rr.pad2[0] : u_bonus ? *u_bonus : philox_uniforms(__ldg(a.seeds + slot0 + aa)).smp;
       if (aa < k) {
         r.mode = MODE_RESIDUAL;
         r.drow = (long long)c0 + aa;
@@ -714,7 +717,9 @@ __device__ __forceinline__ void draw_mass(const SeqRec& r, int u, int V, const v
   const double tot = warp_sum_vectors<NV>(x);
   if (lane == 0) {
     *mass_out = tot;
-    *ref_out = R.resid ? R.M : (R.m <= -1e30f ? -INFINITY : R.m * R.invT);  // bonus: the reference m / T
+    // bonus: the raw slice max m of t (the weights' reference is m / T; the
+    // select rescales by fl32(m invT), which is monotone in m)
+    *ref_out = R.resid ? R.M : (R.m <= -1e30f ? -INFINITY : R.m);
   }
 }
 
@@ -783,16 +788,16 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   if (r.mode != MODE_RESIDUAL && r.mode != MODE_BONUS) return;
   const bool resid = r.mode == MODE_RESIDUAL;
   const int nsub = a.nsub;
-  float Mg = -INFINITY;
+  float Mg = -INFINITY;  // bonus: the row's largest slice reference fl32(m invT)
   if (!resid && !SMEM) {
     for (int s0 = lane; s0 < nsub; s0 += 32) Mg = max_nan(Mg, src.r(s0));
-    Mg = warp_max_nan(Mg);
+    Mg = __fmul_rn(warp_max_nan(Mg), r.invT);
   }
   auto scale_of = [&](int s0) -> double {  // slice mass scale to the common reference
     if (resid) return 1.0;
     if (SMEM) return src.scale[s0];
     const float ms = src.r(s0);
-    return ms == -INFINITY ? 0.0 : exp((double)ms - (double)Mg);
+    return ms == -INFINITY ? 0.0 : exp((double)__fmul_rn(ms, r.invT) - (double)Mg);
   };
   // shared-memory bonus masses are already rescaled
   auto mass_of = [&](int s0) -> double { return (SMEM || resid) ? src.m(s0) : scale_of(s0) * src.m(s0); };
@@ -888,19 +893,16 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
     us -= a.s_lo;
   }
   const T* dp = resid ? reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d : tp;
-  // the crossing slice's bonus reference: its raw max of t, recomputed exactly
-  // as draw_mass did (the record holds m / T)
-  float m_raw = 0.f;
-  if (!resid) {
-    uint4 rt0[NV];
-    load_vecs<T, NV>(tp, Vl, us, 0, rt0);
-    m_raw = warp_max_nan(lane_tmax<T, NV>(rt0, -INFINITY));
-  }
+  // the crossing slice's bonus reference: the raw slice max draw_mass
+  // recorded (the record index under vocab parallelism is us + s_lo)
+  const float m_raw = resid ? 0.f : src.r(a.tok_out ? us + a.s_lo : us);
   const DrawRef DR = draw_ref(resid, r.M, (float)r.C, r.lam, m_raw, r.invT);
   int tok = -1, last_pos = -1;
   double lo = 0.0, hi = 0.0, lp_lo = 0.0, lp_hi = 0.0, vbase = base;
   // one vector at a time, not unrolled: this runs once per sequence, so its
-  // instructions are cold (a rolled loop fetches one vector's code)
+  // instructions are cold, and the kernel's 64-register budget is shared with
+  // the draw loop (hoisting all the slice's loads spilled there: measured
+  // slower draws and selects)
 #pragma unroll 1
   for (int v = 0; v < NV; ++v) {
     uint4 rt[1], rd[1];

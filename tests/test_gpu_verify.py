@@ -173,6 +173,44 @@ def test_deterministic(m, state):
         assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
 
 
+def test_workspace_reuse_and_garbage(m):
+    """The workspace is scratch (include/dsde.h dsde_verify): a workspace full
+    of garbage, the same workspace reused by one state and by two states, and a
+    state switching between two workspaces must all give the identical,
+    oracle-exact result (the tail's signal counter and the slice records are
+    initialised by the launch itself)."""
+    k = synth.random_k(40, 8, 21)
+    host = make_host_batch(128256, k, seed=22)
+    dev = to_device_inputs(host, torch.bfloat16)
+    cu, n, V = dev["cu_sl"], dev["draft_tokens"].numel(), dev["V"]
+    B = cu.numel() - 1
+    size = m.workspace_size(B, n, V, torch.bfloat16)
+
+    def new_ws():
+        w = torch.full((size + 256,), 0xFF, dtype=torch.uint8, device="cuda")  # garbage counters
+        return w[(-w.data_ptr()) % 256:]
+
+    def run(st, ws):
+        acc = torch.full((B,), -7, dtype=torch.int32, device="cuda")
+        em = torch.full((n + B,), -7, dtype=torch.int32, device="cuda")
+        kl = torch.full((n,), float("nan"), dtype=torch.float32, device="cuda")
+        m.dsde_verify(st, V, n, cu, dev["draft_tokens"], dev["target"], dev["draft"], dev["seeds"],
+                      acc, em, kl, None, ws)
+        torch.cuda.synchronize()
+        return acc.cpu().numpy(), em.cpu().numpy(), kl.cpu().numpy()
+
+    sa, sb = m.State(m.Config.default(), 64), m.State(m.Config.default(), 64)
+    w1, w2 = new_ws(), new_ws()
+    ref = run(sa, w1)
+    rep = parity.compare_verify(host["cu_sl"], *ref, oracle_verify(host))
+    assert rep.ok(), str(rep)
+    for st, ws in ((sa, w1), (sa, w1), (sb, w1), (sa, w1), (sa, w2), (sa, w1), (sb, w2), (sb, w2)):
+        got = run(st, ws)
+        for x, y in zip(ref, got):
+            assert np.array_equal(x.view(np.uint8), y.view(np.uint8))
+    assert sa.device_error() == (0, -1) and sb.device_error() == (0, -1)
+
+
 def test_device_errors(m):
     st = m.State(m.Config.default(), 64)
     k = [2, 3, 2]
