@@ -9,7 +9,7 @@ timeout 600 python bench.py > $O/bench_cfg3.json 2> $O/bench_cfg3.err
 for c in 1 2 4 6; do timeout 600 python bench.py --config $c --steps 100 --warmup 10 > $O/bench_cfg$c.json 2> $O/bench_cfg$c.err; done
 timeout 900 python bench.py --config 5 --steps 30 --warmup 5 --cpu-seconds 10 > $O/bench_cfg5.json 2> $O/bench_cfg5.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $O/reference.json 2> $O/reference.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/launches_cfg3.csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_stream_ldg|k_tail" -c 20 --csv --log-file $O/launches_cfg3.csv \
   python bench.py --steps 6 --warmup 3 --preroll 2 --record 4 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
 for c in 3 4; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_stream_ldg|k_tail" -s 4 -c 2 \
