@@ -78,6 +78,11 @@ CONFIGS = {
 }
 
 
+def _resample(args) -> int:
+    """dsde_config.resample / oracle reading of the recovery draw (D23 or D7)."""
+    return 0 if getattr(args, "resample", "full") == "proposal" else 1
+
+
 def _cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -208,7 +213,7 @@ def run_reference(args):
         host = synth.generate_step(w, s, k, device="cpu").host_arrays()
         t0 = time.perf_counter()
         r = oracle.verify(host["cu_sl"], host["draft_tokens"], host["target"], host["draft"], host["seeds"],
-                          odt, nthreads=nthreads, greedy=args.greedy)
+                          odt, nthreads=nthreads, greedy=args.greedy, resample=_resample(args))
         sl, cal, _ = ost.update_signal(np.arange(per_step), host["cu_sl"], r.kld, r.accepted_len)
         nx, cap = oracle.next_sl(ost.cfg, sl, cal)
         dt = time.perf_counter() - t0
@@ -244,6 +249,7 @@ def _config_dict(args, cfg, n):
             "one distinct input set per replayed step (R of them, cyclic; a step's set is smaller than L2)",
             "replay": "recorded closed-loop DSDE steps replayed in order (cyclic if K+W > R)",
             "verify": "greedy (T=0, draft argmax tokens)" if args.greedy else "rejection sampling (T=1)",
+            "recovery_draw": "D23 proposals from p (then D7)" if _resample(args) == 0 else "D7 full residual CDF",
             "draft_entropy": bool(args.entropy)}
 
 
@@ -272,7 +278,8 @@ def run(args):
         uid = [m.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = m.Comm(uid[0], ws, rank)
-    mcfg = m.Config.default(sl_ceiling=cfg["ceiling"], calib_sl=min(4, cfg["ceiling"]), greedy=int(args.greedy))
+    mcfg = m.Config.default(sl_ceiling=cfg["ceiling"], calib_sl=min(4, cfg["ceiling"]), greedy=int(args.greedy),
+                              resample=_resample(args))
     state = m.State(mcfg, B)
     step = m.Step(state, B, V, tdt, comm=comm)
     if args.entropy:  # the fused draft entropy in the same stream pass
@@ -568,7 +575,7 @@ def _cpu_baseline(args, cfg, rec, R):
         sub = parity.subset_batch(host, ids)
         t0 = time.perf_counter()
         o = oracle.verify(sub["cu_sl"], sub["draft_tokens"], sub["target"], sub["draft"], sub["seeds"], odt,
-                          nthreads=cores, greedy=args.greedy)
+                          nthreads=cores, greedy=args.greedy, resample=_resample(args))
         sl, cal, _ = ost.update_signal(np.arange(len(ids)), sub["cu_sl"], o.kld, o.accepted_len)
         oracle.next_sl(ost.cfg, sl, cal)
         elapsed += time.perf_counter() - t0
@@ -581,7 +588,7 @@ def _cpu_baseline(args, cfg, rec, R):
     sub1 = parity.subset_batch(host, ids[:max(1, min(len(ids), 8))])
     t0 = time.perf_counter()
     oracle.verify(sub1["cu_sl"], sub1["draft_tokens"], sub1["target"], sub1["draft"], sub1["seeds"], odt,
-                  nthreads=1, greedy=args.greedy)
+                  nthreads=1, greedy=args.greedy, resample=_resample(args))
     one = int(sub1["cu_sl"][-1]) / (time.perf_counter() - t0)
     cpu = {"value": positions / elapsed, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
            "one_thread_value": one,
@@ -611,6 +618,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seqs", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--resample", default="full", choices=["proposal", "full"],
+                    help="the recovery draw's reading: D7 full residual CDF (default) or D23 proposals from p")
     ap.add_argument("--greedy", action="store_true",
                     help="T = 0 verification (dsde_config.greedy; draft tokens = draft argmax)")
     ap.add_argument("--entropy", action="store_true",

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define DSDE_ABI_VERSION 3
+#define DSDE_ABI_VERSION 4
 
 typedef enum {
     DSDE_OK = 0,
@@ -75,13 +75,39 @@ typedef enum { DSDE_F32 = 0, DSDE_BF16 = 1 } dsde_dtype;
 #define DSDE_FLAG_ACCEPT_NEAR_TIE 1  /* |u_acc - min(1, p/q)| < 1e-6 at this position      */
 #define DSDE_FLAG_SAMPLE_NEAR_TIE 2  /* |u_smp - C/R| < 1e-6 at a CDF edge of the draw      */
 #define DSDE_FLAG_FALLBACK 4         /* residual mass 0: the token was drawn from p (D7)  */
+#define DSDE_FLAG_PROPOSAL_FALLBACK 8 /* D23: none of the DSDE_RESAMPLE_PROPOSALS proposals was
+                                        kept; the recovery token is the D7 draw              */
+
+/* The recovery draw (the resample from normalize(max(0, p - q)) at the first
+ * rejection; S:127, P:260 — the paper does not say how it is sampled):
+ *   DSDE_RESAMPLE_FULL (default, D7): the inverse CDF over max(0, p - q) with
+ *     u_smp (one pass over the drawn row's logits after the finalize).
+ *   DSDE_RESAMPLE_PROPOSAL (D23): proposals v_j ~ p (the inverse CDF
+ *     of D7 over p with u_prop of proposal j = 1, 2, ...), each kept with
+ *     probability max(0, p_v - q_v) / p_v (u_keep < that); the first kept
+ *     proposal is the token. Exact: a kept proposal is distributed as
+ *     normalize(max(0, p - q)); each is kept with probability TV(p, q). If
+ *     none of DSDE_RESAMPLE_PROPOSALS is kept, the D7 draw below decides
+ *     (flag DSDE_FLAG_PROPOSAL_FALLBACK). (u_prop, u_keep) of proposal j:
+ *     Philox4x32-10 keyed by the slot's seed at counter (j, 0, 0, 0), res53 of
+ *     words 0-1 / 2-3 (D6 uses counter 0). A proposal needs p's slice masses
+ *     (from the row stream) and one slice of the row, so the recovery draw
+ *     costs ~1/TV slice scans instead of a pass over the row: faster when the
+ *     draft is far from the target (low acceptance), slower when TV is small.
+ * Both are exact samplers of the same distribution; they consume different
+ * random numbers, so they emit different tokens for the same seeds. The
+ * bonus draw (all drafts accepted) is D7 over p in both. The
+ * vocabulary-parallel stages (dsde_vp_*) implement DSDE_RESAMPLE_FULL. */
+#define DSDE_RESAMPLE_PROPOSAL 0
+#define DSDE_RESAMPLE_FULL 1
+#define DSDE_RESAMPLE_PROPOSALS 256
 
 /* Adapter configuration; defaults from the paper / SPEC (dsde_config_default).
  * Validity (S:173-174 plus D11/D17): 0 < delta <= 1; 1 <= n_short < n_long
  * <= DSDE_MAX_WINDOW; sl_min >= 1; sl_min < sl_ceiling <= DSDE_MAX_SL;
  * epsilon > 0; calib_steps >= 0; 1 <= calib_sl <= sl_ceiling;
  * window_unit in {0,1}; cap_mode in {0,1}; greedy in {0,1}; masked in {0,1};
- * entropy_mode in {0,1}; entropy_gamma > 0. */
+ * entropy_mode in {0,1}; entropy_gamma > 0; resample in {0,1}. */
 typedef struct {
     double delta;      /* decay factor of Eq.5, 0.85                         */
     int n_short;       /* short window, 10                                   */
@@ -115,6 +141,8 @@ typedef struct {
                           + SL_min)), H = the mean draft entropy of the step (D22; "optionally combined
                           with entropy"). Needs dsde_set_draft_entropy (else DSDE_ERR_ARG). */
     double entropy_gamma; /* gamma of D22, 0.5 */
+    int resample;      /* the recovery draw's reading: DSDE_RESAMPLE_FULL (default, D7) or
+                          DSDE_RESAMPLE_PROPOSAL (D23); see DSDE_RESAMPLE_FULL above */
 } dsde_config;
 
 typedef struct dsde_state_s* dsde_state; /* per-sequence KLD ring, calibration, SL_max, error word */

@@ -35,6 +35,11 @@ F32, BF16 = 0, 1
 FLAG_ACCEPT_TIE = 1
 FLAG_SAMPLE_TIE = 2
 FLAG_FALLBACK = 4
+FLAG_PROPOSAL_FALLBACK = 8   # D23: no proposal kept, the D7 draw was used
+
+# the recovery draw's reading (D23 proposals from p, or D7 inverse CDF over max(0, p - q))
+RESAMPLE_PROPOSAL, RESAMPLE_FULL = 0, 1
+PROPOSALS = 256
 
 
 def build(force: bool = False) -> str:
@@ -72,7 +77,8 @@ def lib():
         L.oracle_verify.restype = C.c_int
         L.oracle_verify_mode.argtypes = list(L.oracle_verify.argtypes) + [C.c_int]
         L.oracle_verify_mode.restype = C.c_int
-        L.oracle_verify_temp.argtypes = list(L.oracle_verify.argtypes) + [C.c_int, C.c_void_p]
+        L.oracle_verify_temp.argtypes = list(L.oracle_verify.argtypes) + [C.c_int, C.c_void_p, C.c_int]
+        L.oracle_proposal_uniforms.argtypes = [C.c_uint64, C.c_uint32, P, P]
         L.oracle_verify_temp.restype = C.c_int
         L.oracle_weighted_variance.argtypes = [P, C.c_int, C.c_double]
         L.oracle_weighted_variance.restype = C.c_double
@@ -116,6 +122,13 @@ def philox4x32_10(ctr, key) -> np.ndarray:
 
 def res53(a: int, b: int) -> float:
     return lib().oracle_res53(a, b)
+
+
+def proposal_uniforms(seed: int, j: int) -> tuple[float, float]:
+    """D23: (u_prop, u_keep) of proposal j >= 1 (Philox counter (j, 0, 0, 0))."""
+    up, uk = C.c_double(), C.c_double()
+    lib().oracle_proposal_uniforms(C.c_uint64(seed), C.c_uint32(j), C.byref(up), C.byref(uk))
+    return up.value, uk.value
 
 
 def uniforms(seed: int) -> tuple[float, float]:
@@ -167,14 +180,19 @@ class VerifyResult:
 
 
 def verify(cu_sl, draft_tokens, target_logits, draft_logits, seeds, dtype: int,
-           nthreads: int = 1, greedy: bool = False, temperature=None) -> VerifyResult:
+           nthreads: int = 1, greedy: bool = False, temperature=None,
+           resample: int = 1) -> VerifyResult:
     """Batched verification. ``target_logits`` / ``draft_logits`` are 2-D numpy
     arrays of float32 (dtype=F32) or uint16 bf16 bit patterns (dtype=BF16);
     -inf entries are masked tokens (D21).
     greedy=True: T = 0 verification (accept iff x_j = argmax t_j, emit the
     target argmax).
     temperature: optional per-sequence temperatures [B] (D20): p = softmax(t/T),
-    q = softmax(d/T); T = 0 makes that sequence greedy."""
+    q = softmax(d/T); T = 0 makes that sequence greedy.
+    resample: the recovery draw's reading — RESAMPLE_FULL (D7, default: the
+    inverse CDF over max(0, p - q) with u_smp) or RESAMPLE_PROPOSAL (D23: up
+    to PROPOSALS proposals v ~ p, each kept with probability
+    max(0, p_v - q_v) / p_v, then the D7 draw)."""
     cu_sl = np.ascontiguousarray(cu_sl, dtype=np.int32)
     toks = np.ascontiguousarray(draft_tokens, dtype=np.int32)
     tl = np.ascontiguousarray(target_logits)
@@ -197,7 +215,7 @@ def verify(cu_sl, draft_tokens, target_logits, draft_logits, seeds, dtype: int,
                                   dl.shape[1], _p(seeds), _p(r.accepted_len), _p(r.emitted), _p(r.kld),
                                   _p(r.log_ratio), _p(r.u_acc), _p(r.u_smp), _p(r.samp_diag),
                                   _p(r.flags), int(nthreads), int(bool(greedy)),
-                                  None if temps is None else _p(temps))
+                                  None if temps is None else _p(temps), int(resample))
     if rc != 0:
         raise ValueError(f"oracle_verify failed: {rc}")
     return r

@@ -97,6 +97,19 @@ OR_EXPORT void oracle_uniforms(uint64_t seed, double* u_acc, double* u_smp) {
     *u_smp = oracle_res53(w[2], w[3]);
 }
 
+/* D23: the uniforms of proposal j >= 1 of a recovery draw: Philox keyed by the
+ * slot's seed, counter (j, 0, 0, 0); words 0-1 -> u_prop (the proposal's
+ * inverse CDF over p), words 2-3 -> u_keep (its accept test). Counter 0 is
+ * D6's (u_acc, u_smp). */
+OR_EXPORT void oracle_proposal_uniforms(uint64_t seed, uint32_t j, double* u_prop, double* u_keep) {
+    const uint32_t ctr[4] = {j, 0u, 0u, 0u};
+    const uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    uint32_t w[4];
+    oracle_philox4x32_10(ctr, key, w);
+    *u_prop = oracle_res53(w[0], w[1]);
+    *u_keep = oracle_res53(w[2], w[3]);
+}
+
 /* ------------------------------------------------------------------ */
 /* C1. Verify                                                           */
 /* ------------------------------------------------------------------ */
@@ -207,6 +220,10 @@ static int inverse_cdf(const double* w, int V, double u, double* R_out, double* 
 #define OR_FLAG_ACCEPT_TIE 1   /* |u_acc - min(1,r)| < 1e-6 at this position */
 #define OR_FLAG_SAMPLE_TIE 2   /* |u_smp - boundary| < 1e-6 for the drawn token */
 #define OR_FLAG_FALLBACK 4     /* residual mass R == 0: sampled from p instead */
+#define OR_FLAG_PROPOSAL_FALLBACK 8  /* D23: none of the OR_PROPOSALS proposals kept: D7 draw */
+
+/* D23: proposals of a recovery draw before the D7 inverse CDF takes over. */
+#define OR_PROPOSALS 256
 
 typedef struct {
     int V, dtype;
@@ -227,6 +244,7 @@ typedef struct {
     int32_t* flags;          /* [sum k + B] */
     int greedy;              /* 1: T = 0 verification (f1) */
     const double* temps;     /* [B] per-sequence temperature (f1) or NULL = 1; T_i == 0: greedy */
+    int resample;            /* recovery draw: 0 = D23 proposals from p, 1 = D7 inverse CDF (default) */
     int b0, b1;              /* sequence range for this worker */
     int status;
 } verify_job;
@@ -313,7 +331,7 @@ static int verify_one(verify_job* J, int i, double* t, double* d, double* w) {
     /* The draw of the final token uses u_smp of slot a (recovery at the
      * first rejected position, or the bonus position a == k) (D6). */
     const double u = J->u_smp[slot0 + a];
-    int tok;
+    int tok, stie = 0;
     double R = 0.0, lo = 0.0, hi = 0.0;
     if (greedy) {
         /* the target argmax of row a (recovery, a < k) or of the bonus row k */
@@ -324,15 +342,44 @@ static int verify_one(verify_job* J, int i, double* t, double* d, double* w) {
         load_row_t(t, J, J->tl, trow0 + a, J->ld_t, i);
         load_row_t(d, J, J->dl, (int64_t)base + a, J->ld_d, i);
         const double lt = row_lse(t, V), ld = row_lse(d, V);
-        for (int v = 0; v < V; ++v) {
-            const double pv = exp(t[v] - lt), qv = exp(d[v] - ld);
-            w[v] = pv - qv > 0.0 ? pv - qv : 0.0;   /* rho_v = max(0, p_v - q_v) */
+        int kept = 0;
+        tok = -1;
+        if (J->resample == 0) {
+            /* D23: propose v ~ p by the inverse CDF (D7) with u_prop of
+             * proposal j, keep it with probability max(0, p_v - q_v) / p_v
+             * (u_keep < that); the first kept proposal is the recovery token.
+             * A kept proposal is distributed as normalize(max(0, p - q))
+             * (P(v kept) = p_v max(0, p_v - q_v) / p_v). */
+            for (int v = 0; v < V; ++v) w[v] = exp(t[v] - lt);   /* p_v */
+            for (uint32_t j = 1; j <= OR_PROPOSALS && !kept; ++j) {
+                double up, uk;
+                oracle_proposal_uniforms(J->seeds[slot0 + a], j, &up, &uk);
+                const int v = inverse_cdf(w, V, up, &R, &lo, &hi);
+                if (v < 0) break;
+                if (fabs(up - lo) < 1e-6 || fabs(up - hi) < 1e-6) stie = 1;
+                const double pv = w[v], qv = exp(d[v] - ld);
+                const double keep = pv > qv ? (pv - qv) / pv : 0.0;
+                if (fabs(uk - keep) < 1e-6) stie = 1;
+                if (uk < keep) {
+                    tok = v;
+                    kept = 1;
+                }
+            }
+            if (!kept) J->flags[slot0 + a] |= OR_FLAG_PROPOSAL_FALLBACK;
         }
-        tok = inverse_cdf(w, V, u, &R, &lo, &hi);
-        if (tok < 0) { /* R == 0: fall back to p (D7) */
-            for (int v = 0; v < V; ++v) w[v] = exp(t[v] - lt);
+        if (!kept) {
+            /* D7: inverse CDF over rho_v = max(0, p_v - q_v) with u_smp */
+            for (int v = 0; v < V; ++v) {
+                const double pv = exp(t[v] - lt), qv = exp(d[v] - ld);
+                w[v] = pv - qv > 0.0 ? pv - qv : 0.0;
+            }
             tok = inverse_cdf(w, V, u, &R, &lo, &hi);
-            J->flags[slot0 + a] |= OR_FLAG_FALLBACK;
+            if (tok < 0) { /* R == 0: fall back to p (D7) */
+                for (int v = 0; v < V; ++v) w[v] = exp(t[v] - lt);
+                tok = inverse_cdf(w, V, u, &R, &lo, &hi);
+                J->flags[slot0 + a] |= OR_FLAG_FALLBACK;
+            }
+            if (fabs(u - lo) < 1e-6 || fabs(u - hi) < 1e-6) stie = 1;
         }
     } else {
         load_row_t(t, J, J->tl, trow0 + k, J->ld_t, i);
@@ -340,8 +387,9 @@ static int verify_one(verify_job* J, int i, double* t, double* d, double* w) {
         const double lt = row_lse(t, V);
         for (int v = 0; v < V; ++v) w[v] = exp(t[v] - lt);  /* p_v */
         tok = inverse_cdf(w, V, u, &R, &lo, &hi);
+        if (fabs(u - lo) < 1e-6 || fabs(u - hi) < 1e-6) stie = 1;
     }
-    if (!greedy && (fabs(u - lo) < 1e-6 || fabs(u - hi) < 1e-6)) J->flags[slot0 + a] |= OR_FLAG_SAMPLE_TIE;
+    if (stie) J->flags[slot0 + a] |= OR_FLAG_SAMPLE_TIE;
     J->samp_diag[3 * i + 0] = R;
     J->samp_diag[3 * i + 1] = lo;
     J->samp_diag[3 * i + 2] = hi;
@@ -368,6 +416,8 @@ static void* verify_worker(void* arg) {
 }
 
 /* Batched verify over B sequences with ragged k_i (Ragged Q).
+ * resample selects the recovery draw's reading: 0 = D23 (proposals from p),
+ * 1 = D7 (inverse CDF over max(0, p - q), the default).
  * Layout: draft row of (i,j) = cu_sl[i]+j; target row of (i,j) =
  * cu_sl[i]+i+j for j in [0,k_i]; per-slot outputs (emitted, u_acc, u_smp,
  * flags) use the target-row index. nthreads <= 1 runs serially.
@@ -377,8 +427,9 @@ OR_EXPORT int oracle_verify_temp(int B, int V, int dtype, const int32_t* cu_sl,
                                  const void* draft_logits, int64_t ld_d, const uint64_t* seeds,
                                  int32_t* accepted_len, int32_t* emitted, double* kld,
                                  double* log_ratio, double* u_acc, double* u_smp, double* samp_diag,
-                                 int32_t* flags, int nthreads, int greedy, const double* temps) {
-    if (B < 1 || V < 2 || (dtype != 0 && dtype != 1)) return -1;
+                                 int32_t* flags, int nthreads, int greedy, const double* temps,
+                                 int resample) {
+    if (B < 1 || V < 2 || (dtype != 0 && dtype != 1) || (resample != 0 && resample != 1)) return -1;
     if (nthreads < 1) nthreads = 1;
     if (nthreads > B) nthreads = B;
     verify_job* jobs = (verify_job*)calloc((size_t)nthreads, sizeof(verify_job));
@@ -409,6 +460,7 @@ OR_EXPORT int oracle_verify_temp(int B, int V, int dtype, const int32_t* cu_sl,
         J->flags = flags;
         J->greedy = greedy;
         J->temps = temps;
+        J->resample = resample;
         J->b0 = (int)((int64_t)B * n / nthreads);
         J->b1 = (int)((int64_t)B * (n + 1) / nthreads);
     }
@@ -435,7 +487,7 @@ OR_EXPORT int oracle_verify_mode(int B, int V, int dtype, const int32_t* cu_sl,
                                  int32_t* flags, int nthreads, int greedy) {
     return oracle_verify_temp(B, V, dtype, cu_sl, draft_tokens, target_logits, ld_t, draft_logits, ld_d,
                               seeds, accepted_len, emitted, kld, log_ratio, u_acc, u_smp, samp_diag, flags,
-                              nthreads, greedy, NULL);
+                              nthreads, greedy, NULL, 1);
 }
 
 /* The rejection-sampling verification (the default, C1). */

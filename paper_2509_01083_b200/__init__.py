@@ -25,7 +25,8 @@ DSDE_F32, DSDE_BF16 = 0, 1
 DSDE_PAD = -1
 DSDE_MAX_SL = 16
 DSDE_MAX_WINDOW = 64
-FLAG_ACCEPT_NEAR_TIE, FLAG_SAMPLE_NEAR_TIE, FLAG_FALLBACK = 1, 2, 4
+FLAG_ACCEPT_NEAR_TIE, FLAG_SAMPLE_NEAR_TIE, FLAG_FALLBACK, FLAG_PROPOSAL_FALLBACK = 1, 2, 4, 8
+RESAMPLE_PROPOSAL, RESAMPLE_FULL = 0, 1  # dsde_config.resample (D23 / D7)
 DERR = {0: "none", 1: "bad_sl", 2: "bad_token", 3: "nonfinite", 4: "rows", 5: "bad_slot", 6: "vp_fallback"}
 
 # Every function the header declares (checked against include/dsde.h by the tests).
@@ -55,7 +56,8 @@ class Config(C.Structure):
                 ("sl_min", C.c_int), ("sl_ceiling", C.c_int), ("epsilon", C.c_double),
                 ("calib_steps", C.c_int), ("calib_sl", C.c_int), ("window_unit", C.c_int),
                 ("cap_mode", C.c_int), ("greedy", C.c_int), ("device_rows", C.c_int),
-                ("masked", C.c_int), ("entropy_mode", C.c_int), ("entropy_gamma", C.c_double)]
+                ("masked", C.c_int), ("entropy_mode", C.c_int), ("entropy_gamma", C.c_double),
+                ("resample", C.c_int)]
 
     @classmethod
     def default(cls, **kw) -> "Config":

@@ -27,6 +27,7 @@ bool cfg_valid(const dsde_config& c) {
          c.calib_sl >= 1 && c.calib_sl <= c.sl_ceiling && (c.window_unit == 0 || c.window_unit == 1) &&
          (c.cap_mode == 0 || c.cap_mode == 1) && (c.greedy == 0 || c.greedy == 1) &&
          (c.device_rows == 0 || c.device_rows == 1) && (c.masked == 0 || c.masked == 1) &&
+         (c.resample == DSDE_RESAMPLE_PROPOSAL || c.resample == DSDE_RESAMPLE_FULL) &&
          (c.entropy_mode == 0 || c.entropy_mode == 1) && c.entropy_gamma > 0.0;
 }
 
@@ -128,6 +129,7 @@ void dsde_config_default(dsde_config* c) {
   c->greedy = 0;
   c->device_rows = 0;
   c->masked = 0;
+  c->resample = DSDE_RESAMPLE_FULL;
   c->entropy_mode = 0;
   c->entropy_gamma = 0.5;
 }

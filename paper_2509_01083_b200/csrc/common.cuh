@@ -35,8 +35,10 @@ struct Uniforms {
   double acc, smp;
 };
 
-__device__ __forceinline__ Uniforms philox_uniforms(uint64_t seed) {
-  uint32_t c0 = 0u, c1 = 0u, c2 = 0u, c3 = 0u;
+// ctr0: the counter's first word — 0 for D6's (u_acc, u_smp); j >= 1 for the
+// (u_prop, u_keep) of recovery-draw proposal j (D23).
+__device__ __forceinline__ Uniforms philox_uniforms(uint64_t seed, uint32_t ctr0 = 0u) {
+  uint32_t c0 = ctr0, c1 = 0u, c2 = 0u, c3 = 0u;
   uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
 #pragma unroll
   for (int r = 0; r < 10; ++r) {

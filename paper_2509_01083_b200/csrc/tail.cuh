@@ -29,6 +29,7 @@ struct TailArgs {
   int no_draw;   // vocab-parallel finalize: stop after the layout, the draw record to fa.rec[i]
   SignalArgs sig;
   CapArgs cap;
+  int proposal;  // D23 recovery draws (dsde_config.resample = DSDE_RESAMPLE_PROPOSAL, sampling)
 };
 
 __device__ __forceinline__ int atomic_add_acq_rel(int* p, int v) {
@@ -69,6 +70,139 @@ __device__ __forceinline__ void tail_stamp(int k) {
 #define TAIL_STAMP(k) do {} while (0)
 #endif
 
+// D23's first proposal of a rejected draft row, by the row's finalize warp
+// right after its finalize (speculative: the row is the recovery row only if
+// no earlier row was rejected). Returns the kept token or -1; *fl gets its
+// tie flags.
+template <typename T>
+__device__ __forceinline__ int first_proposal(const FinArgs& a, const PCdf& cdf, long long slot, long long drow_i,
+                                              float invT, double C, double lam, uint8_t* fl) {
+  const T* trow = reinterpret_cast<const T*>(a.tl) + slot * a.ld_t;
+  const T* drow = reinterpret_cast<const T*>(a.dl) + drow_i * a.ld_d;
+  const Uniforms U = philox_uniforms(__ldg(a.seeds + slot), 1u);  // (u_prop, u_keep) of proposal 1
+  const PSel sel = p_select<T>(cdf, a.nsub, trow, a.V, invT, U.acc);
+  int kept = 0;
+  uint8_t f = sel.fl;
+  if ((threadIdx.x & 31) == 0 && sel.tok >= 0) {
+    const double z = ((double)sel.t - (double)load_logit<T>(drow + sel.tok)) * (double)invT - C + lam;
+    const double keep = z > 0.0 ? -expm1(-z) : 0.0;  // max(0, p - q) / p at the proposal
+    kept = U.smp < keep;
+    if (fabs(U.smp - keep) < 1e-6) f |= DSDE_FLAG_SAMPLE_NEAR_TIE;
+  }
+  kept = __shfl_sync(kFull, kept, 0);
+  *fl = (uint8_t)__shfl_sync(kFull, (int)f, 0);
+  return kept ? sel.tok : -1;
+}
+
+// p's CDF of a sequence's draft rows on the D23 path, built during the
+// finalize (k_tail phase 1) by each row's finalize warp when the row has at
+// most kSpecSub stream slices, with the row's first proposal when the row
+// rejects its draft token (speculative: it is the recovery row only if no
+// earlier row rejected).
+constexpr int kSpecSub = 64;
+struct SpecRows {
+  double pre[DSDE_MAX_SL][kSpecSub];
+  float ml2[DSDE_MAX_SL][kSpecSub];
+  double cdf[DSDE_MAX_SL][2];  // Mr, P
+  int tok[DSDE_MAX_SL];        // the kept first proposal, or -1
+  uint8_t fl[DSDE_MAX_SL];
+};
+
+// a4 on the D23 path (p.proposal), a recovery draw (CTA-uniform result
+// through *s_placed): p's CDF over the drawn row's stream slices (its draft
+// row's partials) comes from the finalize's speculation (sp != NULL) or is
+// built here by warp 0 into pre / ml2 (shared memory, or the workspace beyond
+// kTailMaxSub slices); then proposals v_j ~ p (u_prop of proposal j), each
+// kept iff u_keep < max(0, p_v - q_v) / p_v = -expm1(-z_v), z_v = log p_v/q_v
+// = (t_v - d_v) / T - C + lam (the finalize's frame, in fp64): the speculative
+// first proposal, then rounds of nwp proposals in parallel (one per warp; the
+// signal warp of dsde_step is busy); the first kept j wins. *s_placed = 0 when
+// the D7 draw must decide: no proposal kept in DSDE_RESAMPLE_PROPOSALS
+// (flagged), or not a recovery draw (the bonus row is drawn by the D7 passes).
+template <typename T, int NW>
+__device__ void tail_p_draw(const TailArgs& p, int i, int aa, const SeqRec& r, const SpecRows* sp, double* pre,
+                            float* ml2, double* s_cdf, int* s_ptok, uint8_t* s_pfl, int* s_placed) {
+  const FinArgs& a = p.fa;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) *s_placed = 0;
+  if (r.mode != MODE_RESIDUAL) return;
+  const T* trow = reinterpret_cast<const T*>(a.tl) + r.trow * a.ld_t;
+  uint8_t fl = sp ? sp->fl[aa] : 0;
+  int tok = sp ? sp->tok[aa] : -1;  // the speculative first proposal
+  if (tok >= 0) {
+    if (threadIdx.x == 0) {
+      a.emitted[r.slot] = tok;
+      if (a.flags) a.flags[r.slot] |= fl;
+      *s_placed = 1;
+      if (i == (int)blockIdx.x) TAIL_STAMP(4);
+    }
+    return;
+  }
+  // the proposal warps synchronise among themselves (named barrier 1): the
+  // signal warp of dsde_step runs concurrently and joins at the sequence's end
+  const int nwp = NW - (p.step ? 1 : 0);
+  if (warp >= nwp) return;  // the signal warp
+  auto pbar = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(nwp * 32) : "memory"); };
+  if (!sp) {
+    if (warp == 0) {
+      double Mr;
+      const double P = pcdf_build(PRow{reinterpret_cast<const float*>(a.part + r.drow * a.nsub), 8, 3}, a.nsub, pre,
+                                  ml2, &Mr);
+      if (lane == 0) {
+        s_cdf[0] = Mr;
+        s_cdf[1] = P;
+      }
+    }
+    pbar();
+  }
+  const PCdf cdf = sp ? PCdf{const_cast<double*>(sp->pre[aa]), const_cast<float*>(sp->ml2[aa]), sp->cdf[aa][0],
+                             sp->cdf[aa][1]}
+                      : PCdf{pre, ml2, s_cdf[0], s_cdf[1]};
+  const T* drow = reinterpret_cast<const T*>(a.dl) + r.drow * a.ld_d;
+  const uint64_t seed = __ldg(a.seeds + r.slot);
+  int j0_end = 0;
+  for (int j0 = sp ? 2 : 1; j0 <= DSDE_RESAMPLE_PROPOSALS; j0 += nwp) {
+    j0_end = j0;
+    if (j0 + warp <= DSDE_RESAMPLE_PROPOSALS) {
+      const Uniforms U = philox_uniforms(seed, (uint32_t)(j0 + warp));  // (u_prop, u_keep)
+      const PSel sel = p_select<T>(cdf, a.nsub, trow, a.V, r.invT, U.acc);
+      if (lane == 0) {
+        int kept = 0;
+        uint8_t f = sel.fl;
+        if (sel.tok >= 0) {
+          const double z = ((double)sel.t - (double)load_logit<T>(drow + sel.tok)) * (double)r.invT - r.C + r.lam;
+          const double keep = z > 0.0 ? -expm1(-z) : 0.0;  // max(0, p - q) / p at the proposal
+          kept = U.smp < keep;
+          if (fabs(U.smp - keep) < 1e-6) f |= DSDE_FLAG_SAMPLE_NEAR_TIE;
+        }
+        s_ptok[warp] = kept ? sel.tok : -1;
+        s_pfl[warp] = f;
+      }
+    }
+    pbar();
+    const int nr = min(nwp, DSDE_RESAMPLE_PROPOSALS + 1 - j0);
+    for (int w = 0; w < nr; ++w) {  // the round's first kept proposal (same in every thread)
+      fl |= s_pfl[w];
+      if (s_ptok[w] >= 0) {
+        tok = s_ptok[w];
+        break;
+      }
+    }
+    pbar();  // the records are rewritten by the next round
+    if (tok >= 0) break;
+  }
+  (void)j0_end;
+#if DSDE_TAIL_TRACE
+  if (threadIdx.x == 0 && i == (int)blockIdx.x && blockIdx.x < kTraceMax) g_tail_trace[blockIdx.x * 8 + 7] = j0_end;
+#endif
+  if (threadIdx.x == 0) {
+    if (tok >= 0) a.emitted[r.slot] = tok;
+    if (a.flags) a.flags[r.slot] |= fl | (tok >= 0 ? 0 : DSDE_FLAG_PROPOSAL_FALLBACK);
+    *s_placed = tok >= 0;
+  }
+  if (i == (int)blockIdx.x) TAIL_STAMP(4);
+}
+
 // draw slices per row whose records k_tail keeps in shared memory (V <= 262144
 // bf16 / 131072 fp32; larger vocabularies use the workspace)
 constexpr int kTailMaxSub = 256;
@@ -83,6 +217,11 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
   __shared__ int s_acc, s_bad;
   __shared__ double s_mass[kTailMaxSub], s_scale[kTailMaxSub];
   __shared__ float s_ref[kTailMaxSub], s_wmax[NW];
+  __shared__ int s_ptok[NW];
+  __shared__ uint8_t s_pfl[NW];
+  __shared__ double s_cdf[2];
+  __shared__ int s_placed;
+  __shared__ SpecRows s_sp;
   const bool smem = nd <= kTailMaxSub;
   // while the stream kernel drains: the batch check (cu_sl must be a
   // non-decreasing prefix from 0, else no row can be attributed to a sequence
@@ -130,9 +269,30 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
       continue;  // CTA-uniform
     }
     // 1. a2: row finalize, warp j -> draft row c0 + j
+    // D23 speculation (p.proposal): each finalize warp also builds its row's p
+    // CDF and, when the row rejects its draft token, evaluates the row's first
+    // proposal, so that the layout mostly finds the recovery token ready.
+    const bool spec = p.proposal && a.nsub <= kSpecSub && !seq_greedy(a, i);
     for (int j = warp; j < k; j += NW) {
       const RowRes rr = row_finalize<T>(a, c0 + j, i, (i == pre_i && j == warp) ? &pre : nullptr);
       if (lane == 0) s_rr[j] = rr;
+      if (spec) {
+        double Mr;
+        const double P = pcdf_build(PRow{reinterpret_cast<const float*>(a.part + (long long)(c0 + j) * a.nsub), 8, 3},
+                                    a.nsub, s_sp.pre[j], s_sp.ml2[j], &Mr);
+        __syncwarp();
+        int tk = -1;
+        uint8_t f = 0;
+        if ((rr.bits & RR_FINITE) && !(rr.bits & (RR_ACCEPT | RR_BADTOK)))
+          tk = first_proposal<T>(a, PCdf{s_sp.pre[j], s_sp.ml2[j], Mr, P}, (long long)c0 + i + j, (long long)c0 + j,
+                                 inv_temp(a.temps, i), rr.C, rr.lam, &f);
+        if (lane == 0) {
+          s_sp.cdf[j][0] = Mr;
+          s_sp.cdf[j][1] = P;
+          s_sp.tok[j] = tk;
+          s_sp.fl[j] = f;
+        }
+      }
     }
     __syncthreads();
     if (i == (int)blockIdx.x) TAIL_STAMP(2);
@@ -161,12 +321,31 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
       const double h = (p.sig.ent && lane < k && s_acc >= 0) ? (double)__ldcg(p.sig.ent + c0 + lane) : 0.0;
       tail_signal(p, i, k, x, s_acc, h);
     }
-    if (r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS || r.mode == MODE_ARGMAX) {
+    // D23: the recovery token by proposals from p (CTA-uniform);
+    // false: the D7 draw below (no proposal kept, or the D7 / greedy modes)
+    // (p's CDF in the draw records' space: shared memory, or the workspace
+    // beyond kTailMaxSub stream slices)
+    bool placed = false;
+    if (p.proposal) {
+      tail_p_draw<T, NW>(p, i, s_acc, r, spec ? &s_sp : nullptr, a.nsub <= kTailMaxSub ? s_mass : p.mass + (long long)i * nd,
+                         a.nsub <= kTailMaxSub ? s_ref : p.mref + (long long)i * nd, s_cdf, s_ptok, s_pfl, &s_placed);
+      __syncthreads();
+      placed = s_placed != 0;
+    }
+    if (!placed && (r.mode == MODE_RESIDUAL || r.mode == MODE_BONUS || r.mode == MODE_ARGMAX)) {
       const long long q0 = (long long)i * nd;
       double* gm = p.mass + q0;
       float* gr = p.mref + q0;
-      for (int u = warp; u < nd; u += NW)
-        draw_mass<T>(r, u, a.V, a.tl, a.ld_t, a.dl, a.ld_d, smem ? s_mass + u : gm + u, smem ? s_ref + u : gr + u);
+      if (r.mode == MODE_RESIDUAL) {
+        for (int u = warp; u < nd; u += NW)
+          draw_mass<T>(r, u, a.V, a.tl, a.ld_t, a.dl, a.ld_d, smem ? s_mass + u : gm + u, smem ? s_ref + u : gr + u);
+      } else {  // t-only rows: slices u and u + NW per iteration
+        for (int u = warp; u < nd; u += 2 * NW) {
+          const int u1 = u + NW;
+          draw_mass_t2<T>(r, u, u1, nd, a.V, a.tl, a.ld_t, smem ? s_mass + u : gm + u, smem ? s_ref + u : gr + u,
+                          smem ? s_mass + u1 : gm + u1, smem ? s_ref + u1 : gr + u1);
+        }
+      }
       __syncthreads();
       if (i == (int)blockIdx.x) TAIL_STAMP(4);
       // 4. a4 select (warp 0)

@@ -698,6 +698,7 @@ constexpr int kLdgThreads = 256;
 #define DSDE_EXPERIMENT 0
 #endif
 
+
 #ifndef DSDE_ENT_MINB
 #define DSDE_ENT_MINB 2
 #endif
@@ -811,7 +812,8 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
                           const uint64_t* seeds, int32_t* acc_len, int32_t* emitted, float* kld,
                           uint8_t* flags, const VerifyWs& ws, int32_t* err, Profiler* prof,
                           cudaStream_t s, const StepExtra* step = nullptr, int greedy = 0,
-                          int dev_rows = 0, float* ent = nullptr, const float* temps = nullptr, int masked = 0) {
+                          int dev_rows = 0, float* ent = nullptr, const float* temps = nullptr, int masked = 0,
+                          int resample = DSDE_RESAMPLE_FULL) {
   const bool pr = prof != nullptr && prof->on;
   auto mark = [&]() {
     if (pr) cudaEventRecord(prof->next(), s);
@@ -819,6 +821,8 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   const int ns = n_subs(V, sizeof(T) == 2 ? DSDE_BF16 : DSDE_F32);
   mark();
   // a1: the row stream (persistent warps; grid = resident CTAs)
+  // D23 recovery draws (dsde_config.resample = DSDE_RESAMPLE_PROPOSAL, sampling modes)
+  const bool proposal = resample == DSDE_RESAMPLE_PROPOSAL && !greedy;
   StreamArgs sa{tl, ld_t, dl, ld_d, cu_sl, B, V, ns, total, reinterpret_cast<SubPartial*>(ws.part), dev_rows,
                 ws.counters, temps};
   const int sms = sm_count();
@@ -848,6 +852,7 @@ cudaError_t launch_verify(int B, int V, int total, const int32_t* cu_sl, const i
   p.mass = ws.mass;
   p.mref = ws.mref;
   p.ctl = ws.counters;
+  p.proposal = proposal;
   if (step) {
     p.step = 1;
     p.fuse_cap = step->fuse_cap;
@@ -902,12 +907,12 @@ extern "C" dsde_status dsde_verify(int B, int V, dsde_dtype dtype, int total_dra
     e = launch_verify<uint16_t>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                                 draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld,
                                 flags, ws, st->err, st->prof, s, nullptr, st->cfg.greedy, st->cfg.device_rows,
-                                st->entropy_out, st->temps, st->cfg.masked);
+                                st->entropy_out, st->temps, st->cfg.masked, st->cfg.resample);
   else
     e = launch_verify<float>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                              draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld, flags,
                              ws, st->err, st->prof, s, nullptr, st->cfg.greedy, st->cfg.device_rows,
-                                st->entropy_out, st->temps, st->cfg.masked);
+                             st->entropy_out, st->temps, st->cfg.masked, st->cfg.resample);
   return e == cudaSuccess ? DSDE_OK : DSDE_ERR_CUDA;
 }
 
@@ -957,12 +962,12 @@ extern "C" dsde_status dsde_step(dsde_state st, int B, int V, dsde_dtype dtype, 
     e = launch_verify<uint16_t>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                                 draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld,
                                 flags, ws, st->err, st->prof, s, &x, st->cfg.greedy, st->cfg.device_rows,
-                                st->entropy_out, st->temps, st->cfg.masked);
+                                st->entropy_out, st->temps, st->cfg.masked, st->cfg.resample);
   else
     e = launch_verify<float>(B, V, total_draft_rows, cu_sl, draft_tokens, target_logits, ld_t,
                              draft_logits, ld_d, seeds, accepted_len, emitted_tokens, kld, flags,
                              ws, st->err, st->prof, s, &x, st->cfg.greedy, st->cfg.device_rows,
-                                st->entropy_out, st->temps, st->cfg.masked);
+                             st->entropy_out, st->temps, st->cfg.masked, st->cfg.resample);
   if (e != cudaSuccess) return DSDE_ERR_CUDA;
   if (!comm) return DSDE_OK;
   dsde_status rs = DSDE_OK;

@@ -666,16 +666,11 @@ __device__ __forceinline__ double warp_sum_vectors(double (&x)[NV]) {
 // of t and its first index instead.
 // ---------------------------------------------------------------------------
 template <typename T>
-__device__ __forceinline__ void draw_mass(const SeqRec& r, int u, int V, const void* tl, long long ld_t,
-                                          const void* dl, long long ld_d, double* mass_out, float* ref_out) {
+__device__ __forceinline__ void draw_mass_loaded(const SeqRec& r, const uint4 (&rt)[Traits<T>::NVD],
+                                                 const uint4 (&rd)[Traits<T>::NVD], double* mass_out, float* ref_out) {
   constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NVD;
   const int lane = threadIdx.x & 31;
   const int mode = r.mode;
-  if (mode != MODE_RESIDUAL && mode != MODE_BONUS && mode != MODE_ARGMAX) return;
-  const T* tp = reinterpret_cast<const T*>(tl) + r.trow * ld_t;
-  uint4 rt[NV], rd[NV];
-  load_vecs<T, NV>(tp, V, u, 0, rt);
-  if (mode == MODE_RESIDUAL) load_vecs<T, NV>(reinterpret_cast<const T*>(dl) + r.drow * ld_d, V, u, 0, rd);
   DrawRef R;
   if (mode != MODE_RESIDUAL) {
     // bonus / argmax: the slice max of t first (the reference of the weights)
@@ -721,6 +716,34 @@ __device__ __forceinline__ void draw_mass(const SeqRec& r, int u, int V, const v
     // select rescales by fl32(m invT), which is monotone in m)
     *ref_out = R.resid ? R.M : (R.m <= -1e30f ? -INFINITY : R.m);
   }
+}
+
+template <typename T>
+__device__ __forceinline__ void draw_mass(const SeqRec& r, int u, int V, const void* tl, long long ld_t,
+                                          const void* dl, long long ld_d, double* mass_out, float* ref_out) {
+  constexpr int NV = Traits<T>::NVD;
+  const int mode = r.mode;
+  if (mode != MODE_RESIDUAL && mode != MODE_BONUS && mode != MODE_ARGMAX) return;
+  const T* tp = reinterpret_cast<const T*>(tl) + r.trow * ld_t;
+  uint4 rt[NV], rd[NV];
+  load_vecs<T, NV>(tp, V, u, 0, rt);
+  if (mode == MODE_RESIDUAL) load_vecs<T, NV>(reinterpret_cast<const T*>(dl) + r.drow * ld_d, V, u, 0, rd);
+  draw_mass_loaded<T>(r, rt, rd, mass_out, ref_out);
+}
+
+// Bonus / argmax rows read only t: two draw slices (u0, and u1 < nd when
+// valid) per call with all their loads in flight at once (the per-warp loop is
+// latency-bound on one slice's 4 vectors).
+template <typename T>
+__device__ __forceinline__ void draw_mass_t2(const SeqRec& r, int u0, int u1, int nd, int V, const void* tl,
+                                             long long ld_t, double* m0, float* r0, double* m1, float* r1) {
+  constexpr int NV = Traits<T>::NVD;
+  const T* tp = reinterpret_cast<const T*>(tl) + r.trow * ld_t;
+  uint4 a0[NV], a1[NV];
+  load_vecs<T, NV>(tp, V, u0, 0, a0);
+  if (u1 < nd) load_vecs<T, NV>(tp, V, u1, 0, a1);
+  draw_mass_loaded<T>(r, a0, a0, m0, r0);
+  if (u1 < nd) draw_mass_loaded<T>(r, a1, a1, m1, r1);
 }
 
 // ---------------------------------------------------------------------------
@@ -969,6 +992,198 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
       if (a.flags) a.flags[r.slot] |= fl;
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// D23 path: p's statistics per stream slice of one target row — the draft
+// row's SubPartials (S at +0, M/T at +3, 8 floats per slice) or the streamed
+// bonus row's (S, M/T) pairs (2 floats per slice); written by the stream
+// kernel, read with ld.global.cg.
+// ---------------------------------------------------------------------------
+struct PRow {
+  const float* base;
+  int stride, moff;
+  __device__ __forceinline__ float S(int s) const { return __ldcg(base + (long long)s * stride); }
+  __device__ __forceinline__ float M(int s) const { return __ldcg(base + (long long)s * stride + moff); }
+};
+
+struct PSel {
+  int tok;     // -1: p's mass is not a finite positive number (non-finite row)
+  uint8_t fl;  // DSDE_FLAG_SAMPLE_NEAR_TIE when u is within 1e-6 of the token's CDF edges
+  float t;     // the token's logit (the proposal's accept test)
+};
+
+// lane vector v of stream slice u of a row (padding past V: weight exactly 0),
+// through L1 (p_select prefetched the slice there)
+template <typename T>
+__device__ __forceinline__ uint4 load_svec(const T* row, int V, int u, int v) {
+  constexpr int VEC = Traits<T>::VEC, SUB = sub_elems<T>();
+  const int e0 = u * SUB + (v * 32 + (threadIdx.x & 31)) * VEC;
+  if (e0 + VEC <= V) return __ldg(reinterpret_cast<const uint4*>(row + e0));
+  T b[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) b[e] = (e0 + e < V) ? row[e0 + e] : pad_bits<T>();
+  return *reinterpret_cast<const uint4*>(b);
+}
+
+// p's CDF over the stream slices of one row, shared by a CTA's warps: pre[s] =
+// sum_{s' <= s} e^(M'_s' - M') S_s' in fp64 (slice order), ml2[s] =
+// fl32(M_s/T log2 e) (the stream's exact base-2 reference, -inf: no mass),
+// Mr = M' (nats) and P = pre[nsub - 1].
+struct PCdf {
+  double* pre;
+  float* ml2;
+  double Mr, P;
+};
+
+// One warp builds the PCdf of a row from its streamed slice statistics (lanes
+// own contiguous slice spans; one fp64 warp scan). Returns P in every lane
+// (not a finite positive number: a non-finite row).
+__device__ __noinline__ double pcdf_build(const PRow src, int nsub, double* pre, float* ml2, double* Mr_out) {
+  const int lane = threadIdx.x & 31;
+  float Mg = -INFINITY;
+  for (int s0 = lane; s0 < nsub; s0 += 32) Mg = max_nan(Mg, src.M(s0));
+  Mg = warp_max_nan(Mg);
+  const double Mr = ref_nats(Mg);
+  const int cw = (nsub + 31) >> 5;
+  const int s_lo = min(lane * cw, nsub), s_hi = min(s_lo + cw, nsub);
+  double lsum = 0.0;
+  for (int s0 = s_lo; s0 < s_hi; ++s0) {  // the masses (pre[] holds them until the scan)
+    const float m = src.M(s0);
+    const double ms = m != -INFINITY ? exp(ref_nats(m) - Mr) * (double)src.S(s0) : 0.0;
+    pre[s0] = ms;
+    ml2[s0] = m == -INFINITY ? -INFINITY : __fmul_rn(m, kLog2e);
+    lsum += ms;
+  }
+  const double lincl = wscan_d(lsum, lane);
+  double cum = lincl - lsum;
+  for (int s0 = s_lo; s0 < s_hi; ++s0) {
+    cum += pre[s0];
+    pre[s0] = cum;
+  }
+  *Mr_out = Mg != Mg ? (double)NAN : Mr;
+  return __shfl_sync(kFull, lincl, 31);
+}
+
+// One warp: p's inverse CDF (D7 applied to p, at the sequence's temperature)
+// from a PCdf: the crossing slice (first s with mass and pre[s] > u P), its
+// NV vectors prefetched at once, then per vector the weights
+// e_v = 2^(t_v L2s - ml2[s]) (bit-identical to the stream's), an fp64 warp
+// scan of the lane sums, and the smallest token with C_v > u P in ascending
+// token order. Rounding
+// corners (u P within rounding of a slice total) take the last positive-weight
+// token and are flagged.
+template <typename T>
+__device__ __noinline__ PSel p_select(const PCdf c, int nsub, const T* trow, int V, float invT, double u) {
+  constexpr int VEC = Traits<T>::VEC, NV = Traits<T>::NV, SUB = sub_elems<T>();
+  const int lane = threadIdx.x & 31;
+  PSel out{-1, 0, 0.f};
+  const double P = c.P;
+  if (!(P > 0.0) || !isfinite(P) || c.Mr != c.Mr) return out;
+  const double target = u * P;
+  int us = -1;
+  for (int s0 = 0; s0 < nsub && us < 0; s0 += 32) {
+    const int sl = s0 + lane;
+    const double prev = sl == 0 ? 0.0 : sl < nsub ? c.pre[sl - 1] : 0.0;
+    const bool cross = sl < nsub && c.pre[sl] > prev && c.pre[sl] > target;
+    const unsigned b = __ballot_sync(kFull, cross);
+    if (b) us = s0 + __ffs(b) - 1;
+  }
+  if (us < 0) {  // rounding corner: the last slice with mass
+    out.fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
+    for (int s0 = ((nsub - 1) & ~31); s0 >= 0 && us < 0; s0 -= 32) {
+      const int sl = s0 + lane;
+      const double prev = sl == 0 ? 0.0 : sl < nsub ? c.pre[sl - 1] : 0.0;
+      const unsigned b = __ballot_sync(kFull, sl < nsub && c.pre[sl] > prev);
+      if (b) us = s0 + 31 - __clz(b);
+    }
+    if (us < 0) return out;
+  }
+  const double base = us == 0 ? 0.0 : c.pre[us - 1];
+  const float ML2 = c.ml2[us], l2 = __fmul_rn(kLog2e, invT);
+  const double f = exp((double)ML2 * kLn2d - c.Mr);
+  // the slice's NV vectors requested at once (into L1), then scanned one vector
+  // at a time in a rolled loop: this code runs once per draw, cold, so its
+  // size (instruction fetch) costs more than its arithmetic
+  {
+    const int e0 = us * SUB + (threadIdx.x & 31) * VEC;
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      if (e0 + v * 32 * VEC + VEC <= V) asm volatile("prefetch.global.L1 [%0];" ::"l"(trow + e0 + v * 32 * VEC));
+  }
+  int tok = -1, last_pos = -1;
+  double lo = 0.0, hi = 0.0, lp_lo = 0.0, lp_hi = 0.0, vbase = base;
+  float tk = 0.f, lpt = 0.f;
+#pragma unroll 1
+  for (int v = 0; v < NV; ++v) {
+    const uint4 xv[1] = {load_svec<T>(trow, V, us, v)};
+    float wv[VEC], tv[VEC];
+#pragma unroll
+    for (int h = 0; h < VEC; h += 2) {
+      const float2 tt = pair_of<T>(xv, h);
+      tv[h] = tt.x;
+      tv[h + 1] = tt.y;
+      wv[h] = fast_exp2(__fmaf_rn(tt.x, l2, -ML2));
+      wv[h + 1] = fast_exp2(__fmaf_rn(tt.y, l2, -ML2));
+    }
+    float ls = 0.f;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) ls += wv[e];
+    const double incl = wscan_d((double)ls, lane);
+    const double pre = vbase + f * (incl - (double)ls);
+    int cand = -1, lpos = -1;
+    double clo = 0.0, chi = 0.0, llo = 0.0, lhi = 0.0;
+    float ct = 0.f, lt = 0.f, run = 0.f;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const float before = run;
+      run += wv[e];
+      const double cb = pre + f * (double)before, ca = pre + f * (double)run;
+      if (cand < 0 && wv[e] > 0.f && ca > target) {
+        cand = e;
+        clo = cb;
+        chi = ca;
+        ct = tv[e];
+      }
+      if (wv[e] > 0.f) {
+        lpos = e;
+        llo = cb;
+        lhi = ca;
+        lt = tv[e];
+      }
+    }
+    const int tok_base = us * SUB + v * 32 * VEC;
+    const unsigned bc = __ballot_sync(kFull, cand >= 0);
+    if (bc) {
+      const int lc = __ffs(bc) - 1;
+      tok = tok_base + lc * VEC + __shfl_sync(kFull, cand, lc);
+      lo = __shfl_sync(kFull, clo, lc);
+      hi = __shfl_sync(kFull, chi, lc);
+      tk = __shfl_sync(kFull, ct, lc);
+      break;
+    }
+    const unsigned bp = __ballot_sync(kFull, lpos >= 0);
+    if (bp) {
+      const int lp = 31 - __clz(bp);
+      last_pos = tok_base + lp * VEC + __shfl_sync(kFull, lpos, lp);
+      lp_lo = __shfl_sync(kFull, llo, lp);
+      lp_hi = __shfl_sync(kFull, lhi, lp);
+      lpt = __shfl_sync(kFull, lt, lp);
+    }
+    vbase += f * __shfl_sync(kFull, incl, 31);
+  }
+  if (tok < 0) {  // rounding corner: u P within rounding of the slice total
+    tok = last_pos;
+    lo = lp_lo;
+    hi = lp_hi;
+    tk = lpt;
+    out.fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
+    if (tok < 0) return out;
+  }
+  out.tok = tok;
+  out.t = tk;
+  if (fabs(u - lo / P) < 1e-6 || fabs(u - hi / P) < 1e-6) out.fl |= DSDE_FLAG_SAMPLE_NEAR_TIE;
+  return out;
 }
 
 __device__ __forceinline__ SeqRec load_seqrec(const SeqRec* p) {

@@ -25,8 +25,9 @@
 // The shard boundaries are slice boundaries, so every partial and mass is
 // bit-identical to the unsharded pass's, and stages 2 and 4 read them in the
 // unsharded order: the outputs are bit-identical to dsde_verify's.
-// Supported: the default sampling mode (no greedy, no temperature, no masks,
-// no draft entropy, no device_rows): DSDE_ERR_ARG otherwise.
+// Supported: sampling at T = 1 with the D7 recovery draw (dsde_config.resample
+// = DSDE_RESAMPLE_FULL; no greedy, no temperature, no masks, no draft entropy,
+// no device_rows): DSDE_ERR_ARG otherwise.
 
 namespace dsde {
 
@@ -157,7 +158,8 @@ dsde_status vp_shape(int V, int nshards, int shard, dsde_dtype dt, VpShape* o) {
   return DSDE_OK;
 }
 bool vp_mode_ok(dsde_state st) {
-  return st && !st->cfg.greedy && !st->cfg.masked && !st->cfg.device_rows && !st->temps && !st->entropy_out;
+  return st && !st->cfg.greedy && !st->cfg.masked && !st->cfg.device_rows && !st->temps && !st->entropy_out &&
+         st->cfg.resample == DSDE_RESAMPLE_FULL;
 }
 }  // namespace
 

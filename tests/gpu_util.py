@@ -60,10 +60,10 @@ def gpu_verify(m, state, dev: dict, with_flags=True):
             flags.cpu().numpy() if flags is not None else None)
 
 
-def oracle_verify(host: dict, nthreads: int = 8):
+def oracle_verify(host: dict, nthreads: int = 8, resample: int = oracle.RESAMPLE_FULL):
     dt = oracle.BF16 if host["target"].dtype == np.uint16 else oracle.F32
     return oracle.verify(host["cu_sl"], host["draft_tokens"], host["target"], host["draft"],
-                         host["seeds"], dt, nthreads=nthreads)
+                         host["seeds"], dt, nthreads=nthreads, resample=resample)
 
 
 def make_host_batch(V, k, seed, dtype=torch.bfloat16, profiles=("code",), step=0):

@@ -4,7 +4,8 @@ Bands (from BASELINE.json north_star and SURVEY §8(c) D16):
 * KLD:           |KL_gpu - KL_o| <= 1e-5 |KL_o| + 1e-9            (fp64 oracle)
 * accept ties:   a_gpu != a_o only if |u_acc - min(1, r_o)| < 1e-6 at j = min(a_gpu, a_o)
 * sample ties:   token_gpu != token_o only if |u_smp - C/R| < 1e-6 at an edge of
-                 the oracle's token (C_{v-1}/R or C_v/R)
+                 the oracle's token (C_{v-1}/R or C_v/R), or (D23 recovery draws)
+                 a proposal's |u_prop - C/P| or |u_keep - max(0, p - q)/p| < 1e-6
 * everything else (accepted lengths, emitted tokens, pads) bit-exact.
 Ties are counted and returned, never silently ignored.
 """
@@ -84,7 +85,11 @@ def compare_verify(cu, acc_g, emit_g, kld_g, o, seq_ids=None) -> Report:
         if eg[ag] != eo[ao]:
             R, lo, hi = o.samp_diag[i]
             u = o.u_smp[s0 + ao]
-            if abs(u - lo) < TIE or abs(u - hi) < TIE:
+            # the oracle flags a sample tie for any uniform it drew within 1e-6 of
+            # a decision edge: the D7 draw's u_smp at a CDF edge, or (D23) a
+            # proposal's u_prop at a CDF edge of p / its u_keep at the keep
+            # probability
+            if (o.flags[s0 + ao] & 2) or abs(u - lo) < TIE or abs(u - hi) < TIE:
                 rep.sample_ties += 1
                 continue
             rep.mismatches.append(("token", sid, int(eg[ag]), int(eo[ao]), float(u), float(lo), float(hi)))

@@ -47,7 +47,8 @@ def test_config_defaults_match_paper(dsde):
     assert (c.delta, c.n_short, c.n_long, c.sl_min, c.epsilon) == (0.85, 10, 30, 2, 1e-6)
     assert (c.sl_ceiling, c.calib_steps, c.calib_sl, c.window_unit, c.cap_mode) == (8, 5, 4, 0, 1)
     assert (c.masked, c.entropy_mode, c.entropy_gamma, c.greedy, c.device_rows) == (0, 0, 0.5, 0, 0)
-    assert dsde.lib().dsde_abi_version() == 3
+    assert c.resample == dsde.RESAMPLE_FULL   # the D7 recovery draw by default
+    assert dsde.lib().dsde_abi_version() == 4
     assert dsde.lib().dsde_status_string(-1) == b"DSDE_ERR_ARG"
 
 
@@ -65,6 +66,8 @@ def test_invalid_args_rejected_without_launch(dsde):
     L = dsde.lib()
     h = C.c_void_p()
     bad = dsde.Config.default(n_short=30)
+    assert L.dsde_state_create(C.byref(bad), 4, C.byref(h)) == dsde.DSDE_ERR_ARG
+    bad = dsde.Config.default(resample=2)
     assert L.dsde_state_create(C.byref(bad), 4, C.byref(h)) == dsde.DSDE_ERR_ARG
     assert L.dsde_verify(0, 10, 1, 0, None, None, None, 10, None, 10, None, None, None, None,
                          None, None, 0, None, None) == dsde.DSDE_ERR_ARG

@@ -51,7 +51,7 @@ def device_subset(s, ids):
                 seeds=np.concatenate([seeds[cu[i] + i:cu[i] + i + ki + 1] for i, ki in zip(ids, k)]))
 
 
-def compare_all(s, out, chunk=256):
+def compare_all(s, out, chunk=256, resample=oracle.RESAMPLE_FULL):
     """Every sequence of the step against the oracle, in chunks of sequences.
     Returns the merged report and the oracle's accepted lengths / KLDs."""
     B = s.cu_sl.numel() - 1
@@ -61,21 +61,26 @@ def compare_all(s, out, chunk=256):
     for c0 in range(0, B, chunk):
         ids = np.arange(c0, min(B, c0 + chunk))
         sub = device_subset(s, ids)
-        o = oracle_verify(sub, nthreads=16)
+        o = oracle_verify(sub, nthreads=16, resample=resample)
         a2, e2, k2 = parity.gather_subset_outputs(cu, ids, acc, em, kl)
         r = parity.compare_verify(sub["cu_sl"], a2, e2, k2, o, seq_ids=ids)
         rep.merge(r)
     return rep
 
 
-@pytest.mark.parametrize("B,profiles,steps,V", [
-    (256, ("code",), 3, V),                        # config 3 (and config 5's per-GPU shard at 8 GPUs)
-    (512, ("low",), 3, V),                         # config 4: low acceptance, residual-heavy
-    (2048, ("code", "dialogue", "low"), 2, V),     # config 5's whole batch on one GPU
-    (64, ("low",), 2, 256000),                     # Gemma-like vocabulary
-], ids=["cfg3_B256", "cfg4_B512", "cfg5_B2048", "gemma_V256000_B64"])
-def test_dsde_step_full_size_every_sequence(m, B, profiles, steps, V):
-    cfg_g = m.Config.default(calib_steps=1, calib_sl=4)
+@pytest.mark.parametrize("B,profiles,steps,V,resample", [
+    (256, ("code",), 3, V, 1),                     # config 3 (and config 5's per-GPU shard at 8 GPUs)
+    (512, ("low",), 3, V, 1),                      # config 4: low acceptance, residual-heavy
+    (2048, ("code", "dialogue", "low"), 2, V, 1),  # config 5's whole batch on one GPU
+    (64, ("low",), 2, 256000, 1),                  # Gemma-like vocabulary
+    (256, ("code",), 2, V, 0),                     # the D23 recovery draw (speculative first proposal)
+    (512, ("low",), 2, V, 0),
+    (2048, ("code", "dialogue", "low"), 1, V, 0),  # 8-warp tail CTAs, several rounds per CTA
+    (64, ("low",), 2, 256000, 0),                  # > kSpecSub slices: proposals built at draw time
+], ids=["cfg3_B256", "cfg4_B512", "cfg5_B2048", "gemma_V256000_B64",
+        "cfg3_B256_d23", "cfg4_B512_d23", "cfg5_B2048_d23", "gemma_V256000_B64_d23"])
+def test_dsde_step_full_size_every_sequence(m, B, profiles, steps, V, resample):
+    cfg_g = m.Config.default(calib_steps=1, calib_sl=4, resample=resample)
     cfg_o = oracle.Config(calib_steps=1, calib_sl=4)
     st = m.State(cfg_g, B)
     ost = oracle.OracleState(cfg_o, B)
@@ -88,7 +93,7 @@ def test_dsde_step_full_size_every_sequence(m, B, profiles, steps, V):
         s = synth.generate_step(w, step + 40, k, device="cuda")
         out = stepper(s.cu_sl, s.draft_tokens, s.target, s.draft, s.seeds, int(k.sum()))
         torch.cuda.synchronize()
-        rep = compare_all(s, out)
+        rep = compare_all(s, out, resample=resample)
         assert rep.ok(), (step, str(rep))
         total.merge(rep)
         # the GPU's own KLDs / accepted lengths into the oracle signal + cap (identical inputs)

@@ -86,11 +86,11 @@ def _masked_host(V, k, seed, mode, keep, dtype=torch.bfloat16, profiles=("code",
     return _redraw_tokens(h, temps, rng)
 
 
-def _oracle(host, temps=None, greedy=False):
+def _oracle(host, temps=None, greedy=False, resample=oracle.RESAMPLE_FULL):
     dt = oracle.BF16 if host["target"].dtype == np.uint16 else oracle.F32
     return oracle.verify(host["cu_sl"], host["draft_tokens"], host["target"], host["draft"], host["seeds"],
                          dt, nthreads=8, greedy=greedy,
-                         temperature=None if temps is None else np.asarray(temps, np.float64))
+                         temperature=None if temps is None else np.asarray(temps, np.float64), resample=resample)
 
 
 def _check(m, st, host, dtype, temps=None):
@@ -99,7 +99,7 @@ def _check(m, st, host, dtype, temps=None):
     st.set_temperature(tt)
     acc, em, kl, _ = gpu_verify(m, st, dev)
     st.set_temperature(None)
-    o = _oracle(host, temps)
+    o = _oracle(host, temps, resample=st.cfg.resample)
     rep = parity.compare_verify(host["cu_sl"], acc, em, kl, o)
     assert rep.ok(), str(rep)
     assert st.device_error() == (0, -1)
@@ -113,8 +113,9 @@ TEMPS = np.float32([0.0, 0.4, 0.7, 1.0, 1.3, 2.0])
     (32000, torch.bfloat16, 8, 64), (8193, torch.float32, 6, 40), (128256, torch.bfloat16, 8, 12),
     (1003, torch.bfloat16, 3, 30),
 ])
-def test_temperature_parity(m, V, dtype, kmax, B):
-    st = m.State(m.Config.default(), 4096)
+@pytest.mark.parametrize("resample", [1, 0])
+def test_temperature_parity(m, V, dtype, kmax, B, resample):
+    st = m.State(m.Config.default(resample=resample), 4096)
     k = synth.random_k(B, kmax, V % 97)
     temps = np.random.default_rng(V).choice(TEMPS, B)
     host = _redraw_tokens(make_host_batch(V, k, 5 + V % 13, dtype=dtype, profiles=("code", "dialogue")), temps,
@@ -139,9 +140,9 @@ def test_temperature_one_is_bit_identical(m):
 @pytest.mark.parametrize("mode", ["same", "target", "draft", "both"])
 @pytest.mark.parametrize("V,dtype,keep", [(32000, torch.bfloat16, 40), (8193, torch.float32, 500),
                                           (128256, torch.bfloat16, 2000)])
-@pytest.mark.parametrize("with_temp", [False, True])
-def test_masked_parity(m, mode, V, dtype, keep, with_temp):
-    st = m.State(m.Config.default(masked=1), 4096)
+@pytest.mark.parametrize("with_temp,resample", [(False, 1), (True, 1), (True, 0)])
+def test_masked_parity(m, mode, V, dtype, keep, with_temp, resample):
+    st = m.State(m.Config.default(masked=1, resample=resample), 4096)
     B = 24 if V > 100000 else 48
     k = synth.random_k(B, 6, len(mode) + V % 7)
     temps = np.random.default_rng(B + len(mode)).choice(TEMPS, B) if with_temp else None
@@ -162,11 +163,12 @@ def test_masked_config_matches_plain_path_without_masks(m):
     assert np.all(np.abs(a[2] - b[2]) <= 2e-5 * np.abs(a[2]) + 1e-9)
 
 
-@pytest.mark.parametrize("mt,md,T", [(0.3, 0.3, 0.8), (0.4, 0.0, 1.0)])
-def test_masked_bruteforce_gpu(m, mt, md, T):
+@pytest.mark.parametrize("mt,md,T,resample", [(0.3, 0.3, 0.8, 1), (0.4, 0.0, 1.0, 1), (0.3, 0.3, 0.8, 0)])
+def test_masked_bruteforce_gpu(m, mt, md, T, resample):
     """Verify-then-resample through the CUDA path with masked tables (and a
-    temperature) reproduces target sampling: chi^2 and TV."""
-    st = m.State(m.Config.default(masked=1), 1)
+    temperature) reproduces target sampling: chi^2 and TV; both
+    recovery-draw readings."""
+    st = m.State(m.Config.default(masked=1, resample=resample), 1)
     tab = spec_sim.Tables(6, 3, 77, mask_t=mt, mask_d=md, temp=T)
 
     def fn(cu, tokens, target, draft, seeds):

@@ -243,9 +243,11 @@ def test_device_errors(m):
     st.close()
 
 
-def test_distribution_bruteforce_gpu(m, state):
-    """S:584 through the CUDA path: V=8, depth 3, 10^6 runs."""
-    st = m.State(m.Config.default(), 1)
+@pytest.mark.parametrize("resample", [1, 0])
+def test_distribution_bruteforce_gpu(m, state, resample):
+    """S:584 through the CUDA path: V=8, depth 3, 10^6 runs, both recovery-draw
+    readings (D7, D23)."""
+    st = m.State(m.Config.default(resample=resample), 1)
 
     def fn(cu, tokens, target, draft, seeds):
         host = dict(cu_sl=cu, draft_tokens=tokens, target=target, draft=draft, seeds=seeds)
@@ -277,3 +279,64 @@ def test_kl_precision_small_and_large(m, state, dtype, sigma_n):
                 seeds=synth.slot_seeds(5, 0, cu))
     rep, _, o = _check(m, state, host, dtype)
     print(f"sigma_n={sigma_n} {dtype}: KL range {o.kld.min():.3e}..{o.kld.max():.3e} max rel {rep.kl_max_rel:.2e}")
+
+
+@pytest.mark.parametrize("V,dtype,kmax,B", [
+    (32000, torch.float32, 4, 4), (32000, torch.bfloat16, 8, 64), (128256, torch.bfloat16, 8, 12),
+    (300007, torch.bfloat16, 3, 6), (140000, torch.float32, 3, 5), (1003, torch.bfloat16, 3, 7),
+    (3, torch.bfloat16, 1, 16),
+])
+def test_verify_parity_proposal_resample(m, V, dtype, kmax, B):
+    """The D23 recovery draw (dsde_config.resample = DSDE_RESAMPLE_PROPOSAL)
+    against the oracle's D23 reading: the speculative first proposal of every
+    rejected row (V <= 131072 bf16) and the proposals built at draw time (larger
+    vocabularies)."""
+    st = m.State(m.Config.default(resample=m.RESAMPLE_PROPOSAL), 4096)
+    k = synth.random_k(B, kmax, V + B + 1)
+    for prof in (("code",), ("dialogue", "low")):
+        host = make_host_batch(V, k, seed=V * 5 + B, dtype=dtype, profiles=prof)
+        dev = to_device_inputs(host, dtype)
+        acc, em, kl, fl = gpu_verify(m, st, dev)
+        rep = parity.compare_verify(host["cu_sl"], acc, em, kl,
+                                    oracle_verify(host, resample=oracle.RESAMPLE_PROPOSAL))
+        assert rep.ok(), str(rep)
+    assert st.device_error() == (0, -1)
+
+
+@pytest.mark.parametrize("dtype,V", [(torch.bfloat16, 4096), (torch.float32, 3001), (torch.bfloat16, 128256)])
+def test_proposal_draws_and_fallback(m, dtype, V):
+    """D23 through the CUDA path on rows close enough (TV ~ 0.001-0.01) that many
+    recovery draws exhaust their 256 proposals and take the D7 draw: every
+    token equals the oracle's (ties counted), and the GPU and the oracle flag
+    the same fallbacks."""
+    st = m.State(m.Config.default(resample=m.RESAMPLE_PROPOSAL), 512)
+    rng = np.random.default_rng(V)
+    B = 2000 if V < 100000 else 48
+    k = np.ones(B, dtype=np.int64)
+    cu = synth.cu_from_k(k)
+    t = rng.normal(0, 1.0, (2 * B, V)).astype(np.float32)
+    sig = rng.uniform(0.002, 0.03, (B, 1))
+    d = (t[0::2] + rng.normal(0, 1.0, (B, V)) * sig).astype(np.float32)
+    if dtype == torch.bfloat16:
+        t = (t.view(np.uint32) >> 16).astype(np.uint16)
+        d = (d.view(np.uint32) >> 16).astype(np.uint16)
+        tf = (t.astype(np.uint32) << 16).view(np.float32)
+        df = (d.astype(np.uint32) << 16).view(np.float32)
+    else:
+        tf, df = t, d
+    # the draft token with the largest q/p: a likely rejection
+    tok = np.argmax(df - tf[0::2], axis=1).astype(np.int32)
+    host = dict(cu_sl=cu, draft_tokens=tok, target=t, draft=d, seeds=synth.slot_seeds(V, 3, cu))
+    acc, em, kl, fl = gpu_verify(m, st, to_device_inputs(host, dtype))
+    o = oracle_verify(host, resample=oracle.RESAMPLE_PROPOSAL)
+    rep = parity.compare_verify(host["cu_sl"], acc, em, kl, o)
+    assert rep.ok(), str(rep)
+    rej = np.nonzero(acc == 0)[0]
+    slots = cu[rej] + rej
+    g_fb = (fl[slots] & m.FLAG_PROPOSAL_FALLBACK) != 0
+    o_fb = (o.flags[slots] & oracle.FLAG_PROPOSAL_FALLBACK) != 0
+    assert rej.size >= 4
+    assert np.array_equal(g_fb, o_fb) or rep.sample_ties > 0
+    if V < 100000:
+        assert 0 < o_fb.sum() < rej.size   # both the proposal and the fallback paths ran
+    assert st.device_error() == (0, -1)

@@ -1,7 +1,8 @@
 """Vocabulary-parallel verification (include/dsde.h dsde_vp_*)
 through the CUDA path: the logit columns split over n shards, the stages run
 in one process with the exchanges as device reductions (VocabParallel.run_local)
-and through dsde_vp_verify (NCCL, one rank). The outputs must be bit-identical
+and through dsde_vp_verify (NCCL, one rank). The vp stages implement the D7
+recovery draw (dsde_config.resample = DSDE_RESAMPLE_FULL). The outputs must be bit-identical
 to the unsharded dsde_verify — accepted lengths, emitted tokens, KLD bits,
 flags — and within the D16 bands of the oracle."""
 import numpy as np
@@ -55,7 +56,7 @@ def _run_vp(m, st, host, dtype, n):
 ])
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
 def test_vocab_parallel_bit_identical(m, V, dtype, kmax, B, n):
-    st = m.State(m.Config.default(), 4096)
+    st = m.State(m.Config.default(resample=m.RESAMPLE_FULL), 4096)  # the vp stages implement D7
     try:
         m.VocabParallel(st, V, n, dtype)
     except m.DsdeError:
@@ -66,14 +67,15 @@ def test_vocab_parallel_bit_identical(m, V, dtype, kmax, B, n):
     got = _run_vp(m, st, host, dtype, n)
     for a, b in zip(ref, got):
         assert np.array_equal(np.asarray(a).view(np.uint8), np.asarray(b).view(np.uint8))
-    rep = parity.compare_verify(host["cu_sl"], got[0], got[1], got[2], oracle_verify(host))
+    rep = parity.compare_verify(host["cu_sl"], got[0], got[1], got[2],
+                                oracle_verify(host, resample=oracle.RESAMPLE_FULL))
     assert rep.ok(), str(rep)
     assert st.device_error() == (0, -1)
 
 
 def test_vp_verify_single_shard_and_one_rank_nccl(m):
     V, B = 32000, 48
-    st = m.State(m.Config.default(), 64)
+    st = m.State(m.Config.default(resample=m.RESAMPLE_FULL), 64)
     k = synth.random_k(B, 8, 5)
     host = make_host_batch(V, k, 6)
     dev = to_device_inputs(host, torch.bfloat16)
@@ -96,7 +98,7 @@ def test_vp_verify_single_shard_and_one_rank_nccl(m):
 
 
 def test_vp_rejects_unsupported_modes(m):
-    for kw in ({"greedy": 1}, {"masked": 1}):
+    for kw in ({"greedy": 1, "resample": 1}, {"masked": 1, "resample": 1}, {"resample": 0}):
         st = m.State(m.Config.default(**kw), 8)
         with pytest.raises(m.DsdeError):
             vp = m.VocabParallel(st, 4096, 2, torch.bfloat16)

@@ -152,7 +152,7 @@ def test_vocab_parallel_exchange_world2_matches_single_process():
         assert p.exitcode == 0
     for ci, (k, seed) in enumerate(cases):
         cu, tok, t, d, seeds = _batch(V, k, seed)
-        o = oracle.verify(cu, tok, t, d, seeds, oracle.F32)
+        o = oracle.verify(cu, tok, t, d, seeds, oracle.F32, resample=oracle.RESAMPLE_FULL)  # the vp exchange is D7
         for r in range(2):
             acc, em, kl = got[r][ci]
             assert np.array_equal(np.asarray(acc), o.accepted_len), (ci, r)

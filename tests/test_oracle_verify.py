@@ -14,17 +14,98 @@ import synth
 from tests import spec_sim
 
 
-def oracle_verify_fn(cu, tokens, target, draft, seeds):
-    r = oracle.verify(cu, tokens, target, draft, seeds, oracle.F32)
+def oracle_verify_fn(cu, tokens, target, draft, seeds, resample=oracle.RESAMPLE_FULL):
+    r = oracle.verify(cu, tokens, target, draft, seeds, oracle.F32, resample=resample)
     return r.accepted_len, r.emitted
 
 
-@pytest.mark.parametrize("V,L,seed", [(4, 3, 11), (8, 3, 12), (2, 3, 13)])
-def test_distribution_exact_bruteforce(V, L, seed):
-    """S:584 acceptance #1: V <= 8, depth 3, 10^6 runs, TV <= 0.01 and chi^2."""
+@pytest.mark.parametrize("V,L,seed,resample", [(4, 3, 11, 0), (8, 3, 12, 0), (2, 3, 13, 0),
+                                               (8, 3, 14, 1), (4, 3, 15, 1)])
+def test_distribution_exact_bruteforce(V, L, seed, resample):
+    """S:584 acceptance #1: V <= 8, depth 3, 10^6 runs, TV <= 0.01 and chi^2,
+    for both readings of the recovery draw (D23 proposals, D7 inverse CDF)."""
     tab = spec_sim.Tables(V, L, seed)
-    codes = spec_sim.run_generation(tab, 10 ** 6, oracle_verify_fn, seed)
+    codes = spec_sim.run_generation(
+        tab, 10 ** 6, lambda *a: oracle_verify_fn(*a, resample=resample), seed)
     spec_sim.check_distribution(tab, codes)
+
+
+def test_proposal_uniforms_are_philox_counter_j():
+    """D23's uniforms: Philox4x32-10 at counter (j, 0, 0, 0) (KAT-pinned), res53 of
+    words 0-1 and 2-3; counter 0 is D6's (u_acc, u_smp)."""
+    for seed in (0, 1, 0xDEADBEEFCAFEF00D):
+        key = [seed & 0xFFFFFFFF, seed >> 32]
+        assert oracle.proposal_uniforms(seed, 0) == oracle.uniforms(seed)
+        for j in (1, 2, 31, 32):
+            w = [int(x) for x in oracle.philox4x32_10([j, 0, 0, 0], key)]
+            r53 = lambda a, b: ((a >> 5) * 67108864.0 + (b >> 6)) / 9007199254740992.0
+            assert oracle.proposal_uniforms(seed, j) == (r53(w[0], w[1]), r53(w[2], w[3]))
+
+
+@pytest.mark.parametrize("seed", [41, 42])
+def test_proposal_draw_reimplemented(seed):
+    """D23 pinned by an independent re-implementation of every recovery draw:
+    scipy softmax for p and q, numpy cumsum + searchsorted for each proposal
+    v_j (smallest v with C_v > u_prop P), keep iff u_keep < max(0, p - q)_v / p_v,
+    the first kept proposal is the token; none kept in 256 -> the D7 draw
+    (flagged)."""
+    V = 29
+    k = np.array([1, 2, 3, 4, 2, 1, 3, 4] * 6)
+    cu, tok, t, d, seeds = _batch(V, k, seed)
+    d = (t[np.concatenate([np.arange(cu[i], cu[i + 1]) + i for i in range(len(k))])] +
+         np.random.default_rng(seed).normal(0, 1.0, (int(cu[-1]), V))).astype(np.float32)
+    r = np.random.default_rng(seed + 1)
+    tok = np.array([r.choice(V, p=qq) for qq in sps.softmax(d.astype(np.float64), axis=1)], dtype=np.int32)
+    res = oracle.verify(cu, tok, t, d, seeds, oracle.F32, resample=oracle.RESAMPLE_PROPOSAL)
+    n_res = 0
+    for i in range(len(k)):
+        a, s0 = int(res.accepted_len[i]), int(cu[i]) + i
+        if a == k[i]:
+            continue
+        n_res += 1
+        p = sps.softmax(t[s0 + a].astype(np.float64))
+        q = sps.softmax(d[cu[i] + a].astype(np.float64))
+        c = np.cumsum(p)
+        want = None
+        for j in range(1, oracle.PROPOSALS + 1):
+            up, uk = oracle.proposal_uniforms(int(seeds[s0 + a]), j)
+            v = int(np.searchsorted(c, up * c[-1], side="right"))
+            if uk < max(0.0, p[v] - q[v]) / p[v]:
+                want = v
+                break
+        if want is None:
+            assert res.flags[s0 + a] & oracle.FLAG_PROPOSAL_FALLBACK
+            w = np.maximum(0.0, p - q)
+            cw = np.cumsum(w)
+            want = int(np.searchsorted(cw, res.u_smp[s0 + a] * cw[-1], side="right"))
+        else:
+            assert not (res.flags[s0 + a] & oracle.FLAG_PROPOSAL_FALLBACK)
+        assert res.emitted[s0 + a] == want, (i, a)
+    assert n_res > 20
+
+
+def test_proposal_fallback_rate_is_one_minus_tv_to_the_k():
+    """A proposal v ~ p is kept with probability sum_v p_v max(0, p_v - q_v) / p_v
+    = TV(p, q), so all 256 proposals fail with probability (1 - TV)^256 (closed
+    form; TV = 0.0033 here); the D7 draw then takes over (flag)."""
+    t = np.float32([[0.0, 0.2, -0.3, 0.1, 0.4]])
+    d = np.float32([[0.01, 0.19, -0.29, 0.1, 0.395]])
+    p = sps.softmax(t[0].astype(np.float64))
+    q = sps.softmax(d[0].astype(np.float64))
+    tv = 0.5 * np.abs(p - q).sum()
+    x = int(np.argmax(q / p))  # a token with p < q: rejected unless u < p/q
+    B = 60000
+    cu = np.arange(B + 1, dtype=np.int32)
+    res = oracle.verify(cu, np.full(B, x, np.int32), np.repeat(t, 2 * B, axis=0), np.repeat(d, B, axis=0),
+                        synth.slot_seeds(7, 0, cu), oracle.F32, nthreads=8, resample=oracle.RESAMPLE_PROPOSAL)
+    rej_i = np.nonzero(res.accepted_len == 0)[0]
+    rej = rej_i.size
+    fb = int(np.sum((res.flags[2 * rej_i] & oracle.FLAG_PROPOSAL_FALLBACK) != 0))
+    assert np.all(p[res.emitted[2 * rej_i]] > q[res.emitted[2 * rej_i]])   # only residual-support tokens
+    want = (1 - tv) ** oracle.PROPOSALS
+    sd = np.sqrt(want * (1 - want) / rej)
+    assert 0.05 < want < 0.95 and rej > 300
+    assert abs(fb / rej - want) < 5 * sd
 
 
 def test_first_position_rejection_rate_is_tv():
@@ -110,9 +191,15 @@ def test_worked_example_v2():
     r0 = oracle.verify(cu, tok, t, d, np.uint64([0, 5]), oracle.F32)
     assert abs(np.exp(r0.log_ratio[0]) - 2 / 3) < 1e-7
     assert r0.accepted_len[0] == 1 and r0.emitted[0] == 1
-    r1 = oracle.verify(cu, tok, t, d, np.uint64([1, 5]), oracle.F32)
-    assert r1.accepted_len[0] == 0 and r1.emitted[0] == 0 and r1.emitted[1] == -1
-    assert abs(r1.samp_diag[0, 0] - 0.25) < 1e-7   # residual mass R = TV = 1/4
+    for mode in (oracle.RESAMPLE_PROPOSAL, oracle.RESAMPLE_FULL):
+        # token 0 is the only token with p > q: both readings must recover it
+        r1 = oracle.verify(cu, tok, t, d, np.uint64([1, 5]), oracle.F32, resample=mode)
+        assert r1.accepted_len[0] == 0 and r1.emitted[0] == 0 and r1.emitted[1] == -1
+        if mode == oracle.RESAMPLE_FULL:
+            assert abs(r1.samp_diag[0, 0] - 0.25) < 1e-7   # residual mass R = TV = 1/4
+        else:
+            assert abs(r1.samp_diag[0, 0] - 1.0) < 1e-7    # D23: the proposals' mass, sum p = 1
+            assert not (r1.flags[0] & oracle.FLAG_PROPOSAL_FALLBACK)
 
 
 def test_prefix_shape_and_layout():
@@ -241,7 +328,7 @@ def test_greedy_emits_the_target_argmax_sequence():
 
 
 @pytest.mark.parametrize("seed", [31, 32, 33])
-def test_sample_diag_edges_pinned(seed):
+def test_sample_diag_edges_pinned_full(seed):
     """The oracle's samp_diag (R, lo, hi) — the CDF edges the sample tie band of
     D16 is measured against — pinned by an independent inverse CDF: weights from
     scipy softmax (max(0, p - q) for a recovery draw, p for a bonus draw),

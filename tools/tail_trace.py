@@ -28,13 +28,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--resample", type=int, default=0, help="dsde_config.resample (0: D23, 1: D7)")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     B, V = cfg["B"], cfg["V"]
     L = m.lib()
     fn = L.dsde_debug_tail_trace
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    mcfg = m.Config.default(sl_ceiling=cfg["ceiling"], calib_sl=min(4, cfg["ceiling"]))
+    mcfg = m.Config.default(sl_ceiling=cfg["ceiling"], calib_sl=min(4, cfg["ceiling"]), resample=args.resample)
     state = m.State(mcfg, B)
     step = m.Step(state, B, V, torch.bfloat16)
     w = synth.Workload(B=B, V=V, dtype=torch.bfloat16, profiles=cfg["profiles"], seed=0)
@@ -53,14 +54,16 @@ def main():
         a = np.frombuffer(buf, dtype=np.uint64).reshape(n, 8).astype(np.int64)
         t0 = a[:, 1].min()
         rows.append(np.stack([(a[:, 1] - a[:, 0]), a[:, 2] - a[:, 1], a[:, 3] - a[:, 2], a[:, 4] - a[:, 3],
-                              a[:, 5] - a[:, 4], a[:, 5] - t0, a[:, 6] & 0xff], 1))
+                              a[:, 5] - a[:, 4], a[:, 5] - t0, a[:, 6] & 0xff, a[:, 7]], 1))
     r = np.concatenate(rows).astype(np.float64)
     r[:, :6] /= 1e3
     print(f"cfg{args.config} B={B}: per CTA (first sequence), µs: wait / finalize / layout / draw / select / end-from-first")
     for mode in np.unique(r[:, 6]).astype(int):
         x = r[r[:, 6] == mode]
         print(f"  {MODES.get(mode, mode):6s} n={len(x):5d} mean " + " / ".join(f"{v:6.2f}" for v in x[:, :6].mean(0))
-              + "   max " + " / ".join(f"{v:6.2f}" for v in x[:, :6].max(0)))
+              + "   max " + " / ".join(f"{v:6.2f}" for v in x[:, :6].max(0))
+              + (f"   D23 first proposal of the last round: mean {x[:, 7].mean():.1f} max {x[:, 7].max():.0f}"
+                 if mode == 1 and x[:, 7].max() > 0 else ""))
 
 
 if __name__ == "__main__":
