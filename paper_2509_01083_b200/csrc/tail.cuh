@@ -95,10 +95,10 @@ __device__ __forceinline__ int first_proposal(const FinArgs& a, const PCdf& cdf,
 }
 
 // p's CDF of a sequence's draft rows on the D23 path, built during the
-// finalize (k_tail phase 1) by each row's finalize warp when the row has at
-// most kSpecSub stream slices, with the row's first proposal when the row
-// rejects its draft token (speculative: it is the recovery row only if no
-// earlier row rejected).
+// finalize (k_tail phase 1) by the finalize warp of every row that rejects
+// its draft token (at most kSpecSub stream slices), with the row's first
+// proposal (speculative: it is the recovery row only if no earlier row
+// rejected).
 constexpr int kSpecSub = 64;
 struct SpecRows {
   double pre[DSDE_MAX_SL][kSpecSub];
@@ -269,23 +269,22 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
       continue;  // CTA-uniform
     }
     // 1. a2: row finalize, warp j -> draft row c0 + j
-    // D23 speculation (p.proposal): each finalize warp also builds its row's p
-    // CDF and, when the row rejects its draft token, evaluates the row's first
+    // D23 speculation (p.proposal): the finalize warp of a row that rejects its
+    // draft token also builds the row's p CDF and evaluates its first
     // proposal, so that the layout mostly finds the recovery token ready.
     const bool spec = p.proposal && a.nsub <= kSpecSub && !seq_greedy(a, i);
     for (int j = warp; j < k; j += NW) {
       const RowRes rr = row_finalize<T>(a, c0 + j, i, (i == pre_i && j == warp) ? &pre : nullptr);
       if (lane == 0) s_rr[j] = rr;
-      if (spec) {
+      // (only a row that rejects its draft token can be the recovery row)
+      if (spec && (rr.bits & RR_FINITE) && !(rr.bits & (RR_ACCEPT | RR_BADTOK))) {
         double Mr;
         const double P = pcdf_build(PRow{reinterpret_cast<const float*>(a.part + (long long)(c0 + j) * a.nsub), 8, 3},
                                     a.nsub, s_sp.pre[j], s_sp.ml2[j], &Mr);
         __syncwarp();
-        int tk = -1;
         uint8_t f = 0;
-        if ((rr.bits & RR_FINITE) && !(rr.bits & (RR_ACCEPT | RR_BADTOK)))
-          tk = first_proposal<T>(a, PCdf{s_sp.pre[j], s_sp.ml2[j], Mr, P}, (long long)c0 + i + j, (long long)c0 + j,
-                                 inv_temp(a.temps, i), rr.C, rr.lam, &f);
+        const int tk = first_proposal<T>(a, PCdf{s_sp.pre[j], s_sp.ml2[j], Mr, P}, (long long)c0 + i + j,
+                                         (long long)c0 + j, inv_temp(a.temps, i), rr.C, rr.lam, &f);
         if (lane == 0) {
           s_sp.cdf[j][0] = Mr;
           s_sp.cdf[j][1] = P;
