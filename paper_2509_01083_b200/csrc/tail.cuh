@@ -221,7 +221,10 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
   __shared__ uint8_t s_pfl[NW];
   __shared__ double s_cdf[2];
   __shared__ int s_placed;
-  __shared__ SpecRows s_sp;
+  // the D23 speculation records: dynamic shared memory, launched only with
+  // p.proposal (a static 13 KB would change the D7 path's launch footprint)
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  SpecRows& s_sp = *reinterpret_cast<SpecRows*>(s_dyn);
   const bool smem = nd <= kTailMaxSub;
   // while the stream kernel drains: the batch check (cu_sl must be a
   // non-decreasing prefix from 0, else no row can be attributed to a sequence
@@ -373,6 +376,17 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
           __syncthreads();
         }
         if (warp == 0) select_seq<T, true>(p.sa, i, r, SliceSrc<true>{s_mass, s_ref, s_scale});
+#if DSDE_TAIL_TRACE == 2
+        // measurement only: the select again (warm instructions and data), its
+        // duration in slot 7
+        if (warp == 0 && i == (int)blockIdx.x && blockIdx.x < kTraceMax) {
+          unsigned long long t0, t1;
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+          select_seq<T, true>(p.sa, i, r, SliceSrc<true>{s_mass, s_ref, s_scale});
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+          if (lane == 0) g_tail_trace[blockIdx.x * 8 + 7] = t1 - t0;
+        }
+#endif
       }
     }
     __syncthreads();  // shared records are reused by the next sequence

@@ -780,11 +780,11 @@ static int sm_count() {
 // previous kernel on the stream drains; it calls griddepcontrol.wait before
 // touching that kernel's results.
 template <typename... KArgs, typename... Args>
-static void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
+static void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, size_t dyn_smem, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = dyn_smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -799,9 +799,10 @@ static void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream
 template <typename T>
 static void launch_tail(const TailArgs& p, int B, cudaStream_t s) {
   const int sms = sm_count();
-  if (B <= sms) launch_pdl(k_tail<T, 32>, B, 1024, s, p);
-  else if (B <= 2 * sms) launch_pdl(k_tail<T, 16>, B, 512, s, p);
-  else launch_pdl(k_tail<T, 8>, std::min(B, 4 * sms), 256, s, p);
+  const size_t dyn = p.proposal ? sizeof(SpecRows) : 0;  // the D23 speculation records
+  if (B <= sms) launch_pdl(k_tail<T, 32>, B, 1024, s, dyn, p);
+  else if (B <= 2 * sms) launch_pdl(k_tail<T, 16>, B, 512, s, dyn, p);
+  else launch_pdl(k_tail<T, 8>, std::min(B, 4 * sms), 256, s, dyn, p);
 }
 
 // step != nullptr: the whole-step launch (dsde_step) with the signal (and, if

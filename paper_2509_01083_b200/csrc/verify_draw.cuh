@@ -586,7 +586,7 @@ __device__ __forceinline__ void vec_weights(const uint4& t4, const uint4& d4, co
 // passes): the non-coherent read-only path without L1 allocation (the logits
 // are never written during a call; measured 2-8% faster tails than
 // ld.global.cg: cfg3 64.7 -> 62.4 us, cfg4 112.7 -> 104.4 us)
-template <typename T, int N, bool L1 = false>
+template <typename T, int N>
 __device__ __forceinline__ void load_vecs(const T* row, int V, int u, int v0, uint4 (&r)[N]) {
   constexpr int VEC = Traits<T>::VEC, SUB = draw_elems<T>();
   const int lane = threadIdx.x & 31;
@@ -597,8 +597,7 @@ __device__ __forceinline__ void load_vecs(const T* row, int V, int u, int v0, ui
     // compiler rebuild the 64-bit row address per vector: measured 35% slower
     // draws)
 #pragma unroll
-    for (int v = 0; v < N; ++v)
-      r[v] = L1 ? __ldg(reinterpret_cast<const uint4*>(base + v * 32 * VEC)) : ld_stream_v4(base + v * 32 * VEC);
+    for (int v = 0; v < N; ++v) r[v] = ld_stream_v4(base + v * 32 * VEC);
     return;
   }
 #pragma unroll
@@ -923,25 +922,15 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
   const DrawRef DR = draw_ref(resid, r.M, (float)r.C, r.lam, m_raw, r.invT);
   int tok = -1, last_pos = -1;
   double lo = 0.0, hi = 0.0, lp_lo = 0.0, lp_hi = 0.0, vbase = base;
-  // the crossing slice's vectors requested into L1 at once, then scanned one
-  // vector at a time, not unrolled: this runs once per sequence, so its
+  // one vector at a time, not unrolled: this runs once per sequence, so its
   // instructions are cold, and the kernel's 64-register budget is shared with
-  // the draw loop (hoisting all the slice's loads into registers spilled
-  // there: measured slower draws and selects)
-  {
-    const int e0 = us * SUB + lane * VEC;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      if (e0 + v * 32 * VEC + VEC > Vl) break;
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + e0 + v * 32 * VEC));
-      if (resid) asm volatile("prefetch.global.L1 [%0];" ::"l"(dp + e0 + v * 32 * VEC));
-    }
-  }
+  // the draw loop (hoisting all the slice's loads spilled there: measured
+  // slower draws and selects; an L1 prefetch of the slice: no gain)
 #pragma unroll 1
   for (int v = 0; v < NV; ++v) {
     uint4 rt[1], rd[1];
-    load_vecs<T, 1, true>(tp, Vl, us, v, rt);
-    if (resid) load_vecs<T, 1, true>(dp, Vl, us, v, rd);
+    load_vecs<T, 1>(tp, Vl, us, v, rt);
+    if (resid) load_vecs<T, 1>(dp, Vl, us, v, rd);
     else rd[0] = rt[0];
     float wv[VEC];
     vec_weights<T>(rt[0], rd[0], DR, wv);

@@ -63,7 +63,8 @@ def main():
         print(f"  {MODES.get(mode, mode):6s} n={len(x):5d} mean " + " / ".join(f"{v:6.2f}" for v in x[:, :6].mean(0))
               + "   max " + " / ".join(f"{v:6.2f}" for v in x[:, :6].max(0))
               + (f"   D23 first proposal of the last round: mean {x[:, 7].mean():.1f} max {x[:, 7].max():.0f}"
-                 if mode == 1 and x[:, 7].max() > 0 else ""))
+                 if mode == 1 and 0 < x[:, 7].max() < 1000 else "")
+              + (f"   (trace 2) repeated select: mean {x[:, 7].mean() / 1e3:.2f} us" if x[:, 7].max() >= 1000 else ""))
 
 
 if __name__ == "__main__":
