@@ -446,7 +446,7 @@ __device__ __forceinline__ int seq_layout(const FinArgs& a, int i, int c0, int k
 //   residual: rho_v = e_v (1 - exp(-z_v)) for z_v > 0, else 0, with
 //             e_v = exp(t_v - M), z_v = w_v + lam, w_v = (t_v - d_v) - C exact,
 //             lam added as hi + lo floats; 1 - exp(-z) = z (1 - z h(-z)) for
-//             |z| < 1 (no cancellation), 1 - 2^(-z log2 e) otherwise;
+//             |z| < 1/2 (no cancellation), 1 - 2^(-z log2 e) otherwise;
 //   bonus:    p_v up to a scale: exp(t_v - m_u) about the slice max m_u,
 //             rescaled by exp(m_u - max_u m_u) in fp64 by the select.
 // The select recomputes every weight bit-identically from the same words.
@@ -457,21 +457,19 @@ __device__ __forceinline__ float2 resid_pair_exact(float2 tt, float2 dd, float2 
   const float l2 = kLog2e * invT;
   const float2 L2 = make_float2(l2, l2), nL2 = make_float2(-kLog2e, -kLog2e);
   const float2 ONE = make_float2(1.f, 1.f);
-  // degree 6 on |z| <= 1 (2.0e-7 relative; tools/fit_g.py --deg 6)
-  const float2 K6 = make_float2(2.5358644052175805e-05f, 2.5358644052175805e-05f);
-  const float2 K5 = make_float2(-2.0329201652202755e-04f, -2.0329201652202755e-04f);
-  const float2 K4 = make_float2(1.3885394437238574e-03f, 1.3885394437238574e-03f);
-  const float2 K3 = make_float2(-8.330884389579296e-03f, -8.330884389579296e-03f);
-  const float2 K2 = make_float2(4.166673496365547e-02f, 4.166673496365547e-02f);
-  const float2 K1 = make_float2(-1.6666696965694427e-01f, -1.6666696965694427e-01f);
+  // degree 5 on |z| <= 1/2 (1.1e-7 relative; tools/fit_g.py --deg 5 --range 0.5)
+  const float2 K5 = make_float2(-1.9962186343036592e-04f, -1.9962186343036592e-04f);
+  const float2 K4 = make_float2(1.3982197269797325e-03f, 1.3982197269797325e-03f);
+  const float2 K3 = make_float2(-8.333181962370872e-03f, -8.333181962370872e-03f);
+  const float2 K2 = make_float2(4.166579246520996e-02f, 4.166579246520996e-02f);
+  const float2 K1 = make_float2(-1.666666716337204e-01f, -1.666666716337204e-01f);
   const float2 K0 = make_float2(0.5f, 0.5f);
   const float2 xt = __ffma2_rn(tt, L2, nML2);
   const float2 ev = make_float2(fast_exp2(xt.x), fast_exp2(xt.y));  // 0 for padding
   // z = (t - d) / T - (C - lam), the constant carried as khi + klo
   float2 z = diff2<T>(tt, dd, khi, invT);  // t - d exact (bf16) or TwoDiff (fp32)
   z = __fadd2_rn(z, make_float2(-klo, -klo));
-  float2 pz = __ffma2_rn(K6, z, K5);
-  pz = __ffma2_rn(pz, z, K4);
+  float2 pz = __ffma2_rn(K5, z, K4);
   pz = __ffma2_rn(pz, z, K3);
   pz = __ffma2_rn(pz, z, K2);
   pz = __ffma2_rn(pz, z, K1);
@@ -479,10 +477,11 @@ __device__ __forceinline__ float2 resid_pair_exact(float2 tt, float2 dd, float2 
   const float2 sm = __fmul2_rn(z, __ffma2_rn(make_float2(-z.x, -z.y), pz, ONE));  // z (1 - z h(-z))
   const float2 xz = __fmul2_rn(z, nL2);
   const float2 bg = __fadd2_rn(ONE, make_float2(-fast_exp2(xz.x), -fast_exp2(xz.y)));  // 1 - e^-z
-  // 1 - e^-z <= 0 for z <= 0 in both forms (the polynomial only on |z| < 1),
-  // so max(0, .) zeroes exactly the tokens with p_v <= q_v (fmaxf drops the NaN
+  // 1 - e^-z <= 0 for z <= 0 in both forms (the polynomial only on |z| < 1/2;
+  // beyond, 1 - 2^(-z log2 e) has a relative error below ~3.4e-7), so
+  // max(0, .) zeroes exactly the tokens with p_v <= q_v (fmaxf drops the NaN
   // of padding, 0 * -inf)
-  const float2 om = make_float2(fabsf(z.x) < 1.f ? sm.x : bg.x, fabsf(z.y) < 1.f ? sm.y : bg.y);
+  const float2 om = make_float2(fabsf(z.x) < 0.5f ? sm.x : bg.x, fabsf(z.y) < 0.5f ? sm.y : bg.y);
   const float2 r = __fmul2_rn(ev, om);
   return make_float2(fmaxf(r.x, 0.f), fmaxf(r.y, 0.f));
 }
