@@ -387,6 +387,22 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
           if (lane == 0) g_tail_trace[blockIdx.x * 8 + 7] = t1 - t0;
         }
 #endif
+#if DSDE_TAIL_TRACE == 3
+        // measurement only: the draw pass again over the previous sequence's
+        // bonus row (warm instructions, cold data), its duration in slot 7
+        if (r.mode == MODE_BONUS && i == (int)blockIdx.x && i > 0 && blockIdx.x < kTraceMax) {
+          __syncthreads();
+          unsigned long long t0, t1;
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+          SeqRec r2 = r;
+          r2.trow = (long long)__ldg(a.cu_sl + i) + i - 1;  // the bonus row of sequence i - 1
+          for (int u = warp; u < nd; u += 2 * NW)
+            draw_mass_t2<T>(r2, u, u + NW, nd, a.V, a.tl, a.ld_t, s_mass + u, s_ref + u, s_mass + u + NW, s_ref + u + NW);
+          __syncthreads();
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+          if (threadIdx.x == 0) g_tail_trace[blockIdx.x * 8 + 7] = t1 - t0;
+        }
+#endif
       }
     }
     __syncthreads();  // shared records are reused by the next sequence

@@ -64,7 +64,8 @@ def main():
               + "   max " + " / ".join(f"{v:6.2f}" for v in x[:, :6].max(0))
               + (f"   D23 first proposal of the last round: mean {x[:, 7].mean():.1f} max {x[:, 7].max():.0f}"
                  if mode == 1 and 0 < x[:, 7].max() < 1000 else "")
-              + (f"   (trace 2) repeated select: mean {x[:, 7].mean() / 1e3:.2f} us" if x[:, 7].max() >= 1000 else ""))
+              + (f"   (trace 2/3) repeated select / draw: mean {x[:, 7][x[:, 7] > 0].mean() / 1e3:.2f} us"
+                 if x[:, 7].max() >= 1000 else ""))
 
 
 if __name__ == "__main__":
