@@ -20,12 +20,13 @@ def m():
     return dsde()
 
 
-@pytest.mark.parametrize("V,dtype", [(32000, torch.bfloat16), (8193, torch.float32)])
-def test_graph_captured_step_replays_any_sl_pattern(m, V, dtype):
+@pytest.mark.parametrize("V,dtype,resample", [(32000, torch.bfloat16, 1), (8193, torch.float32, 1),
+                                              (32000, torch.bfloat16, 0)])
+def test_graph_captured_step_replays_any_sl_pattern(m, V, dtype, resample):
     B, kmax = 32, 8
     cap_rows = B * kmax
-    st_g = m.State(m.Config.default(device_rows=1), B)
-    st_e = m.State(m.Config.default(), B)
+    st_g = m.State(m.Config.default(device_rows=1, resample=resample), B)
+    st_e = m.State(m.Config.default(resample=resample), B)
     sg = m.Step(st_g, B, V, dtype, max_draft_rows=cap_rows)
     se = m.Step(st_e, B, V, dtype, max_draft_rows=cap_rows)
     esz = 2 if dtype == torch.bfloat16 else 4
@@ -50,7 +51,8 @@ def test_graph_captured_step_replays_any_sl_pattern(m, V, dtype):
 
     rng = np.random.default_rng(V)
     # warm-up outside the capture (first-call kernel attributes) on a throwaway state
-    warm = m.Step(m.State(m.Config.default(device_rows=1), B), B, V, dtype, max_draft_rows=cap_rows)
+    warm = m.Step(m.State(m.Config.default(device_rows=1, resample=resample), B), B, V, dtype,
+                  max_draft_rows=cap_rows)
     load(0, np.full(B, 4))
     warm(cu, tok, tgt, dft, seeds, cap_rows)
     torch.cuda.synchronize()
@@ -78,7 +80,7 @@ def test_graph_captured_step_replays_any_sl_pattern(m, V, dtype):
         assert np.array_equal(kl_g.view(np.uint32), se.kld[:n].cpu().numpy().view(np.uint32)), t
         for name in ("sl_hat", "next_sl", "cap"):
             assert torch.equal(getattr(sg, name), getattr(se, name)), (t, name)
-        rep = parity.compare_verify(host["cu_sl"], acc_g, em_g, kl_g, oracle_verify(host))
+        rep = parity.compare_verify(host["cu_sl"], acc_g, em_g, kl_g, oracle_verify(host, resample=resample))
         assert rep.ok(), (t, str(rep))
     assert st_g.device_error()[0] == 0 and st_e.device_error()[0] == 0
 
