@@ -108,6 +108,27 @@ struct SpecRows {
   uint8_t fl[DSDE_MAX_SL];
 };
 
+// D23 speculation for draft row j of sequence i (one warp): the row's p CDF
+// and its first proposal into the SpecRows entry j. (Out of line, the kernel
+// parameters it references would need a per-thread local copy: 1.1 KB of
+// stack.)
+template <typename T>
+__device__ __forceinline__ void spec_row(const FinArgs& a, int i, int c0, int j, double C, double lam, SpecRows* sp) {
+  double Mr;
+  const double P = pcdf_build(PRow{reinterpret_cast<const float*>(a.part + (long long)(c0 + j) * a.nsub), 8, 3},
+                              a.nsub, sp->pre[j], sp->ml2[j], &Mr);
+  __syncwarp();
+  uint8_t f = 0;
+  const int tk = first_proposal<T>(a, PCdf{sp->pre[j], sp->ml2[j], Mr, P}, (long long)c0 + i + j, (long long)c0 + j,
+                                   inv_temp(a.temps, i), C, lam, &f);
+  if ((threadIdx.x & 31) == 0) {
+    sp->cdf[j][0] = Mr;
+    sp->cdf[j][1] = P;
+    sp->tok[j] = tk;
+    sp->fl[j] = f;
+  }
+}
+
 // a4 on the D23 path (p.proposal), a recovery draw (CTA-uniform result
 // through *s_placed): p's CDF over the drawn row's stream slices (its draft
 // row's partials) comes from the finalize's speculation (sp != NULL) or is
@@ -280,21 +301,8 @@ __global__ void __launch_bounds__(NW * 32, 1024 / (NW * 32)) k_tail(TailArgs p) 
       const RowRes rr = row_finalize<T>(a, c0 + j, i, (i == pre_i && j == warp) ? &pre : nullptr);
       if (lane == 0) s_rr[j] = rr;
       // (only a row that rejects its draft token can be the recovery row)
-      if (spec && (rr.bits & RR_FINITE) && !(rr.bits & (RR_ACCEPT | RR_BADTOK))) {
-        double Mr;
-        const double P = pcdf_build(PRow{reinterpret_cast<const float*>(a.part + (long long)(c0 + j) * a.nsub), 8, 3},
-                                    a.nsub, s_sp.pre[j], s_sp.ml2[j], &Mr);
-        __syncwarp();
-        uint8_t f = 0;
-        const int tk = first_proposal<T>(a, PCdf{s_sp.pre[j], s_sp.ml2[j], Mr, P}, (long long)c0 + i + j,
-                                         (long long)c0 + j, inv_temp(a.temps, i), rr.C, rr.lam, &f);
-        if (lane == 0) {
-          s_sp.cdf[j][0] = Mr;
-          s_sp.cdf[j][1] = P;
-          s_sp.tok[j] = tk;
-          s_sp.fl[j] = f;
-        }
-      }
+      if (spec && (rr.bits & RR_FINITE) && !(rr.bits & (RR_ACCEPT | RR_BADTOK)))
+        spec_row<T>(a, i, c0, j, rr.C, rr.lam, &s_sp);
     }
     __syncthreads();
     if (i == (int)blockIdx.x) TAIL_STAMP(2);
