@@ -4,11 +4,15 @@
 //
 // One CTA of NW warps per sequence i (grid-stride over the batch):
 //   1. warp j < k_i merges draft row c0 + j's slice partials in fp64 and runs
-//      its accept test (row_finalize, a2) -> RowRes in shared memory;
+//      its accept test (row_finalize, a2) -> RowRes in shared memory; with the
+//      D23 recovery draw (p.proposal) a row that rejects its draft token also
+//      gets its p CDF and its first proposal (spec_row);
 //   2. warp 0 finds the first rejection a_i, writes the KLDs, the emitted-token
 //      layout and the draw record of row a_i (residual) or k_i (bonus)
 //      (seq_layout, a3);
-//   3. the warps sweep the vocabulary slices of the drawn row and record each
+//   3. D23 (p.proposal, recovery draws): the speculative first proposal or
+//      rounds of proposals (tail_p_draw); otherwise (D7, or no proposal kept)
+//      the warps sweep the vocabulary slices of the drawn row and record each
 //      slice's draw-weight mass (draw_mass, a4 first pass); meanwhile, in
 //      dsde_step, warp NW-1 first updates the sequence's signal and SL^
 //      (signal_seq_vals, a5-a6) and the warp completing the batch's last

@@ -8,7 +8,8 @@
 //      about the slice reference) and write 32-byte slice partials;
 //   2. k_tail (tail.cuh), launched with programmatic dependent launch: one CTA
 //      per sequence merges its rows in fp64 (KL, log p/q, Philox accept test,
-//      a2), lays it out (a3), draws its token (a4) and, in dsde_step, updates
+//      a2), lays it out (a3), draws its token (a4: D7 inverse CDF over the drawn
+//      row, or the D23 proposals from p for a recovery draw) and, in dsde_step, updates
 //      its signal and SL^ (a5-a6); the last signal applies the batch cap (a7,
 //      single GPU);
 //   3. (dsde_step with a communicator) k_cap_partial, ncclAllReduce, k_cap_apply.
