@@ -995,9 +995,8 @@ __device__ __forceinline__ void select_seq(const SelArgs& a, int i, const SeqRec
 
 // ---------------------------------------------------------------------------
 // D23 path: p's statistics per stream slice of one target row — the draft
-// row's SubPartials (S at +0, M/T at +3, 8 floats per slice) or the streamed
-// bonus row's (S, M/T) pairs (2 floats per slice); written by the stream
-// kernel, read with ld.global.cg.
+// row's SubPartials (S at +0, M/T at +3: stride 8 floats, offset 3); written by
+// the stream kernel, read with ld.global.cg.
 // ---------------------------------------------------------------------------
 struct PRow {
   const float* base;
