@@ -65,7 +65,9 @@ __device__ unsigned long long g_tail_trace[kTraceMax * 8];
 __device__ __forceinline__ void tail_stamp(int k) {
   if (threadIdx.x == 0 && blockIdx.x < kTraceMax) {
     unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    // (the memory clobber keeps the read after a preceding __syncthreads: without
+    // it ptxas may hoist the timer read above the barrier)
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)::"memory");
     g_tail_trace[blockIdx.x * 8 + k] = t;
   }
 }

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--resample", type=int, default=0, help="dsde_config.resample (0: D23, 1: D7)")
+    ap.add_argument("--layout-end", action="store_true", help="trace build 4: slot 7 = seq_layout's own end")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     B, V = cfg["B"], cfg["V"]
@@ -53,8 +54,9 @@ def main():
         assert fn(buf, n) == 0
         a = np.frombuffer(buf, dtype=np.uint64).reshape(n, 8).astype(np.int64)
         t0 = a[:, 1].min()
+        slot7 = (a[:, 7] - a[:, 2]) if args.layout_end else a[:, 7]
         rows.append(np.stack([(a[:, 1] - a[:, 0]), a[:, 2] - a[:, 1], a[:, 3] - a[:, 2], a[:, 4] - a[:, 3],
-                              a[:, 5] - a[:, 4], a[:, 5] - t0, a[:, 6] & 0xff, a[:, 7]], 1))
+                              a[:, 5] - a[:, 4], a[:, 5] - t0, a[:, 6] & 0xff, slot7], 1))
     r = np.concatenate(rows).astype(np.float64)
     r[:, :6] /= 1e3
     print(f"cfg{args.config} B={B}: per CTA (first sequence), µs: wait / finalize / layout / draw / select / end-from-first")
