@@ -73,7 +73,9 @@ typedef enum { DSDE_F32 = 0, DSDE_BF16 = 1 } dsde_dtype;
 
 /* Per-slot bits of the optional `flags` output of dsde_verify. */
 #define DSDE_FLAG_ACCEPT_NEAR_TIE 1  /* |u_acc - min(1, p/q)| < 1e-6 at this position      */
-#define DSDE_FLAG_SAMPLE_NEAR_TIE 2  /* |u_smp - C/R| < 1e-6 at a CDF edge of the draw      */
+#define DSDE_FLAG_SAMPLE_NEAR_TIE 2  /* |u_smp - C/R| < 1e-6 at a CDF edge of the draw (D23: also a
+                                        proposal's u_prop at a CDF edge of p or u_keep within
+                                        1e-6 of its keep probability)                        */
 #define DSDE_FLAG_FALLBACK 4         /* residual mass 0: the token was drawn from p (D7)  */
 #define DSDE_FLAG_PROPOSAL_FALLBACK 8 /* D23: none of the DSDE_RESAMPLE_PROPOSALS proposals was
                                         kept; the recovery token is the D7 draw              */
@@ -87,7 +89,7 @@ typedef enum { DSDE_F32 = 0, DSDE_BF16 = 1 } dsde_dtype;
  *     probability max(0, p_v - q_v) / p_v (u_keep < that); the first kept
  *     proposal is the token. Exact: a kept proposal is distributed as
  *     normalize(max(0, p - q)); each is kept with probability TV(p, q). If
- *     none of DSDE_RESAMPLE_PROPOSALS is kept, the D7 draw below decides
+ *     none of DSDE_RESAMPLE_PROPOSALS is kept, the D7 draw above decides
  *     (flag DSDE_FLAG_PROPOSAL_FALLBACK). (u_prop, u_keep) of proposal j:
  *     Philox4x32-10 keyed by the slot's seed at counter (j, 0, 0, 0), res53 of
  *     words 0-1 / 2-3 (D6 uses counter 0). A proposal needs p's slice masses
